@@ -1,0 +1,151 @@
+/*
+ * voxvie_b200 -- C-ABI of the B200-native hot path of the circulant-
+ * preconditioned voxel VIE (arXiv 1903.07884; reference package `voxvie`).
+ *
+ * Every array argument is a DEVICE pointer to interleaved complex128
+ * (vx_c128, 16 bytes) or int32, owned by the caller; every call is
+ * asynchronous on the given CUDA stream (`stream` = cudaStream_t, NULL =
+ * legacy default).  Calls return a status:
+ *
+ *   VX_OK 0  |  VX_EINVAL 1 -> ValueError  |  VX_ESINGULAR 2 -> PreconditionerBuildError
+ *   VX_ECAP 3 -> PreconditionerBuildError  |  VX_ECUDA 4  |  VX_ENCCL 5
+ *
+ * and vx_last_error() returns a thread-local message for the last failure.
+ *
+ * Layouts (reference grid.py:1-9): fields are (3, nz, ny, nx) C-order, x
+ * fastest; the generating tensors are (6, 2nz-1, 2ny-1, 2nx-1) ordered
+ * xx,xy,xz,yy,yz,zz (reference kernel.py:119-141, accel.py:38-41).
+ *
+ * Each entry point names the reference interface it replaces.
+ */
+#ifndef VOXVIE_B200_H
+#define VOXVIE_B200_H
+
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define VX_ABI_VERSION 1
+
+#define VX_OK 0
+#define VX_EINVAL 1
+#define VX_ESINGULAR 2
+#define VX_ECAP 3
+#define VX_ECUDA 4
+#define VX_ENCCL 5
+
+typedef struct vx_c128 { double re, im; } vx_c128;
+
+const char* vx_last_error(void);
+int vx_version(void);
+
+/* ------------------------------------------------------------------ FFT */
+/* 13-smooth length >= n (operator padding), and smoothness test. */
+int vx_fft_good_length(int n);
+int vx_fft_is_smooth(int n);
+
+/* Batched strided 1-D DFT, scipy convention (forward unnormalised, inverse
+ * scaled by `scale`): line l = (o, i), o = l / n_inner, i = l % n_inner,
+ * element e at base + o*os + i*is + e*es.  Input read for e < n_in (zero
+ * padded to n), output written for e < n_out.  Used by every transform below;
+ * exported for the FFT parity tests (scipy.fft.fft on strided axes). */
+int vx_fft_lines(int n, int n_lines, int n_inner, const vx_c128* in, long in_os, long in_is,
+                 long in_es, int n_in, vx_c128* out, long out_os, long out_is, long out_es,
+                 int n_out, int inverse, double scale, void* stream);
+
+/* ------------------------------------------------------------- operator */
+/* Replaces operator.plan_operator (operator.py:61-70): spectra (6, pz, py, px)
+ * of the generators embedded in their (pz, py, px) circulant extension
+ * (operator.py:21-41; any p >= 2n-1 gives the same matvec).  gen strides are
+ * in elements for axes (component, z, y, x). */
+int vx_op_plan(int nx, int ny, int nz, int px, int py, int pz, const vx_c128* gen, long g_sp,
+               long g_sz, long g_sy, long g_sx, vx_c128* spectra, void* stream);
+
+/* Scratch (in vx_c128 elements) needed by vx_op_apply. */
+long vx_op_work_elems(int nx, int ny, int nz, int px, int py, int pz);
+
+/* Replaces operator.apply_n / apply_system (operator.py:82-105):
+ * y = N x (m == NULL) or y = x - m .* (N x), m of shape (nz, ny, nx). */
+int vx_op_apply(int nx, int ny, int nz, int px, int py, int pz, const vx_c128* spectra,
+                const vx_c128* m, const vx_c128* x, vx_c128* y, vx_c128* work, void* stream);
+
+/* --------------------------------------------------- 1-level preconditioner */
+/* Replaces circulant._chan_x_spectra (circulant.py:129-136): lamT (nx, 6, 2nz-1, 2ny-1),
+ * k-major, = fft_x(chan_x(gen)) transposed so block k's generators are contiguous. */
+int vx_chan_x_spectra(int nx, int ny, int nz, const vx_c128* gen, long g_sp, long g_sz, long g_sy,
+                      long g_sx, vx_c128* lamT, void* stream);
+
+/* Proxies (circulant.py:99-110, 328-332): proxy[k] = (ny*nz==1) - m00 * lamT[k,0,0,0]. */
+int vx_proxy(int nx, int ny, int nz, const vx_c128* lamT, vx_c128 m00, vx_c128* proxy, void* stream);
+
+/* Tile geometry used for the stored factors of an n x n block. */
+int vx_lu_tile(int n);
+long vx_lu_block_elems(int n);   /* complex entries per stored block (padded tiles) */
+
+/* Replaces the unfold + lu_factor loop of build_one_level / build_reduced_one_level
+ * (circulant.py:216-224, 341-343; accel.py:157-179): for slot s, block k = kset[s]:
+ * D = I - diag(m_yz) N_k assembled straight into tiled storage and factorised with
+ * partial pivoting (zgetrf semantics, pivot = argmax |Re|+|Im|).  Writes factors,
+ * row permutation perm (n per slot, composed from the LAPACK pivots), piv
+ * (LAPACK ipiv, 0-based) and info[s] (0 ok, j+1 = first zero pivot column). */
+int vx_lu1_build(int nx, int ny, int nz, const vx_c128* lamT, const vx_c128* m_yz, const int* kset,
+                 int nslots, vx_c128* factors, int* perm, int* piv, int* info, void* stream);
+
+/* Replaces OneLevelPrec.apply / ReducedOneLevelPrec.apply (circulant.py:162-188,
+ * 264-269): y = F_x^-1 blockdiag(D_k^-1) F_x x for x of shape (3N, nrhs).
+ * Work list: item t solves slot items[3t] for the frequencies
+ * klist[items[3t+1] .. items[3t+1]+items[3t+2]); items [0, n_single) have one
+ * frequency each, items [n_single, n_items) up to 16 (representative block). */
+long vx_prec1_work_elems(int nx, int ny, int nz, int nrhs);
+int vx_prec1_apply(int nx, int ny, int nz, int nrhs, const vx_c128* factors, const int* perm,
+                   const int* items, int n_single, int n_items, const int* klist,
+                   const vx_c128* x, vx_c128* y, vx_c128* work, void* stream);
+
+/* --------------------------------------------------- 2-level preconditioner */
+/* circulant.py:434-435: lam2T (ny*nx, 6, 2nz-1) = fftn_{y,x}(chan_y(chan_x(gen))). */
+long vx_chan_xy_work_elems(int nx, int ny, int nz);
+int vx_chan_xy_spectra(int nx, int ny, int nz, const vx_c128* gen, long g_sp, long g_sz, long g_sy,
+                       long g_sx, vx_c128* lam2T, vx_c128* work, void* stream);
+/* circulant.py:436-446 + accel.py:181-197: (3nz)^2 blocks for all (l, k). */
+int vx_lu2_build(int nx, int ny, int nz, const vx_c128* lam2T, const vx_c128* m_z,
+                 vx_c128* factors, int* perm, int* piv, int* info, void* stream);
+/* TwoLevelPrec.apply (circulant.py:379-394). */
+long vx_prec2_work_elems(int nx, int ny, int nz, int nrhs);
+int vx_prec2_apply(int nx, int ny, int nz, int nrhs, const vx_c128* factors, const int* perm,
+                   const vx_c128* x, vx_c128* y, vx_c128* work, void* stream);
+
+/* --------------------------------------------------------------- blocked */
+/* BlockedPrec.apply gather/scatter (circulant.py:558-563, 603-607): box
+ * (x0,y0,z0) of size (bx,by,bz) inside the (nx,ny,nz) grid, nrhs columns. */
+int vx_box_gather(int nx, int ny, int nz, int x0, int y0, int z0, int bx, int by, int bz, int nrhs,
+                  const vx_c128* full, vx_c128* box, void* stream);
+int vx_box_scatter(int nx, int ny, int nz, int x0, int y0, int z0, int bx, int by, int bz, int nrhs,
+                   const vx_c128* box, vx_c128* full, void* stream);
+
+/* ---------------------------------------------------------------- GMRES */
+/* Arnoldi orthogonalisation of solver._gmres_cycle (solver.py:62-77) as
+ * classical Gram-Schmidt with the reference's DGKS criterion
+ * (||w1|| < 0.7071 ||w0|| -> second pass).  Deterministic fixed-order
+ * reductions.  V holds nvec = j+1 basis vectors of length n at stride ldv;
+ * w is orthogonalised in place and written (normalised) to V[j+1] when
+ * `vnext` is non-null.  hout receives j+2 complex: h_0..h_j, h_{j+1} = ||w||;
+ * stats receives (||w0||, ||w1||, reorth flag).  part: scratch of
+ * vx_arnoldi_part_elems(n, nvec) entries. */
+long vx_arnoldi_part_elems(long n, int nvec);
+int vx_arnoldi_step(long n, int nvec, const vx_c128* V, long ldv, vx_c128* w, vx_c128* vnext,
+                    vx_c128* hout, double* stats, vx_c128* part, void* stream);
+/* solver.py:110 -- u = sum_i y_i V_i. */
+int vx_basis_combine(long n, int nvec, const vx_c128* V, long ldv, const vx_c128* y, vx_c128* u,
+                     void* stream);
+/* Vector helpers: out = a*x + b*y ; norm2 -> dots[0].re (deterministic). */
+int vx_axpby(long n, vx_c128 a, const vx_c128* x, vx_c128 b, const vx_c128* y, vx_c128* out,
+             void* stream);
+int vx_norm2(long n, const vx_c128* x, double* out, vx_c128* part, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* VOXVIE_B200_H */

@@ -1,0 +1,315 @@
+// Arnoldi orthogonalisation and vector kernels for the device-resident GMRES
+// (reference solver.py:45-111).
+//
+// The reference uses modified Gram-Schmidt with one DGKS re-orthogonalisation
+// pass when ||w1|| < 0.7071 ||w0||.  Here each pass is classical Gram-Schmidt
+// (one multi-dot sweep over the basis, one multi-axpy sweep): mathematically
+// identical, 2 streaming passes over V instead of j+1 dependent ones.  The
+// DGKS decision is taken on the device (flag in `stats`), so the conditional
+// second pass costs two early-exit launches and no host round trip.
+// All reductions are two-stage with a fixed order (per-CTA partials, then one
+// CTA summing them in index order): results are bitwise reproducible.
+#include "common.cuh"
+
+namespace vx {
+
+constexpr int AR_THREADS = 256;
+constexpr int AR_GROUP = 4;  // basis vectors per register group
+
+static int ar_grid(long n) {
+  long g = (n + 2047) / 2048;
+  const long cap = 8L * device_sm_count();
+  if (g > cap) g = cap;
+  if (g < 1) g = 1;
+  return (int)g;
+}
+
+__device__ __forceinline__ double2 warp_sum(double2 v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    v.x += __shfl_down_sync(0xffffffffu, v.x, o);
+    v.y += __shfl_down_sync(0xffffffffu, v.y, o);
+  }
+  return v;
+}
+
+// CTA-wide sum in fixed order; result valid in thread 0.
+__device__ __forceinline__ double2 block_sum(double2 v, double2* sh) {
+  v = warp_sum(v);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) sh[warp] = v;
+  __syncthreads();
+  double2 r = cmk(0.0, 0.0);
+  if (threadIdx.x == 0)
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) r = cadd(r, sh[w]);
+  return r;
+}
+
+__device__ __forceinline__ void chunk(long n, long& beg, long& end) {
+  const long per = (n + gridDim.x - 1) / gridDim.x;
+  beg = (long)blockIdx.x * per;
+  end = beg + per < n ? beg + per : n;
+}
+
+// part[i*G + b] = sum_{e in chunk b} conj(V_i[e]) w[e], i < nvec; part[nvec*G+b] = ||w||^2
+__global__ void __launch_bounds__(AR_THREADS) dots_kernel(long n, int nvec, const double2* __restrict__ V,
+                                                          long ldv, const double2* __restrict__ w,
+                                                          double2* __restrict__ part,
+                                                          const double* cond) {
+  if (cond && cond[2] == 0.0) return;
+  __shared__ double2 sh[AR_THREADS / 32];
+  long beg, end;
+  chunk(n, beg, end);
+  const int G = gridDim.x;
+  double2 nrm = cmk(0.0, 0.0);
+  for (long e = beg + threadIdx.x; e < end; e += AR_THREADS) {
+    const double2 x = w[e];
+    nrm.x = fma(x.x, x.x, nrm.x);
+    nrm.x = fma(x.y, x.y, nrm.x);
+  }
+  double2 r = block_sum(nrm, sh);
+  if (threadIdx.x == 0) part[(long)nvec * G + blockIdx.x] = r;
+  for (int i0 = 0; i0 < nvec; i0 += AR_GROUP) {
+    double2 acc[AR_GROUP];
+#pragma unroll
+    for (int g = 0; g < AR_GROUP; ++g) acc[g] = cmk(0.0, 0.0);
+    for (long e = beg + threadIdx.x; e < end; e += AR_THREADS) {
+      const double2 x = w[e];
+#pragma unroll
+      for (int g = 0; g < AR_GROUP; ++g)
+        if (i0 + g < nvec) {
+          const double2 v = ld_stream(V + (long)(i0 + g) * ldv + e);
+          // conj(v) * x
+          acc[g].x = fma(v.x, x.x, acc[g].x);
+          acc[g].x = fma(v.y, x.y, acc[g].x);
+          acc[g].y = fma(v.x, x.y, acc[g].y);
+          acc[g].y = fma(-v.y, x.x, acc[g].y);
+        }
+    }
+#pragma unroll
+    for (int g = 0; g < AR_GROUP; ++g) {
+      if (i0 + g < nvec) {
+        double2 s = block_sum(acc[g], sh);
+        if (threadIdx.x == 0) part[(long)(i0 + g) * G + blockIdx.x] = s;
+      }
+    }
+  }
+}
+
+// w[e] -= sum_i coef[i] V_i[e]; part[b] = ||w_new||^2 over chunk b
+__global__ void __launch_bounds__(AR_THREADS) update_kernel(long n, int nvec, const double2* __restrict__ V,
+                                                            long ldv, const double2* __restrict__ coef,
+                                                            double2* __restrict__ w,
+                                                            double2* __restrict__ part,
+                                                            const double* cond) {
+  if (cond && cond[2] == 0.0) return;
+  __shared__ double2 sh[AR_THREADS / 32];
+  __shared__ double2 cf[128];
+  long beg, end;
+  chunk(n, beg, end);
+  double2 nrm = cmk(0.0, 0.0);
+  for (int i0 = 0; i0 < nvec; i0 += 128) {
+    const int m = nvec - i0 < 128 ? nvec - i0 : 128;
+    __syncthreads();
+    for (int i = threadIdx.x; i < m; i += AR_THREADS) cf[i] = coef[i0 + i];
+    __syncthreads();
+    const bool last = (i0 + 128 >= nvec);
+    for (long e = beg + threadIdx.x; e < end; e += AR_THREADS) {
+      double2 x = w[e];
+      int i = 0;
+      for (; i + 4 <= m; i += 4) {
+        const double2 v0 = ld_stream(V + (long)(i0 + i) * ldv + e);
+        const double2 v1 = ld_stream(V + (long)(i0 + i + 1) * ldv + e);
+        const double2 v2 = ld_stream(V + (long)(i0 + i + 2) * ldv + e);
+        const double2 v3 = ld_stream(V + (long)(i0 + i + 3) * ldv + e);
+        cfms(x, cf[i], v0);
+        cfms(x, cf[i + 1], v1);
+        cfms(x, cf[i + 2], v2);
+        cfms(x, cf[i + 3], v3);
+      }
+      for (; i < m; ++i) cfms(x, cf[i], ld_stream(V + (long)(i0 + i) * ldv + e));
+      w[e] = x;
+      if (last) {
+        nrm.x = fma(x.x, x.x, nrm.x);
+        nrm.x = fma(x.y, x.y, nrm.x);
+      }
+    }
+  }
+  if (nvec == 0) {
+    for (long e = beg + threadIdx.x; e < end; e += AR_THREADS) {
+      const double2 x = w[e];
+      nrm.x = fma(x.x, x.x, nrm.x);
+      nrm.x = fma(x.y, x.y, nrm.x);
+    }
+  }
+  double2 r = block_sum(nrm, sh);
+  if (threadIdx.x == 0) part[blockIdx.x] = r;
+}
+
+// Fixed-order finalisation of the partial sums (single CTA).
+//  mode 0: h[i] = sum part_i (i<nvec); stats[0] = sqrt(sum part_nvec)
+//  mode 1: stats[1] = sqrt(sum part_0); stats[2] = stats[1] < 0.7071 stats[0]; h[nvec] = stats[1]
+//  mode 2 (cond): c[i] = sum part_i; h[i] += c[i]
+//  mode 3 (cond): h[nvec] = sqrt(sum part_0)
+__global__ void __launch_bounds__(AR_THREADS) finalize_kernel(int nvec, int G, const double2* __restrict__ part,
+                                                              double2* __restrict__ h,
+                                                              double2* __restrict__ c, double* stats,
+                                                              int mode) {
+  if ((mode == 2 || mode == 3) && stats[2] == 0.0) return;
+  __shared__ double2 sh[AR_THREADS / 32];
+  const int rows = (mode == 0) ? nvec + 1 : (mode == 2 ? nvec : 1);
+  for (int i = 0; i < rows; ++i) {
+    double2 v = cmk(0.0, 0.0);
+    for (int b = threadIdx.x; b < G; b += AR_THREADS) v = cadd(v, part[(long)i * G + b]);
+    v = block_sum(v, sh);
+    if (threadIdx.x == 0) {
+      if (mode == 0) {
+        if (i < nvec) h[i] = v;
+        else stats[0] = sqrt(v.x);
+      } else if (mode == 1) {
+        stats[1] = sqrt(v.x);
+        stats[2] = (stats[1] < 0.7071 * stats[0]) ? 1.0 : 0.0;
+        h[nvec] = cmk(stats[1], 0.0);
+      } else if (mode == 2) {
+        c[i] = v;
+        h[i] = cadd(h[i], v);
+      } else {
+        h[nvec] = cmk(sqrt(v.x), 0.0);
+      }
+    }
+  }
+}
+
+__global__ void scale_kernel(long n, const double2* __restrict__ w, double2* __restrict__ out,
+                             const double2* __restrict__ hn) {
+  const double s = hn->x;
+  const double inv = s > 0.0 ? 1.0 / s : 0.0;
+  for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < n; e += (long)gridDim.x * blockDim.x) {
+    const double2 x = w[e];
+    // the reference divides (w / h); division keeps parity with numpy
+    out[e] = s > 0.0 ? cmk(x.x / s, x.y / s) : cmk(x.x * inv, x.y * inv);
+  }
+}
+
+__global__ void combine_kernel(long n, int nvec, const double2* __restrict__ V, long ldv,
+                               const double2* __restrict__ y, double2* __restrict__ u) {
+  __shared__ double2 ys[128];
+  for (long base = (long)blockIdx.x * blockDim.x; base < n; base += (long)gridDim.x * blockDim.x) {
+    const long e = base + threadIdx.x;
+    double2 acc = cmk(0.0, 0.0);
+    for (int i0 = 0; i0 < nvec; i0 += 128) {
+      const int m = nvec - i0 < 128 ? nvec - i0 : 128;
+      __syncthreads();
+      for (int i = threadIdx.x; i < m; i += blockDim.x) ys[i] = y[i0 + i];
+      __syncthreads();
+      if (e < n)
+        for (int i = 0; i < m; ++i) cfma(acc, ys[i], ld_stream(V + (long)(i0 + i) * ldv + e));
+    }
+    if (e < n) u[e] = acc;
+  }
+}
+
+__global__ void axpby_kernel(long n, double2 a, const double2* __restrict__ x, double2 b,
+                             const double2* __restrict__ y, double2* __restrict__ out) {
+  for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < n; e += (long)gridDim.x * blockDim.x) {
+    double2 v = cmul(a, x[e]);
+    if (y) cfma(v, b, y[e]);
+    out[e] = v;
+  }
+}
+
+__global__ void __launch_bounds__(AR_THREADS) norm_part_kernel(long n, const double2* __restrict__ x,
+                                                               double2* __restrict__ part) {
+  __shared__ double2 sh[AR_THREADS / 32];
+  long beg, end;
+  chunk(n, beg, end);
+  double2 nrm = cmk(0.0, 0.0);
+  for (long e = beg + threadIdx.x; e < end; e += AR_THREADS) {
+    const double2 v = x[e];
+    nrm.x = fma(v.x, v.x, nrm.x);
+    nrm.x = fma(v.y, v.y, nrm.x);
+  }
+  double2 r = block_sum(nrm, sh);
+  if (threadIdx.x == 0) part[blockIdx.x] = r;
+}
+
+__global__ void __launch_bounds__(AR_THREADS) norm_final_kernel(int G, const double2* __restrict__ part,
+                                                                double* out) {
+  __shared__ double2 sh[AR_THREADS / 32];
+  double2 v = cmk(0.0, 0.0);
+  for (int b = threadIdx.x; b < G; b += AR_THREADS) v = cadd(v, part[b]);
+  v = block_sum(v, sh);
+  if (threadIdx.x == 0) out[0] = sqrt(v.x);
+}
+
+static unsigned stream_grid(long n) {
+  long g = (n + 255) / 256;
+  const long cap = 16L * device_sm_count();
+  return (unsigned)(g < 1 ? 1 : (g > cap ? cap : g));
+}
+
+}  // namespace vx
+
+using namespace vx;
+
+extern "C" long vx_arnoldi_part_elems(long n, int nvec) {
+  return (long)(nvec + 2) * ar_grid(n) + nvec + 2;
+}
+
+extern "C" int vx_arnoldi_step(long n, int nvec, const vx_c128* V, long ldv, vx_c128* w,
+                               vx_c128* vnext, vx_c128* hout, double* stats, vx_c128* part,
+                               void* stream) {
+  VX_REQUIRE(n >= 1 && nvec >= 0 && ldv >= n, "bad Arnoldi arguments");
+  cudaStream_t s = as_stream(stream);
+  const int G = ar_grid(n);
+  const double2* Vd = reinterpret_cast<const double2*>(V);
+  double2* wd = reinterpret_cast<double2*>(w);
+  double2* hd = reinterpret_cast<double2*>(hout);
+  double2* pd = reinterpret_cast<double2*>(part);
+  double2* cd = pd + (long)(nvec + 2) * G;  // second-pass coefficients
+  dots_kernel<<<G, AR_THREADS, 0, s>>>(n, nvec, Vd, ldv, wd, pd, nullptr);
+  finalize_kernel<<<1, AR_THREADS, 0, s>>>(nvec, G, pd, hd, cd, stats, 0);
+  update_kernel<<<G, AR_THREADS, 0, s>>>(n, nvec, Vd, ldv, hd, wd, pd, nullptr);
+  finalize_kernel<<<1, AR_THREADS, 0, s>>>(nvec, G, pd, hd, cd, stats, 1);
+  // DGKS second pass, executed only if the device flag stats[2] is set
+  dots_kernel<<<G, AR_THREADS, 0, s>>>(n, nvec, Vd, ldv, wd, pd, stats);
+  finalize_kernel<<<1, AR_THREADS, 0, s>>>(nvec, G, pd, hd, cd, stats, 2);
+  update_kernel<<<G, AR_THREADS, 0, s>>>(n, nvec, Vd, ldv, cd, wd, pd, stats);
+  finalize_kernel<<<1, AR_THREADS, 0, s>>>(nvec, G, pd, hd, cd, stats, 3);
+  if (vnext)
+    scale_kernel<<<stream_grid(n), 256, 0, s>>>(n, wd, reinterpret_cast<double2*>(vnext), hd + nvec);
+  VX_CHECK_LAUNCH("arnoldi_step");
+  return VX_OK;
+}
+
+extern "C" int vx_basis_combine(long n, int nvec, const vx_c128* V, long ldv, const vx_c128* y,
+                                vx_c128* u, void* stream) {
+  VX_REQUIRE(n >= 1 && nvec >= 0, "bad combine arguments");
+  combine_kernel<<<stream_grid(n), 256, 0, as_stream(stream)>>>(
+      n, nvec, reinterpret_cast<const double2*>(V), ldv, reinterpret_cast<const double2*>(y),
+      reinterpret_cast<double2*>(u));
+  VX_CHECK_LAUNCH("combine_kernel");
+  return VX_OK;
+}
+
+extern "C" int vx_axpby(long n, vx_c128 a, const vx_c128* x, vx_c128 b, const vx_c128* y,
+                        vx_c128* out, void* stream) {
+  if (n <= 0) return VX_OK;
+  axpby_kernel<<<stream_grid(n), 256, 0, as_stream(stream)>>>(
+      n, make_double2(a.re, a.im), reinterpret_cast<const double2*>(x), make_double2(b.re, b.im),
+      reinterpret_cast<const double2*>(y), reinterpret_cast<double2*>(out));
+  VX_CHECK_LAUNCH("axpby_kernel");
+  return VX_OK;
+}
+
+extern "C" int vx_norm2(long n, const vx_c128* x, double* out, vx_c128* part, void* stream) {
+  VX_REQUIRE(n >= 1, "bad norm arguments");
+  const int G = ar_grid(n);
+  cudaStream_t s = as_stream(stream);
+  norm_part_kernel<<<G, AR_THREADS, 0, s>>>(n, reinterpret_cast<const double2*>(x),
+                                            reinterpret_cast<double2*>(part));
+  norm_final_kernel<<<1, AR_THREADS, 0, s>>>(G, reinterpret_cast<const double2*>(part), out);
+  VX_CHECK_LAUNCH("norm2");
+  return VX_OK;
+}

@@ -1,0 +1,733 @@
+// Chan-circulant preconditioners (reference circulant.py, accel.py unfolds).
+//
+// Build:  Chan + x-DFT of the six generators (k-major output), then one CTA per
+//         frequency block: unfold D_k = I - diag(m) N_k straight into tiled
+//         storage, blocked right-looking LU with partial pivoting (LAPACK
+//         zgetrf pivot rule |Re|+|Im|, first index on ties), diagonal tiles
+//         replaced by their triangular inverses.
+// Apply:  x-DFT (and y-DFT for 2-level) of the field, one CTA per frequency
+//         block streaming its factor tiles exactly once in storage order
+//         (forward: row i = tiles L_i0..L_i,i-1, inv(L_ii); backward: U tiles,
+//         inv(U_ii)), inverse DFTs with 1/n folded into the storer.
+//
+// Factor storage per block: nt x nt tiles of T x T (T <= 32), tile (i, j) at
+// offset (i*nt + j)*T*T, column-major inside the tile; rows/cols >= n are an
+// identity pad.
+#include "fft_lines.cuh"
+
+namespace vx {
+
+struct LuGeom {
+  int n, T, nt, npad;
+  long blk;
+};
+
+static int lu_pick_tile(int n) {
+  if (n <= 32) return n < 1 ? 1 : n;
+  int best = 32, bestpad = (n + 31) / 32 * 32;
+  for (int T = 32; T >= 16; --T) {
+    int pad = (n + T - 1) / T * T;
+    if (pad < bestpad) { best = T; bestpad = pad; }
+  }
+  return best;
+}
+
+static LuGeom lu_geom(int n) {
+  LuGeom g;
+  g.n = n;
+  g.T = lu_pick_tile(n);
+  g.nt = (n + g.T - 1) / g.T;
+  g.npad = g.nt * g.T;
+  g.blk = (long)g.npad * g.npad;
+  return g;
+}
+
+__device__ __forceinline__ long lu_off(const LuGeom& g, int row, int col) {
+  const int it = row / g.T, jt = col / g.T;
+  return ((long)(it * g.nt + jt) * g.T + (col - jt * g.T)) * g.T + (row - it * g.T);
+}
+
+__constant__ int c_pair[9] = {0, 1, 2, 1, 3, 4, 2, 4, 5};
+
+// ----------------------------------------------------------------- spectra
+// Generator line l = (p, dz, dy) of a (6, nzz, nyy, *) tensor with strides.
+struct GenLine {
+  long sp, sz, sy;
+  int nzz, nyy;
+  __device__ __forceinline__ long base(int l) const {
+    const int per = nzz * nyy;
+    const int p = l / per, r = l - p * per;
+    const int dz = r / nyy, dy = r - dz * nyy;
+    return p * sp + dz * sz + dy * sy;
+  }
+};
+
+struct LoadChanGen {
+  const double2* __restrict__ g;
+  GenLine gl;
+  long sx;
+  int n;
+  __device__ __forceinline__ long line_base(int l) const { return gl.base(l); }
+  __device__ __forceinline__ double2 operator()(long b, int s) const {
+    const double2 tp = __ldg(g + b + (long)(n - 1 + s) * sx);
+    if (s == 0) return tp;
+    const double2 tn = __ldg(g + b + (long)(s - 1) * sx);
+    const double fn = (double)n, ws = (double)(n - s), wt = (double)s;
+    return cmk((ws * tp.x + wt * tn.x) / fn, (ws * tp.y + wt * tn.y) / fn);
+  }
+};
+
+__global__ void proxy_kernel(int nx, long Ltot, const double2* __restrict__ lamT, double2 m00,
+                             int q_is_one, double2* __restrict__ proxy) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= nx) return;
+  double2 v = cmul(m00, lamT[(long)k * Ltot]);
+  proxy[k] = cmk((q_is_one ? 1.0 : 0.0) - v.x, -v.y);
+}
+
+// ---------------------------------------------------------------- LU build
+constexpr int LU_WARPS = 4;
+constexpr int LU_THREADS = LU_WARPS * 32;
+constexpr int LU_CW = 8;  // output columns per register chunk
+
+// unfold parameters: rows/cols ordered a*q + iz*nyL + iy (reference accel.py:71-91);
+// the 2-level (3nz)^2 block is the nyL = 1 case (accel.py:94-111).
+struct Unfold {
+  const double2* __restrict__ lamT;  // (blocks, 6, 2nzL-1, 2nyL-1)
+  const double2* __restrict__ m;     // (nzL, nyL)
+  const int* __restrict__ kset;      // slot -> block (null: identity)
+  long Ltot;
+  int nzL, nyL;
+};
+
+__device__ __forceinline__ double2 unfold_entry(const Unfold& u, const double2* lam, int q, int row,
+                                                int col) {
+  const int a = row / q, rr = row - a * q;
+  const int b = col / q, cc = col - b * q;
+  const int iz = rr / u.nyL, iy = rr - iz * u.nyL;
+  const int jz = cc / u.nyL, jy = cc - jz * u.nyL;
+  const int nyy = 2 * u.nyL - 1, nzz = 2 * u.nzL - 1;
+  const double2 t = __ldg(lam + (long)c_pair[3 * a + b] * nzz * nyy + (iz - jz + u.nzL - 1) * nyy +
+                          (iy - jy + u.nyL - 1));
+  double2 v = cmul(__ldg(u.m + rr), t);
+  v = cmk(-v.x, -v.y);
+  if (row == col) v.x += 1.0;
+  return v;
+}
+
+// C(T x T, global) = Aop * Bs  (overwrite)  or  C -= Aop * Bs.
+// Aop column-major T x T (global or smem), lane r reads Aop[k*T + r];
+// Bs column-major in smem, broadcast reads Bs[c*T + k].
+template <bool SUB>
+__device__ __forceinline__ void warp_tile_gemm(const double2* Aop, const double2* Bs, double2* C, int T,
+                                               int lane) {
+  if (lane >= T) return;
+  for (int c0 = 0; c0 < T; c0 += LU_CW) {
+    double2 acc[LU_CW];
+#pragma unroll
+    for (int c = 0; c < LU_CW; ++c)
+      acc[c] = (SUB && c0 + c < T) ? C[(c0 + c) * T + lane] : cmk(0.0, 0.0);
+    for (int k = 0; k < T; ++k) {
+      const double2 a = Aop[k * T + lane];
+#pragma unroll
+      for (int c = 0; c < LU_CW; ++c) {
+        if (c0 + c < T) {
+          if (SUB) cfms(acc[c], a, Bs[(c0 + c) * T + k]);
+          else cfma(acc[c], a, Bs[(c0 + c) * T + k]);
+        }
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < LU_CW; ++c)
+      if (c0 + c < T) C[(c0 + c) * T + lane] = acc[c];
+  }
+}
+
+__global__ void __launch_bounds__(LU_THREADS) lu_build_kernel(Unfold u, LuGeom g, double2* F,
+                                                               int* perm, int* piv, int* info) {
+  extern __shared__ double2 sm[];
+  const int T = g.T, T2 = T * T, nt = g.nt, npad = g.npad, n = g.n;
+  double2* Ls = sm;                    // inv(L_kk), column-major
+  double2* Us = Ls + T2;               // inv(U_kk)
+  double2* Bst = Us + T2;              // LU_WARPS staged B tiles
+  int* pivs = reinterpret_cast<int*>(Bst + LU_WARPS * T2);  // [T]
+  double* redv = reinterpret_cast<double*>(pivs + 32);        // [LU_WARPS]
+  int* redi = reinterpret_cast<int*>(redv + LU_WARPS);        // [LU_WARPS]
+  int* flags = redi + LU_WARPS;                               // [0]=info [1]=any swap
+  int* gpiv = flags + 4;                                      // [npad] full pivot record
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int slot = blockIdx.x;
+  const int k = u.kset ? u.kset[slot] : slot;
+  double2* A = F + (long)slot * g.blk;
+  const double2* lam = u.lamT + (long)k * u.Ltot;
+  const int q = u.nzL * u.nyL;
+
+  // phase 0: D_k = I - diag(m) N_k into tiled storage (identity pad)
+  for (long i = tid; i < g.blk; i += LU_THREADS) {
+    const int r = (int)(i % T);
+    const long t2 = i / T;
+    const int c = (int)(t2 % T);
+    const int tile = (int)(t2 / T);
+    const int row = (tile / nt) * T + r, col = (tile % nt) * T + c;
+    double2 v;
+    if (row < n && col < n) v = unfold_entry(u, lam, q, row, col);
+    else v = cmk(row == col ? 1.0 : 0.0, 0.0);
+    A[i] = v;
+  }
+  if (tid == 0) flags[0] = 0;
+  __syncthreads();
+
+  for (int kt = 0; kt < nt; ++kt) {
+    const int c0 = kt * T;
+    // ---- (1) panel factorisation of tile column kt
+    for (int jj = 0; jj < T; ++jj) {
+      const int j = c0 + jj;
+      double best = -1.0;
+      int bi = j;
+      for (int row = j + tid; row < npad; row += LU_THREADS) {
+        const double2 v = A[lu_off(g, row, j)];
+        const double a = fabs(v.x) + fabs(v.y);
+        if (a > best) { best = a; bi = row; }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ob = __shfl_down_sync(0xffffffffu, best, o);
+        const int oi = __shfl_down_sync(0xffffffffu, bi, o);
+        if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+      }
+      if (lane == 0) { redv[warp] = best; redi[warp] = bi; }
+      __syncthreads();
+      if (tid == 0) {
+        double b = redv[0];
+        int ii = redi[0];
+        for (int w = 1; w < LU_WARPS; ++w)
+          if (redv[w] > b || (redv[w] == b && redi[w] < ii)) { b = redv[w]; ii = redi[w]; }
+        if (!(b > 0.0) && b != 0.0) ii = j;  // all NaN
+        pivs[jj] = ii;
+        gpiv[j] = ii;
+      }
+      __syncthreads();
+      const int p = pivs[jj];
+      if (p != j && tid < T) {
+        const long oa = lu_off(g, j, c0 + tid), ob = lu_off(g, p, c0 + tid);
+        const double2 t = A[oa];
+        A[oa] = A[ob];
+        A[ob] = t;
+      }
+      __syncthreads();
+      const double2 d = A[lu_off(g, j, j)];
+      const bool bad = (d.x == 0.0 && d.y == 0.0) || !isfinite(d.x) || !isfinite(d.y);
+      if (bad) {
+        if (tid == 0 && flags[0] == 0 && j < n) flags[0] = j + 1;
+      } else {
+        const double2 dinv = cinv(d);
+        for (int row = j + 1 + tid; row < npad; row += LU_THREADS) {
+          const long o = lu_off(g, row, j);
+          A[o] = cmul(A[o], dinv);
+        }
+      }
+      __syncthreads();
+      const int ncol = T - jj - 1, nrow = npad - j - 1;
+      if (ncol > 0 && nrow > 0) {
+        const int tot = ncol * nrow;
+        for (int idx = tid; idx < tot; idx += LU_THREADS) {
+          const int cc = idx / nrow, rr = idx - cc * nrow;
+          const int row = j + 1 + rr, col = j + 1 + cc;
+          const double2 l = A[lu_off(g, row, j)];
+          const double2 uu = A[lu_off(g, j, col)];
+          const long o = lu_off(g, row, col);
+          double2 v = A[o];
+          cfms(v, l, uu);
+          A[o] = v;
+        }
+      }
+      __syncthreads();
+    }
+    // ---- (2) the panel's row interchanges on every other tile column (zlaswp)
+    if (tid == 0) {
+      int any = 0;
+      for (int jj = 0; jj < T; ++jj) any |= (pivs[jj] != c0 + jj);
+      flags[1] = any;
+    }
+    __syncthreads();
+    if (flags[1]) {
+      for (int col = tid; col < npad; col += LU_THREADS) {
+        if (col / T == kt) continue;
+        for (int jj = 0; jj < T; ++jj) {
+          const int j = c0 + jj, p = pivs[jj];
+          if (p == j) continue;
+          const long oa = lu_off(g, j, col), ob = lu_off(g, p, col);
+          const double2 t = A[oa];
+          A[oa] = A[ob];
+          A[ob] = t;
+        }
+      }
+    }
+    __syncthreads();
+    // ---- (3) triangular inverses of the diagonal tile (lane = column)
+    const double2* Dg = A + (long)(kt * nt + kt) * T2;
+    if (warp == 0 && lane < T) {
+      const int c = lane;
+      for (int r = 0; r < T; ++r) {
+        double2 x = cmk(r == c ? 1.0 : 0.0, 0.0);
+        if (r > c) {
+          for (int i = c; i < r; ++i) cfms(x, Dg[i * T + r], Ls[c * T + i]);
+        } else if (r < c) {
+          x = cmk(0.0, 0.0);
+        }
+        Ls[c * T + r] = x;
+      }
+    } else if (warp == 1 && lane < T) {
+      const int c = lane;
+      for (int r = T - 1; r >= 0; --r) {
+        double2 x = cmk(0.0, 0.0);
+        if (r <= c) {
+          x = cmk(r == c ? 1.0 : 0.0, 0.0);
+          for (int i = r + 1; i <= c; ++i) cfms(x, Dg[i * T + r], Us[c * T + i]);
+          x = cdiv(x, Dg[r * T + r]);
+        }
+        Us[c * T + r] = x;
+      }
+    }
+    __syncthreads();
+    // ---- (4) U row tiles: A(kt, jt) = inv(L_kk) A(kt, jt); packed diagonal tile
+    {
+      double2* Bw = Bst + warp * T2;
+      for (int jt = kt + 1 + warp; jt < nt; jt += LU_WARPS) {
+        double2* C = A + (long)(kt * nt + jt) * T2;
+        for (int i = lane; i < T2; i += 32) Bw[i] = C[i];
+        __syncwarp();
+        warp_tile_gemm<false>(Ls, Bw, C, T, lane);
+        __syncwarp();
+      }
+      double2* Dw = A + (long)(kt * nt + kt) * T2;
+      for (int i = tid; i < T2; i += LU_THREADS) {
+        const int c = i / T, r = i - c * T;
+        Dw[i] = (r > c) ? Ls[i] : Us[i];
+      }
+    }
+    __syncthreads();
+    // ---- (5) trailing update A(it, jt) -= A(it, kt) A(kt, jt)
+    const int nrem = nt - kt - 1;
+    if (nrem > 0) {
+      double2* Bw = Bst + warp * T2;
+      int staged = -1;
+      const int ntask = nrem * nrem;
+      for (int t = warp; t < ntask; t += LU_WARPS) {
+        const int jt = kt + 1 + t / nrem, it = kt + 1 + t % nrem;
+        if (jt != staged) {
+          __syncwarp();
+          const double2* Bsrc = A + (long)(kt * nt + jt) * T2;
+          for (int i = lane; i < T2; i += 32) Bw[i] = Bsrc[i];
+          __syncwarp();
+          staged = jt;
+        }
+        warp_tile_gemm<true>(A + (long)(it * nt + kt) * T2, Bw, A + (long)(it * nt + jt) * T2, T, lane);
+      }
+    }
+    __syncthreads();
+  }
+  // permutation composed from the interchange sequence (zgetrs applies the
+  // swaps to b in order): b_perm[i] = b[perm[i]]
+  if (tid == 0) {
+    info[slot] = flags[0];
+  }
+  int* pv = reinterpret_cast<int*>(Bst);  // reuse staging smem
+  for (int i = tid; i < npad; i += LU_THREADS) pv[i] = i;
+  __syncthreads();
+  if (tid == 0) {
+    for (int j = 0; j < npad; ++j) {
+      const int p = gpiv[j];
+      if (p != j) { const int t = pv[j]; pv[j] = pv[p]; pv[p] = t; }
+    }
+  }
+  __syncthreads();
+  for (int i = tid; i < n; i += LU_THREADS) {
+    int v = pv[i];
+    perm[(long)slot * n + i] = v < n ? v : i;
+    piv[(long)slot * n + i] = gpiv[i];
+  }
+}
+
+static size_t lu_smem(const LuGeom& g) {
+  return (size_t)(2 + LU_WARPS) * g.T * g.T * sizeof(double2) + 32 * sizeof(int) +
+         LU_WARPS * (sizeof(double) + sizeof(int)) + 4 * sizeof(int) + (size_t)g.npad * sizeof(int) + 64;
+}
+
+static int lu_build(const Unfold& u, int n, int nslots, double2* F, int* perm, int* piv, int* info,
+                    cudaStream_t s) {
+  if (nslots <= 0) return VX_OK;
+  LuGeom g = lu_geom(n);
+  size_t smem = lu_smem(g);
+  // the permutation scratch reuses the staging tiles: make sure they fit npad ints
+  size_t need_perm = (size_t)g.npad * sizeof(int);
+  if ((size_t)LU_WARPS * g.T * g.T * sizeof(double2) < need_perm) smem += need_perm;
+  if (smem > 48 * 1024)
+    VX_CUDA(cudaFuncSetAttribute(lu_build_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 device_smem_optin()));
+  VX_REQUIRE((int)smem <= device_smem_optin(), "block size %d too large for the LU kernel", n);
+  lu_build_kernel<<<nslots, LU_THREADS, smem, s>>>(u, g, F, perm, piv, info);
+  VX_CHECK_LAUNCH("lu_build_kernel");
+  return VX_OK;
+}
+
+// ---------------------------------------------------------------- LU solve
+// One CTA per work item: slot + up to R right-hand sides (frequency k, column j)
+// gathered from Y[row*s_row + k*s_k + j] through the row permutation.
+template <int R, int NW>
+__global__ void __launch_bounds__(NW * 32) lu_solve_kernel(LuGeom g, const double2* __restrict__ F,
+                                                           const int* __restrict__ perm,
+                                                           const int* __restrict__ items, int item0,
+                                                           const int* __restrict__ klist, int nrhs,
+                                                           double2* Y, long s_row, long s_k) {
+  extern __shared__ double2 sm[];
+  const int T = g.T, T2 = T * T, nt = g.nt, npad = g.npad, n = g.n;
+  double2* y = sm;                    // [npad][R]
+  double2* red = y + (long)npad * R;  // [NW][T][R]
+  double2* Ds = red + NW * T * R;     // [T*T]
+  double2* zb = Ds + T2;              // [T][R]
+  __shared__ long rbase[R];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int NT = NW * 32;
+  int slot, beg, cnt;
+  if (items) {
+    const int it = item0 + blockIdx.x;
+    slot = items[3 * it];
+    beg = items[3 * it + 1];
+    cnt = items[3 * it + 2];
+  } else {
+    slot = item0 + blockIdx.x;
+    beg = slot;
+    cnt = 1;
+  }
+  const double2* Fb = F + (long)slot * g.blk;
+  const int* pm = perm + (long)slot * n;
+  const int total = cnt * nrhs;
+  for (int rho0 = 0; rho0 < total; rho0 += R) {
+    const int nr = min(R, total - rho0);
+    if (tid < R) {
+      long b = 0;
+      if (tid < nr) {
+        const int rho = rho0 + tid;
+        const int kk = klist ? klist[beg + rho / nrhs] : beg + rho / nrhs;
+        b = (long)kk * s_k + (rho % nrhs);
+      }
+      rbase[tid] = b;
+    }
+    __syncthreads();
+    for (int idx = tid; idx < npad * R; idx += NT) {
+      const int row = idx / R, rr = idx - row * R;
+      double2 v = cmk(0.0, 0.0);
+      if (row < n && rr < nr) v = Y[(long)pm[row] * s_row + rbase[rr]];
+      y[idx] = v;
+    }
+    __syncthreads();
+    // forward: L (unit lower, diagonal tiles hold inv(L_ii) below the diagonal)
+    for (int i = 0; i < nt; ++i) {
+      double2 acc[R];
+#pragma unroll
+      for (int rr = 0; rr < R; ++rr) acc[rr] = cmk(0.0, 0.0);
+      if (lane < T) {
+        for (int j = warp; j < i; j += NW) {
+          const double2* tile = Fb + (long)(i * nt + j) * T2 + lane;
+          const double2* yj = y + (long)j * T * R;
+#pragma unroll 8
+          for (int c = 0; c < T; ++c) {
+            const double2 a = ld_stream(tile + c * T);
+#pragma unroll
+            for (int rr = 0; rr < R; ++rr) cfma(acc[rr], a, yj[c * R + rr]);
+          }
+        }
+#pragma unroll
+        for (int rr = 0; rr < R; ++rr) red[(warp * T + lane) * R + rr] = acc[rr];
+      }
+      const double2* dt = Fb + (long)(i * nt + i) * T2;
+      for (int idx = tid; idx < T2; idx += NT) Ds[idx] = ld_stream(dt + idx);
+      __syncthreads();
+      for (int idx = tid; idx < T * R; idx += NT) {
+        const int r = idx / R, rr = idx - r * R;
+        double2 z = y[(long)(i * T + r) * R + rr];
+        for (int w = 0; w < NW; ++w) z = csub(z, red[(w * T + r) * R + rr]);
+        zb[idx] = z;
+      }
+      __syncthreads();
+      for (int idx = tid; idx < T * R; idx += NT) {
+        const int r = idx / R, rr = idx - r * R;
+        double2 o = zb[idx];
+        for (int c = 0; c < r; ++c) cfma(o, Ds[c * T + r], zb[c * R + rr]);
+        y[(long)(i * T + r) * R + rr] = o;
+      }
+      __syncthreads();
+    }
+    // backward: U (diagonal tiles hold inv(U_ii) on and above the diagonal)
+    for (int i = nt - 1; i >= 0; --i) {
+      double2 acc[R];
+#pragma unroll
+      for (int rr = 0; rr < R; ++rr) acc[rr] = cmk(0.0, 0.0);
+      if (lane < T) {
+        for (int j = i + 1 + warp; j < nt; j += NW) {
+          const double2* tile = Fb + (long)(i * nt + j) * T2 + lane;
+          const double2* yj = y + (long)j * T * R;
+#pragma unroll 8
+          for (int c = 0; c < T; ++c) {
+            const double2 a = ld_stream(tile + c * T);
+#pragma unroll
+            for (int rr = 0; rr < R; ++rr) cfma(acc[rr], a, yj[c * R + rr]);
+          }
+        }
+#pragma unroll
+        for (int rr = 0; rr < R; ++rr) red[(warp * T + lane) * R + rr] = acc[rr];
+      }
+      const double2* dt = Fb + (long)(i * nt + i) * T2;
+      for (int idx = tid; idx < T2; idx += NT) Ds[idx] = ld_stream(dt + idx);
+      __syncthreads();
+      for (int idx = tid; idx < T * R; idx += NT) {
+        const int r = idx / R, rr = idx - r * R;
+        double2 z = y[(long)(i * T + r) * R + rr];
+        for (int w = 0; w < NW; ++w) z = csub(z, red[(w * T + r) * R + rr]);
+        zb[idx] = z;
+      }
+      __syncthreads();
+      for (int idx = tid; idx < T * R; idx += NT) {
+        const int r = idx / R, rr = idx - r * R;
+        double2 o = cmk(0.0, 0.0);
+        for (int c = r; c < T; ++c) cfma(o, Ds[c * T + r], zb[c * R + rr]);
+        y[(long)(i * T + r) * R + rr] = o;
+      }
+      __syncthreads();
+    }
+    for (int idx = tid; idx < n * R; idx += NT) {
+      const int row = idx / R, rr = idx - row * R;
+      if (rr < nr) Y[(long)row * s_row + rbase[rr]] = y[idx];
+    }
+    __syncthreads();
+  }
+}
+
+template <int R, int NW>
+static int launch_solve(const LuGeom& g, const double2* F, const int* perm, const int* items,
+                        int item0, int nblocks, const int* klist, int nrhs, double2* Y, long s_row,
+                        long s_k, cudaStream_t s) {
+  if (nblocks <= 0) return VX_OK;
+  const size_t smem = ((size_t)g.npad * R + (size_t)NW * g.T * R + (size_t)g.T * g.T +
+                       (size_t)g.T * R) * sizeof(double2);
+  auto kern = lu_solve_kernel<R, NW>;
+  if (smem > 48 * 1024)
+    VX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 device_smem_optin()));
+  VX_REQUIRE((int)smem <= device_smem_optin(), "block size %d too large for the solve kernel", g.n);
+  kern<<<nblocks, NW * 32, smem, s>>>(g, F, perm, items, item0, klist, nrhs, Y, s_row, s_k);
+  VX_CHECK_LAUNCH("lu_solve_kernel");
+  return VX_OK;
+}
+
+constexpr int SOLVE_WARPS = 8;
+constexpr int MULTI_R = 8;
+
+// ---------------------------------------------------------------- blocked
+__global__ void box_copy_kernel(int nx, int ny, int nz, int x0, int y0, int z0, int bx, int by,
+                                int bz, int nrhs, const double2* __restrict__ src,
+                                double2* __restrict__ dst, int to_box) {
+  const long total = 3L * bz * by * bx * nrhs;
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < total; i += (long)gridDim.x * blockDim.x) {
+    long r = i;
+    const int j = (int)(r % nrhs); r /= nrhs;
+    const int x = (int)(r % bx); r /= bx;
+    const int y = (int)(r % by); r /= by;
+    const int z = (int)(r % bz); r /= bz;
+    const int c = (int)r;
+    const long full = ((((long)c * nz + z0 + z) * ny + y0 + y) * nx + x0 + x) * nrhs + j;
+    if (to_box) dst[i] = src[full];
+    else dst[full] = src[i];
+  }
+}
+
+}  // namespace vx
+
+using namespace vx;
+
+extern "C" int vx_chan_x_spectra(int nx, int ny, int nz, const vx_c128* gen, long g_sp, long g_sz,
+                                 long g_sy, long g_sx, vx_c128* lamT, void* stream) {
+  VX_REQUIRE(nx >= 1 && ny >= 1 && nz >= 1, "grid dims must be >= 1");
+  FftPlan p;
+  int st = fft_get_plan(nx, &p);
+  if (st) return st;
+  const int nzz = 2 * nz - 1, nyy = 2 * ny - 1;
+  const int lines = 6 * nzz * nyy;
+  LoadChanGen ld{reinterpret_cast<const double2*>(gen), {g_sp, g_sz, g_sy, nzz, nyy}, g_sx, nx};
+  StoreStrided sv{reinterpret_cast<double2*>(lamT), {1, 0, lines, 1}, 1.0};
+  return launch_fft_lines(p, ld, sv, lines, nx, nx, false, false, as_stream(stream));
+}
+
+extern "C" int vx_proxy(int nx, int ny, int nz, const vx_c128* lamT, vx_c128 m00, vx_c128* proxy,
+                        void* stream) {
+  const long Ltot = 6L * (2 * nz - 1) * (2 * ny - 1);
+  proxy_kernel<<<div_up(nx, 256), 256, 0, as_stream(stream)>>>(
+      nx, Ltot, reinterpret_cast<const double2*>(lamT), make_double2(m00.re, m00.im),
+      (ny * nz == 1) ? 1 : 0, reinterpret_cast<double2*>(proxy));
+  VX_CHECK_LAUNCH("proxy_kernel");
+  return VX_OK;
+}
+
+extern "C" int vx_lu_tile(int n) { return lu_geom(n).T; }
+extern "C" long vx_lu_block_elems(int n) { return lu_geom(n).blk; }
+
+extern "C" int vx_lu1_build(int nx, int ny, int nz, const vx_c128* lamT, const vx_c128* m_yz,
+                            const int* kset, int nslots, vx_c128* factors, int* perm, int* piv,
+                            int* info, void* stream) {
+  VX_REQUIRE(nx >= 1 && ny >= 1 && nz >= 1 && nslots >= 0, "bad 1-level build arguments");
+  Unfold u{reinterpret_cast<const double2*>(lamT), reinterpret_cast<const double2*>(m_yz), kset,
+           6L * (2 * nz - 1) * (2 * ny - 1), nz, ny};
+  return lu_build(u, 3 * ny * nz, nslots, reinterpret_cast<double2*>(factors), perm, piv, info,
+                  as_stream(stream));
+}
+
+extern "C" long vx_prec1_work_elems(int nx, int ny, int nz, int nrhs) {
+  return 3L * nx * ny * nz * nrhs;
+}
+
+extern "C" int vx_prec1_apply(int nx, int ny, int nz, int nrhs, const vx_c128* factors,
+                              const int* perm, const int* items, int n_single, int n_items,
+                              const int* klist, const vx_c128* x, vx_c128* y, vx_c128* work,
+                              void* stream) {
+  VX_REQUIRE(nx >= 1 && ny >= 1 && nz >= 1 && nrhs >= 1, "bad 1-level apply arguments");
+  VX_REQUIRE(n_single >= 0 && n_items >= n_single, "bad work list");
+  cudaStream_t s = as_stream(stream);
+  FftPlan p;
+  int st = fft_get_plan(nx, &p);
+  if (st) return st;
+  const int q3 = 3 * ny * nz;
+  double2* S = reinterpret_cast<double2*>(work);
+  const long pitch = (long)nx * nrhs;
+  {
+    LoadStrided ld{reinterpret_cast<const double2*>(x), {pitch, 1, nrhs, nrhs}};
+    StoreStrided sv{S, {pitch, 1, nrhs, nrhs}, 1.0};
+    if ((st = launch_fft_lines(p, ld, sv, q3 * nrhs, nx, nx, false, nrhs == 1, s))) return st;
+  }
+  LuGeom g = lu_geom(q3);
+  const double2* F = reinterpret_cast<const double2*>(factors);
+  if (nrhs == 1) {
+    if ((st = launch_solve<1, SOLVE_WARPS>(g, F, perm, items, 0, n_single, klist, 1, S, pitch, nrhs, s)))
+      return st;
+  } else {
+    if ((st = launch_solve<MULTI_R, SOLVE_WARPS>(g, F, perm, items, 0, n_single, klist, nrhs, S, pitch,
+                                                  nrhs, s)))
+      return st;
+  }
+  if ((st = launch_solve<MULTI_R, SOLVE_WARPS>(g, F, perm, items, n_single, n_items - n_single, klist,
+                                                nrhs, S, pitch, nrhs, s)))
+    return st;
+  {
+    LoadStrided ld{S, {pitch, 1, nrhs, nrhs}};
+    StoreStrided sv{reinterpret_cast<double2*>(y), {pitch, 1, nrhs, nrhs}, 1.0 / nx};
+    if ((st = launch_fft_lines(p, ld, sv, q3 * nrhs, nx, nx, true, nrhs == 1, s))) return st;
+  }
+  return VX_OK;
+}
+
+extern "C" long vx_chan_xy_work_elems(int nx, int ny, int nz) {
+  return 6L * (2 * nz - 1) * (2 * ny - 1) * nx;
+}
+
+extern "C" int vx_chan_xy_spectra(int nx, int ny, int nz, const vx_c128* gen, long g_sp, long g_sz,
+                                  long g_sy, long g_sx, vx_c128* lam2T, vx_c128* work,
+                                  void* stream) {
+  VX_REQUIRE(nx >= 1 && ny >= 1 && nz >= 1, "grid dims must be >= 1");
+  cudaStream_t s = as_stream(stream);
+  FftPlan px, py;
+  int st;
+  if ((st = fft_get_plan(nx, &px)) || (st = fft_get_plan(ny, &py))) return st;
+  const int nzz = 2 * nz - 1, nyy = 2 * ny - 1;
+  double2* tmp = reinterpret_cast<double2*>(work);  // (6, nzz, nyy, nx)
+  {
+    LoadChanGen ld{reinterpret_cast<const double2*>(gen), {g_sp, g_sz, g_sy, nzz, nyy}, g_sx, nx};
+    StoreStrided sv{tmp, {nx, 0, 1, 1}, 1.0};
+    if ((st = launch_fft_lines(px, ld, sv, 6 * nzz * nyy, nx, nx, false, g_sx == 1, s))) return st;
+  }
+  {
+    // lines (p, dz) x k along dy; Chan along y, DFT length ny, k-major output
+    LoadChan ld{tmp, {(long)nyy * nx, 1, nx, nx}, ny};
+    StoreStrided sv{reinterpret_cast<double2*>(lam2T), {1, 6L * nzz, 6L * nzz * nx, nx}, 1.0};
+    if ((st = launch_fft_lines(py, ld, sv, 6 * nzz * nx, ny, ny, false, false, s))) return st;
+  }
+  return VX_OK;
+}
+
+extern "C" int vx_lu2_build(int nx, int ny, int nz, const vx_c128* lam2T, const vx_c128* m_z,
+                            vx_c128* factors, int* perm, int* piv, int* info, void* stream) {
+  VX_REQUIRE(nx >= 1 && ny >= 1 && nz >= 1, "bad 2-level build arguments");
+  Unfold u{reinterpret_cast<const double2*>(lam2T), reinterpret_cast<const double2*>(m_z), nullptr,
+           6L * (2 * nz - 1), nz, 1};
+  return lu_build(u, 3 * nz, nx * ny, reinterpret_cast<double2*>(factors), perm, piv, info,
+                  as_stream(stream));
+}
+
+extern "C" long vx_prec2_work_elems(int nx, int ny, int nz, int nrhs) {
+  return 3L * nx * ny * nz * nrhs;
+}
+
+extern "C" int vx_prec2_apply(int nx, int ny, int nz, int nrhs, const vx_c128* factors,
+                              const int* perm, const vx_c128* x, vx_c128* y, vx_c128* work,
+                              void* stream) {
+  VX_REQUIRE(nx >= 1 && ny >= 1 && nz >= 1 && nrhs >= 1, "bad 2-level apply arguments");
+  cudaStream_t s = as_stream(stream);
+  FftPlan px, py;
+  int st;
+  if ((st = fft_get_plan(nx, &px)) || (st = fft_get_plan(ny, &py))) return st;
+  double2* S = reinterpret_cast<double2*>(work);
+  const long pitch = (long)nx * nrhs;      // x line pitch
+  const long plane = (long)ny * pitch;     // (c, z) plane
+  const int q3 = 3 * ny * nz;
+  {
+    LoadStrided ld{reinterpret_cast<const double2*>(x), {pitch, 1, nrhs, nrhs}};
+    StoreStrided sv{S, {pitch, 1, nrhs, nrhs}, 1.0};
+    if ((st = launch_fft_lines(px, ld, sv, q3 * nrhs, nx, nx, false, nrhs == 1, s))) return st;
+  }
+  {
+    LoadStrided ld{S, {plane, 1, pitch, (int)pitch}};
+    StoreStrided sv{S, {plane, 1, pitch, (int)pitch}, 1.0};
+    if ((st = launch_fft_lines(py, ld, sv, 3 * nz * (int)pitch, ny, ny, false, false, s))) return st;
+  }
+  LuGeom g = lu_geom(3 * nz);
+  const double2* F = reinterpret_cast<const double2*>(factors);
+  if (nrhs == 1) {
+    if ((st = launch_solve<1, 1>(g, F, perm, nullptr, 0, nx * ny, nullptr, 1, S, plane, 1, s))) return st;
+  } else {
+    if ((st = launch_solve<MULTI_R, 1>(g, F, perm, nullptr, 0, nx * ny, nullptr, nrhs, S, plane, nrhs, s)))
+      return st;
+  }
+  {
+    LoadStrided ld{S, {plane, 1, pitch, (int)pitch}};
+    StoreStrided sv{S, {plane, 1, pitch, (int)pitch}, 1.0};
+    if ((st = launch_fft_lines(py, ld, sv, 3 * nz * (int)pitch, ny, ny, true, false, s))) return st;
+  }
+  {
+    LoadStrided ld{S, {pitch, 1, nrhs, nrhs}};
+    StoreStrided sv{reinterpret_cast<double2*>(y), {pitch, 1, nrhs, nrhs}, 1.0 / ((double)nx * ny)};
+    if ((st = launch_fft_lines(px, ld, sv, q3 * nrhs, nx, nx, true, nrhs == 1, s))) return st;
+  }
+  return VX_OK;
+}
+
+extern "C" int vx_box_gather(int nx, int ny, int nz, int x0, int y0, int z0, int bx, int by, int bz,
+                             int nrhs, const vx_c128* full, vx_c128* box, void* stream) {
+  const long total = 3L * bx * by * bz * nrhs;
+  if (total == 0) return VX_OK;
+  box_copy_kernel<<<div_up(total, 256) < 4096 ? div_up(total, 256) : 4096, 256, 0, as_stream(stream)>>>(
+      nx, ny, nz, x0, y0, z0, bx, by, bz, nrhs, reinterpret_cast<const double2*>(full),
+      reinterpret_cast<double2*>(box), 1);
+  VX_CHECK_LAUNCH("box_copy_kernel");
+  return VX_OK;
+}
+
+extern "C" int vx_box_scatter(int nx, int ny, int nz, int x0, int y0, int z0, int bx, int by, int bz,
+                              int nrhs, const vx_c128* box, vx_c128* full, void* stream) {
+  const long total = 3L * bx * by * bz * nrhs;
+  if (total == 0) return VX_OK;
+  box_copy_kernel<<<div_up(total, 256) < 4096 ? div_up(total, 256) : 4096, 256, 0, as_stream(stream)>>>(
+      nx, ny, nz, x0, y0, z0, bx, by, bz, nrhs, reinterpret_cast<const double2*>(box),
+      reinterpret_cast<double2*>(full), 0);
+  VX_CHECK_LAUNCH("box_copy_kernel");
+  return VX_OK;
+}

@@ -1,0 +1,166 @@
+// Generic batched line-FFT kernel: W lines per CTA, shared-memory transform,
+// templated loader (zero-pad / Chan / embed hooks) and storer (crop / scale /
+// operator epilogue hooks) so pads, crops and elementwise epilogues never
+// cost an extra HBM round trip.
+#pragma once
+
+#include "fft.cuh"
+
+namespace vx {
+
+// Line l = (o, i) with o = l / n_inner, i = l % n_inner; element e at
+// base + o*os + i*is + e*es.
+struct LineAddr {
+  long os, is, es;
+  int n_inner;
+  __device__ __forceinline__ long base(int l) const {
+    const int o = l / n_inner;
+    return (long)o * os + (long)(l - o * n_inner) * is;
+  }
+};
+
+struct LoadStrided {
+  const double2* __restrict__ p;
+  LineAddr a;
+  __device__ __forceinline__ long line_base(int l) const { return a.base(l); }
+  __device__ __forceinline__ double2 operator()(long b, int e) const { return __ldg(p + b + e * a.es); }
+};
+
+// T. Chan optimal circulant generator from a (2n-1)-long offset line
+// (reference circulant.py:61-73): c_0 = t_0, c_s = ((n-s) t_s + s t_{s-n}) / n.
+struct LoadChan {
+  const double2* __restrict__ p;
+  LineAddr a;
+  int n;
+  __device__ __forceinline__ long line_base(int l) const { return a.base(l); }
+  __device__ __forceinline__ double2 operator()(long b, int s) const {
+    const double2 tp = __ldg(p + b + (long)(n - 1 + s) * a.es);
+    if (s == 0) return tp;
+    const double2 tn = __ldg(p + b + (long)(s - 1) * a.es);
+    const double fn = (double)n, ws = (double)(n - s), wt = (double)s;
+    return cmk((ws * tp.x + wt * tn.x) / fn, (ws * tp.y + wt * tn.y) / fn);
+  }
+};
+
+struct StoreStrided {
+  double2* __restrict__ p;
+  LineAddr a;
+  double scale;
+  __device__ __forceinline__ long line_base(int l) const { return a.base(l); }
+  __device__ __forceinline__ void operator()(long b, int e, double2 v) const {
+    p[b + e * a.es] = cscale(v, scale);
+  }
+};
+
+// Contiguous-line storer with the operator epilogue
+// y = x - m .* (scale*v)   (reference operator.py:101-105), or y = scale*v.
+struct StoreSystem {
+  double2* __restrict__ y;
+  const double2* __restrict__ x;
+  const double2* __restrict__ m;  // may be null -> apply_n
+  long pitch;                     // = nx
+  long nvox;                      // = N (m is broadcast over the 3 components)
+  double scale;
+  __device__ __forceinline__ long line_base(int l) const { return (long)l * pitch; }
+  __device__ __forceinline__ void operator()(long b, int e, double2 v) const {
+    const long i = b + e;
+    v = cscale(v, scale);
+    if (m) {
+      const double2 mv = __ldg(m + (i % nvox));
+      const double2 xv = __ldg(x + i);
+      v = csub(xv, cmul(mv, v));
+    }
+    y[i] = v;
+  }
+};
+
+template <class Loader, class Storer>
+__global__ void fft_lines_kernel(FftPlan p, Loader ld, Storer st, int n_lines, int W, int n_in,
+                                 int n_out, int inv, int contig) {
+  extern __shared__ double2 smem[];
+  long* lbase_in = reinterpret_cast<long*>(smem + (size_t)W * p.L);
+  long* lbase_out = lbase_in + W;
+  const int l0 = blockIdx.x * W;
+  const int L = p.L;
+  SmemLay lay = contig ? SmemLay{1, L} : SmemLay{W, 1};
+  for (int w = threadIdx.x; w < W; w += blockDim.x) {
+    const int l = l0 + w;
+    lbase_in[w] = (l < n_lines) ? ld.line_base(l) : 0;
+    lbase_out[w] = (l < n_lines) ? st.line_base(l) : 0;
+  }
+  __syncthreads();
+  const int total = W * L;
+  for (int i = threadIdx.x; i < total; i += blockDim.x) {
+    int w, e;
+    if (contig) { w = i / L; e = i - w * L; }
+    else        { e = i / W; w = i - e * W; }
+    double2 v = cmk(0.0, 0.0);
+    if (e < n_in && l0 + w < n_lines) v = fft_pre(p, e, ld(lbase_in[w], e), inv);
+    smem[w * lay.ldw + e * lay.lde] = v;
+  }
+  __syncthreads();
+  fft_exec(smem, lay, W, p, inv);
+  const int tot_out = W * n_out;
+  for (int i = threadIdx.x; i < tot_out; i += blockDim.x) {
+    int w, e;
+    if (contig) { w = i / n_out; e = i - w * n_out; }
+    else        { e = i / W;     w = i - e * W; }
+    if (l0 + w < n_lines)
+      st(lbase_out[w], e, fft_post(p, e, smem[w * lay.ldw + fft_out_pos(p, e) * lay.lde], inv));
+  }
+}
+
+// Choose lines-per-CTA and threads for a line FFT of executed length L.
+struct LineLaunch {
+  int W, threads;
+  size_t smem;
+};
+
+inline int pick_line_launch(const FftPlan& p, bool contig, int n_lines, LineLaunch* out) {
+  const int budget = device_smem_optin() - 1024;
+  int W;
+  if (contig) {
+    W = (int)(4096 / p.L);  // ~64 KB of data per CTA
+    if (W < 1) W = 1;
+  } else {
+    W = 16;
+    while (W > 1 && (size_t)W * p.L * sizeof(double2) > 96 * 1024) W /= 2;
+  }
+  if (W > n_lines) W = n_lines > 0 ? n_lines : 1;
+  for (;;) {
+    size_t smem = (size_t)W * p.L * sizeof(double2) + 2 * W * sizeof(long);
+    int thr = fft_threads_for(p, W);
+    if (smem <= (size_t)budget) {
+      out->W = W;
+      out->threads = thr;
+      out->smem = smem;
+      return VX_OK;
+    }
+    if (W == 1) break;
+    W = W / 2;
+  }
+  set_error("FFT length %d (executed %d) does not fit one CTA's shared memory", p.n, p.L);
+  return VX_EINVAL;
+}
+
+template <class Loader, class Storer>
+int launch_fft_lines(const FftPlan& p, const Loader& ld, const Storer& st, int n_lines, int n_in,
+                     int n_out, bool inv, bool contig, cudaStream_t stream) {
+  if (n_lines <= 0) return VX_OK;
+  LineLaunch ll;
+  int s = pick_line_launch(p, contig, n_lines, &ll);
+  if (s) return s;
+  auto kern = fft_lines_kernel<Loader, Storer>;
+  static thread_local int configured = 0;
+  if (ll.smem > 48 * 1024 && configured < (int)ll.smem) {
+    VX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 device_smem_optin()));
+    configured = (int)ll.smem;
+  }
+  kern<<<div_up(n_lines, ll.W), ll.threads, ll.smem, stream>>>(p, ld, st, n_lines, ll.W, n_in,
+                                                                n_out, inv ? 1 : 0, contig ? 1 : 0);
+  VX_CHECK_LAUNCH("fft_lines_kernel");
+  return VX_OK;
+}
+
+}  // namespace vx

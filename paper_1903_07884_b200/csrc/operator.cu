@@ -1,0 +1,205 @@
+// Three-level Toeplitz operator N on the padded grid (reference operator.py).
+//
+// apply = 5 launches over the pruned padded FFT:
+//   K1  x-forward   lines (c,z,y) of x, zero-pad nx -> px            -> A (3,nz,ny,px)
+//   K2  y-forward   strided lines, pad ny -> py, only z < nz          -> B (3,nz,py,px)
+//   K3  z-forward + 9-term spectral multiply (6 unique spectra) + z-inverse,
+//       crop z < nz, 1/(px py pz) folded in                           -> B (in place)
+//   K4  y-inverse   crop y < ny                                       -> A
+//   K5  x-inverse   crop x < nx, epilogue y = x - m .* (N x)          -> y
+// Zero padding and cropping happen in the loaders/storers, so the padded
+// volume is only touched where it carries data.
+#include "fft_lines.cuh"
+
+namespace vx {
+
+// Loader for the plan: line l = (p, iz, iy) of the padded grid, generator
+// embedded in its circulant extension (reference operator.py:21-41).
+struct LoadEmbed {
+  const double2* __restrict__ g;
+  long sp, sz, sy, sx;
+  int nx, ny, nz, px, py, pz;
+  __device__ __forceinline__ static int off(int i, int n, int P) {
+    if (i < n) return i;
+    if (i > P - n) return i - P;
+    return INT32_MIN;
+  }
+  __device__ __forceinline__ long line_base(int l) const {
+    const int p = l / (pz * py);
+    const int r = l - p * pz * py;
+    const int iz = r / py, iy = r - (r / py) * py;
+    const int dz = off(iz, nz, pz), dy = off(iy, ny, py);
+    if (dz == INT32_MIN || dy == INT32_MIN) return -1;
+    return p * sp + (long)(dz + nz - 1) * sz + (long)(dy + ny - 1) * sy;
+  }
+  __device__ __forceinline__ double2 operator()(long b, int e) const {
+    if (b < 0) return cmk(0.0, 0.0);
+    const int dx = off(e, nx, px);
+    if (dx == INT32_MIN) return cmk(0.0, 0.0);
+    return __ldg(g + b + (long)(dx + nx - 1) * sx);
+  }
+};
+
+__constant__ int c_pair_of[9] = {0, 1, 2, 1, 3, 4, 2, 4, 5};
+
+// K3: per column (ky,kx) of the padded spectrum: forward z-DFT of the three
+// components, y_a = sum_b S[PAIR_OF[a,b]] x_b, inverse z-DFT, crop.
+__global__ void op_zmul_kernel(FftPlan pzp, double2* __restrict__ B, const double2* __restrict__ S,
+                               int nz, long cols, int W, double scale) {
+  extern __shared__ double2 smem[];
+  const int Pz = pzp.L;
+  const int W3 = 3 * W;
+  const long col0 = (long)blockIdx.x * W;
+  SmemLay lay{W3, 1};
+  for (int i = threadIdx.x; i < Pz * W3; i += blockDim.x) {
+    const int e = i / W3, lw = i - e * W3;
+    const int c = lw / W, w = lw - c * W;
+    const long col = col0 + w;
+    double2 v = cmk(0.0, 0.0);
+    if (e < nz && col < cols) v = __ldg(B + ((long)c * nz + e) * cols + col);
+    smem[lw + e * W3] = v;
+  }
+  __syncthreads();
+  fft_dif(smem, lay, W3, pzp, -1.0);  // natural -> digit-reversed positions
+  for (int i = threadIdx.x; i < Pz * W; i += blockDim.x) {
+    const int e = i / W, w = i - e * W;  // e = smem position
+    const long col = col0 + w;
+    if (col >= cols) continue;
+    double2* q = smem + e * W3 + w;
+    const double2 x0 = q[0], x1 = q[W], x2 = q[2 * W];
+    const int kz = __ldg(pzp.k_of + e);
+    const long so = (long)kz * cols + col, sstr = (long)Pz * cols;
+    double2 s[6];
+#pragma unroll
+    for (int p = 0; p < 6; ++p) s[p] = ld_stream(S + p * sstr + so);
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      double2 acc = cmul(s[c_pair_of[3 * a + 0]], x0);
+      cfma(acc, s[c_pair_of[3 * a + 1]], x1);
+      cfma(acc, s[c_pair_of[3 * a + 2]], x2);
+      q[a * W] = cscale(acc, scale);
+    }
+  }
+  __syncthreads();
+  fft_dit(smem, lay, W3, pzp, 1.0);  // digit-reversed -> natural
+  for (int i = threadIdx.x; i < nz * W3; i += blockDim.x) {
+    const int e = i / W3, lw = i - e * W3;
+    const int c = lw / W, w = lw - c * W;
+    const long col = col0 + w;
+    if (col < cols) B[((long)c * nz + e) * cols + col] = smem[lw + e * W3];
+  }
+}
+
+static int check_dims(int nx, int ny, int nz, int px, int py, int pz) {
+  VX_REQUIRE(nx >= 1 && ny >= 1 && nz >= 1, "grid dims must be >= 1");
+  VX_REQUIRE(px >= 2 * nx - 1 && py >= 2 * ny - 1 && pz >= 2 * nz - 1,
+             "padded dims (%d,%d,%d) must be >= 2n-1 for grid (%d,%d,%d)", px, py, pz, nx, ny, nz);
+  VX_REQUIRE(fft_is_smooth(px) && fft_is_smooth(py) && fft_is_smooth(pz),
+             "padded dims (%d,%d,%d) must be 13-smooth", px, py, pz);
+  return VX_OK;
+}
+
+}  // namespace vx
+
+using namespace vx;
+
+extern "C" int vx_fft_lines(int n, int n_lines, int n_inner, const vx_c128* in, long in_os,
+                            long in_is, long in_es, int n_in, vx_c128* out, long out_os,
+                            long out_is, long out_es, int n_out, int inverse, double scale,
+                            void* stream) {
+  VX_REQUIRE(n >= 1 && n_lines >= 0 && n_inner >= 1, "bad fft_lines geometry");
+  VX_REQUIRE(n_in >= 0 && n_in <= n && n_out >= 0 && n_out <= n, "n_in/n_out must be in [0, n]");
+  FftPlan p;
+  int st = fft_get_plan(n, &p);
+  if (st) return st;
+  LoadStrided ld{reinterpret_cast<const double2*>(in), {in_os, in_is, in_es, n_inner}};
+  StoreStrided sv{reinterpret_cast<double2*>(out), {out_os, out_is, out_es, n_inner}, scale};
+  const bool contig = (in_es == 1 && out_es == 1);
+  return launch_fft_lines(p, ld, sv, n_lines, n_in, n_out, inverse != 0, contig, as_stream(stream));
+}
+
+extern "C" int vx_op_plan(int nx, int ny, int nz, int px, int py, int pz, const vx_c128* gen,
+                          long g_sp, long g_sz, long g_sy, long g_sx, vx_c128* spectra,
+                          void* stream) {
+  int st = check_dims(nx, ny, nz, px, py, pz);
+  if (st) return st;
+  cudaStream_t s = as_stream(stream);
+  FftPlan fx, fy, fz;
+  if ((st = fft_get_plan(px, &fx)) || (st = fft_get_plan(py, &fy)) || (st = fft_get_plan(pz, &fz)))
+    return st;
+  double2* S = reinterpret_cast<double2*>(spectra);
+  const long cols = (long)py * px;
+  // x pass over every padded (p, z, y) line, generator embedded on load
+  LoadEmbed le{reinterpret_cast<const double2*>(gen), g_sp, g_sz, g_sy, g_sx, nx, ny, nz, px, py, pz};
+  StoreStrided sx{S, {px, 0, 1, 1}, 1.0};
+  if ((st = launch_fft_lines(fx, le, sx, 6 * pz * py, px, px, false, true, s))) return st;
+  // y pass (in place), lines (p,z) x kx
+  LoadStrided ly{S, {cols, 1, px, px}};
+  StoreStrided sy{S, {cols, 1, px, px}, 1.0};
+  if ((st = launch_fft_lines(fy, ly, sy, 6 * pz * px, py, py, false, false, s))) return st;
+  // z pass (in place), lines p x (ky,kx)
+  LoadStrided lz{S, {(long)pz * cols, 1, cols, (int)cols}};
+  StoreStrided sz{S, {(long)pz * cols, 1, cols, (int)cols}, 1.0};
+  return launch_fft_lines(fz, lz, sz, (int)(6 * cols), pz, pz, false, false, s);
+}
+
+extern "C" long vx_op_work_elems(int nx, int ny, int nz, int px, int py, int pz) {
+  (void)pz;
+  return 3L * nz * px * ((long)ny + py);
+}
+
+extern "C" int vx_op_apply(int nx, int ny, int nz, int px, int py, int pz, const vx_c128* spectra,
+                           const vx_c128* m, const vx_c128* x, vx_c128* y, vx_c128* work,
+                           void* stream) {
+  int st = check_dims(nx, ny, nz, px, py, pz);
+  if (st) return st;
+  cudaStream_t s = as_stream(stream);
+  FftPlan fx, fy, fz;
+  if ((st = fft_get_plan(px, &fx)) || (st = fft_get_plan(py, &fy)) || (st = fft_get_plan(pz, &fz)))
+    return st;
+  const double2* X = reinterpret_cast<const double2*>(x);
+  double2* A = reinterpret_cast<double2*>(work);
+  double2* B = A + 3L * nz * ny * px;
+  const long cols = (long)py * px;
+  const int lines_xyz = 3 * nz * ny;
+  // K1
+  {
+    LoadStrided ld{X, {nx, 0, 1, 1}};
+    StoreStrided sv{A, {px, 0, 1, 1}, 1.0};
+    if ((st = launch_fft_lines(fx, ld, sv, lines_xyz, nx, px, false, true, s))) return st;
+  }
+  // K2: lines (c,z) x kx, along y
+  {
+    LoadStrided ld{A, {(long)ny * px, 1, px, px}};
+    StoreStrided sv{B, {cols, 1, px, px}, 1.0};
+    if ((st = launch_fft_lines(fy, ld, sv, 3 * nz * px, ny, py, false, false, s))) return st;
+  }
+  // K3
+  {
+    int W = 32;
+    while (W > 1 && (long)W > cols) W /= 2;
+    const size_t smem = (size_t)3 * W * fz.L * sizeof(double2);
+    int thr = fft_threads_for(fz, 3 * W);
+    if (smem > 48 * 1024)
+      VX_CUDA(cudaFuncSetAttribute(op_zmul_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   device_smem_optin()));
+    const double scale = 1.0 / ((double)px * py * pz);
+    op_zmul_kernel<<<div_up(cols, W), thr, smem, s>>>(fz, B, reinterpret_cast<const double2*>(spectra),
+                                                       nz, cols, W, scale);
+    VX_CHECK_LAUNCH("op_zmul_kernel");
+  }
+  // K4: inverse y, crop to ny
+  {
+    LoadStrided ld{B, {cols, 1, px, px}};
+    StoreStrided sv{A, {(long)ny * px, 1, px, px}, 1.0};
+    if ((st = launch_fft_lines(fy, ld, sv, 3 * nz * px, py, ny, true, false, s))) return st;
+  }
+  // K5: inverse x, crop to nx, operator epilogue
+  {
+    LoadStrided ld{A, {px, 0, 1, 1}};
+    StoreSystem sv{reinterpret_cast<double2*>(y), X, reinterpret_cast<const double2*>(m), nx,
+                   (long)nx * ny * nz, 1.0};
+    if ((st = launch_fft_lines(fx, ld, sv, lines_xyz, px, nx, true, true, s))) return st;
+  }
+  return VX_OK;
+}

@@ -1,0 +1,155 @@
+"""Drop-in ``voxvie.operator`` on the GPU (reference: pkg/src/voxvie/operator.py).
+
+``plan_operator`` uploads the generating tensors once and transforms them on
+the device (C-ABI ``vx_op_plan``); ``apply_n`` / ``apply_system`` run the
+fused padded-FFT convolution (``vx_op_apply``: 5 launches, pad / crop /
+``x - m*(Nx)`` fused into the transforms).
+
+Type behaviour: numpy in -> numpy out (host copies at the boundary); a CUDA
+``torch.Tensor`` in -> CUDA tensor out, no host traffic.  Inputs are never
+modified.  Padding: each axis uses ``2n`` when that length is 13-smooth
+(exactly the reference grid), otherwise the next 13-smooth length >= 2n-1;
+any such padding yields the same linear convolution (``padded_shape`` and
+``storage_bytes`` report what is actually stored).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native as nv
+from .grid import Physics, VoxelGrid
+from .kernel import ToeplitzKernel
+
+
+def padded_length(n: int) -> int:
+    nv.load()
+    two_n = 2 * n
+    return two_n if nv.query("vx_fft_is_smooth", two_n) else nv.query("vx_fft_good_length", two_n - 1)
+
+
+def upload_tensors(kernel: ToeplitzKernel):
+    """Device copy of the generators (cached on the kernel object)."""
+    cache = getattr(kernel, "_vx_device_tensors", None)
+    if cache is not None:
+        return cache
+    t = nv.device_c128(kernel.tensors)
+    try:
+        object.__setattr__(kernel, "_vx_device_tensors", t)
+    except Exception:  # pragma: no cover - exotic kernel objects
+        pass
+    return t
+
+
+@dataclass(frozen=True)
+class OperatorPlan:
+    """Device-resident padded spectra (6, pz, py, px); immutable."""
+
+    grid: VoxelGrid
+    k0: float
+    spectra_device: object = field(repr=False)
+    workers: int = 1
+
+    @property
+    def padded_shape(self):
+        return tuple(int(v) for v in self.spectra_device.shape[1:])
+
+    def storage_bytes(self) -> int:
+        return int(self.spectra_device.numel()) * 16
+
+    @property
+    def spectra(self) -> np.ndarray:
+        """Host copy of the spectra (read-only numpy array, made on demand)."""
+        h = self.spectra_device.cpu().numpy()
+        h.setflags(write=False)
+        return h
+
+
+def plan_operator(kernel: ToeplitzKernel, workers: int = 1) -> OperatorPlan:
+    """reference operator.py:61-70."""
+    nv.require_cuda()
+    nx, ny, nz = kernel.grid.dims
+    px, py, pz = padded_length(nx), padded_length(ny), padded_length(nz)
+    gen = upload_tensors(kernel)
+    spec = nv.empty_c128((6, pz, py, px))
+    s = gen.stride()
+    nv.call("vx_op_plan", nx, ny, nz, px, py, pz, gen.data_ptr(), s[0], s[1], s[2], s[3],
+            spec.data_ptr(), nv.stream_ptr())
+    return OperatorPlan(grid=kernel.grid, k0=float(kernel.k0), spectra_device=spec, workers=workers)
+
+
+def _field_in(plan: OperatorPlan, x):
+    """Validate the flat field size (reference operator.py:73-79) and move to device."""
+    n = plan.grid.n_unknowns
+    if nv.is_tensor(x):
+        if x.numel() != n:
+            raise ValueError(f"field vector has {x.numel()} entries, expected {n}")
+        return nv.device_c128(x.reshape(-1)), True
+    a = np.asarray(x, dtype=np.complex128)
+    if a.size != n:
+        raise ValueError(f"field vector has {a.size} entries, expected {n}")
+    return nv.device_c128(a.reshape(-1)), False
+
+
+def _medium_in(plan: OperatorPlan, m):
+    if m is None:
+        return None
+    if nv.is_tensor(m):
+        if m.numel() != plan.grid.n_voxels:
+            raise ValueError("coefficient map size does not match grid")
+        return nv.device_c128(m.reshape(-1))
+    cached = getattr(plan, "_m_cache", None)
+    if cached is not None and cached[0] is m:
+        return cached[1]
+    a = np.asarray(m, dtype=np.complex128)
+    if a.size != plan.grid.n_voxels:
+        raise ValueError("coefficient map size does not match grid")
+    d = nv.device_c128(a.reshape(-1))
+    object.__setattr__(plan, "_m_cache", (m, d))
+    return d
+
+
+def apply_device(plan: OperatorPlan, m_dev, x_dev, out=None):
+    """y = N x or x - m*(N x) on device tensors (no validation, no host copies)."""
+    nx, ny, nz = plan.grid.dims
+    pz, py, px = plan.padded_shape
+    y = nv.empty_c128(plan.grid.n_unknowns) if out is None else out
+    work = nv.empty_c128(int(nv.query("vx_op_work_elems", nx, ny, nz, px, py, pz)))
+    nv.call("vx_op_apply", nx, ny, nz, px, py, pz, plan.spectra_device.data_ptr(),
+            nv.ptr(m_dev), x_dev.data_ptr(), y.data_ptr(), work.data_ptr(), nv.stream_ptr())
+    return y
+
+
+def apply_n(plan: OperatorPlan, x):
+    """y = N x (reference operator.py:82-98)."""
+    xd, is_dev = _field_in(plan, x)
+    y = apply_device(plan, None, xd)
+    return y if is_dev else y.cpu().numpy()
+
+
+def apply_system(plan: OperatorPlan, m, x):
+    """y = (I - M N) x (reference operator.py:101-105)."""
+    xd, is_dev = _field_in(plan, x)
+    y = apply_device(plan, _medium_in(plan, m), xd)
+    return y if is_dev else y.cpu().numpy()
+
+
+def rhs_from_incident(m, e_inc, physics: Physics) -> np.ndarray:
+    """b = j w eps0 M e_inc (reference operator.py:108-112); once per solve, host side."""
+    m = np.asarray(m, dtype=np.complex128)
+    e = np.asarray(e_inc, dtype=np.complex128).reshape((3,) + m.shape)
+    return (1j * physics.omega * physics.eps0 * m[None] * e).reshape(-1)
+
+
+def field_from_currents(plan: OperatorPlan, w, e_inc, physics: Physics):
+    """e = e_inc + (N w - w)/(j w eps0) (reference operator.py:115-121); N w on the GPU."""
+    if nv.is_tensor(w):
+        wd = nv.device_c128(w.reshape(-1))
+        e = nv.device_c128(e_inc).reshape(-1)
+        return e + (apply_device(plan, None, wd) - wd) / (1j * physics.omega * physics.eps0)
+    w = np.asarray(w, dtype=np.complex128).reshape(-1)
+    e_inc = np.asarray(e_inc, dtype=np.complex128).reshape(-1)
+    nw = apply_n(plan, w)
+    return e_inc + (nw - w) / (1j * physics.omega * physics.eps0)

@@ -1,0 +1,177 @@
+"""GPU parity: FFT engine vs scipy, operator vs the oracle / dense matrix / golden."""
+
+import numpy as np
+import pytest
+import scipy.fft
+
+import voxvie_oracle as O
+from conftest import random_field, relerr
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def torch():
+    import torch
+
+    assert torch.cuda.is_available()
+    return torch
+
+
+def _fft_lines(torch, a, axis, inverse, n_out=None, n=None):
+    """Run vx_fft_lines over one axis of a C-contiguous complex array."""
+    from paper_1903_07884_b200 import _native as nv
+
+    a = np.ascontiguousarray(a, np.complex128)
+    n = a.shape[axis] if n is None else n
+    n_out = n if n_out is None else n_out
+    shp_out = list(a.shape)
+    shp_out[axis] = n_out
+    outer = int(np.prod(a.shape[:axis]))
+    inner = int(np.prod(a.shape[axis + 1:]))
+    x = nv.device_c128(a)
+    y = nv.empty_c128(tuple(shp_out))
+    nin = a.shape[axis]
+    nv.call("vx_fft_lines", n, outer * inner, inner, x.data_ptr(), nin * inner, 1, inner, nin,
+            y.data_ptr(), n_out * inner, 1, inner, n_out, int(inverse),
+            (1.0 / n) if inverse else 1.0, nv.stream_ptr())
+    return y.cpu().numpy()
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 4, 5, 7, 8, 11, 13, 16, 17, 24, 31, 45, 64, 97, 200, 367,
+                               400, 734, 735, 1500, 2500, 5000, 10000])
+def test_fft_contiguous_lengths(torch, rng, n):
+    lines = max(1, min(64, 20000 // n))
+    a = random_field(rng, lines * n).reshape(lines, n)
+    assert relerr(_fft_lines(torch, a, 1, False), scipy.fft.fft(a, axis=1)) < 1e-13
+    assert relerr(_fft_lines(torch, a, 1, True), scipy.fft.ifft(a, axis=1)) < 1e-13
+
+
+@pytest.mark.parametrize("shape,axis", [((3, 10, 7), 1), ((2, 44, 33), 1), ((5, 19, 16), 1),
+                                        ((6, 16, 9), 0), ((4, 800, 3), 1), ((3, 11, 2, 5), 1)])
+def test_fft_strided(torch, rng, shape, axis):
+    a = random_field(rng, int(np.prod(shape))).reshape(shape)
+    assert relerr(_fft_lines(torch, a, axis, False), scipy.fft.fft(a, axis=axis)) < 1e-13
+    assert relerr(_fft_lines(torch, a, axis, True), scipy.fft.ifft(a, axis=axis)) < 1e-13
+
+
+def test_fft_zero_pad_and_crop(torch, rng):
+    a = random_field(rng, 6 * 7).reshape(6, 7)
+    got = _fft_lines(torch, a, 1, False, n=16)
+    assert relerr(got, scipy.fft.fft(a, 16, axis=1)) < 1e-14
+    got = _fft_lines(torch, a, 1, True, n=7, n_out=3)
+    assert relerr(got, scipy.fft.ifft(a, axis=1)[:, :3]) < 1e-14
+
+
+OP_TAGS = ["small", "cube", "one", "odd", "prime", "long"]
+
+
+@pytest.mark.parametrize("tag", OP_TAGS)
+def test_operator_matches_golden(golden_small, tag):
+    from paper_1903_07884_b200.grid import VoxelGrid
+    from paper_1903_07884_b200.kernel import ToeplitzKernel
+    from paper_1903_07884_b200.operator import apply_n, apply_system, plan_operator
+
+    g = golden_small
+    dims = tuple(int(v) for v in g[f"op_{tag}_dims"])
+    kern = ToeplitzKernel(VoxelGrid(*dims, 0.05), 2 * np.pi, g[f"op_{tag}_tensors"])
+    plan = plan_operator(kern)
+    x = g[f"op_{tag}_x"]
+    assert relerr(apply_n(plan, x), g[f"op_{tag}_n"]) < 1e-12
+    assert relerr(apply_system(plan, g[f"op_{tag}_m"], x), g[f"op_{tag}_a"]) < 1e-12
+
+
+def test_operator_columns_vs_dense(golden_small):
+    """test_operator.py:48-59 -- every column of A against the dense oracle."""
+    from paper_1903_07884_b200.grid import VoxelGrid
+    from paper_1903_07884_b200.kernel import ToeplitzKernel
+    from paper_1903_07884_b200.operator import apply_system, plan_operator
+
+    g = golden_small
+    dims = (4, 3, 2)
+    t = g["op_small_tensors"]
+    m = g["op_small_m"]
+    plan = plan_operator(ToeplitzKernel(VoxelGrid(*dims, 0.05), 2 * np.pi, t))
+    a = O.dense_operator(t, dims, m)
+    scale = np.abs(a).max()
+    for col in range(a.shape[0]):
+        e = np.zeros(a.shape[0], complex)
+        e[col] = 1.0
+        assert np.abs(apply_system(plan, m, e) - a[:, col]).max() / scale < 1e-12
+
+
+def test_operator_padded_shape_and_plan(golden_small):
+    from paper_1903_07884_b200.grid import VoxelGrid
+    from paper_1903_07884_b200.kernel import ToeplitzKernel
+    from paper_1903_07884_b200.operator import plan_operator
+
+    g = golden_small
+    kern = ToeplitzKernel(VoxelGrid(4, 3, 2, 0.05), 2 * np.pi, g["op_small_tensors"])
+    p1, p2 = plan_operator(kern), plan_operator(kern)
+    assert p1.padded_shape == (4, 6, 8)
+    assert np.array_equal(p1.spectra, p2.spectra)
+    ref = O.plan_spectra(g["op_small_tensors"], (4, 3, 2))
+    assert relerr(p1.spectra, ref) < 1e-13
+
+
+def test_operator_torch_in_torch_out(torch, rng):
+    from paper_1903_07884_b200 import workloads
+    from paper_1903_07884_b200.operator import apply_system, plan_operator
+
+    W = workloads.small(40, 6, 3)
+    plan = plan_operator(W.kernel())
+    x = random_field(rng, W.grid.n_unknowns)
+    xd = torch.from_numpy(x).cuda()
+    y = apply_system(plan, W.m, xd)
+    assert isinstance(y, torch.Tensor) and y.is_cuda
+    spec = O.plan_spectra(W.kernel().tensors, W.grid.dims)
+    assert relerr(y.cpu().numpy(), O.apply_system(spec, W.grid.dims, W.m, x)) < 1e-12
+    assert np.array_equal(xd.cpu().numpy(), x)  # input untouched
+
+
+@pytest.mark.parametrize("dims", [(200, 10, 5), (367, 40, 8), (64, 22, 11)])
+def test_operator_vs_oracle_waveguides(rng, dims):
+    from paper_1903_07884_b200 import workloads
+    from paper_1903_07884_b200.operator import apply_system, plan_operator
+
+    W = workloads.small(*dims, delta=0.03e-6)
+    plan = plan_operator(W.kernel())
+    x = random_field(rng, W.grid.n_unknowns)
+    spec = O.plan_spectra(W.kernel().tensors, W.grid.dims)
+    assert relerr(apply_system(plan, W.m, x), O.apply_system(spec, W.grid.dims, W.m, x)) < 1e-12
+
+
+def test_operator_linearity_and_shape_error(rng, golden_small):
+    from paper_1903_07884_b200.grid import VoxelGrid
+    from paper_1903_07884_b200.kernel import ToeplitzKernel
+    from paper_1903_07884_b200.operator import apply_n, plan_operator
+
+    g = golden_small
+    plan = plan_operator(ToeplitzKernel(VoxelGrid(4, 3, 2, 0.05), 2 * np.pi, g["op_small_tensors"]))
+    x1, x2 = random_field(rng, 72), random_field(rng, 72)
+    a, b = 1.3 - 0.4j, -0.7 + 2.1j
+    lhs = apply_n(plan, a * x1 + b * x2)
+    rhs = a * apply_n(plan, x1) + b * apply_n(plan, x2)
+    assert np.abs(lhs - rhs).max() / np.abs(lhs).max() < 1e-13
+    assert np.all(apply_n(plan, np.zeros(72, complex)) == 0)
+    with pytest.raises(ValueError):
+        apply_n(plan, np.zeros(7, complex))
+
+
+def test_operator_air_identity_and_concurrency(rng, golden_small):
+    from concurrent.futures import ThreadPoolExecutor
+
+    from paper_1903_07884_b200.grid import VoxelGrid
+    from paper_1903_07884_b200.kernel import ToeplitzKernel
+    from paper_1903_07884_b200.operator import apply_system, plan_operator
+
+    g = golden_small
+    plan = plan_operator(ToeplitzKernel(VoxelGrid(4, 3, 2, 0.05), 2 * np.pi, g["op_small_tensors"]))
+    x = random_field(rng, 72)
+    assert np.array_equal(apply_system(plan, np.zeros((2, 3, 4)), x), x)
+    m = g["op_small_m"]
+    serial = apply_system(plan, m, x)
+    with ThreadPoolExecutor(max_workers=4) as pool:
+        res = list(pool.map(lambda _: apply_system(plan, m, x), range(8)))
+    for r in res:
+        assert np.array_equal(r, serial)
