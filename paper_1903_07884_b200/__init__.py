@@ -22,3 +22,14 @@ __all__ = [
     "apply_n", "apply_system", "assemble_kernel", "homogenize", "medium_coefficient",
     "plan_operator", "__version__",
 ]
+from .circulant import (  # noqa: E402
+    BlockedPrec, Box, OneLevelPrec, Partition, ReducedOneLevelPrec, TwoLevelPrec, build_blocked,
+    build_one_level, build_reduced_one_level, build_two_level, partition_boxes, reduce_one_level,
+)
+from .solver import SolveReport, gmres  # noqa: E402
+
+__all__ += [
+    "BlockedPrec", "Box", "OneLevelPrec", "Partition", "ReducedOneLevelPrec", "SolveReport",
+    "TwoLevelPrec", "build_blocked", "build_one_level", "build_reduced_one_level", "build_two_level",
+    "gmres", "partition_boxes", "reduce_one_level",
+]

@@ -1,0 +1,666 @@
+"""Drop-in ``voxvie.circulant`` on the GPU (reference: pkg/src/voxvie/circulant.py).
+
+Builds and applies the Chan-circulant preconditioners through the C-ABI:
+``vx_chan_x_spectra`` / ``vx_chan_xy_spectra`` (Chan + DFT of the generators),
+``vx_lu1_build`` / ``vx_lu2_build`` (unfold + batched pivoted LU, one CTA per
+frequency block) and ``vx_prec1_apply`` / ``vx_prec2_apply`` (DFT -> streaming
+block solves -> inverse DFT).  Factors live on the device in tiled storage;
+``.lu`` / ``.piv`` are reconstructed host views in LAPACK layout for
+inspection (small problems).
+
+Host-side pieces are the reference's host logic only: argument validation,
+the memory cap, the kept-set selection from the (device-computed) proxies,
+and the geometry partition.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+from scipy.linalg import circulant as _dense_circulant
+
+from . import _native as nv
+from .errors import PartitionError, PreconditionerBuildError
+from .grid import PermittivityMap, VoxelGrid, homogenize
+from .kernel import ToeplitzKernel
+from .operator import upload_tensors
+
+BYTES_PER_ENTRY = 16
+
+
+# ---------------------------------------------------------------------------
+# Chan circulant (host utilities; reference circulant.py:32-73)
+# ---------------------------------------------------------------------------
+
+@dataclass(frozen=True)
+class ChanCirculant:
+    n: int
+    c: np.ndarray
+
+    def to_dense(self) -> np.ndarray:
+        return _dense_circulant(self.c)
+
+
+def chan_circulant(first_col, first_row=None) -> ChanCirculant:
+    """Frobenius-closest circulant of a Toeplitz matrix (reference circulant.py:43-58)."""
+    col = np.asarray(first_col, dtype=np.complex128).reshape(-1)
+    row = col if first_row is None else np.asarray(first_row, np.complex128).reshape(-1)
+    n = col.size
+    if n < 1 or row.size != n:
+        raise ValueError("first column and first row must share a length >= 1")
+    i = np.arange(1, n)
+    c = np.empty(n, np.complex128)
+    c[0] = col[0]
+    c[1:] = ((n - i) * col[1:] + i * row[n - i]) / n
+    return ChanCirculant(n=n, c=c)
+
+
+def chan_along_axis(gen: np.ndarray, axis: int) -> np.ndarray:
+    """Chan formula along one offset axis (reference circulant.py:61-73)."""
+    g = np.moveaxis(np.asarray(gen, np.complex128), axis, -1)
+    n = (g.shape[-1] + 1) // 2
+    s = np.arange(1, n)
+    out = np.empty(g.shape[:-1] + (n,), np.complex128)
+    out[..., 0] = g[..., n - 1]
+    out[..., 1:] = ((n - s) * g[..., n - 1 + s] + s * g[..., s - 1]) / n
+    return np.moveaxis(out, -1, axis)
+
+
+# ---------------------------------------------------------------------------
+# host-side validation (reference circulant.py:81-126)
+# ---------------------------------------------------------------------------
+
+def _constant_along(m: np.ndarray, axis: int, what: str) -> None:
+    lead = np.take(m, [0], axis=axis)
+    if not np.allclose(m, lead, rtol=0.0, atol=1e-12 * max(1.0, np.abs(m).max())):
+        raise ValueError(f"homogenized coefficient must be constant along {what}")
+
+
+def _coerce_mtilde(grid: VoxelGrid, mtilde) -> np.ndarray:
+    m = np.asarray(mtilde, dtype=np.complex128)
+    if m.shape == grid.shape:
+        _constant_along(m, 2, "x")
+        return np.ascontiguousarray(m[:, :, 0])
+    if m.shape == (grid.nz, grid.ny):
+        return np.ascontiguousarray(m)
+    raise ValueError(f"mtilde shape {m.shape} not compatible with grid {grid.shape}")
+
+
+def _proxy_column(ny: int, nz: int) -> int:
+    """Proxy = unfactorised entry (row 1, col ny*nz) 1-based (reference circulant.py:99-110)."""
+    return ny * nz - 1
+
+
+def _check_cap(bytes_needed: int, cap_bytes: int, hint: str):
+    if bytes_needed > cap_bytes:
+        raise PreconditionerBuildError(
+            f"preconditioner needs {bytes_needed} bytes, above the cap {cap_bytes}; {hint}")
+
+
+def _select_kept(proxy: np.ndarray, nx: int, tol: float):
+    """reference circulant.py:283-294."""
+    if not 0.0 <= tol <= 1.0:
+        raise ValueError(f"reduction tolerance must lie in [0, 1], got {tol}")
+    mag = np.abs(proxy)
+    vmax = mag.max()
+    v_hat = mag / vmax if vmax > 0 else np.zeros(proxy.shape)
+    rep = int(np.ceil(nx / 2)) - 1
+    mask = v_hat > tol
+    mask[rep] = True
+    kept = np.flatnonzero(mask)
+    slot_of = np.full(nx, int(np.searchsorted(kept, rep)), dtype=np.int64)
+    slot_of[kept] = np.arange(kept.size)
+    return kept, slot_of, rep, v_hat
+
+
+# ---------------------------------------------------------------------------
+# device helpers
+# ---------------------------------------------------------------------------
+
+def _torch():
+    return nv.require_cuda()
+
+
+def _gen_strides(g):
+    s = g.stride()
+    return s[0], s[1], s[2], s[3]
+
+
+def _lamhat_x(gen, nx, ny, nz):
+    """lamT (nx, 6*(2nz-1)*(2ny-1)) on device (reference circulant.py:129-136)."""
+    lam = nv.empty_c128((nx, 6 * (2 * nz - 1) * (2 * ny - 1)))
+    nv.call("vx_chan_x_spectra", nx, ny, nz, gen.data_ptr(), *_gen_strides(gen), lam.data_ptr(),
+            nv.stream_ptr())
+    return lam
+
+
+def _proxies(lam, nx, ny, nz, m00):
+    proxy = nv.empty_c128(nx)
+    nv.call("vx_proxy", nx, ny, nz, lam.data_ptr(), nv.cval(m00), proxy.data_ptr(), nv.stream_ptr())
+    return proxy
+
+
+def _lu1(lam, m_yz_dev, kset_dev, nslots, nx, ny, nz):
+    t = _torch()
+    n = 3 * ny * nz
+    blk = int(nv.query("vx_lu_block_elems", n))
+    fac = t.empty((nslots, blk), dtype=t.complex128, device="cuda")
+    perm = t.empty((nslots, n), dtype=t.int32, device="cuda")
+    piv = t.empty((nslots, n), dtype=t.int32, device="cuda")
+    info = t.empty((nslots,), dtype=t.int32, device="cuda")
+    nv.call("vx_lu1_build", nx, ny, nz, lam.data_ptr(), m_yz_dev.data_ptr(), nv.ptr(kset_dev), nslots,
+            fac.data_ptr(), perm.data_ptr(), piv.data_ptr(), info.data_ptr(), nv.stream_ptr())
+    return fac, perm, piv, info
+
+
+def _first_bad(info) -> int:
+    bad = (info != 0).nonzero()
+    return -1 if bad.numel() == 0 else int(bad[0, 0])
+
+
+def _untile(fac_row: np.ndarray, n: int) -> np.ndarray:
+    """Tiled factor storage -> LAPACK combined LU (n, n) (host, for inspection)."""
+    from scipy.linalg import solve_triangular
+
+    nv.load()
+    T = int(nv.query("vx_lu_tile", n))
+    nt = -(-n // T)
+    npad = nt * T
+    tiles = fac_row.reshape(nt, nt, T, T)            # (it, jt, col, row)
+    full = tiles.transpose(0, 3, 1, 2).reshape(npad, npad)
+    eye = np.eye(T)
+    for i in range(nt):
+        d = full[i * T:(i + 1) * T, i * T:(i + 1) * T]
+        linv = np.tril(d, -1) + eye
+        uinv = np.triu(d)
+        L = solve_triangular(linv, eye, lower=True, unit_diagonal=True)
+        U = solve_triangular(uinv, eye, lower=False)
+        full[i * T:(i + 1) * T, i * T:(i + 1) * T] = np.tril(L, -1) + np.triu(U)
+    return full[:n, :n]
+
+
+def _as_rhs(x, nunk):
+    """-> (device tensor (nunk, r) contiguous, r, flat_in, was_tensor, orig_shape)."""
+    is_t = nv.is_tensor(x)
+    if is_t:
+        xd = nv.device_c128(x)
+        shape = tuple(x.shape)
+    else:
+        a = np.asarray(x, dtype=np.complex128)
+        shape = a.shape
+        xd = nv.device_c128(a)
+    flat = len(shape) == 1
+    if xd.numel() % nunk != 0 or (not flat and shape[0] != nunk) or (flat and shape[0] != nunk):
+        raise ValueError(f"vector has {xd.numel()} entries, expected {nunk} x r")
+    r = xd.numel() // nunk
+    return xd.reshape(nunk, r).contiguous(), r, flat, is_t, shape
+
+
+def _ret(yd, flat, is_t, shape):
+    out = yd.reshape(shape)
+    return out if is_t else out.cpu().numpy()
+
+
+# ---------------------------------------------------------------------------
+# 1-level (reference circulant.py:144-225)
+# ---------------------------------------------------------------------------
+
+class _OneLevelBase:
+    grid: VoxelGrid
+
+    def _apply_dev(self, xd, r):
+        nx, ny, nz = self.grid.dims
+        y = nv.empty_c128((self.grid.n_unknowns, r))
+        work = nv.empty_c128(int(nv.query("vx_prec1_work_elems", nx, ny, nz, r)))
+        nv.call("vx_prec1_apply", nx, ny, nz, r, self._fac.data_ptr(), self._perm.data_ptr(),
+                self._items.data_ptr(), self._n_single, self._n_items, self._klist.data_ptr(),
+                xd.data_ptr(), y.data_ptr(), work.data_ptr(), nv.stream_ptr())
+        return y
+
+    def apply(self, x):
+        xd, r, flat, is_t, shape = _as_rhs(x, self.grid.n_unknowns)
+        return _ret(self._apply_dev(xd, r), flat, is_t, shape)
+
+    @property
+    def block_size(self) -> int:
+        return 3 * self.grid.ny * self.grid.nz
+
+    @property
+    def storage_bytes(self) -> int:
+        """Bytes actually resident on the device for the factors (padded tiles)."""
+        return int(self._fac.numel()) * 16
+
+    @property
+    def lu(self) -> np.ndarray:
+        f = self._fac.cpu().numpy()
+        return np.stack([_untile(f[s], self.block_size) for s in range(f.shape[0])])
+
+    @property
+    def piv(self) -> np.ndarray:
+        return self._piv.cpu().numpy()
+
+
+def _items_single(slots, ks):
+    t = _torch()
+    items = np.stack([np.asarray(slots), np.arange(len(ks)), np.ones(len(ks), int)], 1).astype(np.int32)
+    return (t.from_numpy(items.reshape(-1).copy()).cuda(),
+            t.from_numpy(np.asarray(ks, np.int32).copy()).cuda())
+
+
+class OneLevelPrec(_OneLevelBase):
+    """Per-x-frequency LU blocks on the device (reference circulant.py:144-171)."""
+
+    level = "one-level"
+
+    def __init__(self, grid, fac, perm, piv, proxy):
+        self.grid = grid
+        self._fac, self._perm, self._piv, self._proxy = fac, perm, piv, proxy
+        nx = grid.nx
+        self._items, self._klist = _items_single(np.arange(nx), np.arange(nx))
+        self._n_single = self._n_items = nx
+
+    @property
+    def proxy(self) -> np.ndarray:
+        return self._proxy.cpu().numpy()
+
+    @property
+    def bytes(self) -> int:
+        return self.grid.nx * self.block_size ** 2 * BYTES_PER_ENTRY
+
+    def summary(self) -> dict:
+        return {"level": self.level, "blocks": int(self.grid.nx),
+                "block_size": int(self.block_size), "bytes": int(self.bytes)}
+
+
+def _build_one_level_dev(grid, gen, m_yz, cap_bytes, tol=None):
+    """Shared device build for full (tol None) and reduced 1-level."""
+    t = _torch()
+    nx, ny, nz = grid.dims
+    q = ny * nz
+    if tol is None:
+        _check_cap(nx * (3 * q) ** 2 * BYTES_PER_ENTRY, cap_bytes, "consider the 2-level preconditioner")
+    lam = _lamhat_x(gen, nx, ny, nz)
+    proxy = _proxies(lam, nx, ny, nz, m_yz[0, 0])
+    m_dev = nv.device_c128(m_yz)
+    if tol is None:
+        fac, perm, piv, info = _lu1(lam, m_dev, None, nx, nx, ny, nz)
+        bad = _first_bad(info)
+        if bad >= 0:
+            raise PreconditionerBuildError(f"1-level build failed: singular frequency block k={bad}")
+        return OneLevelPrec(grid, fac, perm, piv, proxy)
+    ph = proxy.cpu().numpy()
+    kept, slot_of, rep, v_hat = _select_kept(ph, nx, tol)
+    _check_cap(kept.size * (3 * q) ** 2 * BYTES_PER_ENTRY, cap_bytes, "consider the 2-level preconditioner")
+    kset = t.from_numpy(kept.astype(np.int32)).cuda()
+    fac, perm, piv, info = _lu1(lam, m_dev, kset, int(kept.size), nx, ny, nz)
+    bad = _first_bad(info)
+    if bad >= 0:
+        raise PreconditionerBuildError(f"singular frequency block k={int(kept[bad])}")
+    return ReducedOneLevelPrec(grid, kept, slot_of, rep, fac, perm, piv, ph, v_hat, float(tol))
+
+
+def build_one_level(kernel: ToeplitzKernel, mtilde, *, cap_bytes: int = 2 ** 31) -> OneLevelPrec:
+    """reference circulant.py:191-225."""
+    grid = kernel.grid
+    m_yz = _coerce_mtilde(grid, mtilde)
+    nx, ny, nz = grid.dims
+    _check_cap(nx * (3 * ny * nz) ** 2 * BYTES_PER_ENTRY, cap_bytes, "consider the 2-level preconditioner")
+    return _build_one_level_dev(grid, upload_tensors(kernel), m_yz, cap_bytes)
+
+
+# ---------------------------------------------------------------------------
+# reduced 1-level (reference circulant.py:233-354)
+# ---------------------------------------------------------------------------
+
+class ReducedOneLevelPrec(_OneLevelBase):
+    """Kept blocks only; discarded frequencies solved with the representative block."""
+
+    level = "reduced-one-level"
+
+    def __init__(self, grid, kept, slot_of, representative, fac, perm, piv, proxy, v_hat, tol):
+        self.grid = grid
+        self.kept = np.asarray(kept)
+        self.slot_of = np.asarray(slot_of)
+        self.representative = int(representative)
+        self._fac, self._perm, self._piv = fac, perm, piv
+        self.proxy = np.asarray(proxy)
+        self.proxy_normalized = np.asarray(v_hat)
+        self.tol = float(tol)
+        self._make_worklist()
+
+    def _make_worklist(self):
+        t = _torch()
+        rep_slot = int(self.slot_of[self.representative])
+        singles = [(s, int(k)) for s, k in enumerate(self.kept) if s != rep_slot]
+        rep_ks = np.flatnonzero(self.slot_of == rep_slot)
+        items, klist = [], []
+        for s, k in singles:
+            items.append((s, len(klist), 1))
+            klist.append(k)
+        n_single = len(items)
+        for c0 in range(0, rep_ks.size, 8):
+            chunk = rep_ks[c0:c0 + 8]
+            items.append((rep_slot, len(klist), int(chunk.size)))
+            klist.extend(int(k) for k in chunk)
+        self._items = t.from_numpy(np.asarray(items, np.int32).reshape(-1).copy()).cuda()
+        self._klist = t.from_numpy(np.asarray(klist, np.int32)).cuda()
+        self._n_single, self._n_items = n_single, len(items)
+
+    @property
+    def n_kept(self) -> int:
+        return int(self.kept.size)
+
+    @property
+    def bytes(self) -> int:
+        return self.n_kept * self.block_size ** 2 * BYTES_PER_ENTRY
+
+    def summary(self) -> dict:
+        return {"level": self.level, "blocks": int(self.grid.nx), "kept": int(self.n_kept),
+                "discarded": int(self.grid.nx - self.n_kept), "block_size": int(self.block_size),
+                "tol": self.tol, "bytes": int(self.bytes)}
+
+
+def reduce_one_level(prec: OneLevelPrec, tol: float = 1e-3) -> ReducedOneLevelPrec:
+    """Keep only significant-proxy factors of a built 1-level (reference circulant.py:297-311)."""
+    t = _torch()
+    nx = prec.grid.nx
+    proxy = prec.proxy
+    kept, slot_of, rep, v_hat = _select_kept(proxy, nx, tol)
+    idx = t.from_numpy(kept.astype(np.int64)).cuda()
+    return ReducedOneLevelPrec(prec.grid, kept, slot_of, rep, prec._fac.index_select(0, idx),
+                               prec._perm.index_select(0, idx), prec._piv.index_select(0, idx),
+                               proxy.copy(), v_hat, float(tol))
+
+
+def build_reduced_one_level(kernel: ToeplitzKernel, mtilde, tol: float = 1e-3, *,
+                            cap_bytes: int = 2 ** 31) -> ReducedOneLevelPrec:
+    """Proxies first, LU only for kept blocks (reference circulant.py:314-354)."""
+    grid = kernel.grid
+    m_yz = _coerce_mtilde(grid, mtilde)
+    if not 0.0 <= tol <= 1.0:
+        raise ValueError(f"reduction tolerance must lie in [0, 1], got {tol}")
+    return _build_one_level_dev(grid, upload_tensors(kernel), m_yz, cap_bytes, tol=tol)
+
+
+# ---------------------------------------------------------------------------
+# 2-level (reference circulant.py:362-447)
+# ---------------------------------------------------------------------------
+
+class TwoLevelPrec:
+    """(3nz)^2 LU blocks per (x, y) frequency pair, on the device."""
+
+    level = "two-level"
+
+    def __init__(self, grid, fac, perm, piv):
+        self.grid = grid
+        self._fac, self._perm, self._piv = fac, perm, piv
+
+    @property
+    def block_size(self) -> int:
+        return 3 * self.grid.nz
+
+    @property
+    def bytes(self) -> int:
+        return self.grid.nx * self.grid.ny * self.block_size ** 2 * BYTES_PER_ENTRY
+
+    @property
+    def lu(self) -> np.ndarray:
+        f = self._fac.cpu().numpy()
+        n = self.block_size
+        out = np.stack([_untile(f[s], n) for s in range(f.shape[0])])
+        return out.reshape(self.grid.ny, self.grid.nx, n, n)
+
+    @property
+    def piv(self) -> np.ndarray:
+        return self._piv.cpu().numpy().reshape(self.grid.ny, self.grid.nx, -1)
+
+    def _apply_dev(self, xd, r):
+        nx, ny, nz = self.grid.dims
+        y = nv.empty_c128((self.grid.n_unknowns, r))
+        work = nv.empty_c128(int(nv.query("vx_prec2_work_elems", nx, ny, nz, r)))
+        nv.call("vx_prec2_apply", nx, ny, nz, r, self._fac.data_ptr(), self._perm.data_ptr(),
+                xd.data_ptr(), y.data_ptr(), work.data_ptr(), nv.stream_ptr())
+        return y
+
+    def apply(self, x):
+        xd, r, flat, is_t, shape = _as_rhs(x, self.grid.n_unknowns)
+        return _ret(self._apply_dev(xd, r), flat, is_t, shape)
+
+    def summary(self) -> dict:
+        return {"level": self.level, "blocks": int(self.grid.nx * self.grid.ny),
+                "block_size": int(self.block_size), "bytes": int(self.bytes)}
+
+
+def _build_two_level_dev(grid, gen, mtilde, cap_bytes):
+    t = _torch()
+    nx, ny, nz = grid.dims
+    m = np.asarray(mtilde, dtype=np.complex128)
+    if m.shape == grid.shape:
+        _constant_along(m, 2, "x")
+        _constant_along(m, 1, "y")
+        m_z = m[:, 0, 0]
+    elif m.shape == (nz,):
+        m_z = m
+    elif m.ndim == 0:
+        m_z = np.full(nz, m, dtype=np.complex128)
+    else:
+        raise ValueError(f"mtilde shape {m.shape} not usable for a 2-level build")
+    _check_cap(nx * ny * (3 * nz) ** 2 * BYTES_PER_ENTRY, cap_bytes, "reduce the box size or cross-section")
+    work = nv.empty_c128(int(nv.query("vx_chan_xy_work_elems", nx, ny, nz)))
+    lam2 = nv.empty_c128((nx * ny, 6 * (2 * nz - 1)))
+    nv.call("vx_chan_xy_spectra", nx, ny, nz, gen.data_ptr(), *_gen_strides(gen), lam2.data_ptr(),
+            work.data_ptr(), nv.stream_ptr())
+    del work
+    n = 3 * nz
+    nb = nx * ny
+    blk = int(nv.query("vx_lu_block_elems", n))
+    fac = t.empty((nb, blk), dtype=t.complex128, device="cuda")
+    perm = t.empty((nb, n), dtype=t.int32, device="cuda")
+    piv = t.empty((nb, n), dtype=t.int32, device="cuda")
+    info = t.empty((nb,), dtype=t.int32, device="cuda")
+    m_dev = nv.device_c128(np.ascontiguousarray(m_z))
+    nv.call("vx_lu2_build", nx, ny, nz, lam2.data_ptr(), m_dev.data_ptr(), fac.data_ptr(),
+            perm.data_ptr(), piv.data_ptr(), info.data_ptr(), nv.stream_ptr())
+    bad = _first_bad(info)
+    if bad >= 0:
+        l, k = divmod(bad, nx)
+        raise PreconditionerBuildError(f"2-level build failed: singular block (k={k}, l={l})")
+    return TwoLevelPrec(grid, fac, perm, piv)
+
+
+def build_two_level(kernel: ToeplitzKernel, mtilde, *, cap_bytes: int = 2 ** 31) -> TwoLevelPrec:
+    """reference circulant.py:405-447."""
+    return _build_two_level_dev(kernel.grid, upload_tensors(kernel), mtilde, cap_bytes)
+
+
+def apply_one_level(prec, x):
+    return prec.apply(x)
+
+
+def apply_two_level(prec: TwoLevelPrec, x):
+    return prec.apply(x)
+
+
+# ---------------------------------------------------------------------------
+# partition + blocked (reference circulant.py:464-651)
+# ---------------------------------------------------------------------------
+
+@dataclass(frozen=True)
+class Box:
+    """Half-open voxel box [x0,x1) x [y0,y1) x [z0,z1)."""
+
+    label: str
+    x0: int
+    x1: int
+    y0: int
+    y1: int
+    z0: int
+    z1: int
+
+    @property
+    def dims(self):
+        return (self.x1 - self.x0, self.y1 - self.y0, self.z1 - self.z0)
+
+    def n_voxels(self) -> int:
+        bx, by, bz = self.dims
+        return bx * by * bz
+
+    def overlaps(self, other: "Box") -> bool:
+        return all(a0 < b1 and b0 < a1 for a0, a1, b0, b1 in (
+            (self.x0, self.x1, other.x0, other.x1),
+            (self.y0, self.y1, other.y0, other.y1),
+            (self.z0, self.z1, other.z0, other.z1)))
+
+
+@dataclass(frozen=True)
+class Partition:
+    grid: VoxelGrid
+    boxes: tuple
+
+    @property
+    def covered_voxels(self) -> int:
+        return sum(b.n_voxels() for b in self.boxes)
+
+    @property
+    def identity_voxels(self) -> int:
+        return self.grid.n_voxels - self.covered_voxels
+
+
+def partition_boxes(grid: VoxelGrid, boxes) -> Partition:
+    """Validate boxes: inside the grid, pairwise disjoint (reference circulant.py:509-530)."""
+    boxes = tuple(boxes)
+    outside = [b.label for b in boxes if not (0 <= b.x0 < b.x1 <= grid.nx and 0 <= b.y0 < b.y1 <= grid.ny
+                                              and 0 <= b.z0 < b.z1 <= grid.nz)]
+    if outside:
+        raise PartitionError(f"boxes out of grid bounds: {outside}")
+    clash = [(a.label, b.label) for i, a in enumerate(boxes) for b in boxes[i + 1:] if a.overlaps(b)]
+    if clash:
+        raise PartitionError(f"overlapping boxes: {clash}")
+    return Partition(grid=grid, boxes=boxes)
+
+
+_DEFAULT_HOMOG = {"one-level": "real_mean_x", "reduced-one-level": "real_mean_x", "two-level": "mode"}
+
+
+def _sub_grid(grid: VoxelGrid, box: Box) -> VoxelGrid:
+    bx, by, bz = box.dims
+    ox, oy, oz = grid.origin
+    d = grid.delta
+    return VoxelGrid(bx, by, bz, d, origin=(ox + d * box.x0, oy + d * box.y0, oz + d * box.z0))
+
+
+def _slice_kernel(kernel: ToeplitzKernel, box: Box) -> ToeplitzKernel:
+    """Host copy of the box's offset range (reference circulant.py:577-600)."""
+    nz, ny, nx = kernel.grid.shape
+    bx, by, bz = box.dims
+    cz, cy, cx = nz - 1, ny - 1, nx - 1
+    sub = kernel.tensors[:, cz - (bz - 1):cz + bz, cy - (by - 1):cy + by, cx - (bx - 1):cx + bx]
+    return ToeplitzKernel(grid=_sub_grid(kernel.grid, box), k0=kernel.k0, tensors=np.ascontiguousarray(sub))
+
+
+def _slice_device(gen, grid: VoxelGrid, box: Box):
+    """Strided device view of the box's generators (no copy)."""
+    nz, ny, nx = grid.shape
+    bx, by, bz = box.dims
+    cz, cy, cx = nz - 1, ny - 1, nx - 1
+    return gen[:, cz - (bz - 1):cz + bz, cy - (by - 1):cy + by, cx - (bx - 1):cx + bx]
+
+
+def _box_dof_indices(grid: VoxelGrid, box: Box) -> np.ndarray:
+    idx = np.arange(grid.n_unknowns).reshape((3,) + grid.shape)
+    return np.ascontiguousarray(idx[:, box.z0:box.z1, box.y0:box.y1, box.x0:box.x1]).reshape(-1)
+
+
+class BlockedPrec:
+    """Block-diagonal circulant preconditioner over a partition; identity outside."""
+
+    level = "blocked"
+
+    def __init__(self, grid, partition, box_precs):
+        self.grid = grid
+        self.partition = partition
+        self.box_precs = list(box_precs)
+
+    @property
+    def box_dofs(self):
+        return [_box_dof_indices(self.grid, b) for b in self.partition.boxes]
+
+    @property
+    def bytes(self) -> int:
+        return sum(p.bytes for p in self.box_precs)
+
+    def _apply_dev(self, xd, r):
+        nx, ny, nz = self.grid.dims
+        y = nv.empty_c128(tuple(xd.shape))  # identity outside every box
+        nv.call("vx_axpby", xd.numel(), nv.cval(1.0), xd.data_ptr(), nv.cval(0.0), None, y.data_ptr(),
+                nv.stream_ptr())
+        for box, prec in zip(self.partition.boxes, self.box_precs):
+            bx, by, bz = box.dims
+            sub = nv.empty_c128((3 * bx * by * bz, r))
+            nv.call("vx_box_gather", nx, ny, nz, box.x0, box.y0, box.z0, bx, by, bz, r,
+                    xd.data_ptr(), sub.data_ptr(), nv.stream_ptr())
+            ys = prec._apply_dev(sub, r)
+            nv.call("vx_box_scatter", nx, ny, nz, box.x0, box.y0, box.z0, bx, by, bz, r,
+                    ys.data_ptr(), y.data_ptr(), nv.stream_ptr())
+        return y
+
+    def apply(self, x):
+        xd, r, flat, is_t, shape = _as_rhs(x, self.grid.n_unknowns)
+        return _ret(self._apply_dev(xd, r), flat, is_t, shape)
+
+    def summary(self) -> dict:
+        return {"level": self.level,
+                "boxes": [dict(label=b.label, **p.summary())
+                          for b, p in zip(self.partition.boxes, self.box_precs)],
+                "identity_voxels": int(self.partition.identity_voxels),
+                "bytes": int(self.bytes)}
+
+
+def build_blocked(kernel: ToeplitzKernel, pmap: PermittivityMap, partition: Partition, levels: dict,
+                  *, homog: dict | None = None, reduce_tol: float = 1e-3,
+                  cap_bytes: int = 2 ** 31) -> BlockedPrec:
+    """Per-box circulant preconditioners (reference circulant.py:610-651)."""
+    homog = homog or {}
+    gen = upload_tensors(kernel)
+    precs = []
+    for box in partition.boxes:
+        choice = levels[box.label]
+        sgrid = _sub_grid(kernel.grid, box)
+        smap = PermittivityMap(sgrid, pmap.eps_r[box.z0:box.z1, box.y0:box.y1, box.x0:box.x1])
+        mt = homogenize(smap, homog.get(box.label, _DEFAULT_HOMOG.get(choice, "real_mean_x")))
+        sgen = _slice_device(gen, kernel.grid, box)
+        if choice == "one-level":
+            m_yz = _coerce_mtilde(sgrid, mt)
+            bx, by, bz = box.dims
+            _check_cap(bx * (3 * by * bz) ** 2 * BYTES_PER_ENTRY, cap_bytes,
+                       "consider the 2-level preconditioner")
+            p = _build_one_level_dev(sgrid, sgen, m_yz, cap_bytes)
+        elif choice == "reduced-one-level":
+            if not 0.0 <= reduce_tol <= 1.0:
+                raise ValueError(f"reduction tolerance must lie in [0, 1], got {reduce_tol}")
+            p = _build_one_level_dev(sgrid, sgen, _coerce_mtilde(sgrid, mt), cap_bytes, tol=reduce_tol)
+        elif choice == "two-level":
+            p = _build_two_level_dev(sgrid, sgen, mt, cap_bytes)
+        else:
+            raise ValueError(f"unknown per-box level {choice!r} for {box.label!r}")
+        precs.append(p)
+    return BlockedPrec(kernel.grid, partition, precs)
+
+
+# ---------------------------------------------------------------------------
+# test helpers: artificially circulant kernels (reference circulant.py:659-677)
+# ---------------------------------------------------------------------------
+
+def wrap_circulant_x(kernel: ToeplitzKernel) -> ToeplitzKernel:
+    nx = kernel.grid.nx
+    t = np.array(kernel.tensors, copy=True)
+    t[..., :nx - 1] = t[..., nx:2 * nx - 1]
+    return ToeplitzKernel(grid=kernel.grid, k0=kernel.k0, tensors=t)
+
+
+def wrap_circulant_xy(kernel: ToeplitzKernel) -> ToeplitzKernel:
+    ny = kernel.grid.ny
+    t = np.array(wrap_circulant_x(kernel).tensors, copy=True)
+    t[:, :, :ny - 1, :] = t[:, :, ny:2 * ny - 1, :]
+    return ToeplitzKernel(grid=kernel.grid, k0=kernel.k0, tensors=t)

@@ -365,7 +365,7 @@ static int lu_build(const Unfold& u, int n, int nslots, double2* F, int* perm, i
   if ((size_t)LU_WARPS * g.T * g.T * sizeof(double2) < need_perm) smem += need_perm;
   if (smem > 48 * 1024)
     VX_CUDA(cudaFuncSetAttribute(lu_build_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 device_smem_optin()));
+                                 (int)smem));
   VX_REQUIRE((int)smem <= device_smem_optin(), "block size %d too large for the LU kernel", n);
   lu_build_kernel<<<nslots, LU_THREADS, smem, s>>>(u, g, F, perm, piv, info);
   VX_CHECK_LAUNCH("lu_build_kernel");
@@ -513,10 +513,9 @@ static int launch_solve(const LuGeom& g, const double2* F, const int* perm, cons
   const size_t smem = ((size_t)g.npad * R + (size_t)NW * g.T * R + (size_t)g.T * g.T +
                        (size_t)g.T * R) * sizeof(double2);
   auto kern = lu_solve_kernel<R, NW>;
+  VX_REQUIRE((int)smem + 1024 <= device_smem_optin(), "block size %d too large for the solve kernel", g.n);
   if (smem > 48 * 1024)
-    VX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 device_smem_optin()));
-  VX_REQUIRE((int)smem <= device_smem_optin(), "block size %d too large for the solve kernel", g.n);
+    VX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   kern<<<nblocks, NW * 32, smem, s>>>(g, F, perm, items, item0, klist, nrhs, Y, s_row, s_k);
   VX_CHECK_LAUNCH("lu_solve_kernel");
   return VX_OK;

@@ -151,12 +151,8 @@ int launch_fft_lines(const FftPlan& p, const Loader& ld, const Storer& st, int n
   int s = pick_line_launch(p, contig, n_lines, &ll);
   if (s) return s;
   auto kern = fft_lines_kernel<Loader, Storer>;
-  static thread_local int configured = 0;
-  if (ll.smem > 48 * 1024 && configured < (int)ll.smem) {
-    VX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 device_smem_optin()));
-    configured = (int)ll.smem;
-  }
+  if (ll.smem > 48 * 1024)
+    VX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ll.smem));
   kern<<<div_up(n_lines, ll.W), ll.threads, ll.smem, stream>>>(p, ld, st, n_lines, ll.W, n_in,
                                                                 n_out, inv ? 1 : 0, contig ? 1 : 0);
   VX_CHECK_LAUNCH("fft_lines_kernel");

@@ -182,7 +182,7 @@ extern "C" int vx_op_apply(int nx, int ny, int nz, int px, int py, int pz, const
     int thr = fft_threads_for(fz, 3 * W);
     if (smem > 48 * 1024)
       VX_CUDA(cudaFuncSetAttribute(op_zmul_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   device_smem_optin()));
+                                   (int)smem));
     const double scale = 1.0 / ((double)px * py * pz);
     op_zmul_kernel<<<div_up(cols, W), thr, smem, s>>>(fz, B, reinterpret_cast<const double2*>(spectra),
                                                        nz, cols, W, scale);
