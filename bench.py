@@ -1,0 +1,501 @@
+#!/usr/bin/env python
+"""Benchmark: preconditioned-GMRES iterations/s and time-to-solution (complex128).
+
+One *step* = one complete right-preconditioned GMRES solve (x0 = 0, tol 1e-5,
+restart 50 (c0-c3) / 100 (c4), maxit 2000) of a BASELINE workload with the
+operator plan and the preconditioner factors resident in HBM.  ``value`` =
+total Arnoldi iterations / device-timed seconds over the K timed steps.
+
+Default workload: BASELINE config c1 (5000 x 22 x 11 straight Si waveguide,
+3.63 M unknowns, 1-level Chan circulant along x: 5000 LU blocks of 726^2,
+42.17 GB of factors) -- configs[1], the configuration the metric is quoted on.
+``--config`` selects c0/c1/c1r(reduced)/c2/c3/c4.
+
+Extra keys: ``roofline`` for the dominant kernel (the factor-streaming block
+solve, timed live with CUDA events on its launch stream), ``iteration_roofline``
+for the whole iteration (SURVEY section 8(d) B_it), ``cpu_baseline`` (the CPU
+oracle port timed on this host on a bounded sample), ``e2e`` (same metric
+through the public API with host numpy buffers, copies inside the timed
+region), ``clocks`` sampled by nvidia-smi during the timed region.
+
+``--impl reference`` times the CPU reference path (oracle port of the
+reference algorithm, scipy/LAPACK; the Python reference cannot travel to the
+GPU box) on the same config and prints the same JSON line with impl=reference.
+Under torchrun (N > 1) every rank solves its own replica (weak scaling); the
+reference arm runs on rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+sys.path.insert(0, str(ROOT / "oracle"))
+
+METRIC = "precond. GMRES iterations/s and time-to-solution (complex128) vs HBM roofline"
+FALLBACK_HBM = 6650.0
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c1", choices=["c0", "c1", "c1r", "c2", "c3", "c4"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-sample-blocks", type=int, default=24)
+    return ap.parse_args()
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d.get("hbm_gbs", FALLBACK_HBM)), "measured"
+    return FALLBACK_HBM, "fallback"
+
+
+# ------------------------------------------------------------------ clocks
+class Clocks:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index=0):
+        self.idx = device_index
+        self.proc = None
+        self.f = None
+
+    def start(self):
+        try:
+            self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.f.flush()
+        rows = [r.split(",") for r in Path(self.f.name).read_text().strip().splitlines() if r.strip()]
+        os.unlink(self.f.name)
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            r = [c.strip() for c in r]
+            if len(r) < 9:
+                continue
+            try:
+                sm.append(float(r[1]))
+                smax = float(r[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, r[5:9]):
+                if v.lower() in ("active", "1"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------ dist helpers
+def dist_setup(torch):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    elif torch.cuda.is_available():
+        torch.cuda.set_device(0)
+    return world, rank, local
+
+
+def barrier(torch, world):
+    if world > 1:
+        torch.distributed.barrier()
+
+
+def reduce_max(torch, world, v):
+    if world == 1:
+        return v
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    return float(t.item())
+
+
+def reduce_sum(torch, world, v):
+    if world == 1:
+        return v
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.SUM)
+    return float(t.item())
+
+
+# --------------------------------------------------------- byte accounting
+def block_sizes(W):
+    """(list of stored block dims, number of stored blocks) per SURVEY 8(d)."""
+    nx, ny, nz = W.grid.dims
+    k = W.prec["kind"]
+    if k == "one-level":
+        return [(3 * ny * nz, nx)]
+    if k == "two-level":
+        return [(3 * nz, nx * ny)]
+    if k == "blocked":
+        out = []
+        for (x0, x1, y0, y1, z0, z1) in W.prec["boxes"]:
+            out.append((3 * (y1 - y0) * (z1 - z0), x1 - x0))
+        return out
+    raise ValueError(k)
+
+
+def iteration_bytes(W, stored_blocks, restart_eff):
+    """B_it = B_mv + B_pc + B_ar."""
+    N = W.grid.n_voxels
+    vec = 48 * N
+    b_mv = 2 * vec + 16 * N + 6 * 16 * 8 * N
+    b_pc = 2 * vec + 16 * sum(n * n * cnt for n, cnt in stored_blocks)
+    b_ar = vec * (restart_eff + 5)
+    return b_mv + b_pc + b_ar, b_mv, b_pc, b_ar
+
+
+# ------------------------------------------------------------ CPU baseline
+def cpu_iteration_sample(W, kern, m, sample_blocks, mean_j, spectra=None):
+    """Seconds of one preconditioned GMRES iteration of the CPU oracle port on a
+    bounded sample: full matvec, prec apply with `sample_blocks` LU solves scaled
+    to all blocks, MGS over mean_j basis vectors.  Returns (sec, cores, desc)."""
+    import scipy.fft
+    from scipy.linalg import lu_factor, lu_solve
+
+    import voxvie_oracle as O
+
+    cores = len(os.sched_getaffinity(0))
+    os.environ.setdefault("OMP_NUM_THREADS", str(cores))
+    dims = W.grid.dims
+    nx, ny, nz = dims
+    rng = np.random.default_rng(20240811)
+    n = W.grid.n_unknowns
+    x = rng.normal(size=n) + 1j * rng.normal(size=n)
+    if spectra is None:
+        spectra = O.plan_spectra(kern.tensors, dims, workers=cores)
+    t0 = time.perf_counter()
+    O.apply_system(spectra, dims, m, x, workers=cores)
+    t_mv = time.perf_counter() - t0
+    kind = W.prec["kind"]
+    if kind in ("one-level", "reduced-one-level", "blocked"):
+        if kind == "blocked":
+            boxes = W.prec["boxes"]
+        else:
+            boxes = [(0, nx, 0, ny, 0, nz)]
+        t_pc = 0.0
+        for box in boxes:
+            sub, sdims = O.slice_kernel(kern.tensors, dims, box)
+            mt = W.mtilde(None if kind != "blocked" else box)
+            m_yz = O.coerce_mtilde(sdims, mt)
+            bx, by, bz = sdims
+            lam = O.chan_x_spectra(sub)
+            ks = np.linspace(0, bx - 1, min(sample_blocks, bx)).astype(int)
+            facs = [lu_factor(O.unfold_block_yz(lam[:, :, :, k], m_yz), check_finite=False) for k in ks]
+            xf = rng.normal(size=(3, bz, by, bx)) + 0j
+            t0 = time.perf_counter()
+            spec = scipy.fft.fft(xf, axis=3)
+            out = scipy.fft.ifft(spec, axis=3)
+            t_fft = time.perf_counter() - t0
+            t0 = time.perf_counter()
+            for k, f in zip(ks, facs):
+                rhs = np.ascontiguousarray(spec[:, :, :, k]).reshape(-1, 1)
+                lu_solve(f, rhs, check_finite=False)
+            t_lu = (time.perf_counter() - t0) * bx / len(ks)
+            t_pc += t_fft + t_lu
+            del out
+        desc = (f"oracle port (scipy.fft + LAPACK zgetrs as the reference) on {W.name}: full matvec "
+                f"(fftn workers={cores}), x-DFT of the full field, {min(sample_blocks, nx)} of the "
+                f"per-frequency lu_solve calls timed and scaled to all blocks, MGS over {mean_j} vectors")
+    else:
+        lam2 = scipy.fft.fftn(O.chan_along_axis(O.chan_along_axis(kern.tensors, 3), 2), axes=(2, 3))
+        m_z = W.mtilde()[:, 0, 0]
+        xf = rng.normal(size=(3, nz, ny, nx)) + 0j
+        t0 = time.perf_counter()
+        spec = scipy.fft.fftn(xf, axes=(2, 3))
+        scipy.fft.ifftn(spec, axes=(2, 3))
+        t_fft = time.perf_counter() - t0
+        S = min(sample_blocks * 40, nx * ny)
+        idx = np.linspace(0, nx * ny - 1, S).astype(int)
+        facs = [lu_factor(O.unfold_block_z(lam2[:, :, i // nx, i % nx], m_z), check_finite=False) for i in idx]
+        t0 = time.perf_counter()
+        for i, f in zip(idx, facs):
+            lu_solve(f, np.ascontiguousarray(spec[:, :, i // nx, i % nx]).reshape(-1, 1), check_finite=False)
+        t_pc = t_fft + (time.perf_counter() - t0) * nx * ny / S
+        desc = (f"oracle port on {W.name}: full matvec, 2-D DFT, {S} of {nx * ny} (l,k) lu_solve calls "
+                f"scaled, MGS over {mean_j} vectors")
+    V = [rng.normal(size=n) + 1j * rng.normal(size=n) for _ in range(max(1, mean_j))]
+    w = x.copy()
+    t0 = time.perf_counter()
+    for v in V:
+        h = np.vdot(v, w)
+        w -= h * v
+    np.linalg.norm(w)
+    t_ar = time.perf_counter() - t0
+    return t_mv + t_pc + t_ar, cores, desc, dict(matvec_s=t_mv, prec_s=t_pc, arnoldi_s=t_ar)
+
+
+# -------------------------------------------------------------- our arm
+def build_prec(W, kern):
+    from paper_1903_07884_b200 import circulant as C
+
+    kind = W.prec["kind"]
+    big = 2 ** 62
+    if kind == "one-level":
+        return C.build_one_level(kern, W.mtilde(), cap_bytes=big)
+    if kind == "reduced-one-level":
+        return C.build_reduced_one_level(kern, W.mtilde(), W.prec.get("tol", 1e-3), cap_bytes=big)
+    if kind == "two-level":
+        return C.build_two_level(kern, W.mtilde(), cap_bytes=big)
+    if kind == "blocked":
+        boxes = [C.Box(lbl, *b) for lbl, b in zip(W.prec["labels"], W.prec["boxes"])]
+        part = C.partition_boxes(W.grid, boxes)
+        levels = dict(zip(W.prec["labels"], W.prec["levels"]))
+        return C.build_blocked(kern, W.pmap, part, levels,
+                               homog={lbl: W.prec["homogenization"] for lbl in W.prec["labels"]},
+                               cap_bytes=big)
+    raise ValueError(kind)
+
+
+def stored_blocks_of(W, prec):
+    kind = W.prec["kind"]
+    if kind == "reduced-one-level":
+        return [(prec.block_size, prec.n_kept)]
+    if kind == "blocked":
+        return [(p.block_size, p.grid.nx) for p in prec.box_precs]
+    return block_sizes(W)
+
+
+def run_ours(args):
+    import torch
+
+    from paper_1903_07884_b200 import _native as nv
+    from paper_1903_07884_b200 import workloads
+    from paper_1903_07884_b200.operator import apply_system, plan_operator
+    from paper_1903_07884_b200.solver import gmres
+
+    world, rank, local = dist_setup(torch)
+    name = args.config
+    W = workloads.make(name)
+    kern = W.kernel()
+    m_host = W.m
+    b_host = W.b
+    torch.cuda.synchronize()
+
+    # ---- setup (time-to-solution part 1): plan + preconditioner build
+    t0 = time.perf_counter()
+    plan = plan_operator(kern)
+    torch.cuda.synchronize()
+    plan_s = time.perf_counter() - t0
+    ev_a, ev_b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev_a.record()
+    prec = build_prec(W, kern)
+    ev_b.record()
+    torch.cuda.synchronize()
+    build_s = ev_a.elapsed_time(ev_b) / 1e3
+
+    m_dev = torch.from_numpy(np.ascontiguousarray(m_host).reshape(-1)).cuda()
+    b_dev = torch.from_numpy(b_host.copy()).cuda()
+    A = lambda v: apply_system(plan, m_dev, v)  # noqa: E731
+
+    def solve(b):
+        return gmres(A, b, apply_pinv=prec.apply, tol=W.tol, maxit=W.maxit, restart=W.restart)
+
+    for _ in range(args.warmup):
+        _, rep = solve(b_dev)
+    torch.cuda.synchronize()
+
+    # ---- timed region (device resident)
+    clocks = Clocks(local)
+    barrier(torch, world)
+    torch.cuda.synchronize()
+    nv.timing_enable(True)
+    for sp in ("prec_solve", "op_apply", "prec_apply", "arnoldi_step"):
+        nv.timing_read(sp)
+    clocks.start()
+    l0 = nv.launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    its = 0
+    reports = []
+    for _ in range(args.steps):
+        x, rep = solve(b_dev)
+        its += rep.iterations
+        reports.append(rep)
+    e1.record()
+    torch.cuda.synchronize()
+    launches = nv.launch_count() - l0
+    clk = clocks.stop()
+    barrier(torch, world)
+    t_local = e0.elapsed_time(e1) / 1e3
+    spans = {sp: nv.timing_read(sp) for sp in ("prec_solve", "op_apply", "prec_apply", "arnoldi_step")}
+    nv.timing_enable(False)
+    t_max = reduce_max(torch, world, t_local)
+    its_all = reduce_sum(torch, world, its)
+    value = its_all / t_max
+    ms_per_step = t_max / args.steps * 1e3
+    solve_s = t_local / args.steps
+
+    # ---- roofline of the dominant kernel (factor-streaming block solve)
+    peak, peak_kind = peaks()
+    stored = stored_blocks_of(W, prec)
+    nvec = W.grid.n_unknowns
+    sol_ms, sol_n = spans["prec_solve"]
+    solve_bytes = 16 * sum(n * n * c for n, c in stored) + 2 * 16 * nvec
+    roof = None
+    if sol_n:
+        avg = sol_ms / sol_n / 1e3
+        ach = solve_bytes / avg / 1e9
+        roof = {"kernel": "lu_solve_kernel<1,8> (prec_solve span)", "bound": "hbm", "achieved": ach,
+                "peak": peak, "unit": "GB/s", "frac": ach / peak, "peak_source": peak_kind,
+                "traffic": None, "bytes_per_launch": solve_bytes, "avg_launch_ms": avg * 1e3,
+                "launches": sol_n}
+    its_per_solve = its / args.steps
+    restart_eff = min(W.restart, its_per_solve)
+    b_it, b_mv, b_pc, b_ar = iteration_bytes(W, stored, restart_eff)
+    b_pc = 2 * 48 * W.grid.n_voxels + 16 * sum(n * n * c for n, c in stored)
+    b_it = b_mv + b_pc + b_ar
+    it_roof = {"bytes_per_iteration": b_it, "B_mv": b_mv, "B_pc": b_pc, "B_ar": b_ar,
+               "achieved": b_it * its / t_local / 1e9, "peak": peak, "unit": "GB/s",
+               "frac": b_it * its / t_local / 1e9 / peak}
+    breakdown = {sp: {"ms_total": v[0], "launches": v[1]} for sp, v in spans.items()}
+
+    # ---- e2e through the public API with host numpy buffers
+    e2e = None
+    if not args.no_e2e:
+        torch.cuda.synchronize()
+        barrier(torch, world)
+        t0 = time.perf_counter()
+        its_e = 0
+        for _ in range(args.steps):
+            m_step = np.array(m_host, copy=True)           # forces the H2D copy of m
+            x_h, rep = gmres(lambda v: apply_system(plan, m_step, v), b_host.copy(),
+                             apply_pinv=prec.apply, tol=W.tol, maxit=W.maxit, restart=W.restart)
+            its_e += rep.iterations
+        torch.cuda.synchronize()
+        te = reduce_max(torch, world, time.perf_counter() - t0)
+        its_e_all = reduce_sum(torch, world, its_e)
+        e2e = {"value": its_e_all / te, "unit": "it/s", "h2d_bytes_per_step": int(b_host.nbytes + m_host.nbytes),
+               "d2h_bytes_per_step": int(b_host.nbytes), "ms_per_step": te / args.steps * 1e3,
+               "tts_s": build_s + te / args.steps,
+               "note": "numpy b and m in, numpy x out; plan+factors resident (setup)"}
+
+    # ---- CPU baseline (rank 0, N=1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        mean_j = int(max(1, min(W.restart, its_per_solve) // 2))
+        sec, cores, desc, parts = cpu_iteration_sample(W, kern, m_host, args.cpu_sample_blocks, mean_j,
+                                                       spectra=plan.spectra if plan.padded_shape == tuple(
+                                                           2 * d for d in W.grid.shape) else None)
+        cpu = {"value": 1.0 / sec, "unit": "it/s", "cores": cores, "kind": "port", "sample": desc,
+               "seconds_per_iteration": sec, **parts,
+               "tts_s_estimate": None}
+
+    line = {
+        "metric": METRIC,
+        "value": value,
+        "unit": "it/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms_per_step,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "c128",
+        "data": "synthetic (BASELINE workload, interpretation B, deterministic)",
+        "config": {"workload": f"{name}: {W.grid.nx}x{W.grid.ny}x{W.grid.nz} {W.prec['kind']}",
+                   "unknowns": W.grid.n_unknowns, "restart": W.restart, "tol": W.tol,
+                   "step": "one full preconditioned GMRES solve (x0=0)",
+                   "l2": "inputs larger than L2 (factors %.2f GB >> 126 MB)" % (
+                       16 * sum(n * n * c for n, c in stored) / 1e9),
+                   "parallelism": "replicas" if world > 1 else "single-gpu"},
+        "iterations_per_solve": its_per_solve,
+        "build_s": build_s,
+        "plan_s": plan_s,
+        "solve_s": solve_s,
+        "tts_s": build_s + solve_s,
+        "true_residual": reports[-1].true_residual,
+        "roofline": roof,
+        "iteration_roofline": it_roof,
+        "breakdown": breakdown,
+        "e2e": e2e,
+        "gpu_launches": launches,
+        "clocks": clk,
+        "cpu_baseline": cpu,
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+# --------------------------------------------------------- reference arm
+def run_reference(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from paper_1903_07884_b200 import workloads
+
+    import voxvie_oracle as O
+
+    W = workloads.make(args.config)
+    kern = W.kernel()
+    m = W.m
+    cores = len(os.sched_getaffinity(0))
+    spectra = O.plan_spectra(kern.tensors, W.grid.dims, workers=cores)
+    mean_j = 10
+    for _ in range(args.warmup):
+        cpu_iteration_sample(W, kern, m, 4, 2, spectra=spectra)
+    tot = 0.0
+    desc = ""
+    for _ in range(args.steps):
+        sec, cores, desc, _ = cpu_iteration_sample(W, kern, m, args.cpu_sample_blocks, mean_j, spectra=spectra)
+        tot += sec
+    value = args.steps / tot
+    line = {
+        "metric": METRIC, "impl": "reference", "value": value, "unit": "it/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128",
+        "data": "synthetic (BASELINE workload, interpretation B, deterministic)",
+        "config": {"workload": f"{args.config}: {W.grid.nx}x{W.grid.ny}x{W.grid.nz} {W.prec['kind']}",
+                   "unknowns": W.grid.n_unknowns, "restart": W.restart, "tol": W.tol,
+                   "step": "one preconditioned GMRES iteration of the CPU path (bounded sample)"},
+        "cpu_baseline": {"value": value, "unit": "it/s", "cores": cores, "kind": "port", "sample": desc},
+        "e2e": {"value": value, "unit": "it/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_ours(a)

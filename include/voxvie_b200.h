@@ -144,6 +144,16 @@ int vx_axpby(long n, vx_c128 a, const vx_c128* x, vx_c128 b, const vx_c128* y, v
              void* stream);
 int vx_norm2(long n, const vx_c128* x, double* out, vx_c128* part, void* stream);
 
+/* -------------------------------------------------------------- runtime */
+/* Number of kernels this library has launched since it was loaded. */
+long vx_launch_count(void);
+/* Named CUDA-event spans recorded on the launching stream while enabled:
+ * "op_apply", "prec_apply", "prec_solve" (the factor-streaming solve kernel),
+ * "arnoldi_step", "lu_build".  vx_timing_read synchronises on the recorded
+ * events, returns their summed duration and count, and clears them. */
+int vx_timing_enable(int on);
+int vx_timing_read(const char* span, double* total_ms, long* count);
+
 #ifdef __cplusplus
 }
 #endif

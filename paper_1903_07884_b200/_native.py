@@ -68,6 +68,9 @@ _SIGS = {
     "vx_basis_combine": (c_int, [c_long, c_int, P, c_long, P, P, P]),
     "vx_axpby": (c_int, [c_long, c128, P, c128, P, P, P]),
     "vx_norm2": (c_int, [c_long, P, P, P, P]),
+    "vx_launch_count": (c_long, []),
+    "vx_timing_enable": (c_int, [c_int]),
+    "vx_timing_read": (c_int, [C.c_char_p, C.POINTER(C.c_double), C.POINTER(C.c_long)]),
 }
 
 
@@ -177,3 +180,18 @@ def is_tensor(a) -> bool:
     except ImportError:  # pragma: no cover
         return False
     return isinstance(a, _t.Tensor)
+
+
+def timing_enable(on: bool):
+    query("vx_timing_enable", 1 if on else 0)
+
+
+def timing_read(span: str):
+    """(total_ms, count) of the named event span since the last read."""
+    ms, cnt = C.c_double(0.0), C.c_long(0)
+    call("vx_timing_read", span.encode(), C.byref(ms), C.byref(cnt))
+    return ms.value, cnt.value
+
+
+def launch_count() -> int:
+    return int(query("vx_launch_count"))

@@ -262,6 +262,7 @@ extern "C" int vx_arnoldi_step(long n, int nvec, const vx_c128* V, long ldv, vx_
                                void* stream) {
   VX_REQUIRE(n >= 1 && nvec >= 0 && ldv >= n, "bad Arnoldi arguments");
   cudaStream_t s = as_stream(stream);
+  Span span("arnoldi_step", s);
   const int G = ar_grid(n);
   const double2* Vd = reinterpret_cast<const double2*>(V);
   double2* wd = reinterpret_cast<double2*>(w);
@@ -279,6 +280,8 @@ extern "C" int vx_arnoldi_step(long n, int nvec, const vx_c128* V, long ldv, vx_
   finalize_kernel<<<1, AR_THREADS, 0, s>>>(nvec, G, pd, hd, cd, stats, 3);
   if (vnext)
     scale_kernel<<<stream_grid(n), 256, 0, s>>>(n, wd, reinterpret_cast<double2*>(vnext), hd + nvec);
+  if (vnext) count_launch();
+  count_launch(7);
   VX_CHECK_LAUNCH("arnoldi_step");
   return VX_OK;
 }
@@ -310,6 +313,7 @@ extern "C" int vx_norm2(long n, const vx_c128* x, double* out, vx_c128* part, vo
   norm_part_kernel<<<G, AR_THREADS, 0, s>>>(n, reinterpret_cast<const double2*>(x),
                                             reinterpret_cast<double2*>(part));
   norm_final_kernel<<<1, AR_THREADS, 0, s>>>(G, reinterpret_cast<const double2*>(part), out);
+  count_launch();
   VX_CHECK_LAUNCH("norm2");
   return VX_OK;
 }

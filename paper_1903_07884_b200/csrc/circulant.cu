@@ -358,6 +358,7 @@ static size_t lu_smem(const LuGeom& g) {
 static int lu_build(const Unfold& u, int n, int nslots, double2* F, int* perm, int* piv, int* info,
                     cudaStream_t s) {
   if (nslots <= 0) return VX_OK;
+  Span span("lu_build", s);
   LuGeom g = lu_geom(n);
   size_t smem = lu_smem(g);
   // the permutation scratch reuses the staging tiles: make sure they fit npad ints
@@ -593,6 +594,7 @@ extern "C" int vx_prec1_apply(int nx, int ny, int nz, int nrhs, const vx_c128* f
   VX_REQUIRE(nx >= 1 && ny >= 1 && nz >= 1 && nrhs >= 1, "bad 1-level apply arguments");
   VX_REQUIRE(n_single >= 0 && n_items >= n_single, "bad work list");
   cudaStream_t s = as_stream(stream);
+  Span span("prec_apply", s);
   FftPlan p;
   int st = fft_get_plan(nx, &p);
   if (st) return st;
@@ -607,6 +609,7 @@ extern "C" int vx_prec1_apply(int nx, int ny, int nz, int nrhs, const vx_c128* f
   LuGeom g = lu_geom(q3);
   const double2* F = reinterpret_cast<const double2*>(factors);
   if (nrhs == 1) {
+    Span span("prec_solve", s);
     if ((st = launch_solve<1, SOLVE_WARPS>(g, F, perm, items, 0, n_single, klist, 1, S, pitch, nrhs, s)))
       return st;
   } else {
@@ -671,6 +674,7 @@ extern "C" int vx_prec2_apply(int nx, int ny, int nz, int nrhs, const vx_c128* f
                               void* stream) {
   VX_REQUIRE(nx >= 1 && ny >= 1 && nz >= 1 && nrhs >= 1, "bad 2-level apply arguments");
   cudaStream_t s = as_stream(stream);
+  Span span("prec_apply", s);
   FftPlan px, py;
   int st;
   if ((st = fft_get_plan(nx, &px)) || (st = fft_get_plan(ny, &py))) return st;
@@ -691,6 +695,7 @@ extern "C" int vx_prec2_apply(int nx, int ny, int nz, int nrhs, const vx_c128* f
   LuGeom g = lu_geom(3 * nz);
   const double2* F = reinterpret_cast<const double2*>(factors);
   if (nrhs == 1) {
+    Span span2("prec_solve", s);
     if ((st = launch_solve<1, 1>(g, F, perm, nullptr, 0, nx * ny, nullptr, 1, S, plane, 1, s))) return st;
   } else {
     if ((st = launch_solve<MULTI_R, 1>(g, F, perm, nullptr, 0, nx * ny, nullptr, nrhs, S, plane, nrhs, s)))

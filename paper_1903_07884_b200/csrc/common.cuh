@@ -20,6 +20,7 @@ int cuda_status(cudaError_t e, const char* where);
 
 #define VX_CHECK_LAUNCH(where)                                      \
   do {                                                              \
+    ::vx::count_launch();                                           \
     cudaError_t _e = cudaGetLastError();                            \
     if (_e != cudaSuccess) return ::vx::cuda_status(_e, where);     \
   } while (0)
@@ -101,5 +102,16 @@ inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s
 
 int device_smem_optin();   // max dynamic shared memory per block (bytes)
 int device_sm_count();
+
+// runtime.cu: launch accounting and optional event spans (vx_timing_enable)
+void count_launch(int n = 1);
+struct Span {
+  const char* nm;
+  cudaStream_t st;
+  cudaEvent_t a;
+  bool on;
+  Span(const char* name, cudaStream_t s);
+  ~Span();
+};
 
 }  // namespace vx

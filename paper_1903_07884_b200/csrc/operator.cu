@@ -154,6 +154,7 @@ extern "C" int vx_op_apply(int nx, int ny, int nz, int px, int py, int pz, const
   int st = check_dims(nx, ny, nz, px, py, pz);
   if (st) return st;
   cudaStream_t s = as_stream(stream);
+  Span span("op_apply", s);
   FftPlan fx, fy, fz;
   if ((st = fft_get_plan(px, &fx)) || (st = fft_get_plan(py, &fy)) || (st = fft_get_plan(pz, &fz)))
     return st;
