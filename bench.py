@@ -57,6 +57,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-sample-blocks", type=int, default=24)
+    ap.add_argument("--solve-classic", action="store_true",
+                    help="use the non-pipelined block-solve kernel (A/B measurement)")
     return ap.parse_args()
 
 
@@ -300,6 +302,8 @@ def run_ours(args):
     from paper_1903_07884_b200.solver import gmres
 
     world, rank, local = dist_setup(torch)
+    nv.load()
+    nv.query("vx_solve_variant", 1 if args.solve_classic else 0)
     name = args.config
     W = workloads.make(name)
     kern = W.kernel()

@@ -103,6 +103,10 @@ int vx_prec1_apply(int nx, int ny, int nz, int nrhs, const vx_c128* factors, con
                    const int* items, int n_single, int n_items, const int* klist,
                    const vx_c128* x, vx_c128* y, vx_c128* work, void* stream);
 
+/* Select the block-solve kernel: 0 (default) = TMA-bulk pipelined producer/
+ * consumer kernel, 1 = the classic synchronous kernel (kept for A/B timing). */
+int vx_solve_variant(int classic);
+
 /* --------------------------------------------------- 2-level preconditioner */
 /* circulant.py:434-435: lam2T (ny*nx, 6, 2nz-1) = fftn_{y,x}(chan_y(chan_x(gen))). */
 long vx_chan_xy_work_elems(int nx, int ny, int nz);

@@ -524,6 +524,234 @@ static int launch_solve(const LuGeom& g, const double2* F, const int* perm, cons
 
 constexpr int SOLVE_WARPS = 8;
 constexpr int MULTI_R = 8;
+static int g_solve_classic = 0;  // vx_solve_variant(1): non-pipelined kernel (A/B measurement)
+
+// --------------------------------------------------- pipelined (TMA bulk) solve
+// One producer warp streams the block's factor tiles, in exactly the order the
+// substitution consumes them, into a ring of S shared-memory slots with
+// cp.async.bulk (TMA bulk copies completing on mbarriers); NWC consumer warps
+// do the tile GEMVs.  Loads never wait on the substitution's dependencies, so
+// up to S tiles per CTA are always in flight.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "W%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra W%=;\n}\n" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void consumers_sync(int nthreads) {
+  asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
+}
+
+constexpr int PIPE_CONSUMERS = 8;
+
+template <int R>
+__global__ void __launch_bounds__((PIPE_CONSUMERS + 1) * 32)
+    lu_solve_pipe_kernel(LuGeom g, const double2* __restrict__ F, const int* __restrict__ perm,
+                         const int* __restrict__ items, int item0, const int* __restrict__ klist,
+                         int nrhs, double2* Y, long s_row, long s_k, int S) {
+  extern __shared__ __align__(128) unsigned char smraw[];
+  constexpr int NWC = PIPE_CONSUMERS;
+  constexpr int NC = NWC * 32;
+  const int T = g.T, T2 = T * T, nt = g.nt, npad = g.npad, n = g.n;
+  const uint32_t tile_bytes = (uint32_t)T2 * sizeof(double2);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smraw);
+  uint64_t* empty = full + S;
+  long* rbase = reinterpret_cast<long*>(empty + S);
+  double2* slots = reinterpret_cast<double2*>(smraw + ((2 * S + R) * 8 + 127) / 128 * 128);
+  double2* y = slots + (long)S * T2;       // [npad][R]
+  double2* red = y + (long)npad * R;       // [NWC][T][R]
+  double2* zb = red + NWC * T * R;         // [T][R]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+
+  int slot, beg, cnt;
+  if (items) {
+    const int it = item0 + blockIdx.x;
+    slot = items[3 * it];
+    beg = items[3 * it + 1];
+    cnt = items[3 * it + 2];
+  } else {
+    slot = item0 + blockIdx.x;
+    beg = slot;
+    cnt = 1;
+  }
+  const double2* Fb = F + (long)slot * g.blk;
+  const int total = cnt * nrhs;
+  const int nchunks = (total + R - 1) / R;
+
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(full + s, 1);
+      mbar_init(empty + s, 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp == NWC) {
+    // ---------------- producer: same tile order as the consumers, all chunks
+    if (lane == 0) {
+      long t = 0;
+      for (int ch = 0; ch < nchunks; ++ch) {
+        for (int ph = 0; ph < 2; ++ph) {
+          for (int ii = 0; ii < nt; ++ii) {
+            const int i = ph == 0 ? ii : nt - 1 - ii;
+            const int j0 = ph == 0 ? 0 : i + 1, j1 = ph == 0 ? i : nt;  // off-diagonal range
+            for (int j = j0; j <= j1; ++j) {
+              const int jj = (j == j1) ? i : j;  // off-diagonals first, diagonal last
+              const int s = (int)(t % S);
+              const uint32_t use = (uint32_t)(t / S);
+              if (use > 0) mbar_wait(empty + s, (use - 1) & 1);
+              mbar_expect_tx(full + s, tile_bytes);
+              bulk_g2s(slots + (long)s * T2, Fb + (long)(i * nt + jj) * T2, tile_bytes, full + s);
+              ++t;
+            }
+          }
+        }
+      }
+    }
+    return;
+  }
+
+  // ---------------- consumers
+  long t = 0;
+  for (int ch = 0; ch < nchunks; ++ch) {
+    const int rho0 = ch * R;
+    const int nr = min(R, total - rho0);
+    if (tid < R) {
+      long b = 0;
+      if (tid < nr) {
+        const int rho = rho0 + tid;
+        const int kk = klist ? klist[beg + rho / nrhs] : beg + rho / nrhs;
+        b = (long)kk * s_k + (rho % nrhs);
+      }
+      rbase[tid] = b;
+    }
+    consumers_sync(NC);
+    const int* pm = perm + (long)slot * n;
+    for (int idx = tid; idx < npad * R; idx += NC) {
+      const int row = idx / R, rr = idx - row * R;
+      double2 v = cmk(0.0, 0.0);
+      if (row < n && rr < nr) v = Y[(long)pm[row] * s_row + rbase[rr]];
+      y[idx] = v;
+    }
+    consumers_sync(NC);
+    for (int ph = 0; ph < 2; ++ph) {
+      for (int ii = 0; ii < nt; ++ii) {
+        const int i = ph == 0 ? ii : nt - 1 - ii;
+        const int j0 = ph == 0 ? 0 : i + 1, j1 = ph == 0 ? i : nt;
+        const int noff = j1 - j0;
+        double2 acc[R];
+#pragma unroll
+        for (int rr = 0; rr < R; ++rr) acc[rr] = cmk(0.0, 0.0);
+        // every consumer warp waits on every tile in sequence order (only the
+        // owner computes): a slot is then never waited on more than one phase
+        // ahead, which keeps the mbarrier parity unambiguous.
+        for (int q = 0; q < noff; ++q) {
+          const long tq = t + q;
+          const int s = (int)(tq % S);
+          mbar_wait(full + s, (uint32_t)(tq / S) & 1);
+          if (q % NWC != warp) continue;
+          if (lane < T) {
+            const double2* tile = slots + (long)s * T2 + lane;
+            const double2* yj = y + (long)(j0 + q) * T * R;
+#pragma unroll 4
+            for (int c = 0; c < T; ++c) {
+              const double2 a = tile[c * T];
+#pragma unroll
+              for (int rr = 0; rr < R; ++rr) cfma(acc[rr], a, yj[c * R + rr]);
+            }
+          }
+          __syncwarp();
+          if (lane == 0) mbar_arrive(empty + s);
+        }
+        if (lane < T) {
+#pragma unroll
+          for (int rr = 0; rr < R; ++rr) red[(warp * T + lane) * R + rr] = acc[rr];
+        }
+        t += noff;
+        consumers_sync(NC);
+        for (int idx = tid; idx < T * R; idx += NC) {
+          const int r = idx / R, rr = idx - r * R;
+          double2 z = y[(long)(i * T + r) * R + rr];
+          for (int w = 0; w < NWC; ++w) z = csub(z, red[(w * T + r) * R + rr]);
+          zb[idx] = z;
+        }
+        consumers_sync(NC);
+        {
+          const int s = (int)(t % S);
+          mbar_wait(full + s, (uint32_t)(t / S) & 1);
+          const double2* Ds = slots + (long)s * T2;
+          for (int idx = tid; idx < T * R; idx += NC) {
+            const int r = idx / R, rr = idx - r * R;
+            double2 o;
+            if (ph == 0) {
+              o = zb[idx];
+              for (int c = 0; c < r; ++c) cfma(o, Ds[c * T + r], zb[c * R + rr]);
+            } else {
+              o = cmk(0.0, 0.0);
+              for (int c = r; c < T; ++c) cfma(o, Ds[c * T + r], zb[c * R + rr]);
+            }
+            y[(long)(i * T + r) * R + rr] = o;
+          }
+          consumers_sync(NC);
+          if (tid == 0) mbar_arrive(empty + s);
+          t += 1;
+        }
+      }
+    }
+    for (int idx = tid; idx < n * R; idx += NC) {
+      const int row = idx / R, rr = idx - row * R;
+      if (rr < nr) Y[(long)row * s_row + rbase[rr]] = y[idx];
+    }
+    consumers_sync(NC);
+  }
+}
+
+template <int R>
+static int launch_solve_pipe(const LuGeom& g, const double2* F, const int* perm, const int* items,
+                             int item0, int nblocks, const int* klist, int nrhs, double2* Y, long s_row,
+                             long s_k, cudaStream_t s) {
+  if (nblocks <= 0) return VX_OK;
+  const size_t tile = (size_t)g.T * g.T * sizeof(double2);
+  const size_t fixed = ((size_t)g.npad * R + (size_t)PIPE_CONSUMERS * g.T * R + (size_t)g.T * R) *
+                       sizeof(double2);
+  // two CTAs per SM when the vector state is small, otherwise one
+  const size_t budget = (fixed < 40 * 1024 ? 112 * 1024 : (size_t)device_smem_optin() - 2048);
+  int S = (int)((budget > fixed ? budget - fixed : 0) / tile);
+  if (S > 16) S = 16;
+  VX_REQUIRE(S >= 2, "block size %d too large for the pipelined solve", g.n);
+  const size_t smem = (((size_t)2 * S + R) * 8 + 127) / 128 * 128 + (size_t)S * tile + fixed;
+  auto kern = lu_solve_pipe_kernel<R>;
+  VX_REQUIRE((int)smem + 1024 <= device_smem_optin(), "pipelined solve smem %zu too large", smem);
+  VX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  kern<<<nblocks, (PIPE_CONSUMERS + 1) * 32, smem, s>>>(g, F, perm, items, item0, klist, nrhs, Y, s_row,
+                                                        s_k, S);
+  VX_CHECK_LAUNCH("lu_solve_pipe_kernel");
+  return VX_OK;
+}
 
 // ---------------------------------------------------------------- blocked
 __global__ void box_copy_kernel(int nx, int ny, int nz, int x0, int y0, int z0, int bx, int by,
@@ -608,18 +836,23 @@ extern "C" int vx_prec1_apply(int nx, int ny, int nz, int nrhs, const vx_c128* f
   }
   LuGeom g = lu_geom(q3);
   const double2* F = reinterpret_cast<const double2*>(factors);
+  const bool pipe = g.nt > 1 && !g_solve_classic;
   if (nrhs == 1) {
     Span span("prec_solve", s);
-    if ((st = launch_solve<1, SOLVE_WARPS>(g, F, perm, items, 0, n_single, klist, 1, S, pitch, nrhs, s)))
-      return st;
+    st = pipe ? launch_solve_pipe<1>(g, F, perm, items, 0, n_single, klist, 1, S, pitch, nrhs, s)
+              : launch_solve<1, SOLVE_WARPS>(g, F, perm, items, 0, n_single, klist, 1, S, pitch, nrhs, s);
+    if (st) return st;
   } else {
-    if ((st = launch_solve<MULTI_R, SOLVE_WARPS>(g, F, perm, items, 0, n_single, klist, nrhs, S, pitch,
-                                                  nrhs, s)))
-      return st;
+    st = pipe ? launch_solve_pipe<MULTI_R>(g, F, perm, items, 0, n_single, klist, nrhs, S, pitch, nrhs, s)
+              : launch_solve<MULTI_R, SOLVE_WARPS>(g, F, perm, items, 0, n_single, klist, nrhs, S, pitch,
+                                                   nrhs, s);
+    if (st) return st;
   }
-  if ((st = launch_solve<MULTI_R, SOLVE_WARPS>(g, F, perm, items, n_single, n_items - n_single, klist,
-                                                nrhs, S, pitch, nrhs, s)))
-    return st;
+  st = pipe ? launch_solve_pipe<MULTI_R>(g, F, perm, items, n_single, n_items - n_single, klist, nrhs, S,
+                                         pitch, nrhs, s)
+            : launch_solve<MULTI_R, SOLVE_WARPS>(g, F, perm, items, n_single, n_items - n_single, klist,
+                                                 nrhs, S, pitch, nrhs, s);
+  if (st) return st;
   {
     LoadStrided ld{S, {pitch, 1, nrhs, nrhs}};
     StoreStrided sv{reinterpret_cast<double2*>(y), {pitch, 1, nrhs, nrhs}, 1.0 / nx};
@@ -733,5 +966,10 @@ extern "C" int vx_box_scatter(int nx, int ny, int nz, int x0, int y0, int z0, in
       nx, ny, nz, x0, y0, z0, bx, by, bz, nrhs, reinterpret_cast<const double2*>(box),
       reinterpret_cast<double2*>(full), 0);
   VX_CHECK_LAUNCH("box_copy_kernel");
+  return VX_OK;
+}
+
+extern "C" int vx_solve_variant(int classic) {
+  vx::g_solve_classic = classic ? 1 : 0;
   return VX_OK;
 }
