@@ -63,6 +63,10 @@ int vx_fft_lines(int n, int n_lines, int n_inner, const vx_c128* in, long in_os,
 int vx_op_plan(int nx, int ny, int nz, int px, int py, int pz, const vx_c128* gen, long g_sp,
                long g_sz, long g_sy, long g_sx, vx_c128* spectra, void* stream);
 
+/* Padded FFT length used per axis by the operator plan: 2n when 2n is 7-smooth,
+ * else the smallest 7-smooth length >= 2n-1. */
+int vx_op_padded_length(int n);
+
 /* Scratch (in vx_c128 elements) needed by vx_op_apply. */
 long vx_op_work_elems(int nx, int ny, int nz, int px, int py, int pz);
 

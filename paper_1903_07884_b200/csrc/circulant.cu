@@ -604,7 +604,7 @@ __global__ void __launch_bounds__((PIPE_CONSUMERS + 1) * 32)
   if (tid == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(full + s, 1);
-      mbar_init(empty + s, 1);
+      mbar_init(empty + s, NWC);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -666,15 +666,15 @@ __global__ void __launch_bounds__((PIPE_CONSUMERS + 1) * 32)
         double2 acc[R];
 #pragma unroll
         for (int rr = 0; rr < R; ++rr) acc[rr] = cmk(0.0, 0.0);
-        // every consumer warp waits on every tile in sequence order (only the
-        // owner computes): a slot is then never waited on more than one phase
-        // ahead, which keeps the mbarrier parity unambiguous.
+        // Every consumer warp walks every tile in order (waits, then releases;
+        // only the owner q % NWC computes).  The empty barriers count NWC
+        // arrivals, so no slot can be refilled before all consumers passed
+        // it: parity waits are never more than one phase ahead.
         for (int q = 0; q < noff; ++q) {
           const long tq = t + q;
           const int s = (int)(tq % S);
           mbar_wait(full + s, (uint32_t)(tq / S) & 1);
-          if (q % NWC != warp) continue;
-          if (lane < T) {
+          if (q % NWC == warp && lane < T) {
             const double2* tile = slots + (long)s * T2 + lane;
             const double2* yj = y + (long)(j0 + q) * T * R;
 #pragma unroll 4
@@ -717,7 +717,7 @@ __global__ void __launch_bounds__((PIPE_CONSUMERS + 1) * 32)
             y[(long)(i * T + r) * R + rr] = o;
           }
           consumers_sync(NC);
-          if (tid == 0) mbar_arrive(empty + s);
+          if (lane == 0) mbar_arrive(empty + s);
           t += 1;
         }
       }

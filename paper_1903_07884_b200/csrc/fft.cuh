@@ -210,7 +210,7 @@ __device__ __forceinline__ void fft_stage(double2* s, SmemLay lay, int W, int n,
   __syncthreads();
 }
 
-template <bool DIT>
+template <bool DIT, int RMAX>
 __device__ __forceinline__ void fft_one_stage(int R, double2* s, SmemLay lay, int W, int n, int m,
                                               const double2* tw, double sgn) {
   switch (R) {
@@ -220,26 +220,31 @@ __device__ __forceinline__ void fft_one_stage(int R, double2* s, SmemLay lay, in
     case 3: fft_stage<3, DIT>(s, lay, W, n, m, tw, sgn); break;
     case 5: fft_stage<5, DIT>(s, lay, W, n, m, tw, sgn); break;
     case 7: fft_stage<7, DIT>(s, lay, W, n, m, tw, sgn); break;
-    case 11: fft_stage<11, DIT>(s, lay, W, n, m, tw, sgn); break;
-    case 13: fft_stage<13, DIT>(s, lay, W, n, m, tw, sgn); break;
-    default: break;
+    default:
+      if constexpr (RMAX >= 11) {
+        if (R == 11) fft_stage<11, DIT>(s, lay, W, n, m, tw, sgn);
+        else if (R == 13) fft_stage<13, DIT>(s, lay, W, n, m, tw, sgn);
+      }
+      break;
   }
 }
 
 // natural -> digit-reversed
+template <int RMAX = 13>
 __device__ __forceinline__ void fft_dif(double2* s, SmemLay lay, int W, const FftPlan& p, double sgn) {
   int m = p.L;
   for (int st = 0; st < p.nst; ++st) {
     m /= p.radix[st];
-    fft_one_stage<false>(p.radix[st], s, lay, W, p.L, m, p.tw, sgn);
+    fft_one_stage<false, RMAX>(p.radix[st], s, lay, W, p.L, m, p.tw, sgn);
   }
 }
 
 // digit-reversed -> natural
+template <int RMAX = 13>
 __device__ __forceinline__ void fft_dit(double2* s, SmemLay lay, int W, const FftPlan& p, double sgn) {
   int m = 1;
   for (int st = p.nst - 1; st >= 0; --st) {
-    fft_one_stage<true>(p.radix[st], s, lay, W, p.L, m, p.tw, sgn);
+    fft_one_stage<true, RMAX>(p.radix[st], s, lay, W, p.L, m, p.tw, sgn);
     m *= p.radix[st];
   }
 }
@@ -260,12 +265,13 @@ __device__ __forceinline__ double2 fft_post(const FftPlan& p, int e, double2 v, 
 // Full transform of W lines loaded in natural order (through fft_pre, zero
 // padded to L).  Afterwards output element e of a line sits at smem position
 // fft_out_pos(p, e) (digit-reversed for direct plans, natural for Bluestein).
+template <int RMAX = 13>
 __device__ __forceinline__ void fft_exec(double2* s, SmemLay lay, int W, const FftPlan& p, bool inv) {
   if (!p.bluestein) {
-    fft_dif(s, lay, W, p, inv ? 1.0 : -1.0);
+    fft_dif<RMAX>(s, lay, W, p, inv ? 1.0 : -1.0);
     return;
   }
-  fft_dif(s, lay, W, p, -1.0);
+  fft_dif<RMAX>(s, lay, W, p, -1.0);
   const int total = W * p.L;
   for (int i = threadIdx.x; i < total; i += blockDim.x) {
     int w, e;
@@ -275,7 +281,14 @@ __device__ __forceinline__ void fft_exec(double2* s, SmemLay lay, int W, const F
     *q = cmul(*q, __ldg(p.bhat_rev + e));
   }
   __syncthreads();
-  fft_dit(s, lay, W, p, 1.0);
+  fft_dit<RMAX>(s, lay, W, p, 1.0);
+}
+
+// largest radix of a plan (host and device)
+__host__ __device__ inline int fft_max_radix(const FftPlan& p) {
+  int r = 1;
+  for (int i = 0; i < p.nst; ++i) r = p.radix[i] > r ? p.radix[i] : r;
+  return r;
 }
 
 __device__ __forceinline__ int fft_out_pos(const FftPlan& p, int e) {

@@ -74,9 +74,12 @@ struct StoreSystem {
   }
 };
 
-template <class Loader, class Storer>
-__global__ void fft_lines_kernel(FftPlan p, Loader ld, Storer st, int n_lines, int W, int n_in,
-                                 int n_out, int inv, int contig) {
+// RMAX = largest radix compiled in: 8 (radices 2..8, 3, 5, 7 -> ~64 registers,
+// two 512-thread CTAs per SM) or 13 (adds the 11/13 codelets).
+template <class Loader, class Storer, int RMAX>
+__global__ void __launch_bounds__(512, (RMAX <= 8 ? 2 : 1))
+    fft_lines_kernel(FftPlan p, Loader ld, Storer st, int n_lines, int W, int n_in, int n_out, int inv,
+                     int contig) {
   extern __shared__ double2 smem[];
   long* lbase_in = reinterpret_cast<long*>(smem + (size_t)W * p.L);
   long* lbase_out = lbase_in + W;
@@ -99,7 +102,7 @@ __global__ void fft_lines_kernel(FftPlan p, Loader ld, Storer st, int n_lines, i
     smem[w * lay.ldw + e * lay.lde] = v;
   }
   __syncthreads();
-  fft_exec(smem, lay, W, p, inv);
+  fft_exec<RMAX>(smem, lay, W, p, inv);
   const int tot_out = W * n_out;
   for (int i = threadIdx.x; i < tot_out; i += blockDim.x) {
     int w, e;
@@ -150,7 +153,8 @@ int launch_fft_lines(const FftPlan& p, const Loader& ld, const Storer& st, int n
   LineLaunch ll;
   int s = pick_line_launch(p, contig, n_lines, &ll);
   if (s) return s;
-  auto kern = fft_lines_kernel<Loader, Storer>;
+  auto kern = fft_max_radix(p) <= 8 ? fft_lines_kernel<Loader, Storer, 8>
+                                    : fft_lines_kernel<Loader, Storer, 13>;
   if (ll.smem > 48 * 1024)
     VX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ll.smem));
   kern<<<div_up(n_lines, ll.W), ll.threads, ll.smem, stream>>>(p, ld, st, n_lines, ll.W, n_in,

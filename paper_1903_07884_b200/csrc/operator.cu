@@ -44,8 +44,10 @@ __constant__ int c_pair_of[9] = {0, 1, 2, 1, 3, 4, 2, 4, 5};
 
 // K3: per column (ky,kx) of the padded spectrum: forward z-DFT of the three
 // components, y_a = sum_b S[PAIR_OF[a,b]] x_b, inverse z-DFT, crop.
-__global__ void op_zmul_kernel(FftPlan pzp, double2* __restrict__ B, const double2* __restrict__ S,
-                               int nz, long cols, int W, double scale) {
+template <int RMAX>
+__global__ void __launch_bounds__(512, (RMAX <= 8 ? 2 : 1))
+    op_zmul_kernel(FftPlan pzp, double2* __restrict__ B, const double2* __restrict__ S, int nz, long cols,
+                   int W, double scale) {
   extern __shared__ double2 smem[];
   const int Pz = pzp.L;
   const int W3 = 3 * W;
@@ -60,7 +62,7 @@ __global__ void op_zmul_kernel(FftPlan pzp, double2* __restrict__ B, const doubl
     smem[lw + e * W3] = v;
   }
   __syncthreads();
-  fft_dif(smem, lay, W3, pzp, -1.0);  // natural -> digit-reversed positions
+  fft_dif<RMAX>(smem, lay, W3, pzp, -1.0);  // natural -> digit-reversed positions
   for (int i = threadIdx.x; i < Pz * W; i += blockDim.x) {
     const int e = i / W, w = i - e * W;  // e = smem position
     const long col = col0 + w;
@@ -81,7 +83,7 @@ __global__ void op_zmul_kernel(FftPlan pzp, double2* __restrict__ B, const doubl
     }
   }
   __syncthreads();
-  fft_dit(smem, lay, W3, pzp, 1.0);  // digit-reversed -> natural
+  fft_dit<RMAX>(smem, lay, W3, pzp, 1.0);  // digit-reversed -> natural
   for (int i = threadIdx.x; i < nz * W3; i += blockDim.x) {
     const int e = i / W3, lw = i - e * W3;
     const int c = lw / W, w = lw - c * W;
@@ -143,6 +145,21 @@ extern "C" int vx_op_plan(int nx, int ny, int nz, int px, int py, int pz, const 
   return launch_fft_lines(fz, lz, sz, (int)(6 * cols), pz, pz, false, false, s);
 }
 
+extern "C" int vx_op_padded_length(int n) {
+  // 2n when it is 7-smooth (the reference grid), else the smallest 7-smooth
+  // length >= 2n-1: every such length gives the same linear convolution, and
+  // radices <= 8 keep the transforms in the low-register kernel variants.
+  auto smooth7 = [](int m) {
+    for (int p : {2, 3, 5, 7})
+      while (m % p == 0) m /= p;
+    return m == 1;
+  };
+  if (smooth7(2 * n)) return 2 * n;
+  int m = 2 * n - 1;
+  while (!smooth7(m)) ++m;
+  return m;
+}
+
 extern "C" long vx_op_work_elems(int nx, int ny, int nz, int px, int py, int pz) {
   (void)pz;
   return 3L * nz * px * ((long)ny + py);
@@ -181,12 +198,12 @@ extern "C" int vx_op_apply(int nx, int ny, int nz, int px, int py, int pz, const
     while (W > 1 && (long)W > cols) W /= 2;
     const size_t smem = (size_t)3 * W * fz.L * sizeof(double2);
     int thr = fft_threads_for(fz, 3 * W);
+    auto kern = fft_max_radix(fz) <= 8 ? op_zmul_kernel<8> : op_zmul_kernel<13>;
     if (smem > 48 * 1024)
-      VX_CUDA(cudaFuncSetAttribute(op_zmul_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)smem));
+      VX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const double scale = 1.0 / ((double)px * py * pz);
-    op_zmul_kernel<<<div_up(cols, W), thr, smem, s>>>(fz, B, reinterpret_cast<const double2*>(spectra),
-                                                       nz, cols, W, scale);
+    kern<<<div_up(cols, W), thr, smem, s>>>(fz, B, reinterpret_cast<const double2*>(spectra), nz, cols, W,
+                                            scale);
     VX_CHECK_LAUNCH("op_zmul_kernel");
   }
   // K4: inverse y, crop to ny

@@ -7,8 +7,8 @@ fused padded-FFT convolution (``vx_op_apply``: 5 launches, pad / crop /
 
 Type behaviour: numpy in -> numpy out (host copies at the boundary); a CUDA
 ``torch.Tensor`` in -> CUDA tensor out, no host traffic.  Inputs are never
-modified.  Padding: each axis uses ``2n`` when that length is 13-smooth
-(exactly the reference grid), otherwise the next 13-smooth length >= 2n-1;
+modified.  Padding: each axis uses ``2n`` when that length is 7-smooth
+(exactly the reference grid), otherwise the next 7-smooth length >= 2n-1;
 any such padding yields the same linear convolution (``padded_shape`` and
 ``storage_bytes`` report what is actually stored).
 """
@@ -25,9 +25,9 @@ from .kernel import ToeplitzKernel
 
 
 def padded_length(n: int) -> int:
+    """2n when 7-smooth (the reference's padding), else the next 7-smooth >= 2n-1."""
     nv.load()
-    two_n = 2 * n
-    return two_n if nv.query("vx_fft_is_smooth", two_n) else nv.query("vx_fft_good_length", two_n - 1)
+    return int(nv.query("vx_op_padded_length", n))
 
 
 def upload_tensors(kernel: ToeplitzKernel):
