@@ -22,14 +22,11 @@ struct LuGeom {
   long blk;
 };
 
+// T = n for single-tile blocks (n <= 32), else 32: full warps in the solve and
+// 8x8x4 DMMA blocking in the factorisation (c1: 726 -> 736, +2.8% stored).
 static int lu_pick_tile(int n) {
   if (n <= 32) return n < 1 ? 1 : n;
-  int best = 32, bestpad = (n + 31) / 32 * 32;
-  for (int T = 32; T >= 16; --T) {
-    int pad = (n + T - 1) / T * T;
-    if (pad < bestpad) { best = T; bestpad = pad; }
-  }
-  return best;
+  return 32;
 }
 
 static LuGeom lu_geom(int n) {
@@ -115,42 +112,90 @@ __device__ __forceinline__ double2 unfold_entry(const Unfold& u, const double2* 
   return v;
 }
 
-// C(T x T, global) = Aop * Bs  (overwrite)  or  C -= Aop * Bs.
-// Aop column-major T x T (global or smem), lane r reads Aop[k*T + r];
-// Bs column-major in smem, broadcast reads Bs[c*T + k].
+// FP64 tensor-core (DMMA, mma.sync.m8n8k4.f64) product on one half (16
+// columns) of a 32 x 32 complex tile:
+//   C[:, 16h:16h+16]  =  A * B[:, 16h:16h+16]      (SUB = false)
+//   C[:, 16h:16h+16] -=  A * B[:, 16h:16h+16]      (SUB = true)
+// A is staged in shared memory (column-major, ld 33 to spread banks); B and C
+// are tiles in global memory (column-major, ld 32).  Complex = 4 real DMMAs.
+// Fragments (verified by tools/dmma_probe.cu): A[l/4][l%4], B[l%4][l/4],
+// C[l/4][2(l%4) + {0,1}].
+__device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
 template <bool SUB>
-__device__ __forceinline__ void warp_tile_gemm(const double2* Aop, const double2* Bs, double2* C, int T,
-                                               int lane) {
-  if (lane >= T) return;
-  for (int c0 = 0; c0 < T; c0 += LU_CW) {
-    double2 acc[LU_CW];
+__device__ __forceinline__ void tile_mma_half(const double2* As, const double2* Bg, double2* Cg, int h,
+                                              int lane) {
+  const int r4 = lane >> 2, c4 = lane & 3;
+  double cr[4][2][2], ci[4][2][2];
 #pragma unroll
-    for (int c = 0; c < LU_CW; ++c)
-      acc[c] = (SUB && c0 + c < T) ? C[(c0 + c) * T + lane] : cmk(0.0, 0.0);
-    for (int k = 0; k < T; ++k) {
-      const double2 a = Aop[k * T + lane];
+  for (int rb = 0; rb < 4; ++rb)
 #pragma unroll
-      for (int c = 0; c < LU_CW; ++c) {
-        if (c0 + c < T) {
-          if (SUB) cfms(acc[c], a, Bs[(c0 + c) * T + k]);
-          else cfma(acc[c], a, Bs[(c0 + c) * T + k]);
-        }
+    for (int cb = 0; cb < 2; ++cb)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        double2 v = cmk(0.0, 0.0);
+        if (SUB) v = Cg[(16 * h + cb * 8 + 2 * c4 + e) * 32 + rb * 8 + r4];
+        cr[rb][cb][e] = v.x;
+        ci[rb][cb][e] = v.y;
       }
+#pragma unroll 2
+  for (int k0 = 0; k0 < 32; k0 += 4) {
+    double ar[4], ai[4], nar[4], br[2], bi[2];
+#pragma unroll
+    for (int rb = 0; rb < 4; ++rb) {
+      const double2 a = As[(k0 + c4) * 33 + rb * 8 + r4];
+      ar[rb] = a.x;
+      ai[rb] = a.y;
+      nar[rb] = -a.x;
     }
 #pragma unroll
-    for (int c = 0; c < LU_CW; ++c)
-      if (c0 + c < T) C[(c0 + c) * T + lane] = acc[c];
+    for (int cb = 0; cb < 2; ++cb) {
+      const double2 b = Bg[(16 * h + cb * 8 + r4) * 32 + k0 + c4];
+      br[cb] = b.x;
+      bi[cb] = b.y;
+    }
+#pragma unroll
+    for (int rb = 0; rb < 4; ++rb)
+#pragma unroll
+      for (int cb = 0; cb < 2; ++cb) {
+        if (SUB) {  // C -= A B :  cr += -ar br + ai bi ; ci += -ar bi - ai br
+          const double nai = -ai[rb];
+          dmma884(cr[rb][cb][0], cr[rb][cb][1], nar[rb], br[cb]);
+          dmma884(cr[rb][cb][0], cr[rb][cb][1], ai[rb], bi[cb]);
+          dmma884(ci[rb][cb][0], ci[rb][cb][1], nar[rb], bi[cb]);
+          dmma884(ci[rb][cb][0], ci[rb][cb][1], nai, br[cb]);
+        } else {    // C = A B :  cr += ar br - ai bi ; ci += ar bi + ai br
+          const double nai = -ai[rb];
+          dmma884(cr[rb][cb][0], cr[rb][cb][1], ar[rb], br[cb]);
+          dmma884(cr[rb][cb][0], cr[rb][cb][1], nai, bi[cb]);
+          dmma884(ci[rb][cb][0], ci[rb][cb][1], ar[rb], bi[cb]);
+          dmma884(ci[rb][cb][0], ci[rb][cb][1], ai[rb], br[cb]);
+        }
+      }
   }
+  __syncwarp();
+#pragma unroll
+  for (int rb = 0; rb < 4; ++rb)
+#pragma unroll
+    for (int cb = 0; cb < 2; ++cb)
+#pragma unroll
+      for (int e = 0; e < 2; ++e)
+        Cg[(16 * h + cb * 8 + 2 * c4 + e) * 32 + rb * 8 + r4] = cmk(cr[rb][cb][e], ci[rb][cb][e]);
 }
 
 __global__ void __launch_bounds__(LU_THREADS) lu_build_kernel(Unfold u, LuGeom g, double2* F,
                                                                int* perm, int* piv, int* info) {
   extern __shared__ double2 sm[];
   const int T = g.T, T2 = T * T, nt = g.nt, npad = g.npad, n = g.n;
-  double2* Ls = sm;                    // inv(L_kk), column-major
-  double2* Us = Ls + T2;               // inv(U_kk)
-  double2* Bst = Us + T2;              // LU_WARPS staged B tiles
-  int* pivs = reinterpret_cast<int*>(Bst + LU_WARPS * T2);  // [T]
+  const int LD = T + 1, TL = T * LD;   // padded leading dimension of smem tiles
+  double2* Ls = sm;                    // inv(L_kk), column-major, ld LD
+  double2* Us = Ls + TL;               // inv(U_kk)
+  double2* Bst = Us + TL;              // LU_WARPS staged L tiles (ld LD)
+  int* pivs = reinterpret_cast<int*>(Bst + LU_WARPS * TL);  // [T]
   double* redv = reinterpret_cast<double*>(pivs + 32);        // [LU_WARPS]
   int* redi = reinterpret_cast<int*>(redv + LU_WARPS);        // [LU_WARPS]
   int* flags = redi + LU_WARPS;                               // [0]=info [1]=any swap
@@ -272,11 +317,11 @@ __global__ void __launch_bounds__(LU_THREADS) lu_build_kernel(Unfold u, LuGeom g
       for (int r = 0; r < T; ++r) {
         double2 x = cmk(r == c ? 1.0 : 0.0, 0.0);
         if (r > c) {
-          for (int i = c; i < r; ++i) cfms(x, Dg[i * T + r], Ls[c * T + i]);
+          for (int i = c; i < r; ++i) cfms(x, Dg[i * T + r], Ls[c * LD + i]);
         } else if (r < c) {
           x = cmk(0.0, 0.0);
         }
-        Ls[c * T + r] = x;
+        Ls[c * LD + r] = x;
       }
     } else if (warp == 1 && lane < T) {
       const int c = lane;
@@ -284,46 +329,48 @@ __global__ void __launch_bounds__(LU_THREADS) lu_build_kernel(Unfold u, LuGeom g
         double2 x = cmk(0.0, 0.0);
         if (r <= c) {
           x = cmk(r == c ? 1.0 : 0.0, 0.0);
-          for (int i = r + 1; i <= c; ++i) cfms(x, Dg[i * T + r], Us[c * T + i]);
+          for (int i = r + 1; i <= c; ++i) cfms(x, Dg[i * T + r], Us[c * LD + i]);
           x = cdiv(x, Dg[r * T + r]);
         }
-        Us[c * T + r] = x;
+        Us[c * LD + r] = x;
       }
     }
     __syncthreads();
-    // ---- (4) U row tiles: A(kt, jt) = inv(L_kk) A(kt, jt); packed diagonal tile
+    // ---- (4) U row tiles: A(kt, jt) = inv(L_kk) A(kt, jt)  (DMMA; T == 32
+    //          whenever nt > 1), and the packed diagonal tile
+    for (int jt = kt + 1 + warp; jt < nt; jt += LU_WARPS) {
+      double2* C = A + (long)(kt * nt + jt) * T2;
+      tile_mma_half<false>(Ls, C, C, 0, lane);
+      tile_mma_half<false>(Ls, C, C, 1, lane);
+    }
     {
-      double2* Bw = Bst + warp * T2;
-      for (int jt = kt + 1 + warp; jt < nt; jt += LU_WARPS) {
-        double2* C = A + (long)(kt * nt + jt) * T2;
-        for (int i = lane; i < T2; i += 32) Bw[i] = C[i];
-        __syncwarp();
-        warp_tile_gemm<false>(Ls, Bw, C, T, lane);
-        __syncwarp();
-      }
       double2* Dw = A + (long)(kt * nt + kt) * T2;
       for (int i = tid; i < T2; i += LU_THREADS) {
         const int c = i / T, r = i - c * T;
-        Dw[i] = (r > c) ? Ls[i] : Us[i];
+        Dw[i] = (r > c) ? Ls[c * LD + r] : Us[c * LD + r];
       }
     }
     __syncthreads();
-    // ---- (5) trailing update A(it, jt) -= A(it, kt) A(kt, jt)
-    const int nrem = nt - kt - 1;
-    if (nrem > 0) {
-      double2* Bw = Bst + warp * T2;
-      int staged = -1;
-      const int ntask = nrem * nrem;
-      for (int t = warp; t < ntask; t += LU_WARPS) {
-        const int jt = kt + 1 + t / nrem, it = kt + 1 + t % nrem;
-        if (jt != staged) {
-          __syncwarp();
-          const double2* Bsrc = A + (long)(kt * nt + jt) * T2;
-          for (int i = lane; i < T2; i += 32) Bw[i] = Bsrc[i];
-          __syncwarp();
-          staged = jt;
+    // ---- (5) trailing update A(it, jt) -= A(it, kt) A(kt, jt) on DMMA: a warp
+    //          owns tile rows it; L tile A(it,kt) staged once per row in shared
+    //          memory, U tiles of row kt read as B fragments (L1-shared by the
+    //          warps sweeping the same jt), each trailing tile read+written once.
+    {
+      double2* Aw = Bst + warp * TL;
+      for (int it = kt + 1 + warp; it < nt; it += LU_WARPS) {
+        const double2* Asrc = A + (long)(it * nt + kt) * T2;
+        __syncwarp();
+        for (int i = lane; i < T2; i += 32) {
+          const int c = i / T, r = i - c * T;
+          Aw[c * LD + r] = Asrc[i];
         }
-        warp_tile_gemm<true>(A + (long)(it * nt + kt) * T2, Bw, A + (long)(it * nt + jt) * T2, T, lane);
+        __syncwarp();
+        for (int jt = kt + 1; jt < nt; ++jt) {
+          const double2* B = A + (long)(kt * nt + jt) * T2;
+          double2* C = A + (long)(it * nt + jt) * T2;
+          tile_mma_half<true>(Aw, B, C, 0, lane);
+          tile_mma_half<true>(Aw, B, C, 1, lane);
+        }
       }
     }
     __syncthreads();
@@ -351,7 +398,7 @@ __global__ void __launch_bounds__(LU_THREADS) lu_build_kernel(Unfold u, LuGeom g
 }
 
 static size_t lu_smem(const LuGeom& g) {
-  return (size_t)(2 + LU_WARPS) * g.T * g.T * sizeof(double2) + 32 * sizeof(int) +
+  return (size_t)(2 + LU_WARPS) * g.T * (g.T + 1) * sizeof(double2) + 32 * sizeof(int) +
          LU_WARPS * (sizeof(double) + sizeof(int)) + 4 * sizeof(int) + (size_t)g.npad * sizeof(int) + 64;
 }
 

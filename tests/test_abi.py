@@ -34,7 +34,7 @@ def test_host_only_queries():
     assert nv.query("vx_fft_is_smooth", 10000) == 1
     assert nv.query("vx_fft_is_smooth", 734) == 0
     assert nv.query("vx_fft_good_length", 733) == 735
-    for n, T in [(24, 24), (150, 30), (726, 22), (825, 25), (924, 28)]:
+    for n, T in [(24, 24), (18, 18), (150, 32), (726, 32), (825, 32), (924, 32)]:
         assert nv.query("vx_lu_tile", n) == T
         assert nv.query("vx_lu_block_elems", n) == (-(-n // T) * T) ** 2
 
