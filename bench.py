@@ -57,6 +57,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-sample-blocks", type=int, default=24)
+    ap.add_argument("--replicas", action="store_true",
+                    help="N > 1: independent replicas instead of the sharded solve")
     ap.add_argument("--solve-classic", action="store_true",
                     help="use the non-pipelined block-solve kernel (A/B measurement)")
     return ap.parse_args()
@@ -310,25 +312,52 @@ def run_ours(args):
     m_host = W.m
     b_host = W.b
     torch.cuda.synchronize()
+    # N > 1: the 1-level configs run ONE sharded solve across all ranks (strong
+    # scaling: line-sharded vectors, k-sharded factors, NCCL all-to-all);
+    # blocked / 2-level configs run one replica per rank (weak scaling).
+    sharded = world > 1 and W.prec["kind"] in ("one-level", "reduced-one-level") and not args.replicas
+    mode = "sharded" if sharded else ("replicas" if world > 1 else "single-gpu")
 
     # ---- setup (time-to-solution part 1): plan + preconditioner build
-    t0 = time.perf_counter()
-    plan = plan_operator(kern)
-    torch.cuda.synchronize()
-    plan_s = time.perf_counter() - t0
-    ev_a, ev_b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    ev_a.record()
-    prec = build_prec(W, kern)
-    ev_b.record()
-    torch.cuda.synchronize()
-    build_s = ev_a.elapsed_time(ev_b) / 1e3
-
     m_dev = torch.from_numpy(np.ascontiguousarray(m_host).reshape(-1)).cuda()
-    b_dev = torch.from_numpy(b_host.copy()).cuda()
-    A = lambda v: apply_system(plan, m_dev, v)  # noqa: E731
+    t0 = time.perf_counter()
+    ev_a, ev_b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if sharded:
+        from paper_1903_07884_b200.dist import (CudaBackend, DistOneLevelPrec, DistOperator, Layout, _Comm,
+                                                gmres_sharded)
+        from paper_1903_07884_b200.operator import padded_length
 
-    def solve(b):
-        return gmres(A, b, apply_pinv=prec.apply, tol=W.tol, maxit=W.maxit, restart=W.restart)
+        Bk, Cm = CudaBackend(), _Comm()
+        L = Layout(W.grid.dims, world, rank, padded_length(W.grid.nx))
+        dop = DistOperator(kern, L, Bk, Cm)
+        torch.cuda.synchronize()
+        plan_s = time.perf_counter() - t0
+        ev_a.record()
+        prec = DistOneLevelPrec(kern, W.mtilde(), L, Bk, Cm,
+                                tol=W.prec.get("tol") if W.prec["kind"] == "reduced-one-level" else None)
+        ev_b.record()
+        torch.cuda.synchronize()
+        build_s = ev_a.elapsed_time(ev_b) / 1e3
+        b_dev = torch.from_numpy(np.ascontiguousarray(L.local_slice(b_host))).cuda()
+        A = lambda v: dop.apply(m_dev, v)  # noqa: E731
+
+        def solve(b):
+            return gmres_sharded(A, b, Bk, Cm, apply_pinv=prec.apply, tol=W.tol, maxit=W.maxit,
+                                 restart=W.restart)
+    else:
+        plan = plan_operator(kern)
+        torch.cuda.synchronize()
+        plan_s = time.perf_counter() - t0
+        ev_a.record()
+        prec = build_prec(W, kern)
+        ev_b.record()
+        torch.cuda.synchronize()
+        build_s = ev_a.elapsed_time(ev_b) / 1e3
+        b_dev = torch.from_numpy(b_host.copy()).cuda()
+        A = lambda v: apply_system(plan, m_dev, v)  # noqa: E731
+
+        def solve(b):
+            return gmres(A, b, apply_pinv=prec.apply, tol=W.tol, maxit=W.maxit, restart=W.restart)
 
     for _ in range(args.warmup):
         _, rep = solve(b_dev)
@@ -360,15 +389,24 @@ def run_ours(args):
     spans = {sp: nv.timing_read(sp) for sp in ("prec_solve", "op_apply", "prec_apply", "arnoldi_step")}
     nv.timing_enable(False)
     t_max = reduce_max(torch, world, t_local)
-    its_all = reduce_sum(torch, world, its)
+    its_all = its if sharded else reduce_sum(torch, world, its)
     value = its_all / t_max
     ms_per_step = t_max / args.steps * 1e3
     solve_s = t_local / args.steps
 
     # ---- roofline of the dominant kernel (factor-streaming block solve)
     peak, peak_kind = peaks()
-    stored = stored_blocks_of(W, prec)
-    nvec = W.grid.n_unknowns
+    if sharded:
+        stored_global = [(3 * W.grid.ny * W.grid.nz, prec.n_stored_global)]
+        stored = [(3 * W.grid.ny * W.grid.nz, prec.bytes_local // (16 * (3 * W.grid.ny * W.grid.nz) ** 2))]
+        nvec = W.grid.n_unknowns // world
+    else:
+        stored = stored_global = stored_blocks_of(W, prec)
+        nvec = W.grid.n_unknowns
+        if W.prec["kind"] == "blocked":   # one solve launch per box: per-launch bytes of one box
+            x0, x1, y0, y1, z0, z1 = W.prec["boxes"][0]
+            stored = stored[:1]
+            nvec = 3 * (x1 - x0) * (y1 - y0) * (z1 - z0)
     sol_ms, sol_n = spans["prec_solve"]
     solve_bytes = 16 * sum(n * n * c for n, c in stored) + 2 * 16 * nvec
     roof = None
@@ -381,12 +419,12 @@ def run_ours(args):
                 "launches": sol_n}
     its_per_solve = its / args.steps
     restart_eff = min(W.restart, its_per_solve)
-    b_it, b_mv, b_pc, b_ar = iteration_bytes(W, stored, restart_eff)
-    b_pc = 2 * 48 * W.grid.n_voxels + 16 * sum(n * n * c for n, c in stored)
+    b_it, b_mv, b_pc, b_ar = iteration_bytes(W, stored_global, restart_eff)
+    b_pc = 2 * 48 * W.grid.n_voxels + 16 * sum(n * n * c for n, c in stored_global)
     b_it = b_mv + b_pc + b_ar
     it_roof = {"bytes_per_iteration": b_it, "B_mv": b_mv, "B_pc": b_pc, "B_ar": b_ar,
-               "achieved": b_it * its / t_local / 1e9, "peak": peak, "unit": "GB/s",
-               "frac": b_it * its / t_local / 1e9 / peak}
+               "achieved": b_it * its_all / t_max / 1e9, "peak": peak * (world if sharded else 1),
+               "unit": "GB/s", "frac": b_it * its_all / t_max / 1e9 / (peak * (world if sharded else 1))}
     breakdown = {sp: {"ms_total": v[0], "launches": v[1]} for sp, v in spans.items()}
 
     # ---- e2e through the public API with host numpy buffers
@@ -398,14 +436,23 @@ def run_ours(args):
         its_e = 0
         for _ in range(args.steps):
             m_step = np.array(m_host, copy=True)           # forces the H2D copy of m
-            x_h, rep = gmres(lambda v: apply_system(plan, m_step, v), b_host.copy(),
-                             apply_pinv=prec.apply, tol=W.tol, maxit=W.maxit, restart=W.restart)
+            if sharded:
+                # host buffers through the sharded API: local slice of b in, local x out
+                m_d = torch.from_numpy(m_step.reshape(-1)).cuda()
+                b_d = torch.from_numpy(np.ascontiguousarray(L.local_slice(b_host))).cuda()
+                xs, rep = gmres_sharded(lambda v: dop.apply(m_d, v), b_d, Bk, Cm, apply_pinv=prec.apply,
+                                        tol=W.tol, maxit=W.maxit, restart=W.restart)
+                x_h = xs.cpu().numpy()
+            else:
+                x_h, rep = gmres(lambda v: apply_system(plan, m_step, v), b_host.copy(),
+                                 apply_pinv=prec.apply, tol=W.tol, maxit=W.maxit, restart=W.restart)
             its_e += rep.iterations
         torch.cuda.synchronize()
         te = reduce_max(torch, world, time.perf_counter() - t0)
-        its_e_all = reduce_sum(torch, world, its_e)
-        e2e = {"value": its_e_all / te, "unit": "it/s", "h2d_bytes_per_step": int(b_host.nbytes + m_host.nbytes),
-               "d2h_bytes_per_step": int(b_host.nbytes), "ms_per_step": te / args.steps * 1e3,
+        its_e_all = its_e if sharded else reduce_sum(torch, world, its_e)
+        nb_loc = b_host.nbytes // world if sharded else b_host.nbytes
+        e2e = {"value": its_e_all / te, "unit": "it/s", "h2d_bytes_per_step": int(nb_loc + m_host.nbytes),
+               "d2h_bytes_per_step": int(nb_loc), "ms_per_step": te / args.steps * 1e3,
                "tts_s": build_s + te / args.steps,
                "note": "numpy b and m in, numpy x out; plan+factors resident (setup)"}
 
@@ -429,7 +476,7 @@ def run_ours(args):
         "warmup": args.warmup,
         "ms_per_step": ms_per_step,
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "strong" if sharded else "weak",
         "vs_baseline": None,
         "dtype": "c128",
         "data": "synthetic (BASELINE workload, interpretation B, deterministic)",
@@ -438,7 +485,7 @@ def run_ours(args):
                    "step": "one full preconditioned GMRES solve (x0=0)",
                    "l2": "inputs larger than L2 (factors %.2f GB >> 126 MB)" % (
                        16 * sum(n * n * c for n, c in stored) / 1e9),
-                   "parallelism": "replicas" if world > 1 else "single-gpu"},
+                   "parallelism": mode},
         "iterations_per_solve": its_per_solve,
         "build_s": build_s,
         "plan_s": plan_s,

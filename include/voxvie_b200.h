@@ -124,6 +124,34 @@ long vx_prec2_work_elems(int nx, int ny, int nz, int nrhs);
 int vx_prec2_apply(int nx, int ny, int nz, int nrhs, const vx_c128* factors, const int* perm,
                    const vx_c128* x, vx_c128* y, vx_c128* work, void* stream);
 
+/* ------------------------------------------------------ sharded (multi-GPU) */
+/* Pieces of vx_op_apply for the x-slab/line-sharded matvec:
+ * forward x-DFT of local lines, the y/z work on the locally owned x-frequency
+ * columns (A is (3, nz, ny, nkx), spectra (6, pz, py, nkx)), inverse x-DFT +
+ * epilogue of local lines (global line offset line0 for the medium map). */
+int vx_op_x_forward(int nx, int px, int nlines, const vx_c128* x, vx_c128* A, void* stream);
+long vx_op_yz_work_elems(int ny, int nz, int nkx, int py);
+int vx_op_yz(int ny, int nz, int nkx, int px, int py, int pz, const vx_c128* spectra_local, vx_c128* A,
+             vx_c128* work, void* stream);
+int vx_op_x_inverse(int nx, int ny, int nz, int px, int nlines, long line0, const vx_c128* A,
+                    const vx_c128* m, const vx_c128* x_local, vx_c128* y_local, void* stream);
+/* All-to-all pack/unpack: out = concat_s A[:, colmap[col_off[s]:col_off[s+1]]]. */
+int vx_gather_cols(long nrows, const vx_c128* A, long lda, int P, const int* col_off, const int* colmap,
+                   long total_cols, vx_c128* out, void* stream);
+int vx_scatter_cols(long nrows, const vx_c128* in, int P, const int* col_off, const int* colmap,
+                    long total_cols, vx_c128* A, long lda, void* stream);
+/* Block solves only (no DFTs): RHS element (row, k, j) at Y[row*s_row + k*s_k + j]. */
+int vx_prec1_solve(int n, int nrhs, const vx_c128* factors, const int* perm, const int* items,
+                   int n_single, int n_items, const int* klist, vx_c128* Y, long s_row, long s_k,
+                   void* stream);
+/* Local halves of one classical Gram-Schmidt pass (the all-reduce goes in
+ * between): out[0..nvec) = V^H w, out[nvec] = ||w||^2; then w -= V coef and
+ * out_norm2 = ||w||^2. */
+int vx_cgs_dots(long n, int nvec, const vx_c128* V, long ldv, const vx_c128* w, vx_c128* out,
+                vx_c128* part, void* stream);
+int vx_cgs_update(long n, int nvec, const vx_c128* V, long ldv, const vx_c128* coef, vx_c128* w,
+                  vx_c128* out_norm2, vx_c128* part, void* stream);
+
 /* --------------------------------------------------------------- blocked */
 /* BlockedPrec.apply gather/scatter (circulant.py:558-563, 603-607): box
  * (x0,y0,z0) of size (bx,by,bz) inside the (nx,ny,nz) grid, nrhs columns. */

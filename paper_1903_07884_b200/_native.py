@@ -69,6 +69,15 @@ _SIGS = {
     "vx_basis_combine": (c_int, [c_long, c_int, P, c_long, P, P, P]),
     "vx_axpby": (c_int, [c_long, c128, P, c128, P, P, P]),
     "vx_norm2": (c_int, [c_long, P, P, P, P]),
+    "vx_op_x_forward": (c_int, [c_int, c_int, c_int, P, P, P]),
+    "vx_op_yz_work_elems": (c_long, [c_int] * 4),
+    "vx_op_yz": (c_int, [c_int] * 6 + [P, P, P, P]),
+    "vx_op_x_inverse": (c_int, [c_int] * 5 + [c_long, P, P, P, P, P]),
+    "vx_gather_cols": (c_int, [c_long, P, c_long, c_int, P, P, c_long, P, P]),
+    "vx_scatter_cols": (c_int, [c_long, P, c_int, P, P, c_long, P, c_long, P]),
+    "vx_prec1_solve": (c_int, [c_int, c_int, P, P, P, c_int, c_int, P, P, c_long, c_long, P]),
+    "vx_cgs_dots": (c_int, [c_long, c_int, P, c_long, P, P, P, P]),
+    "vx_cgs_update": (c_int, [c_long, c_int, P, c_long, P, P, P, P, P]),
     "vx_launch_count": (c_long, []),
     "vx_solve_variant": (c_int, [c_int]),
     "vx_timing_enable": (c_int, [c_int]),

@@ -181,6 +181,18 @@ __global__ void __launch_bounds__(AR_THREADS) finalize_kernel(int nvec, int G, c
   }
 }
 
+// out[i] = sum_b part[i*G + b], fixed order (single CTA)
+__global__ void __launch_bounds__(AR_THREADS) sum_rows_kernel(int rows, int G, const double2* __restrict__ part,
+                                                              double2* __restrict__ out) {
+  __shared__ double2 sh[AR_THREADS / 32];
+  for (int i = 0; i < rows; ++i) {
+    double2 v = cmk(0.0, 0.0);
+    for (int b = threadIdx.x; b < G; b += AR_THREADS) v = cadd(v, part[(long)i * G + b]);
+    v = block_sum(v, sh);
+    if (threadIdx.x == 0) out[i] = v;
+  }
+}
+
 __global__ void scale_kernel(long n, const double2* __restrict__ w, double2* __restrict__ out,
                              const double2* __restrict__ hn) {
   const double s = hn->x;
@@ -315,5 +327,34 @@ extern "C" int vx_norm2(long n, const vx_c128* x, double* out, vx_c128* part, vo
   norm_final_kernel<<<1, AR_THREADS, 0, s>>>(G, reinterpret_cast<const double2*>(part), out);
   count_launch();
   VX_CHECK_LAUNCH("norm2");
+  return VX_OK;
+}
+
+extern "C" int vx_cgs_dots(long n, int nvec, const vx_c128* V, long ldv, const vx_c128* w, vx_c128* out,
+                           vx_c128* part, void* stream) {
+  VX_REQUIRE(n >= 1 && nvec >= 0 && ldv >= n, "bad cgs_dots arguments");
+  cudaStream_t s = as_stream(stream);
+  const int G = ar_grid(n);
+  double2* pd = reinterpret_cast<double2*>(part);
+  dots_kernel<<<G, AR_THREADS, 0, s>>>(n, nvec, reinterpret_cast<const double2*>(V), ldv,
+                                       reinterpret_cast<const double2*>(w), pd, nullptr);
+  sum_rows_kernel<<<1, AR_THREADS, 0, s>>>(nvec + 1, G, pd, reinterpret_cast<double2*>(out));
+  count_launch();
+  VX_CHECK_LAUNCH("cgs_dots");
+  return VX_OK;
+}
+
+extern "C" int vx_cgs_update(long n, int nvec, const vx_c128* V, long ldv, const vx_c128* coef, vx_c128* w,
+                             vx_c128* out_norm2, vx_c128* part, void* stream) {
+  VX_REQUIRE(n >= 1 && nvec >= 0 && ldv >= n, "bad cgs_update arguments");
+  cudaStream_t s = as_stream(stream);
+  const int G = ar_grid(n);
+  double2* pd = reinterpret_cast<double2*>(part);
+  update_kernel<<<G, AR_THREADS, 0, s>>>(n, nvec, reinterpret_cast<const double2*>(V), ldv,
+                                         reinterpret_cast<const double2*>(coef), reinterpret_cast<double2*>(w),
+                                         pd, nullptr);
+  sum_rows_kernel<<<1, AR_THREADS, 0, s>>>(1, G, pd, reinterpret_cast<double2*>(out_norm2));
+  count_launch();
+  VX_CHECK_LAUNCH("cgs_update");
   return VX_OK;
 }

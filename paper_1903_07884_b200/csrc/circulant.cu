@@ -800,6 +800,25 @@ static int launch_solve_pipe(const LuGeom& g, const double2* F, const int* perm,
   return VX_OK;
 }
 
+// ------------------------------------------------------- sharding transposes
+// out = concat_s A[:, colmap[col_off[s] : col_off[s+1]]] (each block row-major):
+// the per-destination send buffers of the all-to-all transposes.
+__global__ void cols_copy_kernel(long nrows, double2* A, long lda, int P, const int* __restrict__ col_off,
+                                 const int* __restrict__ colmap, double2* buf, int to_buf) {
+  const long total = nrows * col_off[P];
+  for (long idx = blockIdx.x * (long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long)gridDim.x * blockDim.x) {
+    int sdst = 0;
+    while (sdst + 1 < P && idx >= nrows * col_off[sdst + 1]) ++sdst;
+    const long ncol = col_off[sdst + 1] - col_off[sdst];
+    const long loc = idx - nrows * col_off[sdst];
+    const long row = loc / ncol, j = loc - row * ncol;
+    const long a = row * lda + colmap[col_off[sdst] + j];
+    if (to_buf) buf[idx] = A[a];
+    else A[a] = buf[idx];
+  }
+}
+
 // ---------------------------------------------------------------- blocked
 __global__ void box_copy_kernel(int nx, int ny, int nz, int x0, int y0, int z0, int bx, int by,
                                 int bz, int nrhs, const double2* __restrict__ src,
@@ -1019,4 +1038,55 @@ extern "C" int vx_box_scatter(int nx, int ny, int nz, int x0, int y0, int z0, in
 extern "C" int vx_solve_variant(int classic) {
   vx::g_solve_classic = classic ? 1 : 0;
   return VX_OK;
+}
+
+extern "C" int vx_gather_cols(long nrows, const vx_c128* A, long lda, int P, const int* col_off,
+                              const int* colmap, long total_cols, vx_c128* out, void* stream) {
+  VX_REQUIRE(nrows >= 0 && P >= 1 && total_cols >= 0, "bad gather_cols arguments");
+  const long total = nrows * total_cols;
+  if (total == 0) return VX_OK;
+  const unsigned g = div_up(total, 256) < 8192 ? div_up(total, 256) : 8192;
+  cols_copy_kernel<<<g, 256, 0, as_stream(stream)>>>(nrows, const_cast<double2*>(reinterpret_cast<const double2*>(A)),
+                                                     lda, P, col_off, colmap, reinterpret_cast<double2*>(out), 1);
+  VX_CHECK_LAUNCH("cols_copy_kernel");
+  return VX_OK;
+}
+
+extern "C" int vx_scatter_cols(long nrows, const vx_c128* in, int P, const int* col_off, const int* colmap,
+                               long total_cols, vx_c128* A, long lda, void* stream) {
+  VX_REQUIRE(nrows >= 0 && P >= 1 && total_cols >= 0, "bad scatter_cols arguments");
+  const long total = nrows * total_cols;
+  if (total == 0) return VX_OK;
+  const unsigned g = div_up(total, 256) < 8192 ? div_up(total, 256) : 8192;
+  cols_copy_kernel<<<g, 256, 0, as_stream(stream)>>>(nrows, reinterpret_cast<double2*>(A), lda, P, col_off,
+                                                     colmap, const_cast<double2*>(reinterpret_cast<const double2*>(in)), 0);
+  VX_CHECK_LAUNCH("cols_copy_kernel");
+  return VX_OK;
+}
+
+extern "C" int vx_prec1_solve(int n, int nrhs, const vx_c128* factors, const int* perm, const int* items,
+                              int n_single, int n_items, const int* klist, vx_c128* Y, long s_row, long s_k,
+                              void* stream) {
+  VX_REQUIRE(n >= 1 && nrhs >= 1 && n_single >= 0 && n_items >= n_single, "bad solve arguments");
+  cudaStream_t s = as_stream(stream);
+  LuGeom g = lu_geom(n);
+  const double2* F = reinterpret_cast<const double2*>(factors);
+  double2* Yd = reinterpret_cast<double2*>(Y);
+  const bool pipe = g.nt > 1 && !g_solve_classic;
+  int st;
+  {
+    Span span("prec_solve", s);
+    if (nrhs == 1)
+      st = pipe ? launch_solve_pipe<1>(g, F, perm, items, 0, n_single, klist, 1, Yd, s_row, s_k, s)
+                : launch_solve<1, SOLVE_WARPS>(g, F, perm, items, 0, n_single, klist, 1, Yd, s_row, s_k, s);
+    else
+      st = pipe ? launch_solve_pipe<MULTI_R>(g, F, perm, items, 0, n_single, klist, nrhs, Yd, s_row, s_k, s)
+                : launch_solve<MULTI_R, SOLVE_WARPS>(g, F, perm, items, 0, n_single, klist, nrhs, Yd, s_row,
+                                                     s_k, s);
+    if (st) return st;
+  }
+  return pipe ? launch_solve_pipe<MULTI_R>(g, F, perm, items, n_single, n_items - n_single, klist, nrhs, Yd,
+                                           s_row, s_k, s)
+              : launch_solve<MULTI_R, SOLVE_WARPS>(g, F, perm, items, n_single, n_items - n_single, klist,
+                                                   nrhs, Yd, s_row, s_k, s);
 }

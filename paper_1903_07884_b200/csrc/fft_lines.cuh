@@ -61,12 +61,13 @@ struct StoreSystem {
   long pitch;                     // = nx
   long nvox;                      // = N (m is broadcast over the 3 components)
   double scale;
+  long moff = 0;                  // global index of this slice's first element (sharded runs)
   __device__ __forceinline__ long line_base(int l) const { return (long)l * pitch; }
   __device__ __forceinline__ void operator()(long b, int e, double2 v) const {
     const long i = b + e;
     v = cscale(v, scale);
     if (m) {
-      const double2 mv = __ldg(m + (i % nvox));
+      const double2 mv = __ldg(m + ((moff + i) % nvox));
       const double2 xv = __ldg(x + i);
       v = csub(xv, cmul(mv, v));
     }

@@ -165,6 +165,59 @@ extern "C" long vx_op_work_elems(int nx, int ny, int nz, int px, int py, int pz)
   return 3L * nz * px * ((long)ny + py);
 }
 
+namespace vx {
+
+// K1: forward x-DFT of nlines contiguous x-lines, zero-padded nx -> px.
+static int op_x_forward(const FftPlan& fx, int nx, int px, int nlines, const double2* X, double2* A,
+                        cudaStream_t s) {
+  LoadStrided ld{X, {nx, 0, 1, 1}};
+  StoreStrided sv{A, {px, 0, 1, 1}, 1.0};
+  return launch_fft_lines(fx, ld, sv, nlines, nx, px, false, true, s);
+}
+
+// K2-K4 on nkx x-frequency columns held as A (3, nz, ny, nkx): y-DFT (pad ny ->
+// py), z-DFT + spectral multiply + inverse z-DFT (crop nz), inverse y-DFT
+// (crop ny), result back in A.  Spectra for these columns: (6, pz, py, nkx).
+// `scale` = 1/(px py pz) of the full transform.
+static int op_yz(const FftPlan& fy, const FftPlan& fz, int ny, int nz, int nkx, int py, int pz,
+                 const double2* spectra, double2* A, double2* B, double scale, cudaStream_t s) {
+  int st;
+  const long cols = (long)py * nkx;
+  {
+    LoadStrided ld{A, {(long)ny * nkx, 1, nkx, nkx}};
+    StoreStrided sv{B, {cols, 1, nkx, nkx}, 1.0};
+    if ((st = launch_fft_lines(fy, ld, sv, 3 * nz * nkx, ny, py, false, false, s))) return st;
+  }
+  {
+    int W = 32;
+    while (W > 1 && (long)W > cols) W /= 2;
+    const size_t smem = (size_t)3 * W * fz.L * sizeof(double2);
+    int thr = fft_threads_for(fz, 3 * W);
+    auto kern = fft_max_radix(fz) <= 8 ? op_zmul_kernel<8> : op_zmul_kernel<13>;
+    if (smem > 48 * 1024)
+      VX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kern<<<div_up(cols, W), thr, smem, s>>>(fz, B, spectra, nz, cols, W, scale);
+    VX_CHECK_LAUNCH("op_zmul_kernel");
+  }
+  {
+    LoadStrided ld{B, {cols, 1, nkx, nkx}};
+    StoreStrided sv{A, {(long)ny * nkx, 1, nkx, nkx}, 1.0};
+    if ((st = launch_fft_lines(fy, ld, sv, 3 * nz * nkx, py, ny, true, false, s))) return st;
+  }
+  return VX_OK;
+}
+
+// K5: inverse x-DFT of nlines lines (global line index line0 + l), crop to nx,
+// epilogue y = x - m .* v (m indexed by the global voxel) or y = v.
+static int op_x_inverse(const FftPlan& fx, int nx, int px, int nlines, long line0, long nvox,
+                        const double2* A, const double2* X, const double2* m, double2* Y, cudaStream_t s) {
+  LoadStrided ld{A, {px, 0, 1, 1}};
+  StoreSystem sv{Y, X, m, nx, nvox, 1.0, line0 * nx};
+  return launch_fft_lines(fx, ld, sv, nlines, px, nx, true, true, s);
+}
+
+}  // namespace vx
+
 extern "C" int vx_op_apply(int nx, int ny, int nz, int px, int py, int pz, const vx_c128* spectra,
                            const vx_c128* m, const vx_c128* x, vx_c128* y, vx_c128* work,
                            void* stream) {
@@ -178,46 +231,50 @@ extern "C" int vx_op_apply(int nx, int ny, int nz, int px, int py, int pz, const
   const double2* X = reinterpret_cast<const double2*>(x);
   double2* A = reinterpret_cast<double2*>(work);
   double2* B = A + 3L * nz * ny * px;
-  const long cols = (long)py * px;
   const int lines_xyz = 3 * nz * ny;
-  // K1
-  {
-    LoadStrided ld{X, {nx, 0, 1, 1}};
-    StoreStrided sv{A, {px, 0, 1, 1}, 1.0};
-    if ((st = launch_fft_lines(fx, ld, sv, lines_xyz, nx, px, false, true, s))) return st;
-  }
-  // K2: lines (c,z) x kx, along y
-  {
-    LoadStrided ld{A, {(long)ny * px, 1, px, px}};
-    StoreStrided sv{B, {cols, 1, px, px}, 1.0};
-    if ((st = launch_fft_lines(fy, ld, sv, 3 * nz * px, ny, py, false, false, s))) return st;
-  }
-  // K3
-  {
-    int W = 32;
-    while (W > 1 && (long)W > cols) W /= 2;
-    const size_t smem = (size_t)3 * W * fz.L * sizeof(double2);
-    int thr = fft_threads_for(fz, 3 * W);
-    auto kern = fft_max_radix(fz) <= 8 ? op_zmul_kernel<8> : op_zmul_kernel<13>;
-    if (smem > 48 * 1024)
-      VX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    const double scale = 1.0 / ((double)px * py * pz);
-    kern<<<div_up(cols, W), thr, smem, s>>>(fz, B, reinterpret_cast<const double2*>(spectra), nz, cols, W,
-                                            scale);
-    VX_CHECK_LAUNCH("op_zmul_kernel");
-  }
-  // K4: inverse y, crop to ny
-  {
-    LoadStrided ld{B, {cols, 1, px, px}};
-    StoreStrided sv{A, {(long)ny * px, 1, px, px}, 1.0};
-    if ((st = launch_fft_lines(fy, ld, sv, 3 * nz * px, py, ny, true, false, s))) return st;
-  }
-  // K5: inverse x, crop to nx, operator epilogue
-  {
-    LoadStrided ld{A, {px, 0, 1, 1}};
-    StoreSystem sv{reinterpret_cast<double2*>(y), X, reinterpret_cast<const double2*>(m), nx,
-                   (long)nx * ny * nz, 1.0};
-    if ((st = launch_fft_lines(fx, ld, sv, lines_xyz, px, nx, true, true, s))) return st;
-  }
-  return VX_OK;
+  if ((st = op_x_forward(fx, nx, px, lines_xyz, X, A, s))) return st;
+  if ((st = op_yz(fy, fz, ny, nz, px, py, pz, reinterpret_cast<const double2*>(spectra), A, B,
+                  1.0 / ((double)px * py * pz), s)))
+    return st;
+  return op_x_inverse(fx, nx, px, lines_xyz, 0, (long)nx * ny * nz, A, X,
+                      reinterpret_cast<const double2*>(m), reinterpret_cast<double2*>(y), s);
+}
+
+extern "C" int vx_op_x_forward(int nx, int px, int nlines, const vx_c128* x, vx_c128* A, void* stream) {
+  VX_REQUIRE(nx >= 1 && px >= nx && nlines >= 0, "bad x-forward arguments");
+  FftPlan fx;
+  int st = fft_get_plan(px, &fx);
+  if (st) return st;
+  return op_x_forward(fx, nx, px, nlines, reinterpret_cast<const double2*>(x),
+                      reinterpret_cast<double2*>(A), as_stream(stream));
+}
+
+extern "C" long vx_op_yz_work_elems(int ny, int nz, int nkx, int py) {
+  (void)ny;
+  return 3L * nz * py * nkx;
+}
+
+extern "C" int vx_op_yz(int ny, int nz, int nkx, int px, int py, int pz, const vx_c128* spectra_local,
+                        vx_c128* A, vx_c128* work, void* stream) {
+  VX_REQUIRE(ny >= 1 && nz >= 1 && nkx >= 0, "bad yz arguments");
+  VX_REQUIRE(fft_is_smooth(py) && fft_is_smooth(pz), "padded dims must be 13-smooth");
+  if (nkx == 0) return VX_OK;
+  FftPlan fy, fz;
+  int st;
+  if ((st = fft_get_plan(py, &fy)) || (st = fft_get_plan(pz, &fz))) return st;
+  return op_yz(fy, fz, ny, nz, nkx, py, pz, reinterpret_cast<const double2*>(spectra_local),
+               reinterpret_cast<double2*>(A), reinterpret_cast<double2*>(work),
+               1.0 / ((double)px * py * pz), as_stream(stream));
+}
+
+extern "C" int vx_op_x_inverse(int nx, int ny, int nz, int px, int nlines, long line0,
+                               const vx_c128* A, const vx_c128* m, const vx_c128* x_local,
+                               vx_c128* y_local, void* stream) {
+  VX_REQUIRE(nx >= 1 && px >= nx && nlines >= 0 && line0 >= 0, "bad x-inverse arguments");
+  FftPlan fx;
+  int st = fft_get_plan(px, &fx);
+  if (st) return st;
+  return op_x_inverse(fx, nx, px, nlines, line0, (long)nx * ny * nz, reinterpret_cast<const double2*>(A),
+                      reinterpret_cast<const double2*>(x_local), reinterpret_cast<const double2*>(m),
+                      reinterpret_cast<double2*>(y_local), as_stream(stream));
 }

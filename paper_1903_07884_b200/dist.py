@@ -1,0 +1,381 @@
+"""Sharded (multi-GPU) preconditioned GMRES -- SURVEY section 8(e).
+
+One process per GPU, ``torch.distributed`` (NCCL) for the exchanges.  Every
+field vector is distributed by *lines*: the 3*ny*nz lines (c, z, y) of length nx
+(reference grid.py:1-9 layout) are split into P contiguous ranges, so a rank's
+part of a vector is one contiguous slice and every x-direction transform is
+local.  Then:
+
+* operator ``A = I - M N`` (reference operator.py:82-105): local forward
+  x-DFT of the owned lines, one all-to-all to x-frequency-column ownership
+  (contiguous kx blocks; the rank holds only its columns of the six spectra),
+  y/z transforms + spectral multiply on owned columns, all-to-all back,
+  local inverse x-DFT with the ``x - m(Nx)`` epilogue;
+* 1-level / reduced preconditioner (reference circulant.py:174-188, 264-269):
+  local x-DFT, one all-to-all to frequency ownership -- frequencies dealt
+  **cyclically** (k = s mod P) so the reduced scheme's kept modes, clustered
+  at both spectral ends, spread evenly -- local block solves against the
+  rank's factors only (1/P of the memory; the representative block replicated),
+  all-to-all back, local inverse DFT;
+* Arnoldi: classical Gram-Schmidt with partial dot products all-reduced
+  (one all-reduce for the j+2 projections + norm, one for the updated norm,
+  two more only when the reference's DGKS test fires).
+
+The GMRES control flow and Givens arithmetic are the single-GPU ones
+(``solver.GivensQR``), replicated on every rank on identical all-reduced
+scalars.  Local compute goes through a *backend*: ``CudaBackend`` calls the
+C-ABI kernels; the CPU multi-process tests (gloo) plug in a numpy backend
+from ``tests/`` to check the data movement against the oracle.
+"""
+
+from __future__ import annotations
+
+import time
+
+import numpy as np
+
+from . import _native as nv
+from .circulant import _coerce_mtilde, _select_kept
+from .errors import BreakdownError, PreconditionerBuildError
+from .solver import GivensQR, SolveReport
+
+
+def split_even(n: int, P: int) -> list:
+    return [(n * r) // P for r in range(P + 1)]
+
+
+class Layout:
+    """Ownership maps of the sharded solve (host logic, identical on every rank)."""
+
+    def __init__(self, dims, P: int, rank: int, px: int):
+        nx, ny, nz = dims
+        self.dims, self.P, self.rank, self.px = tuple(dims), P, rank, px
+        self.nlines = 3 * ny * nz
+        self.lb = split_even(self.nlines, P)
+        self.line0, self.line1 = self.lb[rank], self.lb[rank + 1]
+        self.nl = self.line1 - self.line0
+        self.nloc = self.nl * nx
+        self.kxb = split_even(px, P)
+        self.nkx = self.kxb[rank + 1] - self.kxb[rank]
+        self.kown = [np.arange(s, nx, P) for s in range(P)]
+        self.nk = self.kown[rank].size
+
+    def lines_of(self, r):
+        return self.lb[r + 1] - self.lb[r]
+
+    def op_cols(self):
+        """(col_off, colmap) packing contiguous kx blocks per destination."""
+        return np.asarray(self.kxb, np.int32), np.arange(self.px, dtype=np.int32)
+
+    def prec_cols(self):
+        off = np.cumsum([0] + [k.size for k in self.kown]).astype(np.int32)
+        return off, np.concatenate(self.kown).astype(np.int32)
+
+    def local_slice(self, full):
+        nx = self.dims[0]
+        return full[self.line0 * nx:self.line1 * nx]
+
+
+class _Comm:
+    def __init__(self, group=None):
+        import torch.distributed as dist
+
+        self.d = dist
+        self.group = group
+
+    def all_to_all(self, out, inp, out_splits, in_splits):
+        self.d.all_to_all_single(out, inp, [int(v) for v in out_splits], [int(v) for v in in_splits],
+                                 group=self.group)
+
+    def all_reduce(self, t):
+        self.d.all_reduce(t, group=self.group)
+        return t
+
+
+# ---------------------------------------------------------------- backends
+class CudaBackend:
+    """Local compute on the C-ABI kernels (product path)."""
+
+    def __init__(self):
+        self.t = nv.require_cuda()
+
+    def empty(self, shape):
+        return nv.empty_c128(shape)
+
+    def ints(self, a):
+        return self.t.from_numpy(np.ascontiguousarray(a, np.int32)).cuda()
+
+    def to_dev(self, a):
+        return nv.device_c128(a)
+
+    def spectra(self, kernel):
+        from .operator import plan_operator
+
+        return plan_operator(kernel).spectra_device
+
+    def x_forward(self, x_loc, nl, nx, px):
+        A = self.empty((nl, px))
+        nv.call("vx_op_x_forward", nx, px, nl, x_loc.data_ptr(), A.data_ptr(), nv.stream_ptr())
+        return A
+
+    def op_yz(self, A, spectra_loc, dims, nkx, px, py, pz):
+        nx, ny, nz = dims
+        work = self.empty(int(nv.query("vx_op_yz_work_elems", ny, nz, nkx, py)))
+        nv.call("vx_op_yz", ny, nz, nkx, px, py, pz, spectra_loc.data_ptr(), A.data_ptr(), work.data_ptr(),
+                nv.stream_ptr())
+
+    def x_inverse(self, A, dims, px, nl, line0, m_full, x_loc):
+        nx, ny, nz = dims
+        y = self.empty(nl * nx)
+        nv.call("vx_op_x_inverse", nx, ny, nz, px, nl, line0, A.data_ptr(), nv.ptr(m_full), x_loc.data_ptr(),
+                y.data_ptr(), nv.stream_ptr())
+        return y
+
+    def dft_lines(self, x, nl, n, inverse):
+        y = self.empty((nl, n))
+        nv.call("vx_fft_lines", n, nl, 1, x.data_ptr(), n, 0, 1, n, y.data_ptr(), n, 0, 1, n,
+                1 if inverse else 0, (1.0 / n) if inverse else 1.0, nv.stream_ptr())
+        return y
+
+    def gather_cols(self, A, nrows, lda, col_off, colmap, total):
+        out = self.empty(max(1, nrows * total))
+        nv.call("vx_gather_cols", nrows, A.data_ptr(), lda, col_off.numel() - 1, col_off.data_ptr(),
+                colmap.data_ptr(), total, out.data_ptr(), nv.stream_ptr())
+        return out
+
+    def scatter_cols(self, buf, A, nrows, lda, col_off, colmap, total):
+        nv.call("vx_scatter_cols", nrows, buf.data_ptr(), col_off.numel() - 1, col_off.data_ptr(),
+                colmap.data_ptr(), total, A.data_ptr(), lda, nv.stream_ptr())
+
+    def chan_x(self, kernel):
+        from .circulant import _lamhat_x
+        from .operator import upload_tensors
+
+        nx, ny, nz = kernel.grid.dims
+        return _lamhat_x(upload_tensors(kernel), nx, ny, nz)
+
+    def proxies(self, lam, dims, m00):
+        from .circulant import _proxies
+
+        nx, ny, nz = dims
+        return _proxies(lam, nx, ny, nz, m00).cpu().numpy()
+
+    def build_factors(self, lam, dims, m_yz, kset):
+        from .circulant import _first_bad, _lu1
+
+        nx, ny, nz = dims
+        fac, perm, piv, info = _lu1(lam, nv.device_c128(m_yz), self.ints(kset), len(kset), nx, ny, nz)
+        bad = _first_bad(info)
+        if bad >= 0:
+            raise PreconditionerBuildError(f"1-level build failed: singular frequency block k={int(kset[bad])}")
+        return fac, perm
+
+    def solve(self, Y, n, factors, perm, items, n_single, n_items, klist, s_row):
+        nv.call("vx_prec1_solve", n, 1, factors.data_ptr(), perm.data_ptr(), items.data_ptr(), n_single, n_items,
+                klist.data_ptr(), Y.data_ptr(), s_row, 1, nv.stream_ptr())
+
+    def cgs_dots(self, V, nvec, w, part):
+        out = self.empty(nvec + 1)
+        nv.call("vx_cgs_dots", w.numel(), nvec, V.data_ptr(), V.shape[1], w.data_ptr(), out.data_ptr(),
+                part.data_ptr(), nv.stream_ptr())
+        return out
+
+    def cgs_update(self, V, nvec, coef, w, part):
+        out = self.empty(1)
+        nv.call("vx_cgs_update", w.numel(), nvec, V.data_ptr(), V.shape[1], coef.data_ptr(), w.data_ptr(),
+                out.data_ptr(), part.data_ptr(), nv.stream_ptr())
+        return out
+
+    def part(self, n, nvec):
+        return self.empty(int(nv.query("vx_arnoldi_part_elems", n, nvec + 2)))
+
+    def axpby(self, a, x, b, y, out=None):
+        out = self.empty(x.numel()) if out is None else out
+        nv.call("vx_axpby", x.numel(), nv.cval(a), x.data_ptr(), nv.cval(b), nv.ptr(y), out.data_ptr(),
+                nv.stream_ptr())
+        return out
+
+    def combine(self, V, nvec, y):
+        u = self.empty(V.shape[1])
+        yd = nv.device_c128(y)
+        nv.call("vx_basis_combine", V.shape[1], nvec, V.data_ptr(), V.shape[1], yd.data_ptr(), u.data_ptr(),
+                nv.stream_ptr())
+        return u
+
+    def to_host(self, t):
+        return t.cpu().numpy()
+
+
+# ------------------------------------------------------------------ operator
+class DistOperator:
+    """Line-sharded ``A = I - M N`` (or ``N`` with m None)."""
+
+    def __init__(self, kernel, layout: Layout, backend, comm: _Comm):
+        self.L, self.B, self.C = layout, backend, comm
+        spec = backend.spectra(kernel)
+        self.pz, self.py, self.px = (int(v) for v in spec.shape[1:])
+        assert self.px == layout.px, "layout built for a different x padding"
+        k0, k1 = layout.kxb[layout.rank], layout.kxb[layout.rank + 1]
+        self.spec_loc = spec[..., k0:k1].contiguous()
+        del spec
+        off, cmap = layout.op_cols()
+        self.col_off, self.colmap = backend.ints(off), backend.ints(cmap)
+
+    def apply(self, m_full, x_loc):
+        L, B, C = self.L, self.B, self.C
+        nx, ny, nz = L.dims
+        px, nkx = self.px, L.nkx
+        A = B.x_forward(x_loc, L.nl, nx, px)
+        send = B.gather_cols(A, L.nl, px, self.col_off, self.colmap, px)
+        recv = B.empty(L.nlines * nkx)
+        C.all_to_all(recv, send[:L.nl * px],
+                     [L.lines_of(r) * nkx for r in range(L.P)],
+                     [L.nl * (L.kxb[s + 1] - L.kxb[s]) for s in range(L.P)])
+        B.op_yz(recv, self.spec_loc, L.dims, nkx, px, self.py, self.pz)
+        back = B.empty(L.nl * px)
+        C.all_to_all(back, recv,
+                     [L.nl * (L.kxb[s + 1] - L.kxb[s]) for s in range(L.P)],
+                     [L.lines_of(r) * nkx for r in range(L.P)])
+        B.scatter_cols(back, A, L.nl, px, self.col_off, self.colmap, px)
+        return B.x_inverse(A, L.dims, px, L.nl, L.line0, m_full, x_loc)
+
+
+# ------------------------------------------------------------ preconditioner
+class DistOneLevelPrec:
+    """Frequency-sharded 1-level (``tol=None``) or reduced 1-level preconditioner."""
+
+    def __init__(self, kernel, mtilde, layout: Layout, backend, comm: _Comm, tol=None, cap_bytes=2 ** 62):
+        self.L, self.B, self.C = layout, backend, comm
+        grid = kernel.grid
+        nx, ny, nz = grid.dims
+        m_yz = _coerce_mtilde(grid, mtilde)
+        q3 = 3 * ny * nz
+        self.n = q3
+        lam = backend.chan_x(kernel)
+        owned = layout.kown[layout.rank]
+        col_of = {int(k): i for i, k in enumerate(owned)}
+        if tol is None:
+            kset = owned
+            items = [(i, i, 1) for i in range(owned.size)]
+            klist = list(range(owned.size))
+            n_single = len(items)
+            self.n_stored_global = nx
+        else:
+            proxy = backend.proxies(lam, grid.dims, m_yz[0, 0])
+            kept, slot_of, rep, _ = _select_kept(proxy, nx, tol)
+            self.n_stored_global = int(kept.size)
+            keptset = set(int(k) for k in kept)
+            own_kept = [int(k) for k in owned if int(k) in keptset and int(k) != rep]
+            kset = np.asarray(own_kept + [rep], dtype=np.int64)
+            rep_local = len(own_kept)
+            items, klist = [], []
+            for s, k in enumerate(own_kept):
+                items.append((s, len(klist), 1))
+                klist.append(col_of[k])
+            n_single = len(items)
+            rep_ks = [int(k) for k in owned if int(k) not in keptset or int(k) == rep]
+            for c0 in range(0, len(rep_ks), 8):
+                chunk = rep_ks[c0:c0 + 8]
+                items.append((rep_local, len(klist), len(chunk)))
+                klist.extend(col_of[k] for k in chunk)
+        self.bytes_local = len(kset) * q3 * q3 * 16
+        self.factors, self.perm = backend.build_factors(lam, grid.dims, m_yz, np.asarray(kset))
+        del lam
+        self.items = backend.ints(np.asarray(items, np.int32).reshape(-1) if items else np.zeros(3, np.int32))
+        self.klist = backend.ints(np.asarray(klist if klist else [0], np.int32))
+        self.n_single, self.n_items = n_single, len(items)
+        off, cmap = layout.prec_cols()
+        self.col_off, self.colmap = backend.ints(off), backend.ints(cmap)
+
+    def apply(self, x_loc):
+        L, B, C = self.L, self.B, self.C
+        nx = L.dims[0]
+        S = B.dft_lines(x_loc, L.nl, nx, False)
+        send = B.gather_cols(S, L.nl, nx, self.col_off, self.colmap, nx)
+        nk = L.nk
+        recv = B.empty(max(1, L.nlines * nk))
+        C.all_to_all(recv[:L.nlines * nk], send[:L.nl * nx],
+                     [L.lines_of(r) * nk for r in range(L.P)],
+                     [L.nl * L.kown[s].size for s in range(L.P)])
+        if self.n_items:
+            B.solve(recv, self.n, self.factors, self.perm, self.items, self.n_single, self.n_items, self.klist, nk)
+        back = B.empty(max(1, L.nl * nx))
+        C.all_to_all(back[:L.nl * nx], recv[:L.nlines * nk],
+                     [L.nl * L.kown[s].size for s in range(L.P)],
+                     [L.lines_of(r) * nk for r in range(L.P)])
+        B.scatter_cols(back, S, L.nl, nx, self.col_off, self.colmap, nx)
+        return B.dft_lines(S, L.nl, nx, True).reshape(-1)
+
+
+# ------------------------------------------------------------------- GMRES
+def _norm(B, C, x, part):
+    d = B.cgs_dots(x.reshape(1, -1), 0, x, part)
+    C.all_reduce(d)
+    return float(np.sqrt(B.to_host(d)[0].real))
+
+
+def gmres_sharded(apply_a, b_loc, backend, comm: _Comm, *, apply_pinv=None, tol=1e-4, maxit=2000,
+                  restart=None):
+    """Right-preconditioned restarted GMRES on line-sharded vectors (reference
+    solver.py:114-174 control flow; see module docstring for the exchanges)."""
+    if not tol > 0:
+        raise ValueError("tol must be positive")
+    if maxit < 1:
+        raise ValueError("maxit must be >= 1")
+    B, C = backend, comm
+    t0 = time.perf_counter()
+    n = b_loc.numel()
+    mmax = maxit if restart is None else min(restart, maxit)
+    part = B.part(max(n, 1), mmax + 1)
+    bnorm = _norm(B, C, b_loc, part)
+    if bnorm == 0.0:
+        return B.axpby(0.0, b_loc, 0.0, None), SolveReport(iterations=1, residuals=[1.0, 0.0], converged=True,
+                                                           solve_seconds=time.perf_counter() - t0,
+                                                           true_residual=0.0)
+    op = apply_a if apply_pinv is None else (lambda v: apply_a(apply_pinv(v)))
+    x = B.axpby(0.0, b_loc, 0.0, None)
+    V = B.empty((mmax + 1, n))
+    residuals = [1.0]
+    total = 0
+    converged = False
+    while total < maxit and not converged:
+        r0 = B.axpby(1.0, b_loc, -1.0, apply_a(x)) if total else B.axpby(1.0, b_loc, 0.0, None)
+        beta = _norm(B, C, r0, part)
+        if beta / bnorm <= tol:
+            converged = True
+            break
+        m = maxit - total if restart is None else min(restart, maxit - total)
+        B.axpby(1.0 / beta, r0, 0.0, None, out=V[0])
+        qr = GivensQR(beta)
+        j = 0
+        lucky = False
+        while j < m:
+            w = B.axpby(1.0, op(V[j]), 0.0, None)
+            d = C.all_reduce(B.cgs_dots(V, j + 1, w, part))
+            dh = B.to_host(d)
+            h = np.empty(j + 2, np.complex128)
+            h[: j + 1] = dh[: j + 1]
+            n0 = float(np.sqrt(dh[j + 1].real))
+            n1 = float(np.sqrt(B.to_host(C.all_reduce(B.cgs_update(V, j + 1, d, w, part)))[0].real))
+            if n1 < 0.7071 * n0:  # DGKS second pass (reference solver.py:69-73)
+                c = C.all_reduce(B.cgs_dots(V, j + 1, w, part))
+                h[: j + 1] += B.to_host(c)[: j + 1]
+                n1 = float(np.sqrt(B.to_host(C.all_reduce(B.cgs_update(V, j + 1, c, w, part)))[0].real))
+            h[j + 1] = n1
+            lucky = n1 <= 1e-14 * max(n0, 1e-300)
+            B.axpby(1.0 / n1 if n1 > 0 else 0.0, w, 0.0, None, out=V[j + 1])
+            qr.add_column(h, j, residuals, tol)
+            j += 1
+            est = abs(qr.g[j]) / bnorm
+            residuals.append(float(est))
+            if est <= tol or lucky:
+                converged = est <= tol
+                if lucky and not converged:
+                    raise BreakdownError(f"Arnoldi breakdown at iteration {len(residuals) - 1}")
+                break
+        total += j
+        u = B.combine(V, j, qr.solve(j))
+        x = B.axpby(1.0, x, 1.0, u if apply_pinv is None else apply_pinv(u))
+    true_res = _norm(B, C, B.axpby(1.0, b_loc, -1.0, apply_a(x)), part) / bnorm
+    return x, SolveReport(iterations=int(total), residuals=residuals, converged=bool(converged),
+                          solve_seconds=time.perf_counter() - t0, true_residual=float(true_res))

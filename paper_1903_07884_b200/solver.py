@@ -139,13 +139,47 @@ def _aliases(a, b) -> bool:
     return sb <= sa < sb + b.numel() * b.element_size()
 
 
+class GivensQR:
+    """Host-side complex Givens QR of the Arnoldi Hessenberg matrix, exactly
+    the reference's arithmetic (solver.py:78-110); shared by the single-GPU and
+    the sharded GMRES."""
+
+    def __init__(self, beta: float):
+        self.g = [np.complex128(beta + 0.0j)]
+        self.cs, self.sn, self.r_cols = [], [], []
+
+    def add_column(self, h: np.ndarray, j: int, residuals: list, tol: float) -> None:
+        cs, sn = self.cs, self.sn
+        for i in range(j):
+            hi = h[i]
+            h[i] = np.conj(cs[i]) * hi + np.conj(sn[i]) * h[i + 1]
+            h[i + 1] = -sn[i] * hi + cs[i] * h[i + 1]
+        denom = np.hypot(abs(h[j]), abs(h[j + 1]))
+        if denom == 0.0:
+            raise BreakdownError(
+                f"GMRES stalled at iteration {len(residuals)}: zero Hessenberg "
+                f"column with relative residual {residuals[-1]:.3e} above tol {tol:.3e}")
+        c, s = h[j] / denom, h[j + 1] / denom
+        cs.append(c)
+        sn.append(s)
+        h[j] = np.conj(c) * h[j] + np.conj(s) * h[j + 1]
+        self.r_cols.append(h[: j + 1].copy())
+        self.g.append(-s * self.g[j])
+        self.g[j] = np.conj(c) * self.g[j]
+
+    def solve(self, j: int) -> np.ndarray:
+        r_mat = np.zeros((j, j), dtype=np.complex128)
+        for col, vals in enumerate(self.r_cols[:j]):
+            r_mat[: col + 1, col] = vals
+        return np.linalg.solve(r_mat, np.asarray(self.g[:j], dtype=np.complex128))
+
+
 def _gmres_cycle(K: _Krylov, op, r0, beta, bnorm, tol, m, residuals):
     """One Arnoldi/Givens cycle (reference solver.py:45-111)."""
     t = K.t
     K.row(0)
     K.axpby(1.0 / beta, r0, 0.0, None, out=K.V[0])
-    r_cols, cs, sn = [], [], []
-    g = [np.complex128(beta + 0.0j)]
+    qr = GivensQR(beta)
     converged = lucky = False
     j = 0
     while j < m:
@@ -161,24 +195,9 @@ def _gmres_cycle(K: _Krylov, op, r0, beta, bnorm, tol, m, residuals):
         h = K.h_host[: j + 2].numpy().copy()
         norm_before = float(K.s_host[0])
         lucky = h[j + 1].real <= 1e-14 * max(norm_before, 1e-300)
-        for i in range(j):
-            hi = h[i]
-            h[i] = np.conj(cs[i]) * hi + np.conj(sn[i]) * h[i + 1]
-            h[i + 1] = -sn[i] * hi + cs[i] * h[i + 1]
-        denom = np.hypot(abs(h[j]), abs(h[j + 1]))
-        if denom == 0.0:
-            raise BreakdownError(
-                f"GMRES stalled at iteration {len(residuals)}: zero Hessenberg "
-                f"column with relative residual {residuals[-1]:.3e} above tol {tol:.3e}")
-        c, s = h[j] / denom, h[j + 1] / denom
-        cs.append(c)
-        sn.append(s)
-        h[j] = np.conj(c) * h[j] + np.conj(s) * h[j + 1]
-        r_cols.append(h[: j + 1].copy())
-        g.append(-s * g[j])
-        g[j] = np.conj(c) * g[j]
+        qr.add_column(h, j, residuals, tol)
         j += 1
-        est = abs(g[j]) / bnorm
+        est = abs(qr.g[j]) / bnorm
         residuals.append(float(est))
         if est <= tol or lucky:
             converged = est <= tol
@@ -187,10 +206,7 @@ def _gmres_cycle(K: _Krylov, op, r0, beta, bnorm, tol, m, residuals):
                     f"Arnoldi breakdown at iteration {len(residuals) - 1} with "
                     f"relative residual {est:.3e} above tol {tol:.3e}")
             break
-    r_mat = np.zeros((j, j), dtype=np.complex128)
-    for col, vals in enumerate(r_cols):
-        r_mat[: col + 1, col] = vals
-    y = np.linalg.solve(r_mat, np.asarray(g[:j], dtype=np.complex128))
+    y = qr.solve(j)
     yd = nv.device_c128(y)
     u = nv.empty_c128(K.n)
     nv.call("vx_basis_combine", K.n, j, K.V.data_ptr(), K.n, yd.data_ptr(), u.data_ptr(), nv.stream_ptr())

@@ -1,0 +1,90 @@
+"""GPU: the sharded-solve CUDA backend on a single-rank NCCL group (the
+multi-rank data movement is covered on CPU by test_dist_gloo.py), and the
+all-to-all pack/unpack kernels with P > 1 maps against numpy."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+
+import voxvie_oracle as O
+from conftest import random_field, relerr
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def group():
+    import torch
+    import torch.distributed as dist
+
+    if not dist.is_initialized():
+        s = socket.socket()
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+        s.close()
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        torch.cuda.set_device(0)
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    yield None
+    if dist.is_initialized():
+        dist.destroy_process_group()
+
+
+def test_gather_scatter_cols_p3(rng):
+    import torch
+
+    from paper_1903_07884_b200 import _native as nv
+
+    nrows, lda = 7, 23
+    a = random_field(rng, nrows * lda).reshape(nrows, lda)
+    kown = [np.arange(s, lda, 3) for s in range(3)]
+    off = np.cumsum([0] + [k.size for k in kown]).astype(np.int32)
+    cmap = np.concatenate(kown).astype(np.int32)
+    A = torch.from_numpy(a.copy()).cuda()
+    out = nv.empty_c128(nrows * lda)
+    d_off, d_map = torch.from_numpy(off).cuda(), torch.from_numpy(cmap).cuda()
+    nv.call("vx_gather_cols", nrows, A.data_ptr(), lda, 3, d_off.data_ptr(), d_map.data_ptr(), lda,
+            out.data_ptr(), nv.stream_ptr())
+    ref = np.concatenate([a[:, k].reshape(-1) for k in kown])
+    assert np.array_equal(out.cpu().numpy(), ref)
+    B = torch.zeros_like(A)
+    nv.call("vx_scatter_cols", nrows, out.data_ptr(), 3, d_off.data_ptr(), d_map.data_ptr(), lda,
+            B.data_ptr(), lda, nv.stream_ptr())
+    assert np.array_equal(B.cpu().numpy(), a)
+
+
+@pytest.mark.parametrize("tol", [None, 1e-3])
+def test_sharded_path_single_rank_matches(group, tol):
+    import torch
+
+    from paper_1903_07884_b200 import workloads
+    from paper_1903_07884_b200.dist import CudaBackend, DistOneLevelPrec, DistOperator, Layout, _Comm, gmres_sharded
+    from paper_1903_07884_b200.operator import padded_length
+
+    W = workloads.small(60, 8, 5, delta=0.03e-6)
+    kern = W.kernel()
+    dims = W.grid.dims
+    B, C = CudaBackend(), _Comm()
+    L = Layout(dims, 1, 0, padded_length(dims[0]))
+    op = DistOperator(kern, L, B, C)
+    prec = DistOneLevelPrec(kern, W.mtilde(), L, B, C, tol=tol)
+    m = torch.from_numpy(W.m.reshape(-1).copy()).cuda()
+    rng = np.random.default_rng(3)
+    x = random_field(rng, W.grid.n_unknowns)
+    xd = torch.from_numpy(x).cuda()
+    spec = O.plan_spectra(kern.tensors, dims)
+    p = O.build_one_level(kern.tensors, dims, W.mtilde())
+    if tol is not None:
+        p = O.reduce_one_level(p, tol)
+    assert relerr(op.apply(m, xd).cpu().numpy(), O.apply_system(spec, dims, W.m, x)) < 1e-12
+    assert relerr(prec.apply(xd).cpu().numpy(), O.apply_prec(p, x)) < 1e-10
+    b = torch.from_numpy(W.b.copy()).cuda()
+    xs, rep = gmres_sharded(lambda v: op.apply(m, v), b, B, C, apply_pinv=prec.apply, tol=1e-8, maxit=300,
+                            restart=20)
+    xo, ro = O.gmres(lambda v: O.apply_system(spec, dims, W.m, v), W.b,
+                     apply_pinv=lambda v: O.apply_prec(p, v), tol=1e-8, maxit=300, restart=20)
+    assert abs(rep.iterations - ro["iterations"]) <= 2
+    assert relerr(xs.cpu().numpy(), xo) < 1e-6
