@@ -19,6 +19,24 @@ namespace vx {
 
 constexpr int FFT_MAX_STAGES = 24;
 
+// Division by a runtime-invariant divisor with one multiply-high (the stage
+// loops would otherwise spend most of their issue slots in integer division).
+// Valid for numerators < 2^31.
+struct FastDiv {
+  unsigned d, mul, shr;
+  __host__ __device__ FastDiv() : d(1), mul(0), shr(0) {}
+  __host__ explicit FastDiv(unsigned dv) : d(dv) {
+    unsigned l = 0;
+    while ((1ull << l) < dv) ++l;
+    shr = l;
+    mul = (unsigned)(((1ull << 32) * ((1ull << l) - dv)) / dv + 1);
+  }
+  __device__ __forceinline__ unsigned div(unsigned n) const {
+    const unsigned long long t = (unsigned long long)__umulhi(n, mul) + n;
+    return (unsigned)(t >> shr);
+  }
+};
+
 struct FftPlan {
   int n;          // DFT length
   int L;          // executed length: n (direct) or M (Bluestein)
@@ -30,6 +48,11 @@ struct FftPlan {
   const int* k_of;          // [L]  frequency held at smem position pos after the DIF
   const double2* chirp;     // [n]  exp(-pi i j^2 / n)                 (Bluestein)
   const double2* bhat_rev;  // [L]  FFT_L(conj chirp, wrapped)/L at DIF positions
+  const double2* tw_hi;     // [nhi] exp(-2 pi i 64 a / L)   (two-level twiddles:
+  const double2* tw_lo;     // [64]  exp(-2 pi i b / L)       w^t = hi[t>>6] * lo[t&63])
+  int nhi;
+  FastDiv fd_m[FFT_MAX_STAGES];   // butterfly span m of stage st (DIF order)
+  FastDiv fd_nb[FFT_MAX_STAGES];  // butterflies per line L / R_st
 };
 
 // Host: cached plan for length n on the current device (thread-safe).
@@ -169,28 +192,34 @@ __device__ __forceinline__ void dft_codelet(double2* v, double sgn) {
 //   pair DIF -> pointwise -> DIT needs no permutation at all).
 // Butterfly enumeration: line fastest for interleaved smem (lde != 1), butterfly
 // fastest for line-contiguous smem.
+// twiddle w_L^t from the two-level tables staged in shared memory
+__device__ __forceinline__ double2 tw_get(const double2* twsm, int t) {
+  return cmul(twsm[64 + (t >> 6)], twsm[t & 63]);
+}
+
 template <int R, bool DIT>
-__device__ __forceinline__ void fft_stage(double2* s, SmemLay lay, int W, int n, int m,
+__device__ __forceinline__ void fft_stage(double2* s, SmemLay lay, int W, const FastDiv& fdW, int n, int m,
+                                          const FastDiv& fdm, const FastDiv& fdnb,
                                           const double2* __restrict__ tw, double sgn) {
   const int nb = n / R;
   const int total = nb * W;
   const int blockL = m * R;
   const int tws = n / blockL;  // twiddle table stride for w_{blockL}
   const bool bfast = (lay.lde == 1);
+  const int st = m * lay.lde;
   for (int b = threadIdx.x; b < total; b += blockDim.x) {
     int w, f;
-    if (bfast) { w = b / nb; f = b - w * nb; }
-    else       { f = b / W;  w = b - f * W; }
-    const int blk = f / m, j = f - blk * m;
+    if (bfast) { w = (int)fdnb.div(b); f = b - w * nb; }
+    else       { f = (int)fdW.div(b);  w = b - f * W; }
+    const int blk = (int)fdm.div(f), j = f - blk * m;
     double2* q = s + w * lay.ldw + (blk * blockL + j) * lay.lde;
-    const int st = m * lay.lde;
     double2 v[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) v[r] = q[r * st];
     if (DIT && j) {
 #pragma unroll
       for (int r = 1; r < R; ++r) {
-        double2 t = __ldg(tw + j * r * tws);
+        double2 t = tw_get(tw, j * r * tws);
         t.y *= -sgn;
         v[r] = cmul(v[r], t);
       }
@@ -199,7 +228,7 @@ __device__ __forceinline__ void fft_stage(double2* s, SmemLay lay, int W, int n,
     if (!DIT && j) {
 #pragma unroll
       for (int r = 1; r < R; ++r) {
-        double2 t = __ldg(tw + j * r * tws);
+        double2 t = tw_get(tw, j * r * tws);
         t.y *= -sgn;
         v[r] = cmul(v[r], t);
       }
@@ -211,40 +240,52 @@ __device__ __forceinline__ void fft_stage(double2* s, SmemLay lay, int W, int n,
 }
 
 template <bool DIT, int RMAX>
-__device__ __forceinline__ void fft_one_stage(int R, double2* s, SmemLay lay, int W, int n, int m,
-                                              const double2* tw, double sgn) {
-  switch (R) {
-    case 2: fft_stage<2, DIT>(s, lay, W, n, m, tw, sgn); break;
-    case 4: fft_stage<4, DIT>(s, lay, W, n, m, tw, sgn); break;
-    case 8: fft_stage<8, DIT>(s, lay, W, n, m, tw, sgn); break;
-    case 3: fft_stage<3, DIT>(s, lay, W, n, m, tw, sgn); break;
-    case 5: fft_stage<5, DIT>(s, lay, W, n, m, tw, sgn); break;
-    case 7: fft_stage<7, DIT>(s, lay, W, n, m, tw, sgn); break;
+__device__ __forceinline__ void fft_one_stage(int st, const FftPlan& p, const double2* twsm, double2* s,
+                                              SmemLay lay, int W, const FastDiv& fdW, int m, double sgn) {
+  const int n = p.L;
+  const FastDiv& fm = p.fd_m[st];
+  const FastDiv& fnb = p.fd_nb[st];
+  switch (p.radix[st]) {
+    case 2: fft_stage<2, DIT>(s, lay, W, fdW, n, m, fm, fnb, twsm, sgn); break;
+    case 4: fft_stage<4, DIT>(s, lay, W, fdW, n, m, fm, fnb, twsm, sgn); break;
+    case 8: fft_stage<8, DIT>(s, lay, W, fdW, n, m, fm, fnb, twsm, sgn); break;
+    case 3: fft_stage<3, DIT>(s, lay, W, fdW, n, m, fm, fnb, twsm, sgn); break;
+    case 5: fft_stage<5, DIT>(s, lay, W, fdW, n, m, fm, fnb, twsm, sgn); break;
+    case 7: fft_stage<7, DIT>(s, lay, W, fdW, n, m, fm, fnb, twsm, sgn); break;
     default:
       if constexpr (RMAX >= 11) {
-        if (R == 11) fft_stage<11, DIT>(s, lay, W, n, m, tw, sgn);
-        else if (R == 13) fft_stage<13, DIT>(s, lay, W, n, m, tw, sgn);
+        if (p.radix[st] == 11) fft_stage<11, DIT>(s, lay, W, fdW, n, m, fm, fnb, twsm, sgn);
+        else if (p.radix[st] == 13) fft_stage<13, DIT>(s, lay, W, fdW, n, m, fm, fnb, twsm, sgn);
       }
       break;
   }
 }
 
 // natural -> digit-reversed
+// Stage the two-level twiddle tables of a plan into shared memory (64 + nhi
+// entries); must be followed by a barrier before the transform.
+__device__ __forceinline__ void fft_load_twiddles(const FftPlan& p, double2* twsm) {
+  for (int i = threadIdx.x; i < 64 + p.nhi; i += blockDim.x)
+    twsm[i] = i < 64 ? __ldg(p.tw_lo + i) : __ldg(p.tw_hi + (i - 64));
+}
+
 template <int RMAX = 13>
-__device__ __forceinline__ void fft_dif(double2* s, SmemLay lay, int W, const FftPlan& p, double sgn) {
+__device__ __forceinline__ void fft_dif(double2* s, SmemLay lay, int W, const FastDiv& fdW, const FftPlan& p,
+                                        const double2* twsm, double sgn) {
   int m = p.L;
   for (int st = 0; st < p.nst; ++st) {
     m /= p.radix[st];
-    fft_one_stage<false, RMAX>(p.radix[st], s, lay, W, p.L, m, p.tw, sgn);
+    fft_one_stage<false, RMAX>(st, p, twsm, s, lay, W, fdW, m, sgn);
   }
 }
 
 // digit-reversed -> natural
 template <int RMAX = 13>
-__device__ __forceinline__ void fft_dit(double2* s, SmemLay lay, int W, const FftPlan& p, double sgn) {
+__device__ __forceinline__ void fft_dit(double2* s, SmemLay lay, int W, const FastDiv& fdW, const FftPlan& p,
+                                        const double2* twsm, double sgn) {
   int m = 1;
   for (int st = p.nst - 1; st >= 0; --st) {
-    fft_one_stage<true, RMAX>(p.radix[st], s, lay, W, p.L, m, p.tw, sgn);
+    fft_one_stage<true, RMAX>(st, p, twsm, s, lay, W, fdW, m, sgn);
     m *= p.radix[st];
   }
 }
@@ -266,12 +307,13 @@ __device__ __forceinline__ double2 fft_post(const FftPlan& p, int e, double2 v, 
 // padded to L).  Afterwards output element e of a line sits at smem position
 // fft_out_pos(p, e) (digit-reversed for direct plans, natural for Bluestein).
 template <int RMAX = 13>
-__device__ __forceinline__ void fft_exec(double2* s, SmemLay lay, int W, const FftPlan& p, bool inv) {
+__device__ __forceinline__ void fft_exec(double2* s, SmemLay lay, int W, const FastDiv& fdW, const FftPlan& p,
+                                         const double2* twsm, bool inv) {
   if (!p.bluestein) {
-    fft_dif<RMAX>(s, lay, W, p, inv ? 1.0 : -1.0);
+    fft_dif<RMAX>(s, lay, W, fdW, p, twsm, inv ? 1.0 : -1.0);
     return;
   }
-  fft_dif<RMAX>(s, lay, W, p, -1.0);
+  fft_dif<RMAX>(s, lay, W, fdW, p, twsm, -1.0);
   const int total = W * p.L;
   for (int i = threadIdx.x; i < total; i += blockDim.x) {
     int w, e;
@@ -281,7 +323,7 @@ __device__ __forceinline__ void fft_exec(double2* s, SmemLay lay, int W, const F
     *q = cmul(*q, __ldg(p.bhat_rev + e));
   }
   __syncthreads();
-  fft_dit<RMAX>(s, lay, W, p, 1.0);
+  fft_dit<RMAX>(s, lay, W, fdW, p, twsm, 1.0);
 }
 
 // largest radix of a plan (host and device)

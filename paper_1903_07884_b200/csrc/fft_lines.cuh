@@ -79,11 +79,13 @@ struct StoreSystem {
 // two 512-thread CTAs per SM) or 13 (adds the 11/13 codelets).
 template <class Loader, class Storer, int RMAX>
 __global__ void __launch_bounds__(512, (RMAX <= 8 ? 2 : 1))
-    fft_lines_kernel(FftPlan p, Loader ld, Storer st, int n_lines, int W, int n_in, int n_out, int inv,
-                     int contig) {
+    fft_lines_kernel(FftPlan p, Loader ld, Storer st, int n_lines, int W, FastDiv fdW, int n_in, int n_out,
+                     int inv, int contig) {
   extern __shared__ double2 smem[];
-  long* lbase_in = reinterpret_cast<long*>(smem + (size_t)W * p.L);
+  double2* twsm = smem + (size_t)W * p.L;
+  long* lbase_in = reinterpret_cast<long*>(twsm + 64 + p.nhi);
   long* lbase_out = lbase_in + W;
+  fft_load_twiddles(p, twsm);
   const int l0 = blockIdx.x * W;
   const int L = p.L;
   SmemLay lay = contig ? SmemLay{1, L} : SmemLay{W, 1};
@@ -94,16 +96,30 @@ __global__ void __launch_bounds__(512, (RMAX <= 8 ? 2 : 1))
   }
   __syncthreads();
   const int total = W * L;
-  for (int i = threadIdx.x; i < total; i += blockDim.x) {
-    int w, e;
-    if (contig) { w = i / L; e = i - w * L; }
-    else        { e = i / W; w = i - e * W; }
-    double2 v = cmk(0.0, 0.0);
-    if (e < n_in && l0 + w < n_lines) v = fft_pre(p, e, ld(lbase_in[w], e), inv);
-    smem[w * lay.ldw + e * lay.lde] = v;
+  // 4 independent global loads in flight per thread before their smem stores
+  constexpr int U = 4;
+  for (int i0 = threadIdx.x; i0 < total; i0 += U * blockDim.x) {
+    double2 v[U];
+    int pos[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int i = i0 + u * blockDim.x;
+      pos[u] = -1;
+      v[u] = cmk(0.0, 0.0);
+      if (i < total) {
+        int w, e;
+        if (contig) { w = i / L; e = i - w * L; }
+        else        { e = i / W; w = i - e * W; }
+        pos[u] = w * lay.ldw + e * lay.lde;
+        if (e < n_in && l0 + w < n_lines) v[u] = fft_pre(p, e, ld(lbase_in[w], e), inv);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (pos[u] >= 0) smem[pos[u]] = v[u];
   }
   __syncthreads();
-  fft_exec<RMAX>(smem, lay, W, p, inv);
+  fft_exec<RMAX>(smem, lay, W, fdW, p, twsm, inv);
   const int tot_out = W * n_out;
   for (int i = threadIdx.x; i < tot_out; i += blockDim.x) {
     int w, e;
@@ -120,19 +136,27 @@ struct LineLaunch {
   size_t smem;
 };
 
+inline int env_int(const char* name, int dflt) {
+  const char* v = getenv(name);
+  return v ? atoi(v) : dflt;
+}
+
 inline int pick_line_launch(const FftPlan& p, bool contig, int n_lines, LineLaunch* out) {
   const int budget = device_smem_optin() - 1024;
+  static const int contig_elems = env_int("VX_FFT_CONTIG_ELEMS", 4096);
+  static const int strided_w = env_int("VX_FFT_STRIDED_W", 16);
+  static const int strided_kb = env_int("VX_FFT_STRIDED_KB", 96);
   int W;
   if (contig) {
-    W = (int)(4096 / p.L);  // ~64 KB of data per CTA
+    W = (int)(contig_elems / p.L);  // ~64 KB of data per CTA
     if (W < 1) W = 1;
   } else {
-    W = 16;
-    while (W > 1 && (size_t)W * p.L * sizeof(double2) > 96 * 1024) W /= 2;
+    W = strided_w;
+    while (W > 1 && (size_t)W * p.L * sizeof(double2) > (size_t)strided_kb * 1024) W /= 2;
   }
   if (W > n_lines) W = n_lines > 0 ? n_lines : 1;
   for (;;) {
-    size_t smem = (size_t)W * p.L * sizeof(double2) + 2 * W * sizeof(long);
+    size_t smem = ((size_t)W * p.L + 64 + p.nhi) * sizeof(double2) + 2 * W * sizeof(long);
     int thr = fft_threads_for(p, W);
     if (smem <= (size_t)budget) {
       out->W = W;
@@ -158,8 +182,8 @@ int launch_fft_lines(const FftPlan& p, const Loader& ld, const Storer& st, int n
                                     : fft_lines_kernel<Loader, Storer, 13>;
   if (ll.smem > 48 * 1024)
     VX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ll.smem));
-  kern<<<div_up(n_lines, ll.W), ll.threads, ll.smem, stream>>>(p, ld, st, n_lines, ll.W, n_in,
-                                                                n_out, inv ? 1 : 0, contig ? 1 : 0);
+  kern<<<div_up(n_lines, ll.W), ll.threads, ll.smem, stream>>>(p, ld, st, n_lines, ll.W, FastDiv(ll.W),
+                                                                n_in, n_out, inv ? 1 : 0, contig ? 1 : 0);
   VX_CHECK_LAUNCH("fft_lines_kernel");
   return VX_OK;
 }

@@ -147,8 +147,30 @@ int fft_get_plan(int n, FftPlan* out) {
   VX_REQUIRE((int)f.size() <= FFT_MAX_STAGES, "FFT length %d needs too many stages", n);
   p.nst = (int)f.size();
   for (int i = 0; i < p.nst; ++i) p.radix[i] = f[i];
+  {
+    int m = p.L;
+    for (int i = 0; i < p.nst; ++i) {
+      m /= p.radix[i];
+      p.fd_m[i] = FastDiv((unsigned)m);
+      p.fd_nb[i] = FastDiv((unsigned)(p.L / p.radix[i]));
+    }
+  }
   int st = upload(roots(p.L), &p.tw);
   if (st) return st;
+  {
+    const long double two_pi = 6.283185307179586476925286766559005768L;
+    p.nhi = (p.L + 63) / 64;
+    std::vector<double2> hi(p.nhi), lo(64);
+    for (int a = 0; a < p.nhi; ++a) {
+      long double ang = two_pi * (long double)(64L * a) / (long double)p.L;
+      hi[a] = make_double2((double)cosl(ang), (double)-sinl(ang));
+    }
+    for (int b = 0; b < 64; ++b) {
+      long double ang = two_pi * (long double)b / (long double)p.L;
+      lo[b] = make_double2((double)cosl(ang), (double)-sinl(ang));
+    }
+    if ((st = upload(hi, &p.tw_hi)) || (st = upload(lo, &p.tw_lo))) return st;
+  }
   // digit-reversal maps of the DIF with this radix sequence
   std::vector<int> pos_of(p.L), k_of(p.L);
   for (int k = 0; k < p.L; ++k) {

@@ -47,12 +47,14 @@ __constant__ int c_pair_of[9] = {0, 1, 2, 1, 3, 4, 2, 4, 5};
 template <int RMAX>
 __global__ void __launch_bounds__(512, (RMAX <= 8 ? 2 : 1))
     op_zmul_kernel(FftPlan pzp, double2* __restrict__ B, const double2* __restrict__ S, int nz, long cols,
-                   int W, double scale) {
+                   int W, FastDiv fdW3, double scale) {
   extern __shared__ double2 smem[];
   const int Pz = pzp.L;
   const int W3 = 3 * W;
   const long col0 = (long)blockIdx.x * W;
   SmemLay lay{W3, 1};
+  double2* twsm = smem + (size_t)Pz * W3;
+  fft_load_twiddles(pzp, twsm);
   for (int i = threadIdx.x; i < Pz * W3; i += blockDim.x) {
     const int e = i / W3, lw = i - e * W3;
     const int c = lw / W, w = lw - c * W;
@@ -62,7 +64,7 @@ __global__ void __launch_bounds__(512, (RMAX <= 8 ? 2 : 1))
     smem[lw + e * W3] = v;
   }
   __syncthreads();
-  fft_dif<RMAX>(smem, lay, W3, pzp, -1.0);  // natural -> digit-reversed positions
+  fft_dif<RMAX>(smem, lay, W3, fdW3, pzp, twsm, -1.0);  // natural -> digit-reversed positions
   for (int i = threadIdx.x; i < Pz * W; i += blockDim.x) {
     const int e = i / W, w = i - e * W;  // e = smem position
     const long col = col0 + w;
@@ -83,7 +85,7 @@ __global__ void __launch_bounds__(512, (RMAX <= 8 ? 2 : 1))
     }
   }
   __syncthreads();
-  fft_dit<RMAX>(smem, lay, W3, pzp, 1.0);  // digit-reversed -> natural
+  fft_dit<RMAX>(smem, lay, W3, fdW3, pzp, twsm, 1.0);  // digit-reversed -> natural
   for (int i = threadIdx.x; i < nz * W3; i += blockDim.x) {
     const int e = i / W3, lw = i - e * W3;
     const int c = lw / W, w = lw - c * W;
@@ -189,14 +191,15 @@ static int op_yz(const FftPlan& fy, const FftPlan& fz, int ny, int nz, int nkx, 
     if ((st = launch_fft_lines(fy, ld, sv, 3 * nz * nkx, ny, py, false, false, s))) return st;
   }
   {
-    int W = 32;
+    static const int zw = env_int("VX_ZMUL_W", 64);
+    int W = zw;
     while (W > 1 && (long)W > cols) W /= 2;
-    const size_t smem = (size_t)3 * W * fz.L * sizeof(double2);
+    const size_t smem = ((size_t)3 * W * fz.L + 64 + fz.nhi) * sizeof(double2);
     int thr = fft_threads_for(fz, 3 * W);
     auto kern = fft_max_radix(fz) <= 8 ? op_zmul_kernel<8> : op_zmul_kernel<13>;
     if (smem > 48 * 1024)
       VX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    kern<<<div_up(cols, W), thr, smem, s>>>(fz, B, spectra, nz, cols, W, scale);
+    kern<<<div_up(cols, W), thr, smem, s>>>(fz, B, spectra, nz, cols, W, FastDiv(3 * W), scale);
     VX_CHECK_LAUNCH("op_zmul_kernel");
   }
   {

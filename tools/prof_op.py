@@ -28,11 +28,15 @@ m = torch.from_numpy(W.m.reshape(-1).copy()).cuda()
 x = torch.from_numpy(W.b.copy()).cuda()
 prec = build_one_level(kern, W.mtilde(), cap_bytes=2 ** 62) if a.apply in ("prec", "both") else None
 torch.cuda.synchronize()
-t0 = time.perf_counter()
+for _ in range(2):
+    y = apply_device(plan, m, x)
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e0.record()
 for _ in range(a.reps):
     if a.apply in ("op", "both"):
         y = apply_device(plan, m, x)
     if prec is not None:
         y = prec._apply_dev(x.reshape(-1, 1), 1)
+e1.record()
 torch.cuda.synchronize()
-print(f"{a.reps} reps in {(time.perf_counter() - t0) * 1e3:.2f} ms")
+print(f"{a.config} {a.apply}: {e0.elapsed_time(e1) / a.reps:.3f} ms per apply")
