@@ -717,24 +717,61 @@ __global__ void __launch_bounds__((PIPE_CONSUMERS + 1) * 32)
         // only the owner q % NWC computes).  The empty barriers count NWC
         // arrivals, so no slot can be refilled before all consumers passed
         // it: parity waits are never more than one phase ahead.
+        // Multi-RHS blocks (R = 8, T = 32): the tile GEMV becomes a 32x32 by
+        // 32x8 complex product on the FP64 tensor cores (DMMA), fragments
+        // straight from the ring slot and the RHS block in shared memory.
+        constexpr bool USE_DMMA = (R == 8);
+        const bool dmma = USE_DMMA && T == 32;
+        double cr[4][2], ci[4][2];
+#pragma unroll
+        for (int rb = 0; rb < 4; ++rb) cr[rb][0] = cr[rb][1] = ci[rb][0] = ci[rb][1] = 0.0;
         for (int q = 0; q < noff; ++q) {
           const long tq = t + q;
           const int s = (int)(tq % S);
           mbar_wait(full + s, (uint32_t)(tq / S) & 1);
-          if (q % NWC == warp && lane < T) {
-            const double2* tile = slots + (long)s * T2 + lane;
-            const double2* yj = y + (long)(j0 + q) * T * R;
-#pragma unroll 4
-            for (int c = 0; c < T; ++c) {
-              const double2 a = tile[c * T];
+          if (q % NWC == warp) {
+            if (dmma) {
+              if constexpr (USE_DMMA) {
+                const double2* tile = slots + (long)s * T2;
+                const double2* yj = y + (long)(j0 + q) * 32 * R;
+                const int r4 = lane >> 2, c4 = lane & 3;
+#pragma unroll 2
+                for (int k0 = 0; k0 < 32; k0 += 4) {
+                  const double2 b = yj[(k0 + c4) * R + r4];   // B[k][col]: row k0+c4, col r4
 #pragma unroll
-              for (int rr = 0; rr < R; ++rr) cfma(acc[rr], a, yj[c * R + rr]);
+                  for (int rb = 0; rb < 4; ++rb) {
+                    const double2 a = tile[(k0 + c4) * 32 + rb * 8 + r4];  // A[row][k]
+                    dmma884(cr[rb][0], cr[rb][1], a.x, b.x);
+                    dmma884(cr[rb][0], cr[rb][1], -a.y, b.y);
+                    dmma884(ci[rb][0], ci[rb][1], a.x, b.y);
+                    dmma884(ci[rb][0], ci[rb][1], a.y, b.x);
+                  }
+                }
+              }
+            } else if (lane < T) {
+              const double2* tile = slots + (long)s * T2 + lane;
+              const double2* yj = y + (long)(j0 + q) * T * R;
+#pragma unroll 4
+              for (int c = 0; c < T; ++c) {
+                const double2 a = tile[c * T];
+#pragma unroll
+                for (int rr = 0; rr < R; ++rr) cfma(acc[rr], a, yj[c * R + rr]);
+              }
             }
           }
           __syncwarp();
           if (lane == 0) mbar_arrive(empty + s);
         }
-        if (lane < T) {
+        if (dmma) {
+          if constexpr (USE_DMMA) {
+            const int r4 = lane >> 2, c4 = lane & 3;
+#pragma unroll
+            for (int rb = 0; rb < 4; ++rb)
+#pragma unroll
+              for (int e = 0; e < 2; ++e)
+                red[(warp * 32 + rb * 8 + r4) * R + 2 * c4 + e] = cmk(cr[rb][e], ci[rb][e]);
+          }
+        } else if (lane < T) {
 #pragma unroll
           for (int rr = 0; rr < R; ++rr) red[(warp * T + lane) * R + rr] = acc[rr];
         }
