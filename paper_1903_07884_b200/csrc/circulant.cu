@@ -814,6 +814,70 @@ __global__ void __launch_bounds__((PIPE_CONSUMERS + 1) * 32)
   }
 }
 
+// ------------------------------------------------------ single-tile blocks
+// n <= 32 (the 2-level scheme's (3nz)^2 blocks): one warp per work item, lane
+// = row; the packed diagonal tile holds inv(L) below and inv(U) on/above the
+// diagonal, so a solve is two warp-shuffle triangular products.  8 items per
+// CTA, no block-wide barriers.
+constexpr int SMALL_WARPS = 8;
+
+__global__ void __launch_bounds__(SMALL_WARPS * 32)
+    lu_solve_small_kernel(int n, long blk, const double2* __restrict__ F, const int* __restrict__ perm,
+                          const int* __restrict__ items, int item0, int nitems, const int* __restrict__ klist,
+                          int nrhs, double2* Y, long s_row, long s_k) {
+  extern __shared__ double2 smd[];
+  const int lane = threadIdx.x & 31, wrp = threadIdx.x >> 5;
+  const int it = blockIdx.x * SMALL_WARPS + wrp;
+  if (it >= nitems) return;
+  int slot, beg, cnt;
+  if (items) {
+    slot = items[3 * (item0 + it)];
+    beg = items[3 * (item0 + it) + 1];
+    cnt = items[3 * (item0 + it) + 2];
+  } else {
+    slot = item0 + it;
+    beg = slot;
+    cnt = 1;
+  }
+  // stage the packed tile with independent coalesced loads (high MLP)
+  double2* Ds = smd + (long)wrp * n * n;
+  const double2* D = F + (long)slot * blk;
+  for (int i = lane; i < n * n; i += 32) Ds[i] = ld_stream(D + i);
+  const int pr = lane < n ? perm[(long)slot * n + lane] : 0;
+  __syncwarp();
+  for (int rho = 0; rho < cnt * nrhs; ++rho) {
+    const int kk = klist ? klist[beg + rho / nrhs] : beg + rho / nrhs;
+    const long base = (long)kk * s_k + (rho % nrhs);
+    double2 yv = lane < n ? Y[(long)pr * s_row + base] : cmk(0.0, 0.0);
+    // forward: o = inv(L) y (unit lower)
+    double2 o = yv;
+    for (int c = 0; c < n; ++c) {
+      const double2 yc = cmk(__shfl_sync(0xffffffffu, yv.x, c), __shfl_sync(0xffffffffu, yv.y, c));
+      if (lane > c && lane < n) cfma(o, Ds[c * n + lane], yc);
+    }
+    // backward: x = inv(U) o
+    double2 x = cmk(0.0, 0.0);
+    for (int c = 0; c < n; ++c) {
+      const double2 oc = cmk(__shfl_sync(0xffffffffu, o.x, c), __shfl_sync(0xffffffffu, o.y, c));
+      if (c >= lane && lane < n) cfma(x, Ds[c * n + lane], oc);
+    }
+    if (lane < n) Y[(long)lane * s_row + base] = x;
+  }
+}
+
+static int launch_solve_small(const LuGeom& g, const double2* F, const int* perm, const int* items, int item0,
+                              int nitems, const int* klist, int nrhs, double2* Y, long s_row, long s_k,
+                              cudaStream_t s) {
+  if (nitems <= 0) return VX_OK;
+  const size_t smem = (size_t)SMALL_WARPS * g.n * g.n * sizeof(double2);
+  if (smem > 48 * 1024)
+    VX_CUDA(cudaFuncSetAttribute(lu_solve_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  lu_solve_small_kernel<<<div_up(nitems, SMALL_WARPS), SMALL_WARPS * 32, smem, s>>>(
+      g.n, g.blk, F, perm, items, item0, nitems, klist, nrhs, Y, s_row, s_k);
+  VX_CHECK_LAUNCH("lu_solve_small_kernel");
+  return VX_OK;
+}
+
 template <int R>
 static int launch_solve_pipe(const LuGeom& g, const double2* F, const int* perm, const int* items,
                              int item0, int nblocks, const int* klist, int nrhs, double2* Y, long s_row,
@@ -854,6 +918,29 @@ __global__ void cols_copy_kernel(long nrows, double2* A, long lda, int P, const 
     if (to_buf) buf[idx] = A[a];
     else A[a] = buf[idx];
   }
+}
+
+// Dispatch the block solves of a work list: single-tile blocks -> warp-per-block
+// kernel; larger blocks -> TMA-pipelined kernel (items [0, n_single) one RHS
+// each, the rest multi-RHS).  vx_solve_variant(1) selects the synchronous kernel.
+static int solve_items(const LuGeom& g, const double2* F, const int* perm, const int* items, int n_single,
+                       int n_items, const int* klist, int nrhs, double2* Y, long s_row, long s_k, cudaStream_t s) {
+  int st;
+  Span span("prec_solve", s);
+  if (g.nt == 1 && !g_solve_classic)
+    return launch_solve_small(g, F, perm, items, 0, n_items, klist, nrhs, Y, s_row, s_k, s);
+  const bool pipe = g.nt > 1 && !g_solve_classic;
+  if (nrhs == 1)
+    st = pipe ? launch_solve_pipe<1>(g, F, perm, items, 0, n_single, klist, 1, Y, s_row, s_k, s)
+              : launch_solve<1, SOLVE_WARPS>(g, F, perm, items, 0, n_single, klist, 1, Y, s_row, s_k, s);
+  else
+    st = pipe ? launch_solve_pipe<MULTI_R>(g, F, perm, items, 0, n_single, klist, nrhs, Y, s_row, s_k, s)
+              : launch_solve<MULTI_R, SOLVE_WARPS>(g, F, perm, items, 0, n_single, klist, nrhs, Y, s_row, s_k, s);
+  if (st) return st;
+  return pipe ? launch_solve_pipe<MULTI_R>(g, F, perm, items, n_single, n_items - n_single, klist, nrhs, Y,
+                                           s_row, s_k, s)
+              : launch_solve<MULTI_R, SOLVE_WARPS>(g, F, perm, items, n_single, n_items - n_single, klist, nrhs,
+                                                   Y, s_row, s_k, s);
 }
 
 // ---------------------------------------------------------------- blocked
@@ -939,23 +1026,7 @@ extern "C" int vx_prec1_apply(int nx, int ny, int nz, int nrhs, const vx_c128* f
   }
   LuGeom g = lu_geom(q3);
   const double2* F = reinterpret_cast<const double2*>(factors);
-  const bool pipe = g.nt > 1 && !g_solve_classic;
-  if (nrhs == 1) {
-    Span span("prec_solve", s);
-    st = pipe ? launch_solve_pipe<1>(g, F, perm, items, 0, n_single, klist, 1, S, pitch, nrhs, s)
-              : launch_solve<1, SOLVE_WARPS>(g, F, perm, items, 0, n_single, klist, 1, S, pitch, nrhs, s);
-    if (st) return st;
-  } else {
-    st = pipe ? launch_solve_pipe<MULTI_R>(g, F, perm, items, 0, n_single, klist, nrhs, S, pitch, nrhs, s)
-              : launch_solve<MULTI_R, SOLVE_WARPS>(g, F, perm, items, 0, n_single, klist, nrhs, S, pitch,
-                                                   nrhs, s);
-    if (st) return st;
-  }
-  st = pipe ? launch_solve_pipe<MULTI_R>(g, F, perm, items, n_single, n_items - n_single, klist, nrhs, S,
-                                         pitch, nrhs, s)
-            : launch_solve<MULTI_R, SOLVE_WARPS>(g, F, perm, items, n_single, n_items - n_single, klist,
-                                                 nrhs, S, pitch, nrhs, s);
-  if (st) return st;
+  if ((st = solve_items(g, F, perm, items, n_single, n_items, klist, nrhs, S, pitch, nrhs, s))) return st;
   {
     LoadStrided ld{S, {pitch, 1, nrhs, nrhs}};
     StoreStrided sv{reinterpret_cast<double2*>(y), {pitch, 1, nrhs, nrhs}, 1.0 / nx};
@@ -1030,12 +1101,9 @@ extern "C" int vx_prec2_apply(int nx, int ny, int nz, int nrhs, const vx_c128* f
   }
   LuGeom g = lu_geom(3 * nz);
   const double2* F = reinterpret_cast<const double2*>(factors);
-  if (nrhs == 1) {
+  {
     Span span2("prec_solve", s);
-    if ((st = launch_solve<1, 1>(g, F, perm, nullptr, 0, nx * ny, nullptr, 1, S, plane, 1, s))) return st;
-  } else {
-    if ((st = launch_solve<MULTI_R, 1>(g, F, perm, nullptr, 0, nx * ny, nullptr, nrhs, S, plane, nrhs, s)))
-      return st;
+    if ((st = launch_solve_small(g, F, perm, nullptr, 0, nx * ny, nullptr, nrhs, S, plane, nrhs, s))) return st;
   }
   {
     LoadStrided ld{S, {plane, 1, pitch, (int)pitch}};
@@ -1105,25 +1173,6 @@ extern "C" int vx_prec1_solve(int n, int nrhs, const vx_c128* factors, const int
                               int n_single, int n_items, const int* klist, vx_c128* Y, long s_row, long s_k,
                               void* stream) {
   VX_REQUIRE(n >= 1 && nrhs >= 1 && n_single >= 0 && n_items >= n_single, "bad solve arguments");
-  cudaStream_t s = as_stream(stream);
-  LuGeom g = lu_geom(n);
-  const double2* F = reinterpret_cast<const double2*>(factors);
-  double2* Yd = reinterpret_cast<double2*>(Y);
-  const bool pipe = g.nt > 1 && !g_solve_classic;
-  int st;
-  {
-    Span span("prec_solve", s);
-    if (nrhs == 1)
-      st = pipe ? launch_solve_pipe<1>(g, F, perm, items, 0, n_single, klist, 1, Yd, s_row, s_k, s)
-                : launch_solve<1, SOLVE_WARPS>(g, F, perm, items, 0, n_single, klist, 1, Yd, s_row, s_k, s);
-    else
-      st = pipe ? launch_solve_pipe<MULTI_R>(g, F, perm, items, 0, n_single, klist, nrhs, Yd, s_row, s_k, s)
-                : launch_solve<MULTI_R, SOLVE_WARPS>(g, F, perm, items, 0, n_single, klist, nrhs, Yd, s_row,
-                                                     s_k, s);
-    if (st) return st;
-  }
-  return pipe ? launch_solve_pipe<MULTI_R>(g, F, perm, items, n_single, n_items - n_single, klist, nrhs, Yd,
-                                           s_row, s_k, s)
-              : launch_solve<MULTI_R, SOLVE_WARPS>(g, F, perm, items, n_single, n_items - n_single, klist,
-                                                   nrhs, Yd, s_row, s_k, s);
+  return solve_items(lu_geom(n), reinterpret_cast<const double2*>(factors), perm, items, n_single, n_items, klist,
+                     nrhs, reinterpret_cast<double2*>(Y), s_row, s_k, as_stream(stream));
 }
