@@ -126,7 +126,7 @@ __device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double
                : "d"(a), "d"(b));
 }
 
-template <bool SUB>
+template <bool SUB, int LDA = 33>
 __device__ __forceinline__ void tile_mma_half(const double2* As, const double2* Bg, double2* Cg, int h,
                                               int lane) {
   const int r4 = lane >> 2, c4 = lane & 3;
@@ -147,7 +147,7 @@ __device__ __forceinline__ void tile_mma_half(const double2* As, const double2* 
     double ar[4], ai[4], nar[4], br[2], bi[2];
 #pragma unroll
     for (int rb = 0; rb < 4; ++rb) {
-      const double2 a = As[(k0 + c4) * 33 + rb * 8 + r4];
+      const double2 a = As[(k0 + c4) * LDA + rb * 8 + r4];
       ar[rb] = a.x;
       ai[rb] = a.y;
       nar[rb] = -a.x;
@@ -194,8 +194,8 @@ __global__ void __launch_bounds__(LU_THREADS) lu_build_kernel(Unfold u, LuGeom g
   const int LD = T + 1, TL = T * LD;   // padded leading dimension of smem tiles
   double2* Ls = sm;                    // inv(L_kk), column-major, ld LD
   double2* Us = Ls + TL;               // inv(U_kk)
-  double2* Bst = Us + TL;              // LU_WARPS staged L tiles (ld LD)
-  int* pivs = reinterpret_cast<int*>(Bst + LU_WARPS * TL);  // [T]
+  double2* Bst = Us + TL;              // scratch (permutation composition)
+  int* pivs = reinterpret_cast<int*>(Bst + TL);               // [T]
   double* redv = reinterpret_cast<double*>(pivs + 32);        // [LU_WARPS]
   int* redi = reinterpret_cast<int*>(redv + LU_WARPS);        // [LU_WARPS]
   int* flags = redi + LU_WARPS;                               // [0]=info [1]=any swap
@@ -356,21 +356,14 @@ __global__ void __launch_bounds__(LU_THREADS) lu_build_kernel(Unfold u, LuGeom g
     //          memory, U tiles of row kt read as B fragments (L1-shared by the
     //          warps sweeping the same jt), each trailing tile read+written once.
     {
-      double2* Aw = Bst + warp * TL;
-      for (int it = kt + 1 + warp; it < nt; it += LU_WARPS) {
-        const double2* Asrc = A + (long)(it * nt + kt) * T2;
-        __syncwarp();
-        for (int i = lane; i < T2; i += 32) {
-          const int c = i / T, r = i - c * T;
-          Aw[c * LD + r] = Asrc[i];
-        }
-        __syncwarp();
-        for (int jt = kt + 1; jt < nt; ++jt) {
-          const double2* B = A + (long)(kt * nt + jt) * T2;
-          double2* C = A + (long)(it * nt + jt) * T2;
-          tile_mma_half<true>(Aw, B, C, 0, lane);
-          tile_mma_half<true>(Aw, B, C, 1, lane);
-        }
+      // L tile fragments straight from global/L2 (no staging: small shared
+      // memory footprint -> more resident CTAs to hide the fragment latency)
+      const int nrem = nt - kt - 1;
+      for (int task = warp; task < nrem * nrem * 2; task += LU_WARPS) {
+        const int h = task & 1, t2 = task >> 1;
+        const int it = kt + 1 + t2 / nrem, jt = kt + 1 + t2 % nrem;
+        tile_mma_half<true, 32>(A + (long)(it * nt + kt) * T2, A + (long)(kt * nt + jt) * T2,
+                                A + (long)(it * nt + jt) * T2, h, lane);
       }
     }
     __syncthreads();
@@ -398,7 +391,7 @@ __global__ void __launch_bounds__(LU_THREADS) lu_build_kernel(Unfold u, LuGeom g
 }
 
 static size_t lu_smem(const LuGeom& g) {
-  return (size_t)(2 + LU_WARPS) * g.T * (g.T + 1) * sizeof(double2) + 32 * sizeof(int) +
+  return (size_t)3 * g.T * (g.T + 1) * sizeof(double2) + 32 * sizeof(int) +
          LU_WARPS * (sizeof(double) + sizeof(int)) + 4 * sizeof(int) + (size_t)g.npad * sizeof(int) + 64;
 }
 
@@ -409,8 +402,8 @@ static int lu_build(const Unfold& u, int n, int nslots, double2* F, int* perm, i
   LuGeom g = lu_geom(n);
   size_t smem = lu_smem(g);
   // the permutation scratch reuses the staging tiles: make sure they fit npad ints
-  size_t need_perm = (size_t)g.npad * sizeof(int);
-  if ((size_t)LU_WARPS * g.T * g.T * sizeof(double2) < need_perm) smem += need_perm;
+  VX_REQUIRE((size_t)g.npad * sizeof(int) <= (size_t)g.T * (g.T + 1) * sizeof(double2),
+             "block size %d too large for the LU kernel's permutation scratch", n);
   if (smem > 48 * 1024)
     VX_CUDA(cudaFuncSetAttribute(lu_build_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem));

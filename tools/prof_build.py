@@ -1,0 +1,20 @@
+"""Profiling driver: one 1-level preconditioner build of a workload (one
+lu_build_kernel launch over all frequency blocks).  usage: prof_build.py [c1]"""
+import sys
+import time
+from pathlib import Path
+
+import torch
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+from paper_1903_07884_b200 import workloads  # noqa: E402
+from paper_1903_07884_b200.circulant import build_one_level  # noqa: E402
+
+name = sys.argv[1] if len(sys.argv) > 1 else "c1"
+W = workloads.make(name)
+kern = W.kernel()
+torch.cuda.synchronize()
+t0 = time.perf_counter()
+prec = build_one_level(kern, W.mtilde(), cap_bytes=2 ** 62)
+torch.cuda.synchronize()
+print(f"{name} build {time.perf_counter() - t0:.3f} s, {prec.grid.nx} blocks of {prec.block_size}^2")
