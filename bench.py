@@ -442,9 +442,9 @@ def run_ours(args):
                 b_d = torch.from_numpy(np.ascontiguousarray(L.local_slice(b_host))).cuda()
                 xs, rep = gmres_sharded(lambda v: dop.apply(m_d, v), b_d, Bk, Cm, apply_pinv=prec.apply,
                                         tol=W.tol, maxit=W.maxit, restart=W.restart)
-                x_h = xs.cpu().numpy()
+                x_h = nv.to_host(xs)
             else:
-                x_h, rep = gmres(lambda v: apply_system(plan, m_step, v), b_host.copy(),
+                x_h, rep = gmres(lambda v: apply_system(plan, m_step, v), b_host,
                                  apply_pinv=prec.apply, tol=W.tol, maxit=W.maxit, restart=W.restart)
             its_e += rep.iterations
         torch.cuda.synchronize()

@@ -199,7 +199,7 @@ def _as_rhs(x, nunk):
 
 def _ret(yd, flat, is_t, shape):
     out = yd.reshape(shape)
-    return out if is_t else out.cpu().numpy()
+    return out if is_t else nv.to_host(out)
 
 
 # ---------------------------------------------------------------------------

@@ -126,14 +126,14 @@ def apply_n(plan: OperatorPlan, x):
     """y = N x (reference operator.py:82-98)."""
     xd, is_dev = _field_in(plan, x)
     y = apply_device(plan, None, xd)
-    return y if is_dev else y.cpu().numpy()
+    return y if is_dev else nv.to_host(y)
 
 
 def apply_system(plan: OperatorPlan, m, x):
     """y = (I - M N) x (reference operator.py:101-105)."""
     xd, is_dev = _field_in(plan, x)
     y = apply_device(plan, _medium_in(plan, m), xd)
-    return y if is_dev else y.cpu().numpy()
+    return y if is_dev else nv.to_host(y)
 
 
 def rhs_from_incident(m, e_inc, physics: Physics) -> np.ndarray:

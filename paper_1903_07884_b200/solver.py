@@ -230,7 +230,7 @@ def gmres(apply_a, b, *, apply_pinv=None, tol: float = 1e-4, maxit: int = 2000,
     bnorm = K.norm(bd)
 
     def _out(xd):
-        return xd if on_device else xd.cpu().numpy()
+        return xd if on_device else nv.to_host(xd)
 
     if bnorm == 0.0:
         x = t.zeros(n, dtype=t.complex128, device="cuda")
