@@ -53,7 +53,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c1", choices=["c0", "c1", "c1r", "c2", "c3", "c4"])
+    ap.add_argument("--config", default="c1", choices=["c0", "c1", "c1r", "c2", "c3", "c4", "c4b"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-sample-blocks", type=int, default=24)
@@ -168,8 +168,11 @@ def block_sizes(W):
         return [(3 * nz, nx * ny)]
     if k == "blocked":
         out = []
-        for (x0, x1, y0, y1, z0, z1) in W.prec["boxes"]:
-            out.append((3 * (y1 - y0) * (z1 - z0), x1 - x0))
+        for (x0, x1, y0, y1, z0, z1), lvl in zip(W.prec["boxes"], W.prec["levels"]):
+            if lvl == "two-level":
+                out.append((3 * (z1 - z0), (x1 - x0) * (y1 - y0)))
+            else:
+                out.append((3 * (y1 - y0) * (z1 - z0), x1 - x0))
         return out
     raise ValueError(k)
 
@@ -207,52 +210,64 @@ def cpu_iteration_sample(W, kern, m, sample_blocks, mean_j, spectra=None):
     O.apply_system(spectra, dims, m, x, workers=cores)
     t_mv = time.perf_counter() - t0
     kind = W.prec["kind"]
-    if kind in ("one-level", "reduced-one-level", "blocked"):
-        if kind == "blocked":
-            boxes = W.prec["boxes"]
-        else:
-            boxes = [(0, nx, 0, ny, 0, nz)]
-        t_pc = 0.0
-        for box in boxes:
-            sub, sdims = O.slice_kernel(kern.tensors, dims, box)
-            mt = W.mtilde(None if kind != "blocked" else box)
-            m_yz = O.coerce_mtilde(sdims, mt)
-            bx, by, bz = sdims
-            lam = O.chan_x_spectra(sub)
-            ks = np.linspace(0, bx - 1, min(sample_blocks, bx)).astype(int)
-            facs = [lu_factor(O.unfold_block_yz(lam[:, :, :, k], m_yz), check_finite=False) for k in ks]
-            xf = rng.normal(size=(3, bz, by, bx)) + 0j
-            t0 = time.perf_counter()
-            spec = scipy.fft.fft(xf, axis=3)
-            out = scipy.fft.ifft(spec, axis=3)
-            t_fft = time.perf_counter() - t0
-            t0 = time.perf_counter()
-            for k, f in zip(ks, facs):
-                rhs = np.ascontiguousarray(spec[:, :, :, k]).reshape(-1, 1)
-                lu_solve(f, rhs, check_finite=False)
-            t_lu = (time.perf_counter() - t0) * bx / len(ks)
-            t_pc += t_fft + t_lu
-            del out
-        desc = (f"oracle port (scipy.fft + LAPACK zgetrs as the reference) on {W.name}: full matvec "
-                f"(fftn workers={cores}), x-DFT of the full field, {min(sample_blocks, nx)} of the "
-                f"per-frequency lu_solve calls timed and scaled to all blocks, MGS over {mean_j} vectors")
-    else:
-        lam2 = scipy.fft.fftn(O.chan_along_axis(O.chan_along_axis(kern.tensors, 3), 2), axes=(2, 3))
-        m_z = W.mtilde()[:, 0, 0]
-        xf = rng.normal(size=(3, nz, ny, nx)) + 0j
+    from paper_1903_07884_b200.grid import PermittivityMap, VoxelGrid, homogenize
+
+    def box_mtilde(box, level):
+        strat = W.prec.get("homogenization") or ("mode" if level == "two-level" else "real_mean_x")
+        if box is None:
+            return homogenize(W.pmap, strat)
+        x0, x1, y0, y1, z0, z1 = box
+        sub = VoxelGrid(x1 - x0, y1 - y0, z1 - z0, W.grid.delta)
+        return homogenize(PermittivityMap(sub, W.pmap.eps_r[z0:z1, y0:y1, x0:x1]), strat)
+
+    def one_level_box(sub, sdims, mt):
+        m_yz = O.coerce_mtilde(sdims, mt)
+        bx, by, bz = sdims
+        lam = O.chan_x_spectra(sub)
+        ks = np.linspace(0, bx - 1, min(sample_blocks, bx)).astype(int)
+        facs = [lu_factor(O.unfold_block_yz(lam[:, :, :, k], m_yz), check_finite=False) for k in ks]
+        xf = rng.normal(size=(3, bz, by, bx)) + 0j
+        t0 = time.perf_counter()
+        spec = scipy.fft.fft(xf, axis=3)
+        scipy.fft.ifft(spec, axis=3)
+        t_fft = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        for k, f in zip(ks, facs):
+            lu_solve(f, np.ascontiguousarray(spec[:, :, :, k]).reshape(-1, 1), check_finite=False)
+        return t_fft + (time.perf_counter() - t0) * bx / len(ks), len(ks), bx
+
+    def two_level_box(sub, sdims, mt):
+        bx, by, bz = sdims
+        lam2 = scipy.fft.fftn(O.chan_along_axis(O.chan_along_axis(sub, 3), 2), axes=(2, 3))
+        m_z = np.asarray(mt)[:, 0, 0]
+        xf = rng.normal(size=(3, bz, by, bx)) + 0j
         t0 = time.perf_counter()
         spec = scipy.fft.fftn(xf, axes=(2, 3))
         scipy.fft.ifftn(spec, axes=(2, 3))
         t_fft = time.perf_counter() - t0
-        S = min(sample_blocks * 40, nx * ny)
-        idx = np.linspace(0, nx * ny - 1, S).astype(int)
-        facs = [lu_factor(O.unfold_block_z(lam2[:, :, i // nx, i % nx], m_z), check_finite=False) for i in idx]
+        S = min(sample_blocks * 40, bx * by)
+        idx = np.linspace(0, bx * by - 1, S).astype(int)
+        facs = [lu_factor(O.unfold_block_z(lam2[:, :, i // bx, i % bx], m_z), check_finite=False) for i in idx]
         t0 = time.perf_counter()
         for i, f in zip(idx, facs):
-            lu_solve(f, np.ascontiguousarray(spec[:, :, i // nx, i % nx]).reshape(-1, 1), check_finite=False)
-        t_pc = t_fft + (time.perf_counter() - t0) * nx * ny / S
-        desc = (f"oracle port on {W.name}: full matvec, 2-D DFT, {S} of {nx * ny} (l,k) lu_solve calls "
-                f"scaled, MGS over {mean_j} vectors")
+            lu_solve(f, np.ascontiguousarray(spec[:, :, i // bx, i % bx]).reshape(-1, 1), check_finite=False)
+        return t_fft + (time.perf_counter() - t0) * bx * by / S, S, bx * by
+
+    if kind == "blocked":
+        boxes, levels = W.prec["boxes"], W.prec["levels"]
+    else:
+        boxes, levels = [None], [kind]
+    t_pc = 0.0
+    parts_desc = []
+    for box, lvl in zip(boxes, levels):
+        sub, sdims = O.slice_kernel(kern.tensors, dims, box or (0, nx, 0, ny, 0, nz))
+        mt = box_mtilde(box, lvl)
+        t, ns, ntot = (two_level_box if lvl == "two-level" else one_level_box)(sub, sdims, mt)
+        t_pc += t
+        parts_desc.append(f"{ns} of {ntot} {lvl} lu_solve calls")
+    desc = (f"oracle port (scipy.fft + LAPACK zgetrs as the reference) on {W.name}: full matvec "
+            f"(fftn workers={cores}), preconditioner DFTs of the full field, "
+            + "; ".join(parts_desc) + f" timed and scaled to all blocks, MGS over {mean_j} vectors")
     V = [rng.normal(size=n) + 1j * rng.normal(size=n) for _ in range(max(1, mean_j))]
     w = x.copy()
     t0 = time.perf_counter()
@@ -280,9 +295,9 @@ def build_prec(W, kern):
         boxes = [C.Box(lbl, *b) for lbl, b in zip(W.prec["labels"], W.prec["boxes"])]
         part = C.partition_boxes(W.grid, boxes)
         levels = dict(zip(W.prec["labels"], W.prec["levels"]))
-        return C.build_blocked(kern, W.pmap, part, levels,
-                               homog={lbl: W.prec["homogenization"] for lbl in W.prec["labels"]},
-                               cap_bytes=big)
+        homog = ({lbl: W.prec["homogenization"] for lbl in W.prec["labels"]}
+                 if W.prec.get("homogenization") else None)   # None: per-level defaults
+        return C.build_blocked(kern, W.pmap, part, levels, homog=homog, cap_bytes=big)
     raise ValueError(kind)
 
 
@@ -291,7 +306,8 @@ def stored_blocks_of(W, prec):
     if kind == "reduced-one-level":
         return [(prec.block_size, prec.n_kept)]
     if kind == "blocked":
-        return [(p.block_size, p.grid.nx) for p in prec.box_precs]
+        return [(p.block_size, p.n_kept if hasattr(p, "n_kept") else
+                 (p.grid.nx * p.grid.ny if p.level == "two-level" else p.grid.nx)) for p in prec.box_precs]
     return block_sizes(W)
 
 

@@ -134,7 +134,7 @@ def make(name: str, interp: str = "B") -> Workload:
                 "levels": ["one-level", "one-level"], "labels": ["guide1", "guide2"]}
         restart = 50
         e = _incident(grid, mask_yz=np.broadcast_to(g1[None, :], (11, 56)).astype(float))
-    elif name == "c4":
+    elif name in ("c4", "c4b"):
         grid = VoxelGrid(367, 400, 8, 0.03e-6)
         ix = np.arange(367) + 0.5
         iy = np.arange(400) + 0.5
@@ -145,12 +145,21 @@ def make(name: str, interp: str = "B") -> Workload:
         core = zcore[:, None, None] & cols[None]
         bus3 = zcore[:, None, None] & np.broadcast_to(bus[:, None], (400, 367))[None]
         kap = np.where(bus3, _absorber_kappa(367, 73)[None, None, :], 0.0)
-        prec, restart = {"kind": "two-level", "homogenization": "mode"}, 100
+        if name == "c4":
+            prec = {"kind": "two-level", "homogenization": "mode"}
+        else:
+            # the paper's disk-resonator preconditioner (reference
+            # photonics.py:249-255 hint): reduced 1-level on the bus box, 2-level
+            # on the disk box, identity elsewhere
+            prec = {"kind": "blocked", "homogenization": None,
+                    "boxes": [(0, 367, 22, 37, 0, 8), (16, 351, 44, 378, 0, 8)],
+                    "levels": ["reduced-one-level", "two-level"], "labels": ["bus", "disk"]}
+        restart = 100
         e = _incident(grid, mask_3d=bus3.astype(float))
     else:
         raise ValueError(f"unknown workload {name!r}")
     n_r = np.where(core, N_CORE, N_BG)
-    kappa = np.where(core | (name != "c4"), kap, 0.0)
+    kappa = np.where(core | (name not in ("c4", "c4b")), kap, 0.0)
     eps = _eps(n_r, kappa, interp)
     # cladding voxels outside any absorber are exactly background: eps = 1
     eps = np.where((n_r == N_BG) & (kappa == 0.0), 1.0 + 0j, eps)
