@@ -97,20 +97,6 @@ struct Unfold {
   int nzL, nyL;
 };
 
-__device__ __forceinline__ double2 unfold_entry(const Unfold& u, const double2* lam, int q, int row,
-                                                int col) {
-  const int a = row / q, rr = row - a * q;
-  const int b = col / q, cc = col - b * q;
-  const int iz = rr / u.nyL, iy = rr - iz * u.nyL;
-  const int jz = cc / u.nyL, jy = cc - jz * u.nyL;
-  const int nyy = 2 * u.nyL - 1, nzz = 2 * u.nzL - 1;
-  const double2 t = __ldg(lam + (long)c_pair[3 * a + b] * nzz * nyy + (iz - jz + u.nzL - 1) * nyy +
-                          (iy - jy + u.nyL - 1));
-  double2 v = cmul(__ldg(u.m + rr), t);
-  v = cmk(-v.x, -v.y);
-  if (row == col) v.x += 1.0;
-  return v;
-}
 
 // FP64 tensor-core (DMMA, mma.sync.m8n8k4.f64) product on one half (16
 // columns) of a 32 x 32 complex tile:
@@ -208,33 +194,66 @@ __global__ void __launch_bounds__(LU_THREADS) lu_build_kernel(Unfold u, LuGeom g
   const double2* lam = u.lamT + (long)k * u.Ltot;
   const int q = u.nzL * u.nyL;
 
-  // phase 0: D_k = I - diag(m) N_k into tiled storage (identity pad)
-  for (long i = tid; i < g.blk; i += LU_THREADS) {
-    const int r = (int)(i % T);
-    const long t2 = i / T;
-    const int c = (int)(t2 % T);
-    const int tile = (int)(t2 / T);
-    const int row = (tile / nt) * T + r, col = (tile % nt) * T + c;
-    double2 v;
-    if (row < n && col < n) v = unfold_entry(u, lam, q, row, col);
-    else v = cmk(row == col ? 1.0 : 0.0, 0.0);
-    A[i] = v;
+  // phase 0: D_k = I - diag(m) N_k into tiled storage (identity pad).
+  // Per-index decomposition (component a, (z,y) offset, medium value) tabulated
+  // once in shared memory (aliasing the not-yet-used Ls/Us/staging region), so
+  // an entry costs two table lookups, one generator gather and a complex
+  // multiply; a warp writes one 32-entry tile column (coalesced 512 B).
+  {
+    const int nyy = 2 * u.nyL - 1, nzz = 2 * u.nzL - 1;
+    const int P = nzz * nyy, base = (u.nzL - 1) * nyy + (u.nyL - 1);
+    int* key = reinterpret_cast<int*>(sm);
+    double2* mtab = reinterpret_cast<double2*>(key + ((npad + 3) & ~3));
+    for (int idx = tid; idx < npad; idx += LU_THREADS) {
+      if (idx < n) {
+        const int a = idx / q, rr = idx - a * q;
+        const int iz = rr / u.nyL, iy = rr - iz * u.nyL;
+        key[idx] = (a << 24) | (iz * nyy + iy);
+        mtab[idx] = __ldg(u.m + rr);
+      } else {
+        key[idx] = -1;
+      }
+    }
+    __syncthreads();
+    const int ncolw = nt * nt * T;  // (tile, column) pairs
+    for (int w = warp; w < ncolw; w += LU_WARPS) {
+      const int tile = w / T, c = w - tile * T;
+      const int it = tile / nt, jt = tile - it * nt;
+      const int col = jt * T + c;
+      if (lane >= T) continue;
+      const int row = it * T + lane;
+      double2 v = cmk(row == col ? 1.0 : 0.0, 0.0);
+      const int ck = key[col], rk = key[row];
+      if (ck >= 0 && rk >= 0) {
+        const int a = rk >> 24, b = ck >> 24;
+        const double2 t = __ldg(lam + (long)c_pair[3 * a + b] * P + (rk & 0xffffff) - (ck & 0xffffff) + base);
+        const double2 mv = cmul(mtab[row], t);
+        v = cmk(v.x - mv.x, -mv.y);
+      }
+      A[((long)tile * T + c) * T + lane] = v;
+    }
   }
   if (tid == 0) flags[0] = 0;
   __syncthreads();
 
   for (int kt = 0; kt < nt; ++kt) {
     const int c0 = kt * T;
-    // ---- (1) panel factorisation of tile column kt
+    // ---- (1) panel factorisation of tile column kt.  One fused pass per
+    //          column: a thread owns whole panel rows (coalesced across
+    //          threads: rows are contiguous inside a column-major tile), scales
+    //          the multiplier, applies the rank-1 update to the row's remaining
+    //          panel columns with all loads in flight, and already tracks the
+    //          next column's pivot candidate (zgetf2 order, |Re|+|Im| rule).
+    double2* usm = reinterpret_cast<double2*>(gpiv + ((npad + 3) & ~3));  // [T] pivot row (16-B aligned)
+    double best = -1.0;
+    int bi = c0;
+    for (int row = c0 + tid; row < npad; row += LU_THREADS) {
+      const double2 v = A[lu_off(g, row, c0)];
+      const double a = fabs(v.x) + fabs(v.y);
+      if (a > best) { best = a; bi = row; }
+    }
     for (int jj = 0; jj < T; ++jj) {
       const int j = c0 + jj;
-      double best = -1.0;
-      int bi = j;
-      for (int row = j + tid; row < npad; row += LU_THREADS) {
-        const double2 v = A[lu_off(g, row, j)];
-        const double a = fabs(v.x) + fabs(v.y);
-        if (a > best) { best = a; bi = row; }
-      }
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
         const double ob = __shfl_down_sync(0xffffffffu, best, o);
@@ -244,50 +263,59 @@ __global__ void __launch_bounds__(LU_THREADS) lu_build_kernel(Unfold u, LuGeom g
       if (lane == 0) { redv[warp] = best; redi[warp] = bi; }
       __syncthreads();
       if (tid == 0) {
-        double b = redv[0];
+        double bb = redv[0];
         int ii = redi[0];
         for (int w = 1; w < LU_WARPS; ++w)
-          if (redv[w] > b || (redv[w] == b && redi[w] < ii)) { b = redv[w]; ii = redi[w]; }
-        if (!(b > 0.0) && b != 0.0) ii = j;  // all NaN
+          if (redv[w] > bb || (redv[w] == bb && redi[w] < ii)) { bb = redv[w]; ii = redi[w]; }
+        if (!(bb > 0.0) && bb != 0.0) ii = j;  // all NaN
         pivs[jj] = ii;
         gpiv[j] = ii;
       }
       __syncthreads();
       const int p = pivs[jj];
-      if (p != j && tid < T) {
-        const long oa = lu_off(g, j, c0 + tid), ob = lu_off(g, p, c0 + tid);
-        const double2 t = A[oa];
-        A[oa] = A[ob];
-        A[ob] = t;
+      if (tid < T) {
+        const long oa = lu_off(g, j, c0 + tid);
+        double2 vj = A[oa];
+        if (p != j) {
+          const long ob = lu_off(g, p, c0 + tid);
+          const double2 vp = A[ob];
+          A[ob] = vj;
+          A[oa] = vp;
+          vj = vp;
+        }
+        usm[tid] = vj;
       }
       __syncthreads();
-      const double2 d = A[lu_off(g, j, j)];
+      const double2 d = usm[jj];
       const bool bad = (d.x == 0.0 && d.y == 0.0) || !isfinite(d.x) || !isfinite(d.y);
-      if (bad) {
-        if (tid == 0 && flags[0] == 0 && j < n) flags[0] = j + 1;
-      } else {
-        const double2 dinv = cinv(d);
-        for (int row = j + 1 + tid; row < npad; row += LU_THREADS) {
-          const long o = lu_off(g, row, j);
-          A[o] = cmul(A[o], dinv);
+      if (bad && tid == 0 && flags[0] == 0 && j < n) flags[0] = j + 1;
+      const double2 dinv = bad ? cmk(0.0, 0.0) : cinv(d);
+      best = -1.0;
+      bi = j + 1;
+      for (int row = j + 1 + tid; row < npad; row += LU_THREADS) {
+        const int it = row / T, r = row - it * T;
+        double2* rowp = A + (long)(it * nt + kt) * T2 + r;  // element (row, c0 + c) at rowp[c * T]
+        double2 l = rowp[jj * T];
+        if (!bad) l = cmul(l, dinv);
+        rowp[jj * T] = l;
+        constexpr int U = 8;
+        for (int c0u = jj + 1; c0u < T; c0u += U) {
+          double2 v[U];
+#pragma unroll
+          for (int u = 0; u < U; ++u)
+            if (c0u + u < T) v[u] = rowp[(c0u + u) * T];
+#pragma unroll
+          for (int u = 0; u < U; ++u)
+            if (c0u + u < T) {
+              if (!bad) cfms(v[u], l, usm[c0u + u]);
+              rowp[(c0u + u) * T] = v[u];
+            }
+          if (c0u == jj + 1) {  // next column's pivot candidate
+            const double a = fabs(v[0].x) + fabs(v[0].y);
+            if (a > best) { best = a; bi = row; }
+          }
         }
       }
-      __syncthreads();
-      const int ncol = T - jj - 1, nrow = npad - j - 1;
-      if (ncol > 0 && nrow > 0) {
-        const int tot = ncol * nrow;
-        for (int idx = tid; idx < tot; idx += LU_THREADS) {
-          const int cc = idx / nrow, rr = idx - cc * nrow;
-          const int row = j + 1 + rr, col = j + 1 + cc;
-          const double2 l = A[lu_off(g, row, j)];
-          const double2 uu = A[lu_off(g, j, col)];
-          const long o = lu_off(g, row, col);
-          double2 v = A[o];
-          cfms(v, l, uu);
-          A[o] = v;
-        }
-      }
-      __syncthreads();
     }
     // ---- (2) the panel's row interchanges on every other tile column (zlaswp)
     if (tid == 0) {
@@ -392,7 +420,8 @@ __global__ void __launch_bounds__(LU_THREADS) lu_build_kernel(Unfold u, LuGeom g
 
 static size_t lu_smem(const LuGeom& g) {
   return (size_t)3 * g.T * (g.T + 1) * sizeof(double2) + 32 * sizeof(int) +
-         LU_WARPS * (sizeof(double) + sizeof(int)) + 4 * sizeof(int) + (size_t)g.npad * sizeof(int) + 64;
+         LU_WARPS * (sizeof(double) + sizeof(int)) + 4 * sizeof(int) + (size_t)(g.npad + 4) * sizeof(int) + 64 +
+         (size_t)g.T * sizeof(double2);
 }
 
 static int lu_build(const Unfold& u, int n, int nslots, double2* F, int* perm, int* piv, int* info,
@@ -402,8 +431,10 @@ static int lu_build(const Unfold& u, int n, int nslots, double2* F, int* perm, i
   LuGeom g = lu_geom(n);
   size_t smem = lu_smem(g);
   // the permutation scratch reuses the staging tiles: make sure they fit npad ints
-  VX_REQUIRE((size_t)g.npad * sizeof(int) <= (size_t)g.T * (g.T + 1) * sizeof(double2),
-             "block size %d too large for the LU kernel's permutation scratch", n);
+  VX_REQUIRE((size_t)g.npad * sizeof(int) <= (size_t)g.T * (g.T + 1) * sizeof(double2) &&
+                 (size_t)(g.npad + 4) * (sizeof(int) + sizeof(double2)) <=
+                     (size_t)3 * g.T * (g.T + 1) * sizeof(double2),
+             "block size %d too large for the LU kernel's scratch tables", n);
   if (smem > 48 * 1024)
     VX_CUDA(cudaFuncSetAttribute(lu_build_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem));
