@@ -348,9 +348,13 @@ def run_ours(args):
         dop = DistOperator(kern, L, Bk, Cm)
         torch.cuda.synchronize()
         plan_s = time.perf_counter() - t0
+        ptol = W.prec.get("tol") if W.prec["kind"] == "reduced-one-level" else None
+        prec = DistOneLevelPrec(kern, W.mtilde(), L, Bk, Cm, tol=ptol)   # warm build
+        del prec
+        torch.cuda.synchronize()
+        torch.cuda.empty_cache()
         ev_a.record()
-        prec = DistOneLevelPrec(kern, W.mtilde(), L, Bk, Cm,
-                                tol=W.prec.get("tol") if W.prec["kind"] == "reduced-one-level" else None)
+        prec = DistOneLevelPrec(kern, W.mtilde(), L, Bk, Cm, tol=ptol)
         ev_b.record()
         torch.cuda.synchronize()
         build_s = ev_a.elapsed_time(ev_b) / 1e3
@@ -364,6 +368,12 @@ def run_ours(args):
         plan = plan_operator(kern)
         torch.cuda.synchronize()
         plan_s = time.perf_counter() - t0
+        # warm build first (module load, FFT tables, kernel attributes), then the
+        # timed build of the factors that the solves use
+        prec = build_prec(W, kern)
+        del prec
+        torch.cuda.synchronize()
+        torch.cuda.empty_cache()
         ev_a.record()
         prec = build_prec(W, kern)
         ev_b.record()
@@ -504,6 +514,7 @@ def run_ours(args):
                    "parallelism": mode},
         "iterations_per_solve": its_per_solve,
         "build_s": build_s,
+        "build_note": "warm build (second in process): Chan + x-DFT spectra, proxies, unfold + LU of all blocks",
         "plan_s": plan_s,
         "solve_s": solve_s,
         "tts_s": build_s + solve_s,

@@ -107,6 +107,11 @@ int vx_prec1_apply(int nx, int ny, int nz, int nrhs, const vx_c128* factors, con
                    const int* items, int n_single, int n_items, const int* klist,
                    const vx_c128* x, vx_c128* y, vx_c128* work, void* stream);
 
+/* Select the factorisation: 0 (default) = step-batched kernels (unfold, then per
+ * tile column: panel / interchanges / U row / DMMA trailing update over all
+ * blocks), 1 = one CTA per block for the whole LU (A/B timing). */
+int vx_lu_variant(int monolithic);
+
 /* Select the block-solve kernel: 0 (default) = TMA-bulk pipelined producer/
  * consumer kernel, 1 = the classic synchronous kernel (kept for A/B timing). */
 int vx_solve_variant(int classic);

@@ -80,6 +80,7 @@ _SIGS = {
     "vx_cgs_update": (c_int, [c_long, c_int, P, c_long, P, P, P, P, P]),
     "vx_launch_count": (c_long, []),
     "vx_solve_variant": (c_int, [c_int]),
+    "vx_lu_variant": (c_int, [c_int]),
     "vx_timing_enable": (c_int, [c_int]),
     "vx_timing_read": (c_int, [C.c_char_p, C.POINTER(C.c_double), C.POINTER(C.c_long)]),
 }

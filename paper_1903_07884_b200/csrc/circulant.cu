@@ -424,11 +424,303 @@ static size_t lu_smem(const LuGeom& g) {
          (size_t)g.T * sizeof(double2);
 }
 
+// ------------------------------------------------- step-batched LU (default)
+// The factorisation advances all blocks one tile column at a time, with one
+// kernel per phase so each phase gets its own launch shape and register
+// budget, and the DMMA trailing update sees every (block, tile) task of the
+// step at once (no per-block tail where most warps idle):
+//   unfold (once) | per step kt: panel -> row interchanges -> U row -> trailing
+//   update | permutation composition (once).
+constexpr int LUB_WARPS = 8;
+
+__global__ void __launch_bounds__(256) lub_unfold_kernel(Unfold u, LuGeom g, double2* F) {
+  extern __shared__ __align__(16) unsigned char smu[];
+  const int T = g.T, nt = g.nt, npad = g.npad, n = g.n;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int slot = blockIdx.x;
+  const int k = u.kset ? u.kset[slot] : slot;
+  double2* A = F + (long)slot * g.blk;
+  const double2* lam = u.lamT + (long)k * u.Ltot;
+  const int q = u.nzL * u.nyL;
+  const int nyy = 2 * u.nyL - 1, nzz = 2 * u.nzL - 1;
+  const int P = nzz * nyy, base = (u.nzL - 1) * nyy + (u.nyL - 1);
+  int* key = reinterpret_cast<int*>(smu);
+  double2* mtab = reinterpret_cast<double2*>(key + ((npad + 3) & ~3));
+  for (int idx = tid; idx < npad; idx += 256) {
+    if (idx < n) {
+      const int a = idx / q, rr = idx - a * q;
+      const int iz = rr / u.nyL, iy = rr - iz * u.nyL;
+      key[idx] = (a << 24) | (iz * nyy + iy);
+      mtab[idx] = __ldg(u.m + rr);
+    } else {
+      key[idx] = -1;
+    }
+  }
+  __syncthreads();
+  const int ncolw = nt * nt * T;
+  for (int w = warp; w < ncolw; w += 8) {
+    const int tile = w / T, c = w - tile * T;
+    const int it = tile / nt, jt = tile - it * nt;
+    const int col = jt * T + c;
+    if (lane >= T) continue;
+    const int row = it * T + lane;
+    double2 v = cmk(row == col ? 1.0 : 0.0, 0.0);
+    const int ck = key[col], rk = key[row];
+    if (ck >= 0 && rk >= 0) {
+      const int a = rk >> 24, b = ck >> 24;
+      const double2 t = __ldg(lam + (long)c_pair[3 * a + b] * P + (rk & 0xffffff) - (ck & 0xffffff) + base);
+      const double2 mv = cmul(mtab[row], t);
+      v = cmk(v.x - mv.x, -mv.y);
+    }
+    A[((long)tile * T + c) * T + lane] = v;
+  }
+}
+
+// panel factorisation of tile column kt of every block (one CTA per block),
+// then the diagonal tile's triangular inverses, packed in place.
+__global__ void __launch_bounds__(LU_THREADS) lub_panel_kernel(LuGeom g, double2* F, int kt, int* piv,
+                                                               int* info) {
+  __shared__ double redv[LU_WARPS];
+  __shared__ int redi[LU_WARPS];
+  __shared__ int pivs[32];
+  __shared__ double2 usm[32];
+  __shared__ double2 Ls[32 * 33], Us[32 * 33];
+  const int T = g.T, T2 = T * T, nt = g.nt, npad = g.npad, n = g.n;
+  const int LD = T + 1;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int slot = blockIdx.x;
+  double2* A = F + (long)slot * g.blk;
+  const int c0 = kt * T;
+  double best = -1.0;
+  int bi = c0;
+  for (int row = c0 + tid; row < npad; row += LU_THREADS) {
+    const double2 v = A[lu_off(g, row, c0)];
+    const double a = fabs(v.x) + fabs(v.y);
+    if (a > best) { best = a; bi = row; }
+  }
+  for (int jj = 0; jj < T; ++jj) {
+    const int j = c0 + jj;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ob = __shfl_down_sync(0xffffffffu, best, o);
+      const int oi = __shfl_down_sync(0xffffffffu, bi, o);
+      if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+    }
+    if (lane == 0) { redv[warp] = best; redi[warp] = bi; }
+    __syncthreads();
+    if (tid == 0) {
+      double bb = redv[0];
+      int ii = redi[0];
+      for (int w = 1; w < LU_WARPS; ++w)
+        if (redv[w] > bb || (redv[w] == bb && redi[w] < ii)) { bb = redv[w]; ii = redi[w]; }
+      if (!(bb > 0.0) && bb != 0.0) ii = j;  // all NaN
+      if (j >= n) ii = j;                    // identity pad never pivots
+      pivs[jj] = ii;
+      if (j < n) piv[(long)slot * n + j] = ii;
+    }
+    __syncthreads();
+    const int p = pivs[jj];
+    if (tid < T) {
+      const long oa = lu_off(g, j, c0 + tid);
+      double2 vj = A[oa];
+      if (p != j) {
+        const long ob = lu_off(g, p, c0 + tid);
+        const double2 vp = A[ob];
+        A[ob] = vj;
+        A[oa] = vp;
+        vj = vp;
+      }
+      usm[tid] = vj;
+    }
+    __syncthreads();
+    const double2 d = usm[jj];
+    const bool bad = (d.x == 0.0 && d.y == 0.0) || !isfinite(d.x) || !isfinite(d.y);
+    if (bad && tid == 0 && j < n && info[slot] == 0) info[slot] = j + 1;
+    const double2 dinv = bad ? cmk(0.0, 0.0) : cinv(d);
+    best = -1.0;
+    bi = j + 1;
+    for (int row = j + 1 + tid; row < npad; row += LU_THREADS) {
+      const int it = row / T, r = row - it * T;
+      double2* rowp = A + (long)(it * nt + kt) * T2 + r;
+      double2 l = rowp[jj * T];
+      if (!bad) l = cmul(l, dinv);
+      rowp[jj * T] = l;
+      constexpr int U = 8;
+      for (int c0u = jj + 1; c0u < T; c0u += U) {
+        double2 v[U];
+#pragma unroll
+        for (int u2 = 0; u2 < U; ++u2)
+          if (c0u + u2 < T) v[u2] = rowp[(c0u + u2) * T];
+#pragma unroll
+        for (int u2 = 0; u2 < U; ++u2)
+          if (c0u + u2 < T) {
+            if (!bad) cfms(v[u2], l, usm[c0u + u2]);
+            rowp[(c0u + u2) * T] = v[u2];
+          }
+        if (c0u == jj + 1) {
+          const double a = fabs(v[0].x) + fabs(v[0].y);
+          if (a > best) { best = a; bi = row; }
+        }
+      }
+    }
+  }
+  __syncthreads();
+  const double2* Dg = A + (long)(kt * nt + kt) * T2;
+  if (warp == 0 && lane < T) {
+    const int c = lane;
+    for (int r = 0; r < T; ++r) {
+      double2 x = cmk(r == c ? 1.0 : 0.0, 0.0);
+      if (r > c) {
+        for (int i = c; i < r; ++i) cfms(x, Dg[i * T + r], Ls[c * LD + i]);
+      } else if (r < c) {
+        x = cmk(0.0, 0.0);
+      }
+      Ls[c * LD + r] = x;
+    }
+  } else if (warp == 1 && lane < T) {
+    const int c = lane;
+    for (int r = T - 1; r >= 0; --r) {
+      double2 x = cmk(0.0, 0.0);
+      if (r <= c) {
+        x = cmk(r == c ? 1.0 : 0.0, 0.0);
+        for (int i = r + 1; i <= c; ++i) cfms(x, Dg[i * T + r], Us[c * LD + i]);
+        x = cdiv(x, Dg[r * T + r]);
+      }
+      Us[c * LD + r] = x;
+    }
+  }
+  __syncthreads();
+  double2* Dw = A + (long)(kt * nt + kt) * T2;
+  for (int i = tid; i < T2; i += LU_THREADS) {
+    const int c = i / T, r = i - c * T;
+    Dw[i] = (r > c) ? Ls[c * LD + r] : Us[c * LD + r];
+  }
+}
+
+// the step's row interchanges on every column outside the panel (zlaswp)
+__global__ void __launch_bounds__(256) lub_swap_kernel(LuGeom g, double2* F, int kt, const int* piv) {
+  __shared__ int pv[32];
+  __shared__ int any;
+  const int T = g.T, npad = g.npad, n = g.n;
+  const int slot = blockIdx.y;
+  const int c0 = kt * T;
+  if (threadIdx.x < 32) {
+    const int j = c0 + threadIdx.x;
+    pv[threadIdx.x] = (threadIdx.x < T && j < n) ? piv[(long)slot * n + j] : j;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int a = 0;
+    for (int jj = 0; jj < T; ++jj) a |= (pv[jj] != c0 + jj);
+    any = a;
+  }
+  __syncthreads();
+  if (!any) return;
+  double2* A = F + (long)slot * g.blk;
+  for (int col = blockIdx.x * blockDim.x + threadIdx.x; col < npad; col += gridDim.x * blockDim.x) {
+    if (col / T == kt) continue;
+    for (int jj = 0; jj < T; ++jj) {
+      const int j = c0 + jj, p = pv[jj];
+      if (p == j) continue;
+      const long oa = lu_off(g, j, col), ob = lu_off(g, p, col);
+      const double2 t = A[oa];
+      A[oa] = A[ob];
+      A[ob] = t;
+    }
+  }
+}
+
+// U row: A(kt, jt) = inv(L_kk) A(kt, jt) for jt > kt on DMMA (one CTA per block)
+__global__ void __launch_bounds__(LUB_WARPS * 32) lub_urow_kernel(LuGeom g, double2* F, int kt) {
+  __shared__ double2 Ls[32 * 33];
+  const int T2 = 32 * 32, nt = g.nt;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  double2* A = F + (long)blockIdx.x * g.blk;
+  const double2* Dg = A + (long)(kt * nt + kt) * T2;
+  for (int i = tid; i < T2; i += LUB_WARPS * 32) {
+    const int c = i >> 5, r = i & 31;
+    Ls[c * 33 + r] = r > c ? Dg[i] : cmk(r == c ? 1.0 : 0.0, 0.0);
+  }
+  __syncthreads();
+  const int nrem = nt - kt - 1;
+  for (int task = warp; task < 2 * nrem; task += LUB_WARPS) {
+    double2* C = A + (long)(kt * nt + kt + 1 + (task >> 1)) * T2;
+    tile_mma_half<false>(Ls, C, C, task & 1, lane);
+  }
+}
+
+// trailing update of every block: task = (block, it, jt, half), one warp each
+__global__ void __launch_bounds__(LUB_WARPS * 32, 2) lub_trail_kernel(LuGeom g, double2* F, int kt, long ntask) {
+  const int T2 = 32 * 32, nt = g.nt;
+  const int lane = threadIdx.x & 31;
+  const long task = (long)blockIdx.x * LUB_WARPS + (threadIdx.x >> 5);
+  if (task >= ntask) return;
+  const int nrem = nt - kt - 1;
+  const int h = (int)(task & 1);
+  long t2 = task >> 1;
+  const int tj = (int)(t2 % nrem);
+  t2 /= nrem;
+  const int ti = (int)(t2 % nrem);
+  const long slot = t2 / nrem;
+  double2* A = F + slot * g.blk;
+  const int it = kt + 1 + ti, jt = kt + 1 + tj;
+  tile_mma_half<true, 32>(A + (long)(it * nt + kt) * T2, A + (long)(kt * nt + jt) * T2,
+                          A + (long)(it * nt + jt) * T2, h, lane);
+}
+
+// b_perm[i] = b[perm[i]] from zgetrf's interchange sequence (one thread per block)
+__global__ void lub_perm_kernel(int nslots, int n, const int* piv, int* perm, int* scratch) {
+  const int slot = blockIdx.x * blockDim.x + threadIdx.x;
+  if (slot >= nslots) return;
+  int* pv = perm + (long)slot * n;
+  for (int i = 0; i < n; ++i) pv[i] = i;
+  const int* pp = piv + (long)slot * n;
+  for (int j = 0; j < n; ++j) {
+    const int p = pp[j];
+    if (p != j && p < n) { const int t = pv[j]; pv[j] = pv[p]; pv[p] = t; }
+  }
+  (void)scratch;
+}
+
+static int g_lu_monolithic = 0;  // vx_lu_variant(1): single-kernel LU (A/B timing)
+
+static int lu_build_batched(const Unfold& u, const LuGeom& g, int nslots, double2* F, int* perm, int* piv,
+                            int* info, cudaStream_t s) {
+  VX_CUDA(cudaMemsetAsync(info, 0, sizeof(int) * nslots, s));
+  const size_t us = (size_t)((g.npad + 3) & ~3) * sizeof(int) + (size_t)g.npad * sizeof(double2);
+  if (us > 48 * 1024)
+    VX_CUDA(cudaFuncSetAttribute(lub_unfold_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)us));
+  VX_REQUIRE((int)us <= device_smem_optin(), "block size %d too large for the unfold tables", g.n);
+  lub_unfold_kernel<<<nslots, 256, us, s>>>(u, g, F);
+  VX_CHECK_LAUNCH("lub_unfold_kernel");
+  for (int kt = 0; kt < g.nt; ++kt) {
+    lub_panel_kernel<<<nslots, LU_THREADS, 0, s>>>(g, F, kt, piv, info);
+    VX_CHECK_LAUNCH("lub_panel_kernel");
+    if (g.nt > 1) {
+      dim3 sg(div_up(g.npad, 256), nslots);
+      lub_swap_kernel<<<sg, 256, 0, s>>>(g, F, kt, piv);
+      VX_CHECK_LAUNCH("lub_swap_kernel");
+    }
+    const int nrem = g.nt - kt - 1;
+    if (nrem > 0) {
+      lub_urow_kernel<<<nslots, LUB_WARPS * 32, 0, s>>>(g, F, kt);
+      VX_CHECK_LAUNCH("lub_urow_kernel");
+      const long ntask = (long)nslots * nrem * nrem * 2;
+      lub_trail_kernel<<<(unsigned)((ntask + LUB_WARPS - 1) / LUB_WARPS), LUB_WARPS * 32, 0, s>>>(g, F, kt, ntask);
+      VX_CHECK_LAUNCH("lub_trail_kernel");
+    }
+  }
+  lub_perm_kernel<<<div_up(nslots, 128), 128, 0, s>>>(nslots, g.n, piv, perm, nullptr);
+  VX_CHECK_LAUNCH("lub_perm_kernel");
+  return VX_OK;
+}
+
 static int lu_build(const Unfold& u, int n, int nslots, double2* F, int* perm, int* piv, int* info,
                     cudaStream_t s) {
   if (nslots <= 0) return VX_OK;
   Span span("lu_build", s);
   LuGeom g = lu_geom(n);
+  if (!g_lu_monolithic) return lu_build_batched(u, g, nslots, F, perm, piv, info, s);
   size_t smem = lu_smem(g);
   // the permutation scratch reuses the staging tiles: make sure they fit npad ints
   VX_REQUIRE((size_t)g.npad * sizeof(int) <= (size_t)g.T * (g.T + 1) * sizeof(double2) &&
@@ -1199,4 +1491,9 @@ extern "C" int vx_prec1_solve(int n, int nrhs, const vx_c128* factors, const int
   VX_REQUIRE(n >= 1 && nrhs >= 1 && n_single >= 0 && n_items >= n_single, "bad solve arguments");
   return solve_items(lu_geom(n), reinterpret_cast<const double2*>(factors), perm, items, n_single, n_items, klist,
                      nrhs, reinterpret_cast<double2*>(Y), s_row, s_k, as_stream(stream));
+}
+
+extern "C" int vx_lu_variant(int monolithic) {
+  vx::g_lu_monolithic = monolithic ? 1 : 0;
+  return VX_OK;
 }
