@@ -83,12 +83,20 @@ class _Comm:
         self.d = dist
         self.group = group
 
+    @staticmethod
+    def _real(t):
+        import torch
+
+        return torch.view_as_real(t).reshape(-1) if t.is_complex() else t
+
     def all_to_all(self, out, inp, out_splits, in_splits):
-        self.d.all_to_all_single(out, inp, [int(v) for v in out_splits], [int(v) for v in in_splits],
-                                 group=self.group)
+        # complex128 travels as pairs of float64 (backend-agnostic)
+        f = 2 if out.is_complex() else 1
+        self.d.all_to_all_single(self._real(out), self._real(inp), [f * int(v) for v in out_splits],
+                                 [f * int(v) for v in in_splits], group=self.group)
 
     def all_reduce(self, t):
-        self.d.all_reduce(t, group=self.group)
+        self.d.all_reduce(self._real(t), group=self.group)
         return t
 
 
