@@ -71,9 +71,20 @@ int vx_op_padded_length(int n);
 long vx_op_work_elems(int nx, int ny, int nz, int px, int py, int pz);
 
 /* Replaces operator.apply_n / apply_system (operator.py:82-105):
- * y = N x (m == NULL) or y = x - m .* (N x), m of shape (nz, ny, nx). */
-int vx_op_apply(int nx, int ny, int nz, int px, int py, int pz, const vx_c128* spectra,
+ * y = N x (m == NULL) or y = x - m .* (N x), m of shape (nz, ny, nx).
+ * compact = 1: spectra in the symmetry-reduced layout of vx_op_compact. */
+int vx_op_apply(int nx, int ny, int nz, int px, int py, int pz, const vx_c128* spectra, int compact,
                 const vx_c128* m, const vx_c128* x, vx_c128* y, vx_c128* work, void* stream);
+
+/* Parity-symmetric kernels (every Green component even/odd in each offset
+ * coordinate, reference kernel.py:37-51) have spectra with S_p(-k) = +-S_p(k):
+ * vx_gen_asymmetry writes per-CTA (max |t(d) - s t(-d)|, max |t|) pairs (256
+ * CTAs -> 512 doubles); vx_op_compact keeps the k <= P/2 half-octant
+ * (6, pz/2+1, py/2+1, px/2+1) of full spectra. */
+int vx_gen_asymmetry(int nx, int ny, int nz, const vx_c128* gen, long g_sp, long g_sz, long g_sy, long g_sx,
+                     double* out, void* stream);
+long vx_op_compact_elems(int px, int py, int pz);
+int vx_op_compact(int px, int py, int pz, const vx_c128* full, vx_c128* compact, void* stream);
 
 /* --------------------------------------------------- 1-level preconditioner */
 /* Replaces circulant._chan_x_spectra (circulant.py:129-136): lamT (nx, 6, 2nz-1, 2ny-1),

@@ -49,7 +49,10 @@ _SIGS = {
     "vx_op_plan": (c_int, [c_int] * 6 + [P, c_long, c_long, c_long, c_long, P, P]),
     "vx_op_work_elems": (c_long, [c_int] * 6),
     "vx_op_padded_length": (c_int, [c_int]),
-    "vx_op_apply": (c_int, [c_int] * 6 + [P, P, P, P, P, P]),
+    "vx_op_apply": (c_int, [c_int] * 6 + [P, c_int, P, P, P, P, P]),
+    "vx_gen_asymmetry": (c_int, [c_int] * 3 + [P, c_long, c_long, c_long, c_long, P, P]),
+    "vx_op_compact_elems": (c_long, [c_int] * 3),
+    "vx_op_compact": (c_int, [c_int] * 3 + [P, P, P]),
     "vx_chan_x_spectra": (c_int, [c_int] * 3 + [P, c_long, c_long, c_long, c_long, P, P]),
     "vx_proxy": (c_int, [c_int] * 3 + [P, c128, P, P]),
     "vx_lu_tile": (c_int, [c_int]),

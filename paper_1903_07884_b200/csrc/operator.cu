@@ -40,14 +40,32 @@ struct LoadEmbed {
   }
 };
 
-__constant__ int c_pair_of[9] = {0, 1, 2, 1, 3, 4, 2, 4, 5};
+// PAIR_OF[a][b] (reference accel.py:41) as a constexpr so the spectral MAC
+// indexes registers, not local memory
+__host__ __device__ constexpr int pair_of(int a, int b) {
+  return a == b ? (a == 0 ? 0 : (a == 1 ? 3 : 5)) : (a + b == 1 ? 1 : (a + b == 2 ? 2 : 4));
+}
+// parity of component p (xx,xy,xz,yy,yz,zz) under a sign flip of x / y / z
+__host__ __device__ constexpr bool odd_x(int p) { return p == 1 || p == 2; }
+__host__ __device__ constexpr bool odd_y(int p) { return p == 1 || p == 4; }
+__host__ __device__ constexpr bool odd_z(int p) { return p == 2 || p == 4; }
+
+// Compact (symmetry-reduced) spectra: for a parity-symmetric kernel
+// S_p(-k) = +-S_p(k) on every axis, so only k <= P/2 is stored per axis,
+// (6, Hz, Hy, Hx) with H = P/2 + 1 -- 1/8 of the full spectra's bytes.
+struct SpecView {
+  const double2* S;
+  int compact;
+  int Pz, Py, Px, Hz, Hy, Hx;
+  FastDiv fdPx;
+};
 
 // K3: per column (ky,kx) of the padded spectrum: forward z-DFT of the three
 // components, y_a = sum_b S[PAIR_OF[a,b]] x_b, inverse z-DFT, crop.
 template <int RMAX>
 __global__ void __launch_bounds__(512, (RMAX <= 8 ? 2 : 1))
-    op_zmul_kernel(FftPlan pzp, double2* __restrict__ B, const double2* __restrict__ S, int nz, long cols,
-                   int W, FastDiv fdW3, double scale) {
+    op_zmul_kernel(FftPlan pzp, double2* __restrict__ B, SpecView sv, int nz, long cols, int W, FastDiv fdW3,
+                   double scale) {
   extern __shared__ double2 smem[];
   const int Pz = pzp.L;
   const int W3 = 3 * W;
@@ -72,15 +90,29 @@ __global__ void __launch_bounds__(512, (RMAX <= 8 ? 2 : 1))
     double2* q = smem + e * W3 + w;
     const double2 x0 = q[0], x1 = q[W], x2 = q[2 * W];
     const int kz = __ldg(pzp.k_of + e);
-    const long so = (long)kz * cols + col, sstr = (long)Pz * cols;
-    double2 s[6];
+    double2 sp[6];
+    if (!sv.compact) {
+      const long so = (long)kz * cols + col, sstr = (long)Pz * cols;
 #pragma unroll
-    for (int p = 0; p < 6; ++p) s[p] = ld_stream(S + p * sstr + so);
+      for (int p = 0; p < 6; ++p) sp[p] = ld_stream(sv.S + p * sstr + so);
+    } else {
+      const int ky = (int)sv.fdPx.div((unsigned)col), kx = (int)(col - (long)ky * sv.Px);
+      const bool mz = 2 * kz > sv.Pz, my = 2 * ky > sv.Py, mx = 2 * kx > sv.Px;
+      const int kzs = mz ? sv.Pz - kz : kz, kys = my ? sv.Py - ky : ky, kxs = mx ? sv.Px - kx : kx;
+      const long so = ((long)kzs * sv.Hy + kys) * sv.Hx + kxs;
+      const long sstr = (long)sv.Hz * sv.Hy * sv.Hx;
+#pragma unroll
+      for (int p = 0; p < 6; ++p) {
+        double2 v = ld_stream(sv.S + p * sstr + so);
+        const bool neg = (mx && odd_x(p)) ^ (my && odd_y(p)) ^ (mz && odd_z(p));
+        sp[p] = neg ? cmk(-v.x, -v.y) : v;
+      }
+    }
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
-      double2 acc = cmul(s[c_pair_of[3 * a + 0]], x0);
-      cfma(acc, s[c_pair_of[3 * a + 1]], x1);
-      cfma(acc, s[c_pair_of[3 * a + 2]], x2);
+      double2 acc = cmul(sp[pair_of(a, 0)], x0);
+      cfma(acc, sp[pair_of(a, 1)], x1);
+      cfma(acc, sp[pair_of(a, 2)], x2);
       q[a * W] = cscale(acc, scale);
     }
   }
@@ -182,7 +214,7 @@ static int op_x_forward(const FftPlan& fx, int nx, int px, int nlines, const dou
 // (crop ny), result back in A.  Spectra for these columns: (6, pz, py, nkx).
 // `scale` = 1/(px py pz) of the full transform.
 static int op_yz(const FftPlan& fy, const FftPlan& fz, int ny, int nz, int nkx, int py, int pz,
-                 const double2* spectra, double2* A, double2* B, double scale, cudaStream_t s) {
+                 const SpecView& spectra, double2* A, double2* B, double scale, cudaStream_t s) {
   int st;
   const long cols = (long)py * nkx;
   {
@@ -221,8 +253,18 @@ static int op_x_inverse(const FftPlan& fx, int nx, int px, int nlines, long line
 
 }  // namespace vx
 
+static SpecView spec_view(const vx_c128* spectra, int compact, int px, int py, int pz) {
+  SpecView v;
+  v.S = reinterpret_cast<const double2*>(spectra);
+  v.compact = compact;
+  v.Pz = pz; v.Py = py; v.Px = px;
+  v.Hz = pz / 2 + 1; v.Hy = py / 2 + 1; v.Hx = px / 2 + 1;
+  v.fdPx = FastDiv((unsigned)px);
+  return v;
+}
+
 extern "C" int vx_op_apply(int nx, int ny, int nz, int px, int py, int pz, const vx_c128* spectra,
-                           const vx_c128* m, const vx_c128* x, vx_c128* y, vx_c128* work,
+                           int compact, const vx_c128* m, const vx_c128* x, vx_c128* y, vx_c128* work,
                            void* stream) {
   int st = check_dims(nx, ny, nz, px, py, pz);
   if (st) return st;
@@ -236,7 +278,7 @@ extern "C" int vx_op_apply(int nx, int ny, int nz, int px, int py, int pz, const
   double2* B = A + 3L * nz * ny * px;
   const int lines_xyz = 3 * nz * ny;
   if ((st = op_x_forward(fx, nx, px, lines_xyz, X, A, s))) return st;
-  if ((st = op_yz(fy, fz, ny, nz, px, py, pz, reinterpret_cast<const double2*>(spectra), A, B,
+  if ((st = op_yz(fy, fz, ny, nz, px, py, pz, spec_view(spectra, compact, px, py, pz), A, B,
                   1.0 / ((double)px * py * pz), s)))
     return st;
   return op_x_inverse(fx, nx, px, lines_xyz, 0, (long)nx * ny * nz, A, X,
@@ -265,7 +307,7 @@ extern "C" int vx_op_yz(int ny, int nz, int nkx, int px, int py, int pz, const v
   FftPlan fy, fz;
   int st;
   if ((st = fft_get_plan(py, &fy)) || (st = fft_get_plan(pz, &fz))) return st;
-  return op_yz(fy, fz, ny, nz, nkx, py, pz, reinterpret_cast<const double2*>(spectra_local),
+  return op_yz(fy, fz, ny, nz, nkx, py, pz, spec_view(spectra_local, 0, nkx, py, pz),
                reinterpret_cast<double2*>(A), reinterpret_cast<double2*>(work),
                1.0 / ((double)px * py * pz), as_stream(stream));
 }
@@ -280,4 +322,77 @@ extern "C" int vx_op_x_inverse(int nx, int ny, int nz, int px, int nlines, long 
   return op_x_inverse(fx, nx, px, nlines, line0, (long)nx * ny * nz, reinterpret_cast<const double2*>(A),
                       reinterpret_cast<const double2*>(x_local), reinterpret_cast<const double2*>(m),
                       reinterpret_cast<double2*>(y_local), as_stream(stream));
+}
+
+namespace vx {
+// gather the k <= P/2 half-octant of full spectra (6, pz, py, px)
+__global__ void spec_compact_kernel(const double2* __restrict__ full, double2* __restrict__ out, int px, int py,
+                                    int pz) {
+  const int hx = px / 2 + 1, hy = py / 2 + 1, hz = pz / 2 + 1;
+  const long total = 6L * hz * hy * hx;
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < total; i += (long)gridDim.x * blockDim.x) {
+    long r = i;
+    const int kx = (int)(r % hx); r /= hx;
+    const int ky = (int)(r % hy); r /= hy;
+    const int kz = (int)(r % hz);
+    const int p = (int)(r / hz);
+    out[i] = full[(((long)p * pz + kz) * py + ky) * px + kx];
+  }
+}
+
+// per-CTA max |t_p(d) - s_p t_p(-d)| and max |t_p(d)| over the generators
+__global__ void gen_asym_kernel(const double2* __restrict__ g, long sp, long sz, long sy, long sx, int nx, int ny,
+                                int nz, double* __restrict__ out) {
+  __shared__ double sa[256], sm[256];
+  const int X = 2 * nx - 1, Y = 2 * ny - 1, Z = 2 * nz - 1;
+  const long total = 6L * Z * Y * X;
+  double amax = 0.0, tmax = 0.0;
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < total; i += (long)gridDim.x * blockDim.x) {
+    long r = i;
+    const int ix = (int)(r % X); r /= X;
+    const int iy = (int)(r % Y); r /= Y;
+    const int iz = (int)(r % Z);
+    const int p = (int)(r / Z);
+    const double2 a = g[p * sp + iz * sz + iy * sy + ix * sx];
+    const double2 b = g[p * sp + (Z - 1 - iz) * sz + (Y - 1 - iy) * sy + (X - 1 - ix) * sx];
+    const double s = ((odd_x(p) ? -1 : 1) * (odd_y(p) ? -1 : 1) * (odd_z(p) ? -1 : 1));
+    amax = fmax(amax, fmax(fabs(a.x - s * b.x), fabs(a.y - s * b.y)));
+    tmax = fmax(tmax, fmax(fabs(a.x), fabs(a.y)));
+  }
+  sa[threadIdx.x] = amax;
+  sm[threadIdx.x] = tmax;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if ((int)threadIdx.x < o) {
+      sa[threadIdx.x] = fmax(sa[threadIdx.x], sa[threadIdx.x + o]);
+      sm[threadIdx.x] = fmax(sm[threadIdx.x], sm[threadIdx.x + o]);
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    out[2 * blockIdx.x] = sa[0];
+    out[2 * blockIdx.x + 1] = sm[0];
+  }
+}
+}  // namespace vx
+
+extern "C" long vx_op_compact_elems(int px, int py, int pz) {
+  return 6L * (pz / 2 + 1) * (py / 2 + 1) * (px / 2 + 1);
+}
+
+extern "C" int vx_op_compact(int px, int py, int pz, const vx_c128* full, vx_c128* compact, void* stream) {
+  const long total = vx_op_compact_elems(px, py, pz);
+  const unsigned g = div_up(total, 256) < 8192 ? div_up(total, 256) : 8192;
+  spec_compact_kernel<<<g, 256, 0, as_stream(stream)>>>(reinterpret_cast<const double2*>(full),
+                                                        reinterpret_cast<double2*>(compact), px, py, pz);
+  VX_CHECK_LAUNCH("spec_compact_kernel");
+  return VX_OK;
+}
+
+extern "C" int vx_gen_asymmetry(int nx, int ny, int nz, const vx_c128* gen, long g_sp, long g_sz, long g_sy,
+                                long g_sx, double* out, void* stream) {
+  gen_asym_kernel<<<256, 256, 0, as_stream(stream)>>>(reinterpret_cast<const double2*>(gen), g_sp, g_sz, g_sy,
+                                                      g_sx, nx, ny, nz, out);
+  VX_CHECK_LAUNCH("gen_asym_kernel");
+  return VX_OK;
 }

@@ -119,7 +119,7 @@ class CudaBackend:
     def spectra(self, kernel):
         from .operator import plan_operator
 
-        return plan_operator(kernel).spectra_device
+        return plan_operator(kernel, compact=False).spectra_device
 
     def x_forward(self, x_loc, nl, nx, px):
         A = self.empty((nl, px))

@@ -43,17 +43,48 @@ def upload_tensors(kernel: ToeplitzKernel):
     return t
 
 
+_ODD = {"x": (1, 2), "y": (1, 4), "z": (2, 4)}  # components odd in each coordinate (xy, xz, yz)
+
+
+def _expand_compact(c: np.ndarray, shape) -> np.ndarray:
+    """Full (6, pz, py, px) spectra from the k <= P/2 half-octant (host, for inspection)."""
+    pz, py, px = shape
+    out = np.empty((6,) + tuple(shape), np.complex128)
+    kz, ky, kx = np.arange(pz), np.arange(py), np.arange(px)
+    mz, my, mx = 2 * kz > pz, 2 * ky > py, 2 * kx > px
+    iz, iy, ix = np.where(mz, pz - kz, kz), np.where(my, py - ky, ky), np.where(mx, px - kx, kx)
+    for p in range(6):
+        sgn = np.ones(shape)
+        if p in _ODD["z"]:
+            sgn = sgn * np.where(mz, -1.0, 1.0)[:, None, None]
+        if p in _ODD["y"]:
+            sgn = sgn * np.where(my, -1.0, 1.0)[None, :, None]
+        if p in _ODD["x"]:
+            sgn = sgn * np.where(mx, -1.0, 1.0)[None, None, :]
+        out[p] = sgn * c[p][np.ix_(iz, iy, ix)]
+    return out
+
+
 @dataclass(frozen=True)
 class OperatorPlan:
-    """Device-resident padded spectra (6, pz, py, px); immutable."""
+    """Device-resident spectra on the (pz, py, px) padded grid; immutable.
+
+    ``compact``: the kernel is parity-symmetric (every Green component even or
+    odd in each offset coordinate, reference kernel.py:37-51), so only the
+    k <= P/2 half-octant of the spectra is stored (1/8 of the bytes the
+    matvec streams); otherwise the full (6, pz, py, px) spectra."""
 
     grid: VoxelGrid
     k0: float
     spectra_device: object = field(repr=False)
     workers: int = 1
+    compact: bool = False
+    full_shape: tuple = None
 
     @property
     def padded_shape(self):
+        if self.full_shape is not None:
+            return tuple(self.full_shape)
         return tuple(int(v) for v in self.spectra_device.shape[1:])
 
     def storage_bytes(self) -> int:
@@ -61,14 +92,34 @@ class OperatorPlan:
 
     @property
     def spectra(self) -> np.ndarray:
-        """Host copy of the spectra (read-only numpy array, made on demand)."""
+        """Host copy of the full spectra (read-only numpy array, made on demand)."""
         h = self.spectra_device.cpu().numpy()
+        if self.compact:
+            h = _expand_compact(h, self.padded_shape)
         h.setflags(write=False)
         return h
 
 
-def plan_operator(kernel: ToeplitzKernel, workers: int = 1) -> OperatorPlan:
-    """reference operator.py:61-70."""
+SYMMETRY_RTOL = 1e-13
+
+
+def kernel_asymmetry(kernel: ToeplitzKernel) -> float:
+    """max |t_p(d) - s_p t_p(-d)| / max |t| over the generators (device reduction)."""
+    t = nv.require_cuda()
+    nx, ny, nz = kernel.grid.dims
+    gen = upload_tensors(kernel)
+    out = t.empty(512, dtype=t.float64, device="cuda")
+    s = gen.stride()
+    nv.call("vx_gen_asymmetry", nx, ny, nz, gen.data_ptr(), s[0], s[1], s[2], s[3], out.data_ptr(),
+            nv.stream_ptr())
+    o = out.cpu().numpy().reshape(-1, 2)
+    tmax = o[:, 1].max()
+    return float(o[:, 0].max() / tmax) if tmax > 0 else 0.0
+
+
+def plan_operator(kernel: ToeplitzKernel, workers: int = 1, *, compact: bool | None = None) -> OperatorPlan:
+    """reference operator.py:61-70.  ``compact=None``: use the symmetry-reduced
+    spectra when the generators are parity-symmetric to SYMMETRY_RTOL."""
     nv.require_cuda()
     nx, ny, nz = kernel.grid.dims
     px, py, pz = padded_length(nx), padded_length(ny), padded_length(nz)
@@ -77,6 +128,14 @@ def plan_operator(kernel: ToeplitzKernel, workers: int = 1) -> OperatorPlan:
     s = gen.stride()
     nv.call("vx_op_plan", nx, ny, nz, px, py, pz, gen.data_ptr(), s[0], s[1], s[2], s[3],
             spec.data_ptr(), nv.stream_ptr())
+    if compact is None:
+        compact = kernel_asymmetry(kernel) <= SYMMETRY_RTOL
+    if compact:
+        comp = nv.empty_c128((6, pz // 2 + 1, py // 2 + 1, px // 2 + 1))
+        nv.call("vx_op_compact", px, py, pz, spec.data_ptr(), comp.data_ptr(), nv.stream_ptr())
+        del spec
+        return OperatorPlan(grid=kernel.grid, k0=float(kernel.k0), spectra_device=comp, workers=workers,
+                            compact=True, full_shape=(pz, py, px))
     return OperatorPlan(grid=kernel.grid, k0=float(kernel.k0), spectra_device=spec, workers=workers)
 
 
@@ -117,7 +176,7 @@ def apply_device(plan: OperatorPlan, m_dev, x_dev, out=None):
     pz, py, px = plan.padded_shape
     y = nv.empty_c128(plan.grid.n_unknowns) if out is None else out
     work = nv.empty_c128(int(nv.query("vx_op_work_elems", nx, ny, nz, px, py, pz)))
-    nv.call("vx_op_apply", nx, ny, nz, px, py, pz, plan.spectra_device.data_ptr(),
+    nv.call("vx_op_apply", nx, ny, nz, px, py, pz, plan.spectra_device.data_ptr(), 1 if plan.compact else 0,
             nv.ptr(m_dev), x_dev.data_ptr(), y.data_ptr(), work.data_ptr(), nv.stream_ptr())
     return y
 

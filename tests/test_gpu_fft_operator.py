@@ -175,3 +175,27 @@ def test_operator_air_identity_and_concurrency(rng, golden_small):
         res = list(pool.map(lambda _: apply_system(plan, m, x), range(8)))
     for r in res:
         assert np.array_equal(r, serial)
+
+
+def test_compact_spectra_symmetric_kernel(rng, golden_small):
+    """Parity-symmetric kernels use the half-octant spectra; the result must not
+    change; asymmetric kernels (wrapped, reference circulant.py:659-669) keep
+    the full spectra."""
+    from paper_1903_07884_b200 import workloads
+    from paper_1903_07884_b200.circulant import wrap_circulant_x
+    from paper_1903_07884_b200.operator import apply_system, plan_operator
+
+    W = workloads.small(37, 7, 4, delta=0.03e-6)
+    kern = W.kernel()
+    pc = plan_operator(kern)
+    pf = plan_operator(kern, compact=False)
+    assert pc.compact and not pf.compact
+    assert pc.storage_bytes() < pf.storage_bytes() / 4
+    assert pc.padded_shape == pf.padded_shape
+    assert relerr(pc.spectra, pf.spectra) < 1e-13
+    x = random_field(rng, W.grid.n_unknowns)
+    assert relerr(apply_system(pc, W.m, x), apply_system(pf, W.m, x)) < 1e-13
+    spec = O.plan_spectra(kern.tensors, W.grid.dims)
+    assert relerr(apply_system(pc, W.m, x), O.apply_system(spec, W.grid.dims, W.m, x)) < 1e-12
+    wrapped = wrap_circulant_x(kern)
+    assert not plan_operator(wrapped).compact
