@@ -88,3 +88,116 @@ def test_sharded_path_single_rank_matches(group, tol):
                      apply_pinv=lambda v: O.apply_prec(p, v), tol=1e-8, maxit=300, restart=20)
     assert abs(rep.iterations - ro["iterations"]) <= 2
     assert relerr(xs.cpu().numpy(), xo) < 1e-6
+
+
+class LoopbackComm:
+    """TEST INFRASTRUCTURE: P simulated ranks as threads of one process on one
+    GPU.  Collectives synchronise the device, exchange through host-side slots
+    behind a threading barrier, and copy back -- no kernel ever waits on another
+    rank's kernel, so this is safe on a single GPU."""
+
+    def __init__(self, P):
+        import threading
+
+        self.P = P
+        self.bar = threading.Barrier(P)
+        self.slots = [None] * P
+
+    def view(self, rank):
+        comm = self
+
+        class _R:
+            def all_to_all(self, out, inp, out_splits, in_splits):
+                import torch
+
+                torch.cuda.synchronize()
+                chunks, o = [], 0
+                for n in in_splits:
+                    chunks.append(inp[o:o + int(n)].clone())
+                    o += int(n)
+                comm.slots[rank] = chunks
+                comm.bar.wait()
+                parts = [comm.slots[r][rank] for r in range(comm.P)]
+                assert [p.numel() for p in parts] == [int(v) for v in out_splits]
+                out.copy_(torch.cat(parts))
+                torch.cuda.synchronize()
+                comm.bar.wait()
+
+            def all_reduce(self, t):
+                import torch
+
+                torch.cuda.synchronize()
+                comm.slots[rank] = t.clone()
+                comm.bar.wait()
+                tot = comm.slots[0].clone()
+                for r in range(1, comm.P):
+                    tot += comm.slots[r]
+                comm.bar.wait()
+                t.copy_(tot)
+                torch.cuda.synchronize()
+                return t
+
+        return _R()
+
+
+@pytest.mark.parametrize("P,tol", [(2, None), (3, None), (4, 1e-3)])
+def test_sharded_cuda_backend_multi_rank_loopback(P, tol):
+    """The sharded solve with P simulated ranks (threads) on one GPU reproduces
+    the single-GPU operator, preconditioner and GMRES."""
+    import threading
+
+    import torch
+
+    from paper_1903_07884_b200 import workloads
+    from paper_1903_07884_b200.circulant import build_one_level, reduce_one_level
+    from paper_1903_07884_b200.dist import CudaBackend, DistOneLevelPrec, DistOperator, Layout, gmres_sharded
+    from paper_1903_07884_b200.operator import apply_system, padded_length, plan_operator
+    from paper_1903_07884_b200.solver import gmres
+
+    W = workloads.small(48, 6, 4, delta=0.03e-6)
+    kern = W.kernel()
+    dims = W.grid.dims
+    comm = LoopbackComm(P)
+    rng = np.random.default_rng(11)
+    x = random_field(rng, W.grid.n_unknowns)
+    results = [None] * P
+    errors = []
+
+    def run(rank):
+        try:
+            torch.cuda.set_device(0)
+            B, C = CudaBackend(), comm.view(rank)
+            L = Layout(dims, P, rank, padded_length(dims[0]))
+            op = DistOperator(kern, L, B, C)
+            prec = DistOneLevelPrec(kern, W.mtilde(), L, B, C, tol=tol)
+            m = torch.from_numpy(W.m.reshape(-1).copy()).cuda()
+            xl = torch.from_numpy(L.local_slice(x).copy()).cuda()
+            y_op = op.apply(m, xl).cpu().numpy()
+            y_pc = prec.apply(xl).cpu().numpy()
+            bl = torch.from_numpy(L.local_slice(W.b).copy()).cuda()
+            xs, rep = gmres_sharded(lambda v: op.apply(m, v), bl, B, C, apply_pinv=prec.apply, tol=1e-8,
+                                    maxit=300, restart=15)
+            results[rank] = (y_op, y_pc, xs.cpu().numpy(), rep.iterations)
+        except Exception as e:  # surface worker failures in the main thread
+            errors.append(e)
+            comm.bar.abort()
+
+    th = [threading.Thread(target=run, args=(r,)) for r in range(P)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errors, errors
+    plan = plan_operator(kern)
+    p1 = build_one_level(kern, W.mtilde())
+    p = p1 if tol is None else reduce_one_level(p1, tol)
+    y_op = np.concatenate([r[0] for r in results])
+    y_pc = np.concatenate([r[1] for r in results])
+    assert relerr(y_op, apply_system(plan, W.m, x)) < 1e-12
+    assert relerr(y_pc, p.apply(x)) < 1e-11
+    xs = np.concatenate([r[2] for r in results])
+    x1, rep1 = gmres(lambda v: apply_system(plan, W.m, v), W.b, apply_pinv=p.apply, tol=1e-8, maxit=300,
+                     restart=15)
+    assert len({r[3] for r in results}) == 1
+    assert abs(results[0][3] - rep1.iterations) <= 2
+    assert relerr(xs, x1) < 1e-6
