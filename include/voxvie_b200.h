@@ -118,6 +118,30 @@ int vx_prec1_apply(int nx, int ny, int nz, int nrhs, const vx_c128* factors, con
                    const int* items, int n_single, int n_items, const int* klist,
                    const vx_c128* x, vx_c128* y, vx_c128* work, void* stream);
 
+/* Reduced scheme, representative block (ReducedOneLevelPrec.apply,
+ * circulant.py:264-269, which calls lu_solve with the representative factor
+ * for every discarded frequency): vx_rep_inverse forms the explicit inverse of
+ * the representative block from its factors, k-major and zero padded
+ * (vx_rep_inverse_elems entries); vx_prec1_apply_reduced then solves items
+ * [0, n_single) (one frequency each) with the factors and the n_rep
+ * frequencies rep_ks with one FP64 tensor-core GEMM against that inverse, on
+ * a side stream concurrently with the single-block solves.  work holds
+ * vx_prec1_reduced_work_elems entries.  vx_rep_variant(1) runs the GEMM on
+ * the caller's stream (A/B timing). */
+long vx_rep_inverse_elems(int n);
+int vx_rep_inverse(int n, const vx_c128* factors, const int* perm, vx_c128* inv, void* stream);
+long vx_prec1_reduced_work_elems(int nx, int ny, int nz, int nrhs, int n_rep);
+int vx_prec1_apply_reduced(int nx, int ny, int nz, int nrhs, const vx_c128* factors, const int* perm,
+                           const int* items, int n_single, const int* klist, const vx_c128* inv,
+                           const int* rep_ks, int n_rep, const vx_c128* x, vx_c128* y, vx_c128* work,
+                           void* stream);
+int vx_rep_variant(int sequential);
+
+/* Operator y / z passes: 1 (default) = register-resident column FFTs for the
+ * padded lengths that have them (fft_reg.cuh), 0 = shared-memory line engine
+ * only (A/B timing and cross-checks). */
+int vx_op_reg_fft(int on);
+
 /* Select the factorisation: 0 (default) = step-batched kernels (unfold, then per
  * tile column: panel / interchanges / U row / DMMA trailing update over all
  * blocks), 1 = one CTA per block for the whole LU (A/B timing). */

@@ -78,6 +78,12 @@ _SIGS = {
     "vx_op_x_inverse": (c_int, [c_int] * 5 + [c_long, P, P, P, P, P]),
     "vx_gather_cols": (c_int, [c_long, P, c_long, c_int, P, P, c_long, P, P]),
     "vx_scatter_cols": (c_int, [c_long, P, c_int, P, P, c_long, P, c_long, P]),
+    "vx_rep_inverse_elems": (c_long, [c_int]),
+    "vx_rep_inverse": (c_int, [c_int, P, P, P, P]),
+    "vx_prec1_reduced_work_elems": (c_long, [c_int] * 5),
+    "vx_prec1_apply_reduced": (c_int, [c_int] * 4 + [P, P, P, c_int, P, P, P, c_int, P, P, P, P]),
+    "vx_rep_variant": (c_int, [c_int]),
+    "vx_op_reg_fft": (c_int, [c_int]),
     "vx_prec1_solve": (c_int, [c_int, c_int, P, P, P, c_int, c_int, P, P, c_long, c_long, P]),
     "vx_cgs_dots": (c_int, [c_long, c_int, P, c_long, P, P, P, P]),
     "vx_cgs_update": (c_int, [c_long, c_int, P, c_long, P, P, P, P, P]),

@@ -17,6 +17,8 @@ from __future__ import annotations
 
 from dataclasses import dataclass, field
 
+import os
+
 import numpy as np
 from scipy.linalg import circulant as _dense_circulant
 
@@ -346,6 +348,29 @@ class ReducedOneLevelPrec(_OneLevelBase):
         self._items = t.from_numpy(np.asarray(items, np.int32).reshape(-1).copy()).cuda()
         self._klist = t.from_numpy(np.asarray(klist, np.int32)).cuda()
         self._n_single, self._n_items = n_single, len(items)
+        # Multi-tile blocks: the representative's frequencies go through one
+        # dense GEMM with its explicit inverse (vx_rep_inverse), concurrently
+        # with the single-block solves; VX_REP_GEMM=0 keeps the chunked solves.
+        self._inv = None
+        n = self.block_size
+        if n > 32 and rep_ks.size >= 8 and os.environ.get("VX_REP_GEMM", "1") != "0":
+            inv = nv.empty_c128(int(nv.query("vx_rep_inverse_elems", n)))
+            nv.call("vx_rep_inverse", n, self._fac[rep_slot].data_ptr(), self._perm[rep_slot].data_ptr(),
+                    inv.data_ptr(), nv.stream_ptr())
+            self._inv = inv
+            self._rep_ks = t.from_numpy(rep_ks.astype(np.int32)).cuda()
+
+    def _apply_dev(self, xd, r):
+        if self._inv is None:
+            return super()._apply_dev(xd, r)
+        nx, ny, nz = self.grid.dims
+        n_rep = int(self._rep_ks.numel())
+        y = nv.empty_c128((self.grid.n_unknowns, r))
+        work = nv.empty_c128(int(nv.query("vx_prec1_reduced_work_elems", nx, ny, nz, r, n_rep)))
+        nv.call("vx_prec1_apply_reduced", nx, ny, nz, r, self._fac.data_ptr(), self._perm.data_ptr(),
+                self._items.data_ptr(), self._n_single, self._klist.data_ptr(), self._inv.data_ptr(),
+                self._rep_ks.data_ptr(), n_rep, xd.data_ptr(), y.data_ptr(), work.data_ptr(), nv.stream_ptr())
+        return y
 
     @property
     def n_kept(self) -> int:

@@ -15,6 +15,9 @@
 // identity pad.
 #include "fft_lines.cuh"
 
+#include <algorithm>
+#include <vector>
+
 namespace vx {
 
 struct LuGeom {
@@ -933,7 +936,7 @@ constexpr int PIPE_CONSUMERS = 8;
 template <int R>
 __global__ void __launch_bounds__((PIPE_CONSUMERS + 1) * 32)
     lu_solve_pipe_kernel(LuGeom g, const double2* __restrict__ F, const int* __restrict__ perm,
-                         const int* __restrict__ items, int item0, const int* __restrict__ klist,
+                         const int* __restrict__ items, int item0, int nwork, const int* __restrict__ klist,
                          int nrhs, double2* Y, long s_row, long s_k, int S) {
   extern __shared__ __align__(128) unsigned char smraw[];
   constexpr int NWC = PIPE_CONSUMERS;
@@ -949,20 +952,21 @@ __global__ void __launch_bounds__((PIPE_CONSUMERS + 1) * 32)
   double2* zb = red + NWC * T * R;         // [T][R]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
-  int slot, beg, cnt;
-  if (items) {
-    const int it = item0 + blockIdx.x;
-    slot = items[3 * it];
-    beg = items[3 * it + 1];
-    cnt = items[3 * it + 2];
-  } else {
-    slot = item0 + blockIdx.x;
-    beg = slot;
-    cnt = 1;
-  }
-  const double2* Fb = F + (long)slot * g.blk;
-  const int total = cnt * nrhs;
-  const int nchunks = (total + R - 1) / R;
+  // Work items are strided over the grid (gridDim.x == nwork unless the
+  // caller asked for a persistent grid); producer and consumers walk the same
+  // item sequence, so the ring counter t simply continues across items.
+  auto decode = [&](int w, int& slot, int& beg, int& cnt) {
+    if (items) {
+      const int it = item0 + w;
+      slot = items[3 * it];
+      beg = items[3 * it + 1];
+      cnt = items[3 * it + 2];
+    } else {
+      slot = item0 + w;
+      beg = slot;
+      cnt = 1;
+    }
+  };
 
   if (tid == 0) {
     for (int s = 0; s < S; ++s) {
@@ -977,6 +981,11 @@ __global__ void __launch_bounds__((PIPE_CONSUMERS + 1) * 32)
     // ---------------- producer: same tile order as the consumers, all chunks
     if (lane == 0) {
       long t = 0;
+      for (int w = blockIdx.x; w < nwork; w += gridDim.x) {
+      int slot, beg, cnt;
+      decode(w, slot, beg, cnt);
+      const double2* Fb = F + (long)slot * g.blk;
+      const int nchunks = (cnt * nrhs + R - 1) / R;
       for (int ch = 0; ch < nchunks; ++ch) {
         for (int ph = 0; ph < 2; ++ph) {
           for (int ii = 0; ii < nt; ++ii) {
@@ -994,12 +1003,18 @@ __global__ void __launch_bounds__((PIPE_CONSUMERS + 1) * 32)
           }
         }
       }
+      }
     }
     return;
   }
 
   // ---------------- consumers
   long t = 0;
+  for (int w = blockIdx.x; w < nwork; w += gridDim.x) {
+  int slot, beg, cnt;
+  decode(w, slot, beg, cnt);
+  const int total = cnt * nrhs;
+  const int nchunks = (total + R - 1) / R;
   for (int ch = 0; ch < nchunks; ++ch) {
     const int rho0 = ch * R;
     const int nr = min(R, total - rho0);
@@ -1128,6 +1143,7 @@ __global__ void __launch_bounds__((PIPE_CONSUMERS + 1) * 32)
     }
     consumers_sync(NC);
   }
+  }
 }
 
 // ------------------------------------------------------ single-tile blocks
@@ -1197,13 +1213,15 @@ static int launch_solve_small(const LuGeom& g, const double2* F, const int* perm
 template <int R>
 static int launch_solve_pipe(const LuGeom& g, const double2* F, const int* perm, const int* items,
                              int item0, int nblocks, const int* klist, int nrhs, double2* Y, long s_row,
-                             long s_k, cudaStream_t s) {
+                             long s_k, cudaStream_t s, int persist_per_sm = 0) {
   if (nblocks <= 0) return VX_OK;
   const size_t tile = (size_t)g.T * g.T * sizeof(double2);
   const size_t fixed = ((size_t)g.npad * R + (size_t)PIPE_CONSUMERS * g.T * R + (size_t)g.T * R) *
                        sizeof(double2);
   // two CTAs per SM when the vector state is small, otherwise one
-  const size_t budget = (fixed < 40 * 1024 ? 112 * 1024 : (size_t)device_smem_optin() - 2048);
+  static const int budget_kb = env_int("VX_PIPE_BUDGET_KB", 0);
+  size_t budget = (fixed < 40 * 1024 ? 112 * 1024 : (size_t)device_smem_optin() - 2048);
+  if (budget_kb > 0 && R == 1) budget = (size_t)budget_kb * 1024;
   int S = (int)((budget > fixed ? budget - fixed : 0) / tile);
   if (S > 16) S = 16;
   VX_REQUIRE(S >= 2, "block size %d too large for the pipelined solve", g.n);
@@ -1211,8 +1229,10 @@ static int launch_solve_pipe(const LuGeom& g, const double2* F, const int* perm,
   auto kern = lu_solve_pipe_kernel<R>;
   VX_REQUIRE((int)smem + 1024 <= device_smem_optin(), "pipelined solve smem %zu too large", smem);
   VX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  kern<<<nblocks, (PIPE_CONSUMERS + 1) * 32, smem, s>>>(g, F, perm, items, item0, klist, nrhs, Y, s_row,
-                                                        s_k, S);
+  int grid = nblocks;
+  if (persist_per_sm > 0 && grid > persist_per_sm * device_sm_count()) grid = persist_per_sm * device_sm_count();
+  kern<<<grid, (PIPE_CONSUMERS + 1) * 32, smem, s>>>(g, F, perm, items, item0, nblocks, klist, nrhs, Y, s_row,
+                                                     s_k, S);
   VX_CHECK_LAUNCH("lu_solve_pipe_kernel");
   return VX_OK;
 }
@@ -1240,14 +1260,17 @@ __global__ void cols_copy_kernel(long nrows, double2* A, long lda, int P, const 
 // kernel; larger blocks -> TMA-pipelined kernel (items [0, n_single) one RHS
 // each, the rest multi-RHS).  vx_solve_variant(1) selects the synchronous kernel.
 static int solve_items(const LuGeom& g, const double2* F, const int* perm, const int* items, int n_single,
-                       int n_items, const int* klist, int nrhs, double2* Y, long s_row, long s_k, cudaStream_t s) {
+                       int n_items, const int* klist, int nrhs, double2* Y, long s_row, long s_k, cudaStream_t s,
+                       int persist = -1) {
   int st;
   Span span("prec_solve", s);
+  static const int persist_env = env_int("VX_PIPE_PERSIST", 0);
+  if (persist < 0) persist = persist_env;
   if (g.nt == 1 && !g_solve_classic)
     return launch_solve_small(g, F, perm, items, 0, n_items, klist, nrhs, Y, s_row, s_k, s);
   const bool pipe = g.nt > 1 && !g_solve_classic;
   if (nrhs == 1)
-    st = pipe ? launch_solve_pipe<1>(g, F, perm, items, 0, n_single, klist, 1, Y, s_row, s_k, s)
+    st = pipe ? launch_solve_pipe<1>(g, F, perm, items, 0, n_single, klist, 1, Y, s_row, s_k, s, persist)
               : launch_solve<1, SOLVE_WARPS>(g, F, perm, items, 0, n_single, klist, 1, Y, s_row, s_k, s);
   else
     st = pipe ? launch_solve_pipe<MULTI_R>(g, F, perm, items, 0, n_single, klist, nrhs, Y, s_row, s_k, s)
@@ -1275,6 +1298,176 @@ __global__ void box_copy_kernel(int nx, int ny, int nz, int x0, int y0, int z0, 
     if (to_box) dst[i] = src[full];
     else dst[full] = src[i];
   }
+}
+
+
+// ------------------------------------------- representative-block GEMM
+// Reduced 1-level scheme: every discarded frequency is solved with the one
+// representative block, so those solves are ONE product D_rep^-1 * B with B =
+// the gathered spectral columns (726 x 4374 at c1r).  The explicit inverse is
+// formed once at build time (a solve against the identity with the factors),
+// and the apply becomes a dense complex GEMM on the FP64 tensor cores instead
+// of ~550 serial triangular sweeps re-reading the factor from L2.  It runs on a
+// side stream, concurrently with the HBM-bound single-block solves (disjoint
+// spectral columns).
+constexpr int RG_M = 64, RG_N = 64, RG_K = 16;
+constexpr int RG_THREADS = 256;
+
+static inline int rep_kp(int n) { return (n + RG_K - 1) / RG_K * RG_K; }
+static inline int rep_mp(int n) { return (n + RG_M - 1) / RG_M * RG_M; }
+
+__global__ void eye_cols_kernel(int n, long ld, double2* A) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) A[(long)i * ld + i] = make_double2(1.0, 0.0);
+}
+
+// Bt[k][j] (ldb = padded column count) <- S[k*s_row + ks[j/nrhs]*s_k + j%nrhs],
+// zero outside k < n, j < ncols.
+__global__ void rep_gather_kernel(int n, int Kp, int ncols, int Np, int nrhs, const int* __restrict__ ks,
+                                  const double2* __restrict__ S, long s_row, long s_k, double2* __restrict__ Bt) {
+  const long total = (long)Kp * Np;
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < total; i += (long)gridDim.x * blockDim.x) {
+    const int k = (int)(i / Np), j = (int)(i - (long)k * Np);
+    double2 v = make_double2(0.0, 0.0);
+    if (k < n && j < ncols) v = S[(long)k * s_row + (long)ks[j / nrhs] * s_k + j % nrhs];
+    Bt[i] = v;
+  }
+}
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// C = A * Bt scattered into S: A is the inverse stored k-major (A[k*lda + m],
+// Kp x lda, zero padded), Bt from rep_gather_kernel.  CTA tile 64 x 64 complex,
+// K step 16, 3-stage cp.async ring; 8 warps as 2 (m) x 4 (n), warp tile 32 x 16
+// = 4 x 2 DMMA 8x8 blocks, each complex product = 4 real DMMAs.
+__global__ void __launch_bounds__(RG_THREADS, 2)
+    rep_gemm_kernel(int n, int Kp, const double2* __restrict__ A, long lda, const double2* __restrict__ Bt,
+                    long ldb, int ncols, int nrhs, const int* __restrict__ ks, double2* S, long s_row, long s_k,
+                    int RG_STAGES) {
+  extern __shared__ __align__(128) double2 rg_sm[];
+  constexpr int TA = RG_K * RG_M, TB = RG_K * RG_N;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp & 1, wn = warp >> 1;
+  const int r4 = lane >> 2, c4 = lane & 3;
+  const int m0 = blockIdx.y * RG_M, n0 = blockIdx.x * RG_N;
+  const int nk = Kp / RG_K;
+
+  auto load_stage = [&](int kt, int st) {
+    double2* As = rg_sm + st * (TA + TB);
+    double2* Bs = As + TA;
+    const int k0 = kt * RG_K;
+#pragma unroll
+    for (int it = 0; it < TA / RG_THREADS; ++it) {
+      const int e = tid + it * RG_THREADS;
+      const int kk = e / RG_M, mm = e - kk * RG_M;
+      cp_async16(As + e, A + (long)(k0 + kk) * lda + m0 + mm);
+    }
+#pragma unroll
+    for (int it = 0; it < TB / RG_THREADS; ++it) {
+      const int e = tid + it * RG_THREADS;
+      const int kk = e / RG_N, nn = e - kk * RG_N;
+      cp_async16(Bs + e, Bt + (long)(k0 + kk) * ldb + n0 + nn);
+    }
+  };
+
+  double cr[4][2][2], ci[4][2][2];
+#pragma unroll
+  for (int rb = 0; rb < 4; ++rb)
+#pragma unroll
+    for (int cb = 0; cb < 2; ++cb) cr[rb][cb][0] = cr[rb][cb][1] = ci[rb][cb][0] = ci[rb][cb][1] = 0.0;
+
+  for (int st = 0; st < RG_STAGES - 1; ++st) {
+    if (st < nk) load_stage(st, st);
+    cp_async_commit();
+  }
+  for (int kt = 0; kt < nk; ++kt) {
+    if (RG_STAGES == 3) cp_async_wait<1>();
+    else cp_async_wait<0>();
+    __syncthreads();
+    if (kt + RG_STAGES - 1 < nk) load_stage(kt + RG_STAGES - 1, (kt + RG_STAGES - 1) % RG_STAGES);
+    cp_async_commit();
+    const double2* As = rg_sm + (kt % RG_STAGES) * (TA + TB);
+    const double2* Bs = As + TA;
+#pragma unroll
+    for (int k4 = 0; k4 < RG_K; k4 += 4) {
+      const int kk = k4 + c4;
+      double2 a[4], b[2];
+#pragma unroll
+      for (int rb = 0; rb < 4; ++rb) a[rb] = As[kk * RG_M + wm * 32 + rb * 8 + r4];
+#pragma unroll
+      for (int cb = 0; cb < 2; ++cb) b[cb] = Bs[kk * RG_N + wn * 16 + cb * 8 + r4];
+#pragma unroll
+      for (int rb = 0; rb < 4; ++rb)
+#pragma unroll
+        for (int cb = 0; cb < 2; ++cb) {
+          dmma884(cr[rb][cb][0], cr[rb][cb][1], a[rb].x, b[cb].x);
+          dmma884(cr[rb][cb][0], cr[rb][cb][1], -a[rb].y, b[cb].y);
+          dmma884(ci[rb][cb][0], ci[rb][cb][1], a[rb].x, b[cb].y);
+          dmma884(ci[rb][cb][0], ci[rb][cb][1], a[rb].y, b[cb].x);
+        }
+    }
+  }
+  cp_async_wait<0>();
+#pragma unroll
+  for (int rb = 0; rb < 4; ++rb) {
+    const int m = m0 + wm * 32 + rb * 8 + r4;
+    if (m >= n) continue;
+#pragma unroll
+    for (int cb = 0; cb < 2; ++cb)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int j = n0 + wn * 16 + cb * 8 + 2 * c4 + e;
+        if (j < ncols)
+          S[(long)m * s_row + (long)ks[j / nrhs] * s_k + j % nrhs] = make_double2(cr[rb][cb][e], ci[rb][cb][e]);
+      }
+  }
+}
+
+static int g_rep_sequential = 0;  // vx_rep_variant(1): GEMM on the main stream (A/B timing)
+
+struct SideStream {
+  cudaStream_t s = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+};
+static SideStream* side_stream() {
+  static thread_local SideStream ss;
+  if (!ss.s) {
+    if (cudaStreamCreateWithFlags(&ss.s, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ss.fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ss.join, cudaEventDisableTiming) != cudaSuccess) {
+      ss.s = nullptr;
+      return nullptr;
+    }
+  }
+  return &ss;
+}
+
+static int rep_gemm(int n, const double2* inv, int ncols, int nrhs, const int* ks, double2* S, long s_row,
+                    long s_k, double2* Bt, cudaStream_t s) {
+  const int Kp = rep_kp(n), Mp = rep_mp(n);
+  const int Np = (ncols + RG_N - 1) / RG_N * RG_N;
+  const long total = (long)Kp * Np;
+  {
+    const unsigned gb = div_up(total, 256) < 8192 ? div_up(total, 256) : 8192;
+    rep_gather_kernel<<<gb, 256, 0, s>>>(n, Kp, ncols, Np, nrhs, ks, S, s_row, s_k, Bt);
+    VX_CHECK_LAUNCH("rep_gather_kernel");
+  }
+  static const int stages = env_int("VX_RG_STAGES", 3) == 2 ? 2 : 3;
+  const size_t smem = (size_t)stages * (RG_K * RG_M + RG_K * RG_N) * sizeof(double2);
+  static bool attr = false;
+  if (!attr) {
+    VX_CUDA(cudaFuncSetAttribute(rep_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 3 * 32768));
+    attr = true;
+  }
+  dim3 grid(Np / RG_N, Mp / RG_M);
+  rep_gemm_kernel<<<grid, RG_THREADS, smem, s>>>(n, Kp, inv, Mp, Bt, Np, ncols, nrhs, ks, S, s_row, s_k, stages);
+  VX_CHECK_LAUNCH("rep_gemm_kernel");
+  return VX_OK;
 }
 
 }  // namespace vx
@@ -1495,5 +1688,103 @@ extern "C" int vx_prec1_solve(int n, int nrhs, const vx_c128* factors, const int
 
 extern "C" int vx_lu_variant(int monolithic) {
   vx::g_lu_monolithic = monolithic ? 1 : 0;
+  return VX_OK;
+}
+
+extern "C" long vx_rep_inverse_elems(int n) { return (long)rep_kp(n) * rep_mp(n); }
+
+extern "C" int vx_rep_inverse(int n, const vx_c128* factors, const int* perm, vx_c128* inv, void* stream) {
+  VX_REQUIRE(n >= 1, "bad representative-inverse arguments");
+  cudaStream_t s = as_stream(stream);
+  const int Kp = rep_kp(n), Mp = rep_mp(n);
+  double2* A = reinterpret_cast<double2*>(inv);
+  VX_CUDA(cudaMemsetAsync(A, 0, sizeof(double2) * (size_t)Kp * Mp, s));
+  eye_cols_kernel<<<div_up(n, 256), 256, 0, s>>>(n, Mp, A);
+  VX_CHECK_LAUNCH("eye_cols_kernel");
+  // column c of D^-1 = solve(D, e_c), stored k-major: A[c*Mp + m]
+  const int nit = (n + MULTI_R - 1) / MULTI_R;
+  std::vector<int> items(3 * nit), klist(n);
+  for (int c = 0; c < n; ++c) klist[c] = c;
+  for (int t = 0; t < nit; ++t) {
+    items[3 * t] = 0;
+    items[3 * t + 1] = t * MULTI_R;
+    items[3 * t + 2] = std::min(MULTI_R, n - t * MULTI_R);
+  }
+  int* dbuf = nullptr;
+  VX_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&dbuf), sizeof(int) * (items.size() + klist.size()), s));
+  VX_CUDA(cudaMemcpyAsync(dbuf, items.data(), sizeof(int) * items.size(), cudaMemcpyHostToDevice, s));
+  VX_CUDA(cudaMemcpyAsync(dbuf + items.size(), klist.data(), sizeof(int) * n, cudaMemcpyHostToDevice, s));
+  int st = solve_items(lu_geom(n), reinterpret_cast<const double2*>(factors), perm, dbuf, 0, nit,
+                       dbuf + items.size(), 1, A, 1, Mp, s);
+  VX_CUDA(cudaStreamSynchronize(s));  // host item arrays must outlive the copies
+  VX_CUDA(cudaFreeAsync(dbuf, s));
+  return st;
+}
+
+extern "C" long vx_prec1_reduced_work_elems(int nx, int ny, int nz, int nrhs, int n_rep) {
+  const int n = 3 * ny * nz;
+  const long np = ((long)n_rep * nrhs + RG_N - 1) / RG_N * RG_N;
+  return 3L * nx * ny * nz * nrhs + (long)rep_kp(n) * np;
+}
+
+extern "C" int vx_prec1_apply_reduced(int nx, int ny, int nz, int nrhs, const vx_c128* factors, const int* perm,
+                                      const int* items, int n_single, const int* klist, const vx_c128* inv,
+                                      const int* rep_ks, int n_rep, const vx_c128* x, vx_c128* y,
+                                      vx_c128* work, void* stream) {
+  VX_REQUIRE(nx >= 1 && ny >= 1 && nz >= 1 && nrhs >= 1 && n_single >= 0 && n_rep >= 0,
+             "bad reduced 1-level apply arguments");
+  cudaStream_t s = as_stream(stream);
+  Span span("prec_apply", s);
+  FftPlan p;
+  int st = fft_get_plan(nx, &p);
+  if (st) return st;
+  const int q3 = 3 * ny * nz;
+  double2* S = reinterpret_cast<double2*>(work);
+  double2* Bt = S + 3L * nx * ny * nz * nrhs;
+  const long pitch = (long)nx * nrhs;
+  {
+    LoadStrided ld{reinterpret_cast<const double2*>(x), {pitch, 1, nrhs, nrhs}};
+    StoreStrided sv{S, {pitch, 1, nrhs, nrhs}, 1.0};
+    if ((st = launch_fft_lines(p, ld, sv, q3 * nrhs, nx, nx, false, nrhs == 1, s))) return st;
+  }
+  LuGeom g = lu_geom(q3);
+  const double2* F = reinterpret_cast<const double2*>(factors);
+  {
+    Span span2("prec_solve", s);
+    SideStream* ss = g_rep_sequential ? nullptr : side_stream();
+    cudaStream_t sr = ss ? ss->s : s;
+    if (ss && n_rep > 0) {
+      VX_CUDA(cudaEventRecord(ss->fork, s));
+      VX_CUDA(cudaStreamWaitEvent(sr, ss->fork, 0));
+    }
+    static const int singles_first = env_int("VX_REP_ORDER", 1);
+    // VX_REP_PERSIST=k: k single-block solver CTAs per SM (A/B; one CTA per SM
+    // cannot keep enough bytes in flight, so the default is the plain grid)
+    static const int rep_persist = env_int("VX_REP_PERSIST", 0);
+    const int persist = (ss && n_rep > 0) ? rep_persist : -1;
+    if (singles_first && n_single > 0 &&
+        (st = solve_items(g, F, perm, items, n_single, n_single, klist, nrhs, S, pitch, nrhs, s, persist)))
+      return st;
+    if (n_rep > 0 &&
+        (st = rep_gemm(q3, reinterpret_cast<const double2*>(inv), n_rep * nrhs, nrhs, rep_ks, S, pitch, nrhs, Bt, sr)))
+      return st;
+    if (!singles_first && n_single > 0 &&
+        (st = solve_items(g, F, perm, items, n_single, n_single, klist, nrhs, S, pitch, nrhs, s, persist)))
+      return st;
+    if (ss && n_rep > 0) {
+      VX_CUDA(cudaEventRecord(ss->join, sr));
+      VX_CUDA(cudaStreamWaitEvent(s, ss->join, 0));
+    }
+  }
+  {
+    LoadStrided ld{S, {pitch, 1, nrhs, nrhs}};
+    StoreStrided sv{reinterpret_cast<double2*>(y), {pitch, 1, nrhs, nrhs}, 1.0 / nx};
+    if ((st = launch_fft_lines(p, ld, sv, q3 * nrhs, nx, nx, true, nrhs == 1, s))) return st;
+  }
+  return VX_OK;
+}
+
+extern "C" int vx_rep_variant(int sequential) {
+  vx::g_rep_sequential = sequential ? 1 : 0;
   return VX_OK;
 }

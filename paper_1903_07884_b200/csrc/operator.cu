@@ -10,6 +10,7 @@
 // Zero padding and cropping happen in the loaders/storers, so the padded
 // volume is only touched where it carries data.
 #include "fft_lines.cuh"
+#include "fft_reg.cuh"
 
 namespace vx {
 
@@ -197,9 +198,118 @@ extern "C" int vx_op_padded_length(int n) {
 extern "C" long vx_op_work_elems(int nx, int ny, int nz, int px, int py, int pz) {
   (void)pz;
   return 3L * nz * px * ((long)ny + py);
+
 }
 
 namespace vx {
+
+// K3 with the z-transforms in registers (pz <= REG_ZMUL_MAX): one thread per column
+// (ky,kx), the three components' z-lines held in registers, natural order.
+template <int PZ>
+__global__ void __launch_bounds__(128)
+    op_zmul_reg_kernel(double2* __restrict__ B, SpecView sv, int nz, long cols, double scale) {
+  const long col = blockIdx.x * (long)blockDim.x + threadIdx.x;
+  if (col >= cols) return;
+  double2 x[3][PZ];
+#pragma unroll
+  for (int c = 0; c < 3; ++c)
+#pragma unroll
+    for (int e = 0; e < PZ; ++e) x[c][e] = (e < nz) ? __ldg(B + ((long)c * nz + e) * cols + col) : cmk(0.0, 0.0);
+#pragma unroll
+  for (int c = 0; c < 3; ++c) reg_fft<PZ, false>(x[c]);
+  long so0 = col, sstr = (long)PZ * cols, kstr = cols;
+  bool my = false, mx = false;
+  if (sv.compact) {
+    const int ky = (int)sv.fdPx.div((unsigned)col), kx = (int)(col - (long)ky * sv.Px);
+    my = 2 * ky > sv.Py;
+    mx = 2 * kx > sv.Px;
+    so0 = (long)(my ? sv.Py - ky : ky) * sv.Hx + (mx ? sv.Px - kx : kx);
+    sstr = (long)sv.Hz * sv.Hy * sv.Hx;
+    kstr = (long)sv.Hy * sv.Hx;
+  }
+#pragma unroll
+  for (int kz = 0; kz < PZ; ++kz) {
+    double2 sp[6];
+    if (!sv.compact) {
+#pragma unroll
+      for (int p = 0; p < 6; ++p) sp[p] = ld_stream(sv.S + p * sstr + (long)kz * kstr + so0);
+    } else {
+      const bool mz = 2 * kz > PZ;
+      const long so = (long)(mz ? PZ - kz : kz) * kstr + so0;
+#pragma unroll
+      for (int p = 0; p < 6; ++p) {
+        const double2 v = ld_stream(sv.S + p * sstr + so);
+        const bool neg = (mx && odd_x(p)) ^ (my && odd_y(p)) ^ (mz && odd_z(p));
+        sp[p] = neg ? cmk(-v.x, -v.y) : v;
+      }
+    }
+    const double2 x0 = x[0][kz], x1 = x[1][kz], x2 = x[2][kz];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      double2 acc = cmul(sp[pair_of(a, 0)], x0);
+      cfma(acc, sp[pair_of(a, 1)], x1);
+      cfma(acc, sp[pair_of(a, 2)], x2);
+      x[a][kz] = cscale(acc, scale);
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < 3; ++c) reg_fft<PZ, true>(x[c]);
+#pragma unroll
+  for (int c = 0; c < 3; ++c)
+#pragma unroll
+    for (int e = 0; e < PZ; ++e)
+      if (e < nz) B[((long)c * nz + e) * cols + col] = x[c][e];
+}
+
+constexpr int REG_ZMUL_MAX = 8;  // larger pz spill (3 components x pz live)
+
+static int g_reg_fft = -1;  // -1: from VX_REG_FFT (default on); vx_op_reg_fft() overrides
+static bool reg_fft_enabled() {
+  if (g_reg_fft < 0) g_reg_fft = env_int("VX_REG_FFT", 1) != 0;
+  return g_reg_fft != 0;
+}
+
+template <bool INV>
+static int launch_reg_cols(int L, const double2* in, long in_os, long in_es, int n_in, double2* out, long out_os,
+                           long out_es, int n_out, long ncols, int n_inner, double scale, cudaStream_t s) {
+  if (ncols <= 0) return VX_OK;
+  const unsigned grid = (unsigned)div_up(ncols, 128);
+  const FastDiv fd((unsigned)n_inner);
+  switch (L) {
+#define VX_REG_LAUNCH(N)                                                                              \
+  case N:                                                                                             \
+    reg_cols_kernel<N, INV><<<grid, 128, 0, s>>>(in, in_os, in_es, n_in, out, out_os, out_es, n_out, \
+                                                 ncols, fd, n_inner, scale);                          \
+    break;
+    VX_REG_LENGTHS(VX_REG_LAUNCH)
+#undef VX_REG_LAUNCH
+    default:
+      set_error("no register FFT for length %d", L);
+      return VX_EINVAL;
+  }
+  VX_CHECK_LAUNCH("reg_cols_kernel");
+  return VX_OK;
+}
+
+static int launch_zmul_reg(int PZ, double2* B, const SpecView& sv, int nz, long cols, double scale,
+                           cudaStream_t s) {
+  const unsigned grid = (unsigned)div_up(cols, 128);
+  switch (PZ) {
+#define VX_ZREG_LAUNCH(N)                                                   \
+  case N:                                                                   \
+    if constexpr (N <= REG_ZMUL_MAX)                                        \
+      op_zmul_reg_kernel<N><<<grid, 128, 0, s>>>(B, sv, nz, cols, scale);   \
+    break;
+    VX_REG_LENGTHS(VX_ZREG_LAUNCH)
+#undef VX_ZREG_LAUNCH
+    default:
+      set_error("no register z-multiply for length %d", PZ);
+      return VX_EINVAL;
+  }
+  VX_CHECK_LAUNCH("op_zmul_reg_kernel");
+  return VX_OK;
+}
+
 
 // K1: forward x-DFT of nlines contiguous x-lines, zero-padded nx -> px.
 static int op_x_forward(const FftPlan& fx, int nx, int px, int nlines, const double2* X, double2* A,
@@ -217,12 +327,19 @@ static int op_yz(const FftPlan& fy, const FftPlan& fz, int ny, int nz, int nkx, 
                  const SpecView& spectra, double2* A, double2* B, double scale, cudaStream_t s) {
   int st;
   const long cols = (long)py * nkx;
-  {
+  const bool reg_y = reg_fft_enabled() && reg_fft_supported(py);
+  const bool reg_z = reg_fft_enabled() && reg_fft_supported(pz) && pz <= REG_ZMUL_MAX;
+  if (reg_y) {
+    if ((st = launch_reg_cols<false>(py, A, (long)ny * nkx, nkx, ny, B, cols, nkx, py, 3L * nz * nkx, nkx, 1.0, s)))
+      return st;
+  } else {
     LoadStrided ld{A, {(long)ny * nkx, 1, nkx, nkx}};
     StoreStrided sv{B, {cols, 1, nkx, nkx}, 1.0};
     if ((st = launch_fft_lines(fy, ld, sv, 3 * nz * nkx, ny, py, false, false, s))) return st;
   }
-  {
+  if (reg_z) {
+    if ((st = launch_zmul_reg(pz, B, spectra, nz, cols, scale, s))) return st;
+  } else {
     static const int zw = env_int("VX_ZMUL_W", 64);
     int W = zw;
     while (W > 1 && (long)W > cols) W /= 2;
@@ -234,7 +351,10 @@ static int op_yz(const FftPlan& fy, const FftPlan& fz, int ny, int nz, int nkx, 
     kern<<<div_up(cols, W), thr, smem, s>>>(fz, B, spectra, nz, cols, W, FastDiv(3 * W), scale);
     VX_CHECK_LAUNCH("op_zmul_kernel");
   }
-  {
+  if (reg_y) {
+    if ((st = launch_reg_cols<true>(py, B, cols, nkx, py, A, (long)ny * nkx, nkx, ny, 3L * nz * nkx, nkx, 1.0, s)))
+      return st;
+  } else {
     LoadStrided ld{B, {cols, 1, nkx, nkx}};
     StoreStrided sv{A, {(long)ny * nkx, 1, nkx, nkx}, 1.0};
     if ((st = launch_fft_lines(fy, ld, sv, 3 * nz * nkx, py, ny, true, false, s))) return st;
@@ -394,5 +514,10 @@ extern "C" int vx_gen_asymmetry(int nx, int ny, int nz, const vx_c128* gen, long
   gen_asym_kernel<<<256, 256, 0, as_stream(stream)>>>(reinterpret_cast<const double2*>(gen), g_sp, g_sz, g_sy,
                                                       g_sx, nx, ny, nz, out);
   VX_CHECK_LAUNCH("gen_asym_kernel");
+  return VX_OK;
+}
+
+extern "C" int vx_op_reg_fft(int on) {
+  vx::g_reg_fft = on ? 1 : 0;
   return VX_OK;
 }

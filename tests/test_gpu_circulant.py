@@ -327,3 +327,35 @@ def test_two_level_vs_oracle_disk_like(rng, C):
     ref = O.build_two_level(kern.tensors, W.grid.dims, m)
     x = random_field(rng, W.grid.n_unknowns)
     assert relerr(p.apply(x), O.apply_prec(ref, x)) < 1e-10
+
+
+@pytest.mark.parametrize("dims,tol", [((60, 7, 3), 0.05), ((40, 12, 4), 1e-3), ((24, 22, 11), 1e-3)])
+def test_reduced_representative_gemm_path(rng, C, monkeypatch, dims, tol):
+    """The representative block's frequencies through the explicit-inverse GEMM
+    equal the chunked triangular solves and the oracle (1 and 3 RHS; block
+    sizes 63, 144, 726 exercise the K/M padding)."""
+    from paper_1903_07884_b200 import workloads
+
+    W = workloads.small(*dims, delta=0.02e-6)
+    kern = W.kernel()
+    full = C.build_one_level(kern, W.mtilde())
+    red = C.reduce_one_level(full, tol)
+    assert red._inv is not None and red._rep_ks.numel() >= 8
+    monkeypatch.setenv("VX_REP_GEMM", "0")
+    red0 = C.reduce_one_level(full, tol)
+    assert red0._inv is None
+    ref = O.reduce_one_level(O.build_one_level(kern.tensors, W.grid.dims, W.mtilde()), tol)
+    n = W.grid.n_unknowns
+    for r in (1, 3):
+        x = random_field(rng, n * r).reshape(n, r) if r > 1 else random_field(rng, n)
+        a, b = red.apply(x), red0.apply(x)
+        assert relerr(a, b) < 1e-12
+        assert relerr(a, O.apply_prec(ref, x)) < 1e-10
+    from paper_1903_07884_b200 import _native as nv
+
+    nv.call("vx_rep_variant", 1)
+    try:
+        x = random_field(rng, n)
+        assert relerr(red.apply(x), red0.apply(x)) < 1e-12
+    finally:
+        nv.call("vx_rep_variant", 0)

@@ -199,3 +199,28 @@ def test_compact_spectra_symmetric_kernel(rng, golden_small):
     assert relerr(apply_system(pc, W.m, x), O.apply_system(spec, W.grid.dims, W.m, x)) < 1e-12
     wrapped = wrap_circulant_x(kern)
     assert not plan_operator(wrapped).compact
+
+
+@pytest.mark.parametrize("ny", list(range(1, 30)))
+def test_operator_register_fft_lengths(rng, ny):
+    """Every register-FFT length (padded y = 2..56, and pz <= 8 for the
+    register z-multiply) against the oracle and against the shared-memory
+    engine (vx_op_reg_fft(0))."""
+    from paper_1903_07884_b200 import _native as nv
+    from paper_1903_07884_b200 import workloads
+    from paper_1903_07884_b200.operator import apply_system, plan_operator
+
+    nz = 1 + ny % 4
+    W = workloads.small(6, ny, nz, delta=0.03e-6)
+    plan = plan_operator(W.kernel())
+    x = random_field(rng, W.grid.n_unknowns)
+    spec = O.plan_spectra(W.kernel().tensors, W.grid.dims)
+    ref = O.apply_system(spec, W.grid.dims, W.m, x)
+    y_reg = apply_system(plan, W.m, x)
+    nv.call("vx_op_reg_fft", 0)
+    try:
+        y_smem = apply_system(plan, W.m, x)
+    finally:
+        nv.call("vx_op_reg_fft", 1)
+    assert relerr(y_reg, ref) < 1e-12
+    assert relerr(y_reg, y_smem) < 1e-13
