@@ -203,20 +203,36 @@ extern "C" long vx_op_work_elems(int nx, int ny, int nz, int px, int py, int pz)
 
 namespace vx {
 
-// K3 with the z-transforms in registers (pz <= REG_ZMUL_MAX): one thread per column
-// (ky,kx), the three components' z-lines held in registers, natural order.
+// K3 with register z-transforms: one thread per column (ky,kx), 64 columns
+// per CTA.  Each component's z-line is transformed in registers one at a time
+// (holding all three would spill) and parked in the thread's private slice of
+// shared memory ([c][kz][thread]: conflict-free, no barriers), then the
+// spectral multiply runs kz by kz, then the inverse transforms.
+constexpr int ZR_T = 64;
+
 template <int PZ>
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(ZR_T)
     op_zmul_reg_kernel(double2* __restrict__ B, SpecView sv, int nz, long cols, double scale) {
-  const long col = blockIdx.x * (long)blockDim.x + threadIdx.x;
+  extern __shared__ double2 zr_sm[];
+  const int tid = threadIdx.x;
+  long col = blockIdx.x * (long)ZR_T + tid;
   if (col >= cols) return;
-  double2 x[3][PZ];
+  if (sv.compact) {
+    // launch rows ky = 0, 1, Py-1, 2, Py-2, ...: a row and its mirror (same
+    // compact spectra) run back to back, so the second read hits L2
+    const int lr = (int)sv.fdPx.div((unsigned)col);
+    const int ky = (lr == 0) ? 0 : ((lr & 1) ? (lr + 1) / 2 : sv.Py - lr / 2);
+    col += (long)(ky - lr) * sv.Px;
+  }
+#pragma unroll 1
+  for (int c = 0; c < 3; ++c) {
+    double2 v[PZ];
 #pragma unroll
-  for (int c = 0; c < 3; ++c)
+    for (int e = 0; e < PZ; ++e) v[e] = (e < nz) ? __ldg(B + ((long)c * nz + e) * cols + col) : cmk(0.0, 0.0);
+    reg_fft<PZ, false>(v);
 #pragma unroll
-    for (int e = 0; e < PZ; ++e) x[c][e] = (e < nz) ? __ldg(B + ((long)c * nz + e) * cols + col) : cmk(0.0, 0.0);
-#pragma unroll
-  for (int c = 0; c < 3; ++c) reg_fft<PZ, false>(x[c]);
+    for (int e = 0; e < PZ; ++e) zr_sm[(c * PZ + e) * ZR_T + tid] = v[e];
+  }
   long so0 = col, sstr = (long)PZ * cols, kstr = cols;
   bool my = false, mx = false;
   if (sv.compact) {
@@ -227,7 +243,7 @@ __global__ void __launch_bounds__(128)
     sstr = (long)sv.Hz * sv.Hy * sv.Hx;
     kstr = (long)sv.Hy * sv.Hx;
   }
-#pragma unroll
+#pragma unroll 7
   for (int kz = 0; kz < PZ; ++kz) {
     double2 sp[6];
     if (!sv.compact) {
@@ -243,25 +259,29 @@ __global__ void __launch_bounds__(128)
         sp[p] = neg ? cmk(-v.x, -v.y) : v;
       }
     }
-    const double2 x0 = x[0][kz], x1 = x[1][kz], x2 = x[2][kz];
+    double2* q = zr_sm + kz * ZR_T + tid;
+    const double2 x0 = q[0], x1 = q[PZ * ZR_T], x2 = q[2 * PZ * ZR_T];
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
       double2 acc = cmul(sp[pair_of(a, 0)], x0);
       cfma(acc, sp[pair_of(a, 1)], x1);
       cfma(acc, sp[pair_of(a, 2)], x2);
-      x[a][kz] = cscale(acc, scale);
+      q[a * PZ * ZR_T] = cscale(acc, scale);
     }
   }
+#pragma unroll 1
+  for (int c = 0; c < 3; ++c) {
+    double2 v[PZ];
 #pragma unroll
-  for (int c = 0; c < 3; ++c) reg_fft<PZ, true>(x[c]);
-#pragma unroll
-  for (int c = 0; c < 3; ++c)
+    for (int e = 0; e < PZ; ++e) v[e] = zr_sm[(c * PZ + e) * ZR_T + tid];
+    reg_fft<PZ, true>(v);
 #pragma unroll
     for (int e = 0; e < PZ; ++e)
-      if (e < nz) B[((long)c * nz + e) * cols + col] = x[c][e];
+      if (e < nz) B[((long)c * nz + e) * cols + col] = v[e];
+  }
 }
 
-constexpr int REG_ZMUL_MAX = 8;  // larger pz spill (3 components x pz live)
+constexpr int REG_ZMUL_MAX = 32;  // longer z-lines spill; they keep the smem kernel
 
 static int g_reg_fft = -1;  // -1: from VX_REG_FFT (default on); vx_op_reg_fft() overrides
 static bool reg_fft_enabled() {
@@ -293,12 +313,17 @@ static int launch_reg_cols(int L, const double2* in, long in_os, long in_es, int
 
 static int launch_zmul_reg(int PZ, double2* B, const SpecView& sv, int nz, long cols, double scale,
                            cudaStream_t s) {
-  const unsigned grid = (unsigned)div_up(cols, 128);
+  const unsigned grid = (unsigned)div_up(cols, ZR_T);
+  const size_t smem = (size_t)3 * PZ * ZR_T * sizeof(double2);
   switch (PZ) {
-#define VX_ZREG_LAUNCH(N)                                                   \
-  case N:                                                                   \
-    if constexpr (N <= REG_ZMUL_MAX)                                        \
-      op_zmul_reg_kernel<N><<<grid, 128, 0, s>>>(B, sv, nz, cols, scale);   \
+#define VX_ZREG_LAUNCH(N)                                                                            \
+  case N:                                                                                            \
+    if constexpr (N <= REG_ZMUL_MAX) {                                                               \
+      if (smem > 48 * 1024)                                                                          \
+        VX_CUDA(cudaFuncSetAttribute(op_zmul_reg_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                     (int)smem));                                                    \
+      op_zmul_reg_kernel<N><<<grid, ZR_T, smem, s>>>(B, sv, nz, cols, scale);                        \
+    }                                                                                                \
     break;
     VX_REG_LENGTHS(VX_ZREG_LAUNCH)
 #undef VX_ZREG_LAUNCH

@@ -21,6 +21,8 @@ a CUDA tensor -> ``x`` as a CUDA tensor.
 
 from __future__ import annotations
 
+import os
+import threading
 import time
 from dataclasses import dataclass, field
 
@@ -91,12 +93,14 @@ class _Callable:
 class _Krylov:
     """Device workspace: basis V (grown on demand), Arnoldi scratch, pinned mirrors."""
 
-    def __init__(self, n, m):
+    def __init__(self, n, m, keep_z=False):
         self.t = nv.require_cuda()
         self.n = n
         self.cap = 0
         self.maxrows = m + 1
         self.V = None
+        self.Z = None
+        self.keep_z = keep_z
         self._grow(min(m + 1, 32))
         self.h = nv.empty_c128(m + 2)
         self.stats = self.t.zeros(4, dtype=self.t.float64, device="cuda")
@@ -112,6 +116,11 @@ class _Krylov:
         V = nv.empty_c128((rows, self.n))
         if self.V is not None:
             V[: self.cap].copy_(self.V)
+        if self.keep_z:
+            Z = nv.empty_c128((rows, self.n))
+            if self.Z is not None:
+                Z[: self.cap].copy_(self.Z)
+            self.Z = Z
         self.V, self.cap = V, rows
 
     def row(self, i):
@@ -132,6 +141,33 @@ class _Krylov:
         nv.call("vx_axpby", self.n, nv.cval(a), x.data_ptr(), nv.cval(b), nv.ptr(y), out.data_ptr(),
                 nv.stream_ptr())
         return out
+
+
+_WS_LOCK = threading.Lock()
+_WS_CACHE: dict = {}
+
+
+def _workspace(n, m, keep_z):
+    """A reusable Krylov workspace (bases of up to m+1 rows); one per shape,
+    handed to one solve at a time, so repeated solves do not re-allocate
+    gigabytes of basis every call."""
+    key = (nv.require_cuda().cuda.current_device(), n, m, keep_z)
+    with _WS_LOCK:
+        K = _WS_CACHE.pop(key, None)
+    return K if K is not None else _Krylov(n, m, keep_z=keep_z)
+
+
+def _release(K):
+    key = (K.t.cuda.current_device(), K.n, K.maxrows - 1, K.keep_z)
+    with _WS_LOCK:
+        _WS_CACHE.clear()  # keep at most one cached workspace
+        _WS_CACHE[key] = K
+
+
+def clear_workspace() -> None:
+    """Drop the cached Krylov workspace (its device memory returns to torch)."""
+    with _WS_LOCK:
+        _WS_CACHE.clear()
 
 
 def _aliases(a, b) -> bool:
@@ -174,15 +210,31 @@ class GivensQR:
         return np.linalg.solve(r_mat, np.asarray(self.g[:j], dtype=np.complex128))
 
 
-def _gmres_cycle(K: _Krylov, op, r0, beta, bnorm, tol, m, residuals):
-    """One Arnoldi/Givens cycle (reference solver.py:45-111)."""
+def _gmres_cycle(K: _Krylov, op, r0, beta, bnorm, tol, m, residuals, P=None, A=None):
+    """One Arnoldi/Givens cycle (reference solver.py:45-111).
+
+    With ``K.keep_z`` the preconditioned vectors z_j = P^-1 v_j that the
+    operator needs anyway are kept, and the cycle returns u = Z y = P^-1 V y
+    (the reference's correction, solver.py:106-110 then 160-161) without the
+    extra preconditioner apply per cycle."""
     t = K.t
+    if K.keep_z:
+        def op(v):
+            z = P(v)
+            K.Z[op.j].copy_(z)  # row op.j of Z, set by the loop below
+            return A(z)
+    else:
+        op_base = op
+
+        def op(v):
+            return op_base(v)
     K.row(0)
     K.axpby(1.0 / beta, r0, 0.0, None, out=K.V[0])
     qr = GivensQR(beta)
     converged = lucky = False
     j = 0
     while j < m:
+        op.j = j
         w = op(K.V[j])
         K.row(j + 1)
         if _aliases(w, K.V) or not w.is_contiguous():
@@ -209,7 +261,8 @@ def _gmres_cycle(K: _Krylov, op, r0, beta, bnorm, tol, m, residuals):
     y = qr.solve(j)
     yd = nv.device_c128(y)
     u = nv.empty_c128(K.n)
-    nv.call("vx_basis_combine", K.n, j, K.V.data_ptr(), K.n, yd.data_ptr(), u.data_ptr(), nv.stream_ptr())
+    basis = K.Z if K.keep_z else K.V
+    nv.call("vx_basis_combine", K.n, j, basis.data_ptr(), K.n, yd.data_ptr(), u.data_ptr(), nv.stream_ptr())
     return u, j, converged
 
 
@@ -226,7 +279,13 @@ def gmres(apply_a, b, *, apply_pinv=None, tol: float = 1e-4, maxit: int = 2000,
     bd = nv.device_c128(b.reshape(-1) if on_device else np.asarray(b, np.complex128).reshape(-1))
     n = bd.numel()
     mmax = maxit if restart is None else min(restart, maxit)
-    K = _Krylov(n, mmax)
+    # keep Z = P^-1 V when a preconditioner is given and a second basis fits
+    # comfortably (a quarter of the free device memory)
+    keep_z = False
+    if apply_pinv is not None and os.environ.get("VX_KEEP_Z", "1") != "0":
+        free, _ = t.cuda.mem_get_info()
+        keep_z = (mmax + 1) * n * 16 <= free // 4
+    K = _workspace(n, mmax, keep_z)
     bnorm = K.norm(bd)
 
     def _out(xd):
@@ -235,6 +294,7 @@ def gmres(apply_a, b, *, apply_pinv=None, tol: float = 1e-4, maxit: int = 2000,
     if bnorm == 0.0:
         x = t.zeros(n, dtype=t.complex128, device="cuda")
         t.cuda.current_stream().synchronize()
+        _release(K)
         return _out(x), SolveReport(iterations=1, residuals=[1.0, 0.0], converged=True,
                                     solve_seconds=time.perf_counter() - t0, true_residual=0.0)
     A = _Callable(apply_a, n)
@@ -251,10 +311,11 @@ def gmres(apply_a, b, *, apply_pinv=None, tol: float = 1e-4, maxit: int = 2000,
             converged = True
             break
         m = maxit - total if restart is None else min(restart, maxit - total)
-        u, used, converged = _gmres_cycle(K, op, r0, beta, bnorm, tol, m, residuals)
+        u, used, converged = _gmres_cycle(K, op, r0, beta, bnorm, tol, m, residuals, P=P, A=A)
         total += used
-        x = K.axpby(1.0, x, 1.0, u if P is None else P(u))
+        x = K.axpby(1.0, x, 1.0, u if (P is None or K.keep_z) else P(u))
     true_res = K.norm(K.axpby(1.0, bd, -1.0, A(x))) / bnorm
+    _release(K)
     report = SolveReport(iterations=int(total), residuals=residuals, converged=bool(converged),
                          solve_seconds=time.perf_counter() - t0, true_residual=float(true_res))
     return _out(x), report
