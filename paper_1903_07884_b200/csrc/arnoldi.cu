@@ -159,7 +159,8 @@ __global__ void __launch_bounds__(AR_THREADS) finalize_kernel(int nvec, int G, c
   if ((mode == 2 || mode == 3) && stats[2] == 0.0) return;
   __shared__ double2 sh[AR_THREADS / 32];
   const int rows = (mode == 0) ? nvec + 1 : (mode == 2 ? nvec : 1);
-  for (int i = 0; i < rows; ++i) {
+  // one CTA per row (grid-strided): each row is summed in the same fixed order
+  for (int i = blockIdx.x; i < rows; i += gridDim.x) {
     double2 v = cmk(0.0, 0.0);
     for (int b = threadIdx.x; b < G; b += AR_THREADS) v = cadd(v, part[(long)i * G + b]);
     v = block_sum(v, sh);
@@ -185,7 +186,7 @@ __global__ void __launch_bounds__(AR_THREADS) finalize_kernel(int nvec, int G, c
 __global__ void __launch_bounds__(AR_THREADS) sum_rows_kernel(int rows, int G, const double2* __restrict__ part,
                                                               double2* __restrict__ out) {
   __shared__ double2 sh[AR_THREADS / 32];
-  for (int i = 0; i < rows; ++i) {
+  for (int i = blockIdx.x; i < rows; i += gridDim.x) {
     double2 v = cmk(0.0, 0.0);
     for (int b = threadIdx.x; b < G; b += AR_THREADS) v = cadd(v, part[(long)i * G + b]);
     v = block_sum(v, sh);
@@ -282,12 +283,12 @@ extern "C" int vx_arnoldi_step(long n, int nvec, const vx_c128* V, long ldv, vx_
   double2* pd = reinterpret_cast<double2*>(part);
   double2* cd = pd + (long)(nvec + 2) * G;  // second-pass coefficients
   dots_kernel<<<G, AR_THREADS, 0, s>>>(n, nvec, Vd, ldv, wd, pd, nullptr);
-  finalize_kernel<<<1, AR_THREADS, 0, s>>>(nvec, G, pd, hd, cd, stats, 0);
+  finalize_kernel<<<nvec + 1, AR_THREADS, 0, s>>>(nvec, G, pd, hd, cd, stats, 0);
   update_kernel<<<G, AR_THREADS, 0, s>>>(n, nvec, Vd, ldv, hd, wd, pd, nullptr);
   finalize_kernel<<<1, AR_THREADS, 0, s>>>(nvec, G, pd, hd, cd, stats, 1);
   // DGKS second pass, executed only if the device flag stats[2] is set
   dots_kernel<<<G, AR_THREADS, 0, s>>>(n, nvec, Vd, ldv, wd, pd, stats);
-  finalize_kernel<<<1, AR_THREADS, 0, s>>>(nvec, G, pd, hd, cd, stats, 2);
+  finalize_kernel<<<nvec > 0 ? nvec : 1, AR_THREADS, 0, s>>>(nvec, G, pd, hd, cd, stats, 2);
   update_kernel<<<G, AR_THREADS, 0, s>>>(n, nvec, Vd, ldv, cd, wd, pd, stats);
   finalize_kernel<<<1, AR_THREADS, 0, s>>>(nvec, G, pd, hd, cd, stats, 3);
   if (vnext)
@@ -338,7 +339,7 @@ extern "C" int vx_cgs_dots(long n, int nvec, const vx_c128* V, long ldv, const v
   double2* pd = reinterpret_cast<double2*>(part);
   dots_kernel<<<G, AR_THREADS, 0, s>>>(n, nvec, reinterpret_cast<const double2*>(V), ldv,
                                        reinterpret_cast<const double2*>(w), pd, nullptr);
-  sum_rows_kernel<<<1, AR_THREADS, 0, s>>>(nvec + 1, G, pd, reinterpret_cast<double2*>(out));
+  sum_rows_kernel<<<nvec + 1, AR_THREADS, 0, s>>>(nvec + 1, G, pd, reinterpret_cast<double2*>(out));
   count_launch();
   VX_CHECK_LAUNCH("cgs_dots");
   return VX_OK;
