@@ -302,13 +302,11 @@ def build_prec(W, kern):
 
 
 def stored_blocks_of(W, prec):
-    kind = W.prec["kind"]
-    if kind == "reduced-one-level":
-        return [(prec.block_size, prec.n_kept)]
-    if kind == "blocked":
-        return [(p.block_size, p.n_kept if hasattr(p, "n_kept") else
-                 (p.grid.nx * p.grid.ny if p.level == "two-level" else p.grid.nx)) for p in prec.box_precs]
-    return block_sizes(W)
+    """(block dim, factors actually stored and streamed once per apply): with
+    mirror sharing (parity-symmetric kernels) one stored factor serves the
+    blocks k and n-k, so this is about half the reference's block count."""
+    precs = prec.box_precs if W.prec["kind"] == "blocked" else [prec]
+    return [(p.block_size, int(p._fac.shape[0])) for p in precs]
 
 
 def run_ours(args):

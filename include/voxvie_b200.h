@@ -78,8 +78,10 @@ int vx_op_apply(int nx, int ny, int nz, int px, int py, int pz, const vx_c128* s
 
 /* Parity-symmetric kernels (every Green component even/odd in each offset
  * coordinate, reference kernel.py:37-51) have spectra with S_p(-k) = +-S_p(k):
- * vx_gen_asymmetry writes per-CTA (max |t(d) - s t(-d)|, max |t|) pairs (256
- * CTAs -> 512 doubles); vx_op_compact keeps the k <= P/2 half-octant
+ * vx_gen_asymmetry writes per-CTA quadruples (max |t(d) - s_x t(d mirrored in x)|,
+ * the same for y and for z, max |t|) (256 CTAs -> 1024 doubles); the x (and y)
+ * parity also lets the preconditioners share one factor between the frequency
+ * blocks k and n-k (vx_prec1_apply's KFLIP flags); vx_op_compact keeps the k <= P/2 half-octant
  * (6, pz/2+1, py/2+1, px/2+1) of full spectra. */
 int vx_gen_asymmetry(int nx, int ny, int nz, const vx_c128* gen, long g_sp, long g_sz, long g_sy, long g_sx,
                      double* out, void* stream);
@@ -111,11 +113,18 @@ int vx_lu1_build(int nx, int ny, int nz, const vx_c128* lamT, const vx_c128* m_y
 /* Replaces OneLevelPrec.apply / ReducedOneLevelPrec.apply (circulant.py:162-188,
  * 264-269): y = F_x^-1 blockdiag(D_k^-1) F_x x for x of shape (3N, nrhs).
  * Work list: item t solves slot items[3t] for the frequencies
- * klist[items[3t+1] .. items[3t+1]+items[3t+2]); items [0, n_single) have one
- * frequency each, items [n_single, n_items) up to 16 (representative block). */
+ * klist[items[3t+1] .. items[3t+1]+items[3t+2]); items [0, n_single) are
+ * direct items with up to direct_r (1 or 2) frequencies each, items
+ * [n_single, n_items) up to 16 (representative block).  A klist entry is the
+ * frequency k in bits 0-28, plus VX_KFLIP_X (bit 30) when block k is the
+ * x-mirror of the stored one (x-parity-symmetric kernels: D_{nx-k} = S D_k S,
+ * S = -1 on the x-component rows) and VX_KFLIP_Y (bit 29, 2-level) for the
+ * y-mirror; the solve is then y = S D^-1 S b with the stored factors. */
+#define VX_KFLIP_X (1 << 30)
+#define VX_KFLIP_Y (1 << 29)
 long vx_prec1_work_elems(int nx, int ny, int nz, int nrhs);
 int vx_prec1_apply(int nx, int ny, int nz, int nrhs, const vx_c128* factors, const int* perm,
-                   const int* items, int n_single, int n_items, const int* klist,
+                   const int* items, int n_single, int n_items, int direct_r, const int* klist,
                    const vx_c128* x, vx_c128* y, vx_c128* work, void* stream);
 
 /* Reduced scheme, representative block (ReducedOneLevelPrec.apply,
@@ -132,7 +141,7 @@ long vx_rep_inverse_elems(int n);
 int vx_rep_inverse(int n, const vx_c128* factors, const int* perm, vx_c128* inv, void* stream);
 long vx_prec1_reduced_work_elems(int nx, int ny, int nz, int nrhs, int n_rep);
 int vx_prec1_apply_reduced(int nx, int ny, int nz, int nrhs, const vx_c128* factors, const int* perm,
-                           const int* items, int n_single, const int* klist, const vx_c128* inv,
+                           const int* items, int n_single, int direct_r, const int* klist, const vx_c128* inv,
                            const int* rep_ks, int n_rep, const vx_c128* x, vx_c128* y, vx_c128* work,
                            void* stream);
 int vx_rep_variant(int sequential);
@@ -156,12 +165,16 @@ int vx_solve_variant(int classic);
 long vx_chan_xy_work_elems(int nx, int ny, int nz);
 int vx_chan_xy_spectra(int nx, int ny, int nz, const vx_c128* gen, long g_sp, long g_sz, long g_sy,
                        long g_sx, vx_c128* lam2T, vx_c128* work, void* stream);
-/* circulant.py:436-446 + accel.py:181-197: (3nz)^2 blocks for all (l, k). */
-int vx_lu2_build(int nx, int ny, int nz, const vx_c128* lam2T, const vx_c128* m_z,
-                 vx_c128* factors, int* perm, int* piv, int* info, void* stream);
-/* TwoLevelPrec.apply (circulant.py:379-394). */
+/* circulant.py:436-446 + accel.py:181-197: (3nz)^2 blocks; slot s factors block
+ * kset[s] = l*nx + k (kset NULL: all nx*ny blocks in order). */
+int vx_lu2_build(int nx, int ny, int nz, const vx_c128* lam2T, const vx_c128* m_z, const int* kset,
+                 int nslots, vx_c128* factors, int* perm, int* piv, int* info, void* stream);
+/* TwoLevelPrec.apply (circulant.py:379-394).  items/klist as vx_prec1_apply
+ * (frequency = l*nx + k; direct_r 1, 2 or 4 for the x/y mirror orbits);
+ * items NULL: slot b solves block b. */
 long vx_prec2_work_elems(int nx, int ny, int nz, int nrhs);
 int vx_prec2_apply(int nx, int ny, int nz, int nrhs, const vx_c128* factors, const int* perm,
+                   const int* items, int n_items, int direct_r, const int* klist,
                    const vx_c128* x, vx_c128* y, vx_c128* work, void* stream);
 
 /* ------------------------------------------------------ sharded (multi-GPU) */
@@ -182,8 +195,8 @@ int vx_scatter_cols(long nrows, const vx_c128* in, int P, const int* col_off, co
                     long total_cols, vx_c128* A, long lda, void* stream);
 /* Block solves only (no DFTs): RHS element (row, k, j) at Y[row*s_row + k*s_k + j]. */
 int vx_prec1_solve(int n, int nrhs, const vx_c128* factors, const int* perm, const int* items,
-                   int n_single, int n_items, const int* klist, vx_c128* Y, long s_row, long s_k,
-                   void* stream);
+                   int n_single, int n_items, int direct_r, const int* klist, vx_c128* Y, long s_row,
+                   long s_k, void* stream);
 /* Local halves of one classical Gram-Schmidt pass (the all-reduce goes in
  * between): out[0..nvec) = V^H w, out[nvec] = ||w||^2; then w -= V coef and
  * out_norm2 = ||w||^2. */

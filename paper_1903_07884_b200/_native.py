@@ -59,12 +59,12 @@ _SIGS = {
     "vx_lu_block_elems": (c_long, [c_int]),
     "vx_lu1_build": (c_int, [c_int] * 3 + [P, P, P, c_int, P, P, P, P, P]),
     "vx_prec1_work_elems": (c_long, [c_int] * 4),
-    "vx_prec1_apply": (c_int, [c_int] * 4 + [P, P, P, c_int, c_int, P, P, P, P, P]),
+    "vx_prec1_apply": (c_int, [c_int] * 4 + [P, P, P, c_int, c_int, c_int, P, P, P, P, P]),
     "vx_chan_xy_work_elems": (c_long, [c_int] * 3),
     "vx_chan_xy_spectra": (c_int, [c_int] * 3 + [P, c_long, c_long, c_long, c_long, P, P, P]),
-    "vx_lu2_build": (c_int, [c_int] * 3 + [P, P, P, P, P, P, P]),
+    "vx_lu2_build": (c_int, [c_int] * 3 + [P, P, P, c_int, P, P, P, P, P]),
     "vx_prec2_work_elems": (c_long, [c_int] * 4),
-    "vx_prec2_apply": (c_int, [c_int] * 4 + [P, P, P, P, P, P]),
+    "vx_prec2_apply": (c_int, [c_int] * 4 + [P, P, P, c_int, c_int, P, P, P, P, P]),
     "vx_box_gather": (c_int, [c_int] * 10 + [P, P, P]),
     "vx_box_scatter": (c_int, [c_int] * 10 + [P, P, P]),
     "vx_arnoldi_part_elems": (c_long, [c_long, c_int]),
@@ -81,10 +81,10 @@ _SIGS = {
     "vx_rep_inverse_elems": (c_long, [c_int]),
     "vx_rep_inverse": (c_int, [c_int, P, P, P, P]),
     "vx_prec1_reduced_work_elems": (c_long, [c_int] * 5),
-    "vx_prec1_apply_reduced": (c_int, [c_int] * 4 + [P, P, P, c_int, P, P, P, c_int, P, P, P, P]),
+    "vx_prec1_apply_reduced": (c_int, [c_int] * 4 + [P, P, P, c_int, c_int, P, P, P, c_int, P, P, P, P]),
     "vx_rep_variant": (c_int, [c_int]),
     "vx_op_reg_fft": (c_int, [c_int]),
-    "vx_prec1_solve": (c_int, [c_int, c_int, P, P, P, c_int, c_int, P, P, c_long, c_long, P]),
+    "vx_prec1_solve": (c_int, [c_int, c_int, P, P, P, c_int, c_int, c_int, P, P, c_long, c_long, P]),
     "vx_cgs_dots": (c_int, [c_long, c_int, P, c_long, P, P, P, P]),
     "vx_cgs_update": (c_int, [c_long, c_int, P, c_long, P, P, P, P, P]),
     "vx_launch_count": (c_long, []),

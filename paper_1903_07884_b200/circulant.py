@@ -26,9 +26,11 @@ from . import _native as nv
 from .errors import PartitionError, PreconditionerBuildError
 from .grid import PermittivityMap, VoxelGrid, homogenize
 from .kernel import ToeplitzKernel
-from .operator import upload_tensors
+from .operator import SYMMETRY_RTOL, generator_axis_asymmetry, upload_tensors
 
 BYTES_PER_ENTRY = 16
+KFLIP_X = 1 << 30   # klist flag: block is the x-mirror of the stored one (include/voxvie_b200.h)
+KFLIP_Y = 1 << 29   # klist flag: y-mirror (2-level)
 
 
 # ---------------------------------------------------------------------------
@@ -161,6 +163,63 @@ def _first_bad(info) -> int:
     return -1 if bad.numel() == 0 else int(bad[0, 0])
 
 
+# ---------------------------------------------------------------------------
+# mirror sharing of factors (x / y parity of the kernel)
+# ---------------------------------------------------------------------------
+# For a kernel whose Green components are even/odd under x -> -x (reference
+# kernel.py:37-51: the off-diagonal (a, b) entry is odd under a sign flip of
+# either coordinate), the Chan x-spectra satisfy lam_p(nx-k) = s_p lam_p(k)
+# (s = -1 for xy, xz), so D_{nx-k} = S D_k S with S = -1 on the x-component
+# rows.  zgetrf picks the same pivots on S D S (|Re|+|Im| is sign-blind), so
+# the factors of D_{nx-k} are sign flips of D_k's: one stored factor serves
+# both blocks and one streamed read of it solves both right-hand sides.  The
+# 2-level blocks get the same from the y parity (S = -1 on the y rows).
+
+def mirror_axes(gen, dims) -> tuple:
+    """(x_ok, y_ok): the generators are parity-symmetric on x / y to SYMMETRY_RTOL
+    (VX_MIRROR=0 disables the factor sharing)."""
+    if os.environ.get("VX_MIRROR", "1") == "0":
+        return False, False
+    ax, ay, _ = generator_axis_asymmetry(gen, dims)
+    return ax <= SYMMETRY_RTOL, ay <= SYMMETRY_RTOL
+
+
+def _flip_signs(n: int, fx: bool, fy: bool) -> np.ndarray:
+    """Diagonal of S for an (n, n) block with rows ordered a*q + ... (q = n/3)."""
+    q = n // 3
+    s = np.ones(n)
+    if fx:
+        s[:q] = -1.0
+    if fy:
+        s[q:2 * q] = -1.0
+    return s
+
+
+def _lu_mirror(lu: np.ndarray, piv: np.ndarray, s: np.ndarray) -> np.ndarray:
+    """LAPACK LU of S D S from the LU of D (same pivots): L' = S_p L S_p,
+    U' = S_p U S with S_p = P S P^T."""
+    n = lu.shape[0]
+    perm = np.arange(n)
+    for i, p in enumerate(piv):
+        perm[i], perm[p] = perm[p], perm[i]
+    sp = s[perm]
+    out = lu * sp[:, None]
+    lower = np.tril(np.ones((n, n), bool), -1)
+    return np.where(lower, out * sp[None, :], out * s[None, :])
+
+
+def _items_groups(groups):
+    """groups: list of (slot, [klist entries]) -> (items int32 (3t,), klist int32, max group size)."""
+    t = _torch()
+    items, klist = [], []
+    for slot, ks in groups:
+        items.append((slot, len(klist), len(ks)))
+        klist.extend(ks)
+    r = max((len(ks) for _, ks in groups), default=1)
+    return (t.from_numpy(np.asarray(items, np.int32).reshape(-1).copy()).cuda(),
+            t.from_numpy(np.asarray(klist if klist else [0], np.int32)).cuda(), r)
+
+
 def _untile(fac_row: np.ndarray, n: int) -> np.ndarray:
     """Tiled factor storage -> LAPACK combined LU (n, n) (host, for inspection)."""
     from scipy.linalg import solve_triangular
@@ -216,7 +275,7 @@ class _OneLevelBase:
         y = nv.empty_c128((self.grid.n_unknowns, r))
         work = nv.empty_c128(int(nv.query("vx_prec1_work_elems", nx, ny, nz, r)))
         nv.call("vx_prec1_apply", nx, ny, nz, r, self._fac.data_ptr(), self._perm.data_ptr(),
-                self._items.data_ptr(), self._n_single, self._n_items, self._klist.data_ptr(),
+                self._items.data_ptr(), self._n_single, self._n_items, self._direct_r, self._klist.data_ptr(),
                 xd.data_ptr(), y.data_ptr(), work.data_ptr(), nv.stream_ptr())
         return y
 
@@ -233,21 +292,47 @@ class _OneLevelBase:
         """Bytes actually resident on the device for the factors (padded tiles)."""
         return int(self._fac.numel()) * 16
 
+    # per logical block (frequency k for the full scheme, kept index for the
+    # reduced one): storage slot and whether it is the x-mirror of that slot
+    _store: np.ndarray
+    _flip: np.ndarray
+
+    @property
+    def mirror_shared(self) -> bool:
+        """True when mirror blocks share stored factors (x-parity-symmetric kernel)."""
+        return bool(np.any(self._flip))
+
     @property
     def lu(self) -> np.ndarray:
         f = self._fac.cpu().numpy()
-        return np.stack([_untile(f[s], self.block_size) for s in range(f.shape[0])])
+        pv = self._piv.cpu().numpy()
+        n = self.block_size
+        base = [_untile(f[s], n) for s in range(f.shape[0])]
+        sx = _flip_signs(n, True, False)
+        return np.stack([_lu_mirror(base[s], pv[s], sx) if fl else base[s]
+                         for s, fl in zip(self._store, self._flip)])
 
     @property
     def piv(self) -> np.ndarray:
-        return self._piv.cpu().numpy()
+        return self._piv.cpu().numpy()[self._store]
 
 
-def _items_single(slots, ks):
-    t = _torch()
-    items = np.stack([np.asarray(slots), np.arange(len(ks)), np.ones(len(ks), int)], 1).astype(np.int32)
-    return (t.from_numpy(items.reshape(-1).copy()).cuda(),
-            t.from_numpy(np.asarray(ks, np.int32).copy()).cuda())
+def _mirror_store(ks: np.ndarray, nx: int, share: bool):
+    """Storage plan for the logical blocks ks (sorted frequencies): the blocks
+    to factorise (kset), and per block its storage slot and x-flip."""
+    pos = {int(k): i for i, k in enumerate(ks)}
+    store = np.empty(ks.size, np.int64)
+    flip = np.zeros(ks.size, bool)
+    kset = []
+    for i, k in enumerate(ks):
+        km = (nx - int(k)) % nx
+        if share and km < k and km in pos:
+            store[i] = store[pos[km]]
+            flip[i] = True
+        else:
+            store[i] = len(kset)
+            kset.append(int(k))
+    return np.asarray(kset, np.int64), store, flip
 
 
 class OneLevelPrec(_OneLevelBase):
@@ -255,12 +340,17 @@ class OneLevelPrec(_OneLevelBase):
 
     level = "one-level"
 
-    def __init__(self, grid, fac, perm, piv, proxy):
+    def __init__(self, grid, fac, perm, piv, proxy, store=None, flip=None):
         self.grid = grid
         self._fac, self._perm, self._piv, self._proxy = fac, perm, piv, proxy
         nx = grid.nx
-        self._items, self._klist = _items_single(np.arange(nx), np.arange(nx))
-        self._n_single = self._n_items = nx
+        self._store = np.arange(nx) if store is None else np.asarray(store)
+        self._flip = np.zeros(nx, bool) if flip is None else np.asarray(flip, bool)
+        groups = {}
+        for k in range(nx):
+            groups.setdefault(int(self._store[k]), []).append(k | (KFLIP_X if self._flip[k] else 0))
+        self._items, self._klist, self._direct_r = _items_groups(sorted(groups.items()))
+        self._n_single = self._n_items = len(groups)
 
     @property
     def proxy(self) -> np.ndarray:
@@ -282,24 +372,28 @@ def _build_one_level_dev(grid, gen, m_yz, cap_bytes, tol=None):
     q = ny * nz
     if tol is None:
         _check_cap(nx * (3 * q) ** 2 * BYTES_PER_ENTRY, cap_bytes, "consider the 2-level preconditioner")
+    share = mirror_axes(gen, grid.dims)[0]
     lam = _lamhat_x(gen, nx, ny, nz)
     proxy = _proxies(lam, nx, ny, nz, m_yz[0, 0])
     m_dev = nv.device_c128(m_yz)
     if tol is None:
-        fac, perm, piv, info = _lu1(lam, m_dev, None, nx, nx, ny, nz)
+        kset, store, flip = _mirror_store(np.arange(nx), nx, share)
+        kdev = t.from_numpy(kset.astype(np.int32)).cuda()
+        fac, perm, piv, info = _lu1(lam, m_dev, kdev, int(kset.size), nx, ny, nz)
         bad = _first_bad(info)
         if bad >= 0:
-            raise PreconditionerBuildError(f"1-level build failed: singular frequency block k={bad}")
-        return OneLevelPrec(grid, fac, perm, piv, proxy)
+            raise PreconditionerBuildError(f"1-level build failed: singular frequency block k={int(kset[bad])}")
+        return OneLevelPrec(grid, fac, perm, piv, proxy, store, flip)
     ph = proxy.cpu().numpy()
     kept, slot_of, rep, v_hat = _select_kept(ph, nx, tol)
     _check_cap(kept.size * (3 * q) ** 2 * BYTES_PER_ENTRY, cap_bytes, "consider the 2-level preconditioner")
-    kset = t.from_numpy(kept.astype(np.int32)).cuda()
-    fac, perm, piv, info = _lu1(lam, m_dev, kset, int(kept.size), nx, ny, nz)
+    kset, store, flip = _mirror_store(kept, nx, share)
+    kdev = t.from_numpy(kset.astype(np.int32)).cuda()
+    fac, perm, piv, info = _lu1(lam, m_dev, kdev, int(kset.size), nx, ny, nz)
     bad = _first_bad(info)
     if bad >= 0:
-        raise PreconditionerBuildError(f"singular frequency block k={int(kept[bad])}")
-    return ReducedOneLevelPrec(grid, kept, slot_of, rep, fac, perm, piv, ph, v_hat, float(tol))
+        raise PreconditionerBuildError(f"singular frequency block k={int(kset[bad])}")
+    return ReducedOneLevelPrec(grid, kept, slot_of, rep, fac, perm, piv, ph, v_hat, float(tol), store, flip)
 
 
 def build_one_level(kernel: ToeplitzKernel, mtilde, *, cap_bytes: int = 2 ** 31) -> OneLevelPrec:
@@ -320,12 +414,15 @@ class ReducedOneLevelPrec(_OneLevelBase):
 
     level = "reduced-one-level"
 
-    def __init__(self, grid, kept, slot_of, representative, fac, perm, piv, proxy, v_hat, tol):
+    def __init__(self, grid, kept, slot_of, representative, fac, perm, piv, proxy, v_hat, tol,
+                 store=None, flip=None):
         self.grid = grid
         self.kept = np.asarray(kept)
         self.slot_of = np.asarray(slot_of)
         self.representative = int(representative)
         self._fac, self._perm, self._piv = fac, perm, piv
+        self._store = np.arange(self.kept.size) if store is None else np.asarray(store)
+        self._flip = np.zeros(self.kept.size, bool) if flip is None else np.asarray(flip, bool)
         self.proxy = np.asarray(proxy)
         self.proxy_normalized = np.asarray(v_hat)
         self.tol = float(tol)
@@ -333,21 +430,20 @@ class ReducedOneLevelPrec(_OneLevelBase):
 
     def _make_worklist(self):
         t = _torch()
-        rep_slot = int(self.slot_of[self.representative])
-        singles = [(s, int(k)) for s, k in enumerate(self.kept) if s != rep_slot]
-        rep_ks = np.flatnonzero(self.slot_of == rep_slot)
-        items, klist = [], []
-        for s, k in singles:
-            items.append((s, len(klist), 1))
-            klist.append(k)
-        n_single = len(items)
+        rep_idx = int(self.slot_of[self.representative])   # kept index of the representative
+        rep_slot = int(self._store[rep_idx])                 # its storage slot (never flipped)
+        groups = {}
+        for i, k in enumerate(self.kept):
+            if i != rep_idx:
+                groups.setdefault(int(self._store[i]), []).append(int(k) | (KFLIP_X if self._flip[i] else 0))
+        groups = sorted(groups.items())
+        n_single = len(groups)
+        rep_ks = np.flatnonzero(self.slot_of == rep_idx)
         for c0 in range(0, rep_ks.size, 8):
-            chunk = rep_ks[c0:c0 + 8]
-            items.append((rep_slot, len(klist), int(chunk.size)))
-            klist.extend(int(k) for k in chunk)
-        self._items = t.from_numpy(np.asarray(items, np.int32).reshape(-1).copy()).cuda()
-        self._klist = t.from_numpy(np.asarray(klist, np.int32)).cuda()
-        self._n_single, self._n_items = n_single, len(items)
+            groups.append((rep_slot, [int(k) for k in rep_ks[c0:c0 + 8]]))
+        self._items, self._klist, _ = _items_groups(groups)
+        self._direct_r = max((len(ks) for _, ks in groups[:n_single]), default=1)
+        self._n_single, self._n_items = n_single, len(groups)
         # Multi-tile blocks: the representative's frequencies go through one
         # dense GEMM with its explicit inverse (vx_rep_inverse), concurrently
         # with the single-block solves; VX_REP_GEMM=0 keeps the chunked solves.
@@ -368,7 +464,7 @@ class ReducedOneLevelPrec(_OneLevelBase):
         y = nv.empty_c128((self.grid.n_unknowns, r))
         work = nv.empty_c128(int(nv.query("vx_prec1_reduced_work_elems", nx, ny, nz, r, n_rep)))
         nv.call("vx_prec1_apply_reduced", nx, ny, nz, r, self._fac.data_ptr(), self._perm.data_ptr(),
-                self._items.data_ptr(), self._n_single, self._klist.data_ptr(), self._inv.data_ptr(),
+                self._items.data_ptr(), self._n_single, self._direct_r, self._klist.data_ptr(), self._inv.data_ptr(),
                 self._rep_ks.data_ptr(), n_rep, xd.data_ptr(), y.data_ptr(), work.data_ptr(), nv.stream_ptr())
         return y
 
@@ -392,10 +488,15 @@ def reduce_one_level(prec: OneLevelPrec, tol: float = 1e-3) -> ReducedOneLevelPr
     nx = prec.grid.nx
     proxy = prec.proxy
     kept, slot_of, rep, v_hat = _select_kept(proxy, nx, tol)
-    idx = t.from_numpy(kept.astype(np.int64)).cuda()
+    slots = prec._store[kept]
+    uniq, store = np.unique(slots, return_inverse=True)
+    flip = prec._flip[kept].copy()
+    # a kept block whose stored partner was discarded keeps that partner's
+    # factor (stored under the kept block's index, flipped)
+    idx = t.from_numpy(uniq.astype(np.int64)).cuda()
     return ReducedOneLevelPrec(prec.grid, kept, slot_of, rep, prec._fac.index_select(0, idx),
                                prec._perm.index_select(0, idx), prec._piv.index_select(0, idx),
-                               proxy.copy(), v_hat, float(tol))
+                               proxy.copy(), v_hat, float(tol), store, flip)
 
 
 def build_reduced_one_level(kernel: ToeplitzKernel, mtilde, tol: float = 1e-3, *,
@@ -417,9 +518,28 @@ class TwoLevelPrec:
 
     level = "two-level"
 
-    def __init__(self, grid, fac, perm, piv):
+    def __init__(self, grid, fac, perm, piv, store=None, flips=None):
         self.grid = grid
         self._fac, self._perm, self._piv = fac, perm, piv
+        nb = grid.nx * grid.ny
+        # per block b = l*nx + k: storage slot and (x, y) mirror flips
+        self._store = np.arange(nb) if store is None else np.asarray(store)
+        self._flips = np.zeros((nb, 2), bool) if flips is None else np.asarray(flips, bool)
+        if store is None:
+            self._items, self._klist, self._direct_r, self._n_items = None, None, 1, nb
+        else:
+            groups = {}
+            for b in range(nb):
+                fx, fy = self._flips[b]
+                groups.setdefault(int(self._store[b]), []).append(
+                    b | (KFLIP_X if fx else 0) | (KFLIP_Y if fy else 0))
+            self._items, self._klist, r = _items_groups(sorted(groups.items()))
+            self._direct_r = 1 if r == 1 else (2 if r == 2 else 4)
+            self._n_items = len(groups)
+
+    @property
+    def mirror_shared(self) -> bool:
+        return bool(np.any(self._flips))
 
     @property
     def block_size(self) -> int:
@@ -432,19 +552,23 @@ class TwoLevelPrec:
     @property
     def lu(self) -> np.ndarray:
         f = self._fac.cpu().numpy()
+        pv = self._piv.cpu().numpy()
         n = self.block_size
-        out = np.stack([_untile(f[s], n) for s in range(f.shape[0])])
+        base = [_untile(f[s], n) for s in range(f.shape[0])]
+        out = np.stack([_lu_mirror(base[s], pv[s], _flip_signs(n, fx, fy)) if (fx or fy) else base[s]
+                        for s, (fx, fy) in zip(self._store, self._flips)])
         return out.reshape(self.grid.ny, self.grid.nx, n, n)
 
     @property
     def piv(self) -> np.ndarray:
-        return self._piv.cpu().numpy().reshape(self.grid.ny, self.grid.nx, -1)
+        return self._piv.cpu().numpy()[self._store].reshape(self.grid.ny, self.grid.nx, -1)
 
     def _apply_dev(self, xd, r):
         nx, ny, nz = self.grid.dims
         y = nv.empty_c128((self.grid.n_unknowns, r))
         work = nv.empty_c128(int(nv.query("vx_prec2_work_elems", nx, ny, nz, r)))
         nv.call("vx_prec2_apply", nx, ny, nz, r, self._fac.data_ptr(), self._perm.data_ptr(),
+                nv.ptr(self._items), self._n_items, self._direct_r, nv.ptr(self._klist),
                 xd.data_ptr(), y.data_ptr(), work.data_ptr(), nv.stream_ptr())
         return y
 
@@ -472,26 +596,38 @@ def _build_two_level_dev(grid, gen, mtilde, cap_bytes):
     else:
         raise ValueError(f"mtilde shape {m.shape} not usable for a 2-level build")
     _check_cap(nx * ny * (3 * nz) ** 2 * BYTES_PER_ENTRY, cap_bytes, "reduce the box size or cross-section")
+    share_x, share_y = mirror_axes(gen, grid.dims)
     work = nv.empty_c128(int(nv.query("vx_chan_xy_work_elems", nx, ny, nz)))
     lam2 = nv.empty_c128((nx * ny, 6 * (2 * nz - 1)))
     nv.call("vx_chan_xy_spectra", nx, ny, nz, gen.data_ptr(), *_gen_strides(gen), lam2.data_ptr(),
             work.data_ptr(), nv.stream_ptr())
     del work
     n = 3 * nz
-    nb = nx * ny
+    # canonical representative of each (l, k) mirror orbit
+    ks, ls = np.arange(nx), np.arange(ny)
+    kc = np.minimum(ks, (nx - ks) % nx) if share_x else ks
+    lc = np.minimum(ls, (ny - ls) % ny) if share_y else ls
+    canon = (lc[:, None] * nx + kc[None, :]).reshape(-1)
+    kset, store = np.unique(canon, return_inverse=True)
+    flips = np.stack([np.broadcast_to((kc != ks)[None, :], (ny, nx)).reshape(-1),
+                      np.broadcast_to((lc != ls)[:, None], (ny, nx)).reshape(-1)], 1)
+    nb = int(kset.size)
     blk = int(nv.query("vx_lu_block_elems", n))
     fac = t.empty((nb, blk), dtype=t.complex128, device="cuda")
     perm = t.empty((nb, n), dtype=t.int32, device="cuda")
     piv = t.empty((nb, n), dtype=t.int32, device="cuda")
     info = t.empty((nb,), dtype=t.int32, device="cuda")
     m_dev = nv.device_c128(np.ascontiguousarray(m_z))
-    nv.call("vx_lu2_build", nx, ny, nz, lam2.data_ptr(), m_dev.data_ptr(), fac.data_ptr(),
+    kdev = t.from_numpy(kset.astype(np.int32)).cuda()
+    nv.call("vx_lu2_build", nx, ny, nz, lam2.data_ptr(), m_dev.data_ptr(), kdev.data_ptr(), nb, fac.data_ptr(),
             perm.data_ptr(), piv.data_ptr(), info.data_ptr(), nv.stream_ptr())
     bad = _first_bad(info)
     if bad >= 0:
-        l, k = divmod(bad, nx)
+        l, k = divmod(int(kset[bad]), nx)
         raise PreconditionerBuildError(f"2-level build failed: singular block (k={k}, l={l})")
-    return TwoLevelPrec(grid, fac, perm, piv)
+    if nb == nx * ny:
+        return TwoLevelPrec(grid, fac, perm, piv)
+    return TwoLevelPrec(grid, fac, perm, piv, store, flips)
 
 
 def build_two_level(kernel: ToeplitzKernel, mtilde, *, cap_bytes: int = 2 ** 31) -> TwoLevelPrec:

@@ -740,6 +740,21 @@ static int lu_build(const Unfold& u, int n, int nslots, double2* F, int* perm, i
 }
 
 // ---------------------------------------------------------------- LU solve
+// Mirror sharing: for an x-parity-symmetric kernel D_{n-k} = S D_k S with S =
+// -1 on the x-component rows (rows [0, q), q = n/3), and for the 2-level
+// y-mirror S = -1 on the y-component rows [q, 2q); so the mirror block's
+// solve is y = S D_k^-1 S b with D_k's stored factors.  A klist entry carries
+// the frequency in its low 29 bits and the flips in bits 30 (x) / 29 (y).
+constexpr int KFLIP_X = 1 << 30, KFLIP_Y = 1 << 29, KIDX = KFLIP_Y - 1;
+constexpr long ROFF = (1L << 56) - 1;  // rbase: offset in the low 56 bits, flips (kraw >> 29) above
+__device__ __forceinline__ bool flip_row(int f2, int row, int q) {
+  return ((f2 & 2) && row < q) || ((f2 & 1) && row >= q && row < 2 * q);
+}
+__device__ __forceinline__ long rhs_base(int kraw, int rho, int nrhs, long s_k) {
+  return ((long)(kraw & KIDX) * s_k + (rho % nrhs)) | ((long)(kraw >> 29) << 56);
+}
+__device__ __forceinline__ double2 cflip(double2 v, bool f) { return f ? cmk(-v.x, -v.y) : v; }
+
 // One CTA per work item: slot + up to R right-hand sides (frequency k, column j)
 // gathered from Y[row*s_row + k*s_k + j] through the row permutation.
 template <int R, int NW>
@@ -749,7 +764,7 @@ __global__ void __launch_bounds__(NW * 32) lu_solve_kernel(LuGeom g, const doubl
                                                            const int* __restrict__ klist, int nrhs,
                                                            double2* Y, long s_row, long s_k) {
   extern __shared__ double2 sm[];
-  const int T = g.T, T2 = T * T, nt = g.nt, npad = g.npad, n = g.n;
+  const int T = g.T, T2 = T * T, nt = g.nt, npad = g.npad, n = g.n, q = n / 3;
   double2* y = sm;                    // [npad][R]
   double2* red = y + (long)npad * R;  // [NW][T][R]
   double2* Ds = red + NW * T * R;     // [T*T]
@@ -777,8 +792,8 @@ __global__ void __launch_bounds__(NW * 32) lu_solve_kernel(LuGeom g, const doubl
       long b = 0;
       if (tid < nr) {
         const int rho = rho0 + tid;
-        const int kk = klist ? klist[beg + rho / nrhs] : beg + rho / nrhs;
-        b = (long)kk * s_k + (rho % nrhs);
+        const int kraw = klist ? klist[beg + rho / nrhs] : beg + rho / nrhs;
+        b = rhs_base(kraw, rho, nrhs, s_k);
       }
       rbase[tid] = b;
     }
@@ -786,7 +801,11 @@ __global__ void __launch_bounds__(NW * 32) lu_solve_kernel(LuGeom g, const doubl
     for (int idx = tid; idx < npad * R; idx += NT) {
       const int row = idx / R, rr = idx - row * R;
       double2 v = cmk(0.0, 0.0);
-      if (row < n && rr < nr) v = Y[(long)pm[row] * s_row + rbase[rr]];
+      if (row < n && rr < nr) {
+        const long rb = rbase[rr];
+        const int pr = pm[row];
+        v = cflip(Y[(long)pr * s_row + (rb & ROFF)], flip_row((int)(rb >> 56), pr, q));
+      }
       y[idx] = v;
     }
     __syncthreads();
@@ -866,7 +885,10 @@ __global__ void __launch_bounds__(NW * 32) lu_solve_kernel(LuGeom g, const doubl
     }
     for (int idx = tid; idx < n * R; idx += NT) {
       const int row = idx / R, rr = idx - row * R;
-      if (rr < nr) Y[(long)row * s_row + rbase[rr]] = y[idx];
+      if (rr < nr) {
+        const long rb = rbase[rr];
+        Y[(long)row * s_row + (rb & ROFF)] = cflip(y[idx], flip_row((int)(rb >> 56), row, q));
+      }
     }
     __syncthreads();
   }
@@ -941,7 +963,7 @@ __global__ void __launch_bounds__((PIPE_CONSUMERS + 1) * 32)
   extern __shared__ __align__(128) unsigned char smraw[];
   constexpr int NWC = PIPE_CONSUMERS;
   constexpr int NC = NWC * 32;
-  const int T = g.T, T2 = T * T, nt = g.nt, npad = g.npad, n = g.n;
+  const int T = g.T, T2 = T * T, nt = g.nt, npad = g.npad, n = g.n, q = n / 3;
   const uint32_t tile_bytes = (uint32_t)T2 * sizeof(double2);
   uint64_t* full = reinterpret_cast<uint64_t*>(smraw);
   uint64_t* empty = full + S;
@@ -1022,8 +1044,8 @@ __global__ void __launch_bounds__((PIPE_CONSUMERS + 1) * 32)
       long b = 0;
       if (tid < nr) {
         const int rho = rho0 + tid;
-        const int kk = klist ? klist[beg + rho / nrhs] : beg + rho / nrhs;
-        b = (long)kk * s_k + (rho % nrhs);
+        const int kraw = klist ? klist[beg + rho / nrhs] : beg + rho / nrhs;
+        b = rhs_base(kraw, rho, nrhs, s_k);
       }
       rbase[tid] = b;
     }
@@ -1032,7 +1054,11 @@ __global__ void __launch_bounds__((PIPE_CONSUMERS + 1) * 32)
     for (int idx = tid; idx < npad * R; idx += NC) {
       const int row = idx / R, rr = idx - row * R;
       double2 v = cmk(0.0, 0.0);
-      if (row < n && rr < nr) v = Y[(long)pm[row] * s_row + rbase[rr]];
+      if (row < n && rr < nr) {
+        const long rb = rbase[rr];
+        const int pr = pm[row];
+        v = cflip(Y[(long)pr * s_row + (rb & ROFF)], flip_row((int)(rb >> 56), pr, q));
+      }
       y[idx] = v;
     }
     consumers_sync(NC);
@@ -1139,7 +1165,10 @@ __global__ void __launch_bounds__((PIPE_CONSUMERS + 1) * 32)
     }
     for (int idx = tid; idx < n * R; idx += NC) {
       const int row = idx / R, rr = idx - row * R;
-      if (rr < nr) Y[(long)row * s_row + rbase[rr]] = y[idx];
+      if (rr < nr) {
+        const long rb = rbase[rr];
+        Y[(long)row * s_row + (rb & ROFF)] = cflip(y[idx], flip_row((int)(rb >> 56), row, q));
+      }
     }
     consumers_sync(NC);
   }
@@ -1178,9 +1207,10 @@ __global__ void __launch_bounds__(SMALL_WARPS * 32)
   const int pr = lane < n ? perm[(long)slot * n + lane] : 0;
   __syncwarp();
   for (int rho = 0; rho < cnt * nrhs; ++rho) {
-    const int kk = klist ? klist[beg + rho / nrhs] : beg + rho / nrhs;
-    const long base = (long)kk * s_k + (rho % nrhs);
-    double2 yv = lane < n ? Y[(long)pr * s_row + base] : cmk(0.0, 0.0);
+    const int kraw = klist ? klist[beg + rho / nrhs] : beg + rho / nrhs;
+    const long base = (long)(kraw & KIDX) * s_k + (rho % nrhs);
+    const int f2 = kraw >> 29;
+    double2 yv = lane < n ? cflip(Y[(long)pr * s_row + base], flip_row(f2, pr, n / 3)) : cmk(0.0, 0.0);
     // forward: o = inv(L) y (unit lower)
     double2 o = yv;
     for (int c = 0; c < n; ++c) {
@@ -1193,7 +1223,7 @@ __global__ void __launch_bounds__(SMALL_WARPS * 32)
       const double2 oc = cmk(__shfl_sync(0xffffffffu, o.x, c), __shfl_sync(0xffffffffu, o.y, c));
       if (c >= lane && lane < n) cfma(x, Ds[c * n + lane], oc);
     }
-    if (lane < n) Y[(long)lane * s_row + base] = x;
+    if (lane < n) Y[(long)lane * s_row + base] = cflip(x, flip_row(f2, lane, n / 3));
   }
 }
 
@@ -1261,7 +1291,7 @@ __global__ void cols_copy_kernel(long nrows, double2* A, long lda, int P, const 
 // each, the rest multi-RHS).  vx_solve_variant(1) selects the synchronous kernel.
 static int solve_items(const LuGeom& g, const double2* F, const int* perm, const int* items, int n_single,
                        int n_items, const int* klist, int nrhs, double2* Y, long s_row, long s_k, cudaStream_t s,
-                       int persist = -1) {
+                       int persist = -1, int direct_r = 1) {
   int st;
   Span span("prec_solve", s);
   static const int persist_env = env_int("VX_PIPE_PERSIST", 0);
@@ -1269,7 +1299,13 @@ static int solve_items(const LuGeom& g, const double2* F, const int* perm, const
   if (g.nt == 1 && !g_solve_classic)
     return launch_solve_small(g, F, perm, items, 0, n_items, klist, nrhs, Y, s_row, s_k, s);
   const bool pipe = g.nt > 1 && !g_solve_classic;
-  if (nrhs == 1)
+  if (nrhs == 1 && direct_r == 2)  // mirror pairs: one factor stream, two frequencies
+    st = pipe ? launch_solve_pipe<2>(g, F, perm, items, 0, n_single, klist, 1, Y, s_row, s_k, s, persist)
+              : launch_solve<2, SOLVE_WARPS>(g, F, perm, items, 0, n_single, klist, 1, Y, s_row, s_k, s);
+  else if (nrhs == 1 && direct_r == 4)  // 2-level x/y mirror quadruples
+    st = pipe ? launch_solve_pipe<4>(g, F, perm, items, 0, n_single, klist, 1, Y, s_row, s_k, s, persist)
+              : launch_solve<4, SOLVE_WARPS>(g, F, perm, items, 0, n_single, klist, 1, Y, s_row, s_k, s);
+  else if (nrhs == 1)
     st = pipe ? launch_solve_pipe<1>(g, F, perm, items, 0, n_single, klist, 1, Y, s_row, s_k, s, persist)
               : launch_solve<1, SOLVE_WARPS>(g, F, perm, items, 0, n_single, klist, 1, Y, s_row, s_k, s);
   else
@@ -1515,10 +1551,11 @@ extern "C" long vx_prec1_work_elems(int nx, int ny, int nz, int nrhs) {
 }
 
 extern "C" int vx_prec1_apply(int nx, int ny, int nz, int nrhs, const vx_c128* factors,
-                              const int* perm, const int* items, int n_single, int n_items,
+                              const int* perm, const int* items, int n_single, int n_items, int direct_r,
                               const int* klist, const vx_c128* x, vx_c128* y, vx_c128* work,
                               void* stream) {
   VX_REQUIRE(nx >= 1 && ny >= 1 && nz >= 1 && nrhs >= 1, "bad 1-level apply arguments");
+  VX_REQUIRE(direct_r == 1 || direct_r == 2, "direct_r must be 1 or 2");
   VX_REQUIRE(n_single >= 0 && n_items >= n_single, "bad work list");
   cudaStream_t s = as_stream(stream);
   Span span("prec_apply", s);
@@ -1535,7 +1572,8 @@ extern "C" int vx_prec1_apply(int nx, int ny, int nz, int nrhs, const vx_c128* f
   }
   LuGeom g = lu_geom(q3);
   const double2* F = reinterpret_cast<const double2*>(factors);
-  if ((st = solve_items(g, F, perm, items, n_single, n_items, klist, nrhs, S, pitch, nrhs, s))) return st;
+  if ((st = solve_items(g, F, perm, items, n_single, n_items, klist, nrhs, S, pitch, nrhs, s, -1, direct_r)))
+    return st;
   {
     LoadStrided ld{S, {pitch, 1, nrhs, nrhs}};
     StoreStrided sv{reinterpret_cast<double2*>(y), {pitch, 1, nrhs, nrhs}, 1.0 / nx};
@@ -1573,11 +1611,14 @@ extern "C" int vx_chan_xy_spectra(int nx, int ny, int nz, const vx_c128* gen, lo
 }
 
 extern "C" int vx_lu2_build(int nx, int ny, int nz, const vx_c128* lam2T, const vx_c128* m_z,
-                            vx_c128* factors, int* perm, int* piv, int* info, void* stream) {
+                            const int* kset, int nslots, vx_c128* factors, int* perm, int* piv, int* info,
+                            void* stream) {
   VX_REQUIRE(nx >= 1 && ny >= 1 && nz >= 1, "bad 2-level build arguments");
-  Unfold u{reinterpret_cast<const double2*>(lam2T), reinterpret_cast<const double2*>(m_z), nullptr,
+  if (!kset) nslots = nx * ny;
+  VX_REQUIRE(nslots >= 0 && nslots <= nx * ny, "bad 2-level slot count");
+  Unfold u{reinterpret_cast<const double2*>(lam2T), reinterpret_cast<const double2*>(m_z), kset,
            6L * (2 * nz - 1), nz, 1};
-  return lu_build(u, 3 * nz, nx * ny, reinterpret_cast<double2*>(factors), perm, piv, info,
+  return lu_build(u, 3 * nz, nslots, reinterpret_cast<double2*>(factors), perm, piv, info,
                   as_stream(stream));
 }
 
@@ -1586,9 +1627,10 @@ extern "C" long vx_prec2_work_elems(int nx, int ny, int nz, int nrhs) {
 }
 
 extern "C" int vx_prec2_apply(int nx, int ny, int nz, int nrhs, const vx_c128* factors,
-                              const int* perm, const vx_c128* x, vx_c128* y, vx_c128* work,
-                              void* stream) {
+                              const int* perm, const int* items, int n_items, int direct_r, const int* klist,
+                              const vx_c128* x, vx_c128* y, vx_c128* work, void* stream) {
   VX_REQUIRE(nx >= 1 && ny >= 1 && nz >= 1 && nrhs >= 1, "bad 2-level apply arguments");
+  VX_REQUIRE(direct_r == 1 || direct_r == 2 || direct_r == 4, "direct_r must be 1, 2 or 4");
   cudaStream_t s = as_stream(stream);
   Span span("prec_apply", s);
   FftPlan px, py;
@@ -1610,10 +1652,9 @@ extern "C" int vx_prec2_apply(int nx, int ny, int nz, int nrhs, const vx_c128* f
   }
   LuGeom g = lu_geom(3 * nz);
   const double2* F = reinterpret_cast<const double2*>(factors);
-  {
-    Span span2("prec_solve", s);
-    if ((st = launch_solve_small(g, F, perm, nullptr, 0, nx * ny, nullptr, nrhs, S, plane, nrhs, s))) return st;
-  }
+  if (!items) n_items = nx * ny;
+  if ((st = solve_items(g, F, perm, items, n_items, n_items, klist, nrhs, S, plane, nrhs, s, -1, direct_r)))
+    return st;
   {
     LoadStrided ld{S, {plane, 1, pitch, (int)pitch}};
     StoreStrided sv{S, {plane, 1, pitch, (int)pitch}, 1.0};
@@ -1679,11 +1720,12 @@ extern "C" int vx_scatter_cols(long nrows, const vx_c128* in, int P, const int* 
 }
 
 extern "C" int vx_prec1_solve(int n, int nrhs, const vx_c128* factors, const int* perm, const int* items,
-                              int n_single, int n_items, const int* klist, vx_c128* Y, long s_row, long s_k,
-                              void* stream) {
+                              int n_single, int n_items, int direct_r, const int* klist, vx_c128* Y, long s_row,
+                              long s_k, void* stream) {
   VX_REQUIRE(n >= 1 && nrhs >= 1 && n_single >= 0 && n_items >= n_single, "bad solve arguments");
+  VX_REQUIRE(direct_r == 1 || direct_r == 2, "direct_r must be 1 or 2");
   return solve_items(lu_geom(n), reinterpret_cast<const double2*>(factors), perm, items, n_single, n_items, klist,
-                     nrhs, reinterpret_cast<double2*>(Y), s_row, s_k, as_stream(stream));
+                     nrhs, reinterpret_cast<double2*>(Y), s_row, s_k, as_stream(stream), -1, direct_r);
 }
 
 extern "C" int vx_lu_variant(int monolithic) {
@@ -1728,11 +1770,13 @@ extern "C" long vx_prec1_reduced_work_elems(int nx, int ny, int nz, int nrhs, in
 }
 
 extern "C" int vx_prec1_apply_reduced(int nx, int ny, int nz, int nrhs, const vx_c128* factors, const int* perm,
-                                      const int* items, int n_single, const int* klist, const vx_c128* inv,
+                                      const int* items, int n_single, int direct_r, const int* klist,
+                                      const vx_c128* inv,
                                       const int* rep_ks, int n_rep, const vx_c128* x, vx_c128* y,
                                       vx_c128* work, void* stream) {
   VX_REQUIRE(nx >= 1 && ny >= 1 && nz >= 1 && nrhs >= 1 && n_single >= 0 && n_rep >= 0,
              "bad reduced 1-level apply arguments");
+  VX_REQUIRE(direct_r == 1 || direct_r == 2, "direct_r must be 1 or 2");
   cudaStream_t s = as_stream(stream);
   Span span("prec_apply", s);
   FftPlan p;
@@ -1763,13 +1807,13 @@ extern "C" int vx_prec1_apply_reduced(int nx, int ny, int nz, int nrhs, const vx
     static const int rep_persist = env_int("VX_REP_PERSIST", 0);
     const int persist = (ss && n_rep > 0) ? rep_persist : -1;
     if (singles_first && n_single > 0 &&
-        (st = solve_items(g, F, perm, items, n_single, n_single, klist, nrhs, S, pitch, nrhs, s, persist)))
+        (st = solve_items(g, F, perm, items, n_single, n_single, klist, nrhs, S, pitch, nrhs, s, persist, direct_r)))
       return st;
     if (n_rep > 0 &&
         (st = rep_gemm(q3, reinterpret_cast<const double2*>(inv), n_rep * nrhs, nrhs, rep_ks, S, pitch, nrhs, Bt, sr)))
       return st;
     if (!singles_first && n_single > 0 &&
-        (st = solve_items(g, F, perm, items, n_single, n_single, klist, nrhs, S, pitch, nrhs, s, persist)))
+        (st = solve_items(g, F, perm, items, n_single, n_single, klist, nrhs, S, pitch, nrhs, s, persist, direct_r)))
       return st;
     if (ss && n_rep > 0) {
       VX_CUDA(cudaEventRecord(ss->join, sr));

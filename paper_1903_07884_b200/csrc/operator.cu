@@ -485,39 +485,42 @@ __global__ void spec_compact_kernel(const double2* __restrict__ full, double2* _
   }
 }
 
-// per-CTA max |t_p(d) - s_p t_p(-d)| and max |t_p(d)| over the generators
+// per-CTA max |t_p(d) - s_p t_p(d')| for d' = d mirrored in x, in y and in z
+// separately (s_p = the component's parity on that axis), and max |t_p(d)|
 __global__ void gen_asym_kernel(const double2* __restrict__ g, long sp, long sz, long sy, long sx, int nx, int ny,
                                 int nz, double* __restrict__ out) {
-  __shared__ double sa[256], sm[256];
+  __shared__ double sa[4][256];
   const int X = 2 * nx - 1, Y = 2 * ny - 1, Z = 2 * nz - 1;
   const long total = 6L * Z * Y * X;
-  double amax = 0.0, tmax = 0.0;
+  double ax = 0.0, ay = 0.0, az = 0.0, tmax = 0.0;
   for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < total; i += (long)gridDim.x * blockDim.x) {
     long r = i;
     const int ix = (int)(r % X); r /= X;
     const int iy = (int)(r % Y); r /= Y;
     const int iz = (int)(r % Z);
     const int p = (int)(r / Z);
-    const double2 a = g[p * sp + iz * sz + iy * sy + ix * sx];
-    const double2 b = g[p * sp + (Z - 1 - iz) * sz + (Y - 1 - iy) * sy + (X - 1 - ix) * sx];
-    const double s = ((odd_x(p) ? -1 : 1) * (odd_y(p) ? -1 : 1) * (odd_z(p) ? -1 : 1));
-    amax = fmax(amax, fmax(fabs(a.x - s * b.x), fabs(a.y - s * b.y)));
+    const double2* gp = g + p * sp;
+    const double2 a = gp[iz * sz + iy * sy + ix * sx];
+    const double2 bx = gp[iz * sz + iy * sy + (X - 1 - ix) * sx];
+    const double2 by = gp[iz * sz + (Y - 1 - iy) * sy + ix * sx];
+    const double2 bz = gp[(Z - 1 - iz) * sz + iy * sy + ix * sx];
+    const double fx = odd_x(p) ? -1.0 : 1.0, fy = odd_y(p) ? -1.0 : 1.0, fz = odd_z(p) ? -1.0 : 1.0;
+    ax = fmax(ax, fmax(fabs(a.x - fx * bx.x), fabs(a.y - fx * bx.y)));
+    ay = fmax(ay, fmax(fabs(a.x - fy * by.x), fabs(a.y - fy * by.y)));
+    az = fmax(az, fmax(fabs(a.x - fz * bz.x), fabs(a.y - fz * bz.y)));
     tmax = fmax(tmax, fmax(fabs(a.x), fabs(a.y)));
   }
-  sa[threadIdx.x] = amax;
-  sm[threadIdx.x] = tmax;
+  sa[0][threadIdx.x] = ax;
+  sa[1][threadIdx.x] = ay;
+  sa[2][threadIdx.x] = az;
+  sa[3][threadIdx.x] = tmax;
   __syncthreads();
   for (int o = 128; o > 0; o >>= 1) {
-    if ((int)threadIdx.x < o) {
-      sa[threadIdx.x] = fmax(sa[threadIdx.x], sa[threadIdx.x + o]);
-      sm[threadIdx.x] = fmax(sm[threadIdx.x], sm[threadIdx.x + o]);
-    }
+    if ((int)threadIdx.x < o)
+      for (int c = 0; c < 4; ++c) sa[c][threadIdx.x] = fmax(sa[c][threadIdx.x], sa[c][threadIdx.x + o]);
     __syncthreads();
   }
-  if (threadIdx.x == 0) {
-    out[2 * blockIdx.x] = sa[0];
-    out[2 * blockIdx.x + 1] = sm[0];
-  }
+  if (threadIdx.x < 4) out[4 * blockIdx.x + threadIdx.x] = sa[threadIdx.x][0];
 }
 }  // namespace vx
 

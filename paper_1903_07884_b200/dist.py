@@ -180,7 +180,7 @@ class CudaBackend:
 
     def solve(self, Y, n, factors, perm, items, n_single, n_items, klist, s_row):
         nv.call("vx_prec1_solve", n, 1, factors.data_ptr(), perm.data_ptr(), items.data_ptr(), n_single, n_items,
-                klist.data_ptr(), Y.data_ptr(), s_row, 1, nv.stream_ptr())
+                1, klist.data_ptr(), Y.data_ptr(), s_row, 1, nv.stream_ptr())
 
     def cgs_dots(self, V, nvec, w, part):
         out = self.empty(nvec + 1)

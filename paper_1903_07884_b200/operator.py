@@ -103,18 +103,26 @@ class OperatorPlan:
 SYMMETRY_RTOL = 1e-13
 
 
-def kernel_asymmetry(kernel: ToeplitzKernel) -> float:
-    """max |t_p(d) - s_p t_p(-d)| / max |t| over the generators (device reduction)."""
+def generator_axis_asymmetry(gen, dims) -> tuple:
+    """Relative parity defects (ax, ay, az) of device generators ``gen``
+    (a (6, 2nz-1, 2ny-1, 2nx-1) tensor or strided view): max over components
+    of |t_p(d) - s_p t_p(d mirrored on that axis)| / max |t|."""
     t = nv.require_cuda()
-    nx, ny, nz = kernel.grid.dims
-    gen = upload_tensors(kernel)
-    out = t.empty(512, dtype=t.float64, device="cuda")
+    nx, ny, nz = dims
+    out = t.empty(1024, dtype=t.float64, device="cuda")
     s = gen.stride()
     nv.call("vx_gen_asymmetry", nx, ny, nz, gen.data_ptr(), s[0], s[1], s[2], s[3], out.data_ptr(),
             nv.stream_ptr())
-    o = out.cpu().numpy().reshape(-1, 2)
-    tmax = o[:, 1].max()
-    return float(o[:, 0].max() / tmax) if tmax > 0 else 0.0
+    o = out.cpu().numpy().reshape(-1, 4).max(axis=0)
+    tmax = o[3]
+    if tmax <= 0:
+        return (0.0, 0.0, 0.0)
+    return tuple(float(v / tmax) for v in o[:3])
+
+
+def kernel_asymmetry(kernel: ToeplitzKernel) -> float:
+    """max over axes of the relative parity defect of the generators (device reduction)."""
+    return max(generator_axis_asymmetry(upload_tensors(kernel), kernel.grid.dims))
 
 
 def plan_operator(kernel: ToeplitzKernel, workers: int = 1, *, compact: bool | None = None) -> OperatorPlan:
