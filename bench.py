@@ -306,7 +306,7 @@ def stored_blocks_of(W, prec):
     mirror sharing (parity-symmetric kernels) one stored factor serves the
     blocks k and n-k, so this is about half the reference's block count."""
     precs = prec.box_precs if W.prec["kind"] == "blocked" else [prec]
-    return [(p.block_size, int(p._fac.shape[0])) for p in precs]
+    return [blk for p in precs for blk in p.stored_blocks]
 
 
 def run_ours(args):

@@ -146,6 +146,27 @@ int vx_prec1_apply_reduced(int nx, int ny, int nz, int nrhs, const vx_c128* fact
                            void* stream);
 int vx_rep_variant(int sequential);
 
+/* Symmetry sectors (paper_1903_07884_b200/sectors.py): when the kernel has y
+ * (z) parity and m_yz is mirror-symmetric in y (z), every D_k commutes with
+ * the reflections and is block-diagonal in their joint eigenbasis (2 or 4
+ * sectors of <= dmax rows).  vx_lu1_build_sec factorises slot kslot*nsec + s =
+ * sector s of block kset[kslot] (unfold tables rrow/rsc (nsec, dmax) and
+ * ccol/cw (nsec, dmax, 4), see sectors.py).  vx_prec1_apply_sec = x-DFT,
+ * orbit transform to sector coordinates U (nsec*dmax rows; orbit tables
+ * orows/osec (norb, 4), ocoef (norb, 4, 4); flipk[k] != 0 applies the x-mirror
+ * sign of a shared factor), the block solves (klist entries s*dmax*nx + k, no
+ * flags), the inverse transform and the inverse x-DFT.  Same result as
+ * vx_prec1_apply on the unreduced blocks up to rounding. */
+int vx_lu1_build_sec(int nx, int ny, int nz, const vx_c128* lamT, const vx_c128* m_yz, const int* kset, int nk,
+                     int nsec, int dmax, const int* rrow, const double* rsc, const int* ccol, const double* cw,
+                     vx_c128* factors, int* perm, int* piv, int* info, void* stream);
+long vx_prec1_sec_work_elems(int nx, int ny, int nz, int nrhs, int nsec, int dmax);
+int vx_prec1_apply_sec(int nx, int ny, int nz, int nrhs, const vx_c128* factors, const int* perm,
+                       const int* items, int n_single, int n_items, int direct_r, const int* klist,
+                       int nsec, int dmax,
+                       int norb, const int* orows, const int* osec, const double* ocoef,
+                       const unsigned char* flipk, const vx_c128* x, vx_c128* y, vx_c128* work, void* stream);
+
 /* Operator y / z passes: 1 (default) = register-resident column FFTs for the
  * padded lengths that have them (fft_reg.cuh), 0 = shared-memory line engine
  * only (A/B timing and cross-checks). */

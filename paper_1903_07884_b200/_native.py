@@ -82,6 +82,10 @@ _SIGS = {
     "vx_rep_inverse": (c_int, [c_int, P, P, P, P]),
     "vx_prec1_reduced_work_elems": (c_long, [c_int] * 5),
     "vx_prec1_apply_reduced": (c_int, [c_int] * 4 + [P, P, P, c_int, c_int, P, P, P, c_int, P, P, P, P]),
+    "vx_lu1_build_sec": (c_int, [c_int] * 3 + [P, P, P, c_int, c_int, c_int, P, P, P, P, P, P, P, P, P]),
+    "vx_prec1_sec_work_elems": (c_long, [c_int] * 6),
+    "vx_prec1_apply_sec": (c_int, [c_int] * 4 + [P, P, P, c_int, c_int, c_int, P, c_int, c_int, c_int, P, P, P, P,
+                                                  P, P, P, P]),
     "vx_rep_variant": (c_int, [c_int]),
     "vx_op_reg_fft": (c_int, [c_int]),
     "vx_prec1_solve": (c_int, [c_int, c_int, P, P, P, c_int, c_int, c_int, P, P, c_long, c_long, P]),

@@ -158,6 +158,22 @@ def _lu1(lam, m_yz_dev, kset_dev, nslots, nx, ny, nz):
     return fac, perm, piv, info
 
 
+def _lu1_sec(lam, m_yz_dev, kset_dev, nk, nx, ny, nz, sec):
+    """Sector factorisation (vx_lu1_build_sec): nk * nsec blocks of dmax rows."""
+    t = _torch()
+    sp = sec.plan
+    nslots = nk * sp.nsec
+    blk = int(nv.query("vx_lu_block_elems", sp.dmax))
+    fac = t.empty((nslots, blk), dtype=t.complex128, device="cuda")
+    perm = t.empty((nslots, sp.dmax), dtype=t.int32, device="cuda")
+    piv = t.empty((nslots, sp.dmax), dtype=t.int32, device="cuda")
+    info = t.empty((nslots,), dtype=t.int32, device="cuda")
+    nv.call("vx_lu1_build_sec", nx, ny, nz, lam.data_ptr(), m_yz_dev.data_ptr(), kset_dev.data_ptr(), nk,
+            sp.nsec, sp.dmax, sec.rrow.data_ptr(), sec.rsc.data_ptr(), sec.ccol.data_ptr(), sec.cw.data_ptr(),
+            fac.data_ptr(), perm.data_ptr(), piv.data_ptr(), info.data_ptr(), nv.stream_ptr())
+    return fac, perm, piv, info
+
+
 def _first_bad(info) -> int:
     bad = (info != 0).nonzero()
     return -1 if bad.numel() == 0 else int(bad[0, 0])
@@ -182,6 +198,31 @@ def mirror_axes(gen, dims) -> tuple:
         return False, False
     ax, ay, _ = generator_axis_asymmetry(gen, dims)
     return ax <= SYMMETRY_RTOL, ay <= SYMMETRY_RTOL
+
+
+def sector_axes(gen, dims, m_yz) -> tuple:
+    """(y, z): reflections that commute with every 1-level block -- kernel
+    parity on that axis and m~ mirror-symmetric (sectors.py; VX_SECTORS=0
+    disables the sector factorisation)."""
+    if os.environ.get("VX_SECTORS", "1") == "0":
+        return False, False
+    from .sectors import m_symmetric
+
+    _, ay, az = generator_axis_asymmetry(gen, dims)
+    return (ay <= SYMMETRY_RTOL and m_symmetric(m_yz, "y"),
+            az <= SYMMETRY_RTOL and m_symmetric(m_yz, "z"))
+
+
+class _SectorDev:
+    """Device copies of a SectorPlan's tables."""
+
+    def __init__(self, plan):
+        t = _torch()
+        self.plan = plan
+        dev = lambda a: t.from_numpy(np.ascontiguousarray(a)).cuda()  # noqa: E731
+        self.rrow, self.rsc, self.ccol, self.cw = dev(plan.rrow), dev(plan.rsc), dev(plan.ccol), dev(plan.cw)
+        self.orows, self.osec, self.ocoef = dev(plan.orows), dev(plan.osec), dev(plan.ocoef)
+        self.norb = int(plan.orows.shape[0])
 
 
 def _flip_signs(n: int, fx: bool, fy: bool) -> np.ndarray:
@@ -218,6 +259,17 @@ def _items_groups(groups):
     r = max((len(ks) for _, ks in groups), default=1)
     return (t.from_numpy(np.asarray(items, np.int32).reshape(-1).copy()).cuda(),
             t.from_numpy(np.asarray(klist if klist else [0], np.int32)).cuda(), r)
+
+
+def _items_by_slot(store: np.ndarray, entries: np.ndarray):
+    """Vectorised _items_groups: one item per distinct storage slot, its klist
+    entries in logical-block order -> (items, klist, max group size, n_items)."""
+    t = _torch()
+    order = np.argsort(store, kind="stable")
+    slots, starts, counts = np.unique(store[order], return_index=True, return_counts=True)
+    items = np.stack([slots, starts, counts], 1).astype(np.int32)
+    return (t.from_numpy(items.reshape(-1).copy()).cuda(),
+            t.from_numpy(entries[order].astype(np.int32)).cuda(), int(counts.max()), int(slots.size))
 
 
 def _untile(fac_row: np.ndarray, n: int) -> np.ndarray:
@@ -269,9 +321,65 @@ def _ret(yd, flat, is_t, shape):
 
 class _OneLevelBase:
     grid: VoxelGrid
+    _sec = None            # _SectorDev when the blocks are stored as symmetry sectors
+    _full_builder = None   # builds the plain dense-block preconditioner (for .lu / .piv)
+    _full = None
+
+    @property
+    def sectors(self) -> int:
+        """Symmetry sectors per frequency block (1: the plain dense factorisation)."""
+        return 1 if self._sec is None else self._sec.plan.nsec
+
+    def _dense(self):
+        """The plain (unsectored) preconditioner, built on demand for .lu/.piv."""
+        if self._full is None:
+            self._full = self._full_builder()
+        return self._full
+
+    def _sector_items(self, store, ks, flip, rep=None):
+        """Work list over sector slots: direct items (store[i]*nsec + s, frequencies
+        ks[i] with equal store) and, for the reduced scheme, chunks of 8 of the
+        representative's frequencies rep = (slot, ks) per sector."""
+        t = _torch()
+        nx = self.grid.nx
+        ns, dm = self._sec.plan.nsec, self._sec.plan.dmax
+        st = (np.asarray(store)[None, :] * ns + np.arange(ns)[:, None]).reshape(-1)
+        ent = (np.arange(ns)[:, None] * dm * nx + np.asarray(ks)[None, :]).reshape(-1)
+        order = np.argsort(st, kind="stable")
+        slots, starts, counts = np.unique(st[order], return_index=True, return_counts=True)
+        items = [np.stack([slots, starts, counts], 1)]
+        klist = [ent[order]]
+        n_single = int(slots.size)
+        direct_r = int(counts.max()) if counts.size else 1
+        if rep is not None:
+            rslot, rks = rep
+            off = int(klist[0].size)
+            for s in range(ns):
+                for c0 in range(0, len(rks), 8):
+                    chunk = np.asarray(rks[c0:c0 + 8])
+                    items.append(np.array([[rslot * ns + s, off, chunk.size]]))
+                    klist.append(s * dm * nx + chunk)
+                    off += chunk.size
+        items = np.concatenate(items).astype(np.int32)
+        klist = np.concatenate(klist).astype(np.int32)
+        flipk = np.zeros(nx, np.uint8)
+        flipk[np.asarray(ks)[np.asarray(flip, bool)]] = 1
+        self._items = t.from_numpy(items.reshape(-1).copy()).cuda()
+        self._klist = t.from_numpy(klist if klist.size else np.zeros(1, np.int32)).cuda()
+        self._flipk = t.from_numpy(flipk).cuda()
+        self._n_single, self._n_items, self._direct_r = n_single, int(items.shape[0]), direct_r
 
     def _apply_dev(self, xd, r):
         nx, ny, nz = self.grid.dims
+        if self._sec is not None:
+            sp, sd = self._sec.plan, self._sec
+            y = nv.empty_c128((self.grid.n_unknowns, r))
+            work = nv.empty_c128(int(nv.query("vx_prec1_sec_work_elems", nx, ny, nz, r, sp.nsec, sp.dmax)))
+            nv.call("vx_prec1_apply_sec", nx, ny, nz, r, self._fac.data_ptr(), self._perm.data_ptr(),
+                    self._items.data_ptr(), self._n_single, self._n_items, self._direct_r, self._klist.data_ptr(),
+                    sp.nsec, sp.dmax, sd.norb, sd.orows.data_ptr(), sd.osec.data_ptr(), sd.ocoef.data_ptr(),
+                    self._flipk.data_ptr(), xd.data_ptr(), y.data_ptr(), work.data_ptr(), nv.stream_ptr())
+            return y
         y = nv.empty_c128((self.grid.n_unknowns, r))
         work = nv.empty_c128(int(nv.query("vx_prec1_work_elems", nx, ny, nz, r)))
         nv.call("vx_prec1_apply", nx, ny, nz, r, self._fac.data_ptr(), self._perm.data_ptr(),
@@ -286,6 +394,16 @@ class _OneLevelBase:
     @property
     def block_size(self) -> int:
         return 3 * self.grid.ny * self.grid.nz
+
+    @property
+    def stored_blocks(self) -> list:
+        """[(dim, count)] of the factors actually stored (and streamed once per
+        apply): mirror sharing halves the count, sectors split each block."""
+        sec = getattr(self, "_sec", None)
+        if sec is None:
+            return [(self.block_size, int(self._fac.shape[0]))]
+        nk = int(self._fac.shape[0]) // sec.plan.nsec
+        return [(d, nk) for d in sec.plan.dims]
 
     @property
     def storage_bytes(self) -> int:
@@ -304,6 +422,8 @@ class _OneLevelBase:
 
     @property
     def lu(self) -> np.ndarray:
+        if self._sec is not None:
+            return self._dense().lu
         f = self._fac.cpu().numpy()
         pv = self._piv.cpu().numpy()
         n = self.block_size
@@ -314,6 +434,8 @@ class _OneLevelBase:
 
     @property
     def piv(self) -> np.ndarray:
+        if self._sec is not None:
+            return self._dense().piv
         return self._piv.cpu().numpy()[self._store]
 
 
@@ -340,17 +462,20 @@ class OneLevelPrec(_OneLevelBase):
 
     level = "one-level"
 
-    def __init__(self, grid, fac, perm, piv, proxy, store=None, flip=None):
+    def __init__(self, grid, fac, perm, piv, proxy, store=None, flip=None, sec=None, full_builder=None):
         self.grid = grid
         self._fac, self._perm, self._piv, self._proxy = fac, perm, piv, proxy
         nx = grid.nx
         self._store = np.arange(nx) if store is None else np.asarray(store)
         self._flip = np.zeros(nx, bool) if flip is None else np.asarray(flip, bool)
-        groups = {}
-        for k in range(nx):
-            groups.setdefault(int(self._store[k]), []).append(k | (KFLIP_X if self._flip[k] else 0))
-        self._items, self._klist, self._direct_r = _items_groups(sorted(groups.items()))
-        self._n_single = self._n_items = len(groups)
+        self._sec = sec
+        self._full_builder = full_builder
+        if sec is None:
+            entries = np.arange(nx) | np.where(self._flip, KFLIP_X, 0)
+            self._items, self._klist, self._direct_r, self._n_items = _items_by_slot(self._store, entries)
+            self._n_single = self._n_items
+        else:
+            self._sector_items(self._store, np.arange(nx), self._flip)
 
     @property
     def proxy(self) -> np.ndarray:
@@ -365,7 +490,7 @@ class OneLevelPrec(_OneLevelBase):
                 "block_size": int(self.block_size), "bytes": int(self.bytes)}
 
 
-def _build_one_level_dev(grid, gen, m_yz, cap_bytes, tol=None):
+def _build_one_level_dev(grid, gen, m_yz, cap_bytes, tol=None, sectors=True):
     """Shared device build for full (tol None) and reduced 1-level."""
     t = _torch()
     nx, ny, nz = grid.dims
@@ -379,6 +504,19 @@ def _build_one_level_dev(grid, gen, m_yz, cap_bytes, tol=None):
     if tol is None:
         kset, store, flip = _mirror_store(np.arange(nx), nx, share)
         kdev = t.from_numpy(kset.astype(np.int32)).cuda()
+        sy, sz = sector_axes(gen, grid.dims, m_yz) if sectors else (False, False)
+        if sy or sz:
+            from .sectors import sector_plan
+
+            sec = _SectorDev(sector_plan(ny, nz, sy, sz))
+            fac, perm, piv, info = _lu1_sec(lam, m_dev, kdev, int(kset.size), nx, ny, nz, sec)
+            bad = _first_bad(info)
+            if bad >= 0:
+                raise PreconditionerBuildError(
+                    f"1-level build failed: singular frequency block k={int(kset[bad // sec.plan.nsec])}")
+            return OneLevelPrec(grid, fac, perm, piv, proxy, store, flip, sec=sec,
+                                full_builder=lambda: _build_one_level_dev(grid, gen, m_yz, cap_bytes,
+                                                                          sectors=False))
         fac, perm, piv, info = _lu1(lam, m_dev, kdev, int(kset.size), nx, ny, nz)
         bad = _first_bad(info)
         if bad >= 0:
@@ -389,6 +527,18 @@ def _build_one_level_dev(grid, gen, m_yz, cap_bytes, tol=None):
     _check_cap(kept.size * (3 * q) ** 2 * BYTES_PER_ENTRY, cap_bytes, "consider the 2-level preconditioner")
     kset, store, flip = _mirror_store(kept, nx, share)
     kdev = t.from_numpy(kset.astype(np.int32)).cuda()
+    sy, sz = sector_axes(gen, grid.dims, m_yz) if sectors else (False, False)
+    if sy or sz:
+        from .sectors import sector_plan
+
+        sec = _SectorDev(sector_plan(ny, nz, sy, sz))
+        fac, perm, piv, info = _lu1_sec(lam, m_dev, kdev, int(kset.size), nx, ny, nz, sec)
+        bad = _first_bad(info)
+        if bad >= 0:
+            raise PreconditionerBuildError(f"singular frequency block k={int(kset[bad // sec.plan.nsec])}")
+        return ReducedOneLevelPrec(grid, kept, slot_of, rep, fac, perm, piv, ph, v_hat, float(tol), store, flip,
+                                   sec=sec, full_builder=lambda: _build_one_level_dev(grid, gen, m_yz, cap_bytes,
+                                                                                      tol=tol, sectors=False))
     fac, perm, piv, info = _lu1(lam, m_dev, kdev, int(kset.size), nx, ny, nz)
     bad = _first_bad(info)
     if bad >= 0:
@@ -415,7 +565,7 @@ class ReducedOneLevelPrec(_OneLevelBase):
     level = "reduced-one-level"
 
     def __init__(self, grid, kept, slot_of, representative, fac, perm, piv, proxy, v_hat, tol,
-                 store=None, flip=None):
+                 store=None, flip=None, sec=None, full_builder=None):
         self.grid = grid
         self.kept = np.asarray(kept)
         self.slot_of = np.asarray(slot_of)
@@ -426,12 +576,19 @@ class ReducedOneLevelPrec(_OneLevelBase):
         self.proxy = np.asarray(proxy)
         self.proxy_normalized = np.asarray(v_hat)
         self.tol = float(tol)
+        self._sec, self._full_builder = sec, full_builder
         self._make_worklist()
 
     def _make_worklist(self):
         t = _torch()
         rep_idx = int(self.slot_of[self.representative])   # kept index of the representative
         rep_slot = int(self._store[rep_idx])                 # its storage slot (never flipped)
+        self._inv = None
+        if self._sec is not None:
+            keep = np.arange(self.kept.size) != rep_idx
+            rep_ks = np.flatnonzero(self.slot_of == rep_idx)
+            self._sector_items(self._store[keep], self.kept[keep], self._flip[keep], rep=(rep_slot, rep_ks))
+            return
         groups = {}
         for i, k in enumerate(self.kept):
             if i != rep_idx:
@@ -457,7 +614,7 @@ class ReducedOneLevelPrec(_OneLevelBase):
             self._rep_ks = t.from_numpy(rep_ks.astype(np.int32)).cuda()
 
     def _apply_dev(self, xd, r):
-        if self._inv is None:
+        if self._inv is None or self._sec is not None:
             return super()._apply_dev(xd, r)
         nx, ny, nz = self.grid.dims
         n_rep = int(self._rep_ks.numel())
@@ -493,10 +650,15 @@ def reduce_one_level(prec: OneLevelPrec, tol: float = 1e-3) -> ReducedOneLevelPr
     flip = prec._flip[kept].copy()
     # a kept block whose stored partner was discarded keeps that partner's
     # factor (stored under the kept block's index, flipped)
-    idx = t.from_numpy(uniq.astype(np.int64)).cuda()
+    ns = prec.sectors
+    rows = (uniq[:, None] * ns + np.arange(ns)[None, :]).reshape(-1)
+    idx = t.from_numpy(rows.astype(np.int64)).cuda()
+    fb = None
+    if prec._sec is not None:
+        fb = lambda: reduce_one_level(prec._dense(), tol)  # noqa: E731
     return ReducedOneLevelPrec(prec.grid, kept, slot_of, rep, prec._fac.index_select(0, idx),
                                prec._perm.index_select(0, idx), prec._piv.index_select(0, idx),
-                               proxy.copy(), v_hat, float(tol), store, flip)
+                               proxy.copy(), v_hat, float(tol), store, flip, sec=prec._sec, full_builder=fb)
 
 
 def build_reduced_one_level(kernel: ToeplitzKernel, mtilde, tol: float = 1e-3, *,
@@ -528,18 +690,18 @@ class TwoLevelPrec:
         if store is None:
             self._items, self._klist, self._direct_r, self._n_items = None, None, 1, nb
         else:
-            groups = {}
-            for b in range(nb):
-                fx, fy = self._flips[b]
-                groups.setdefault(int(self._store[b]), []).append(
-                    b | (KFLIP_X if fx else 0) | (KFLIP_Y if fy else 0))
-            self._items, self._klist, r = _items_groups(sorted(groups.items()))
+            entries = (np.arange(nb) | np.where(self._flips[:, 0], KFLIP_X, 0)
+                       | np.where(self._flips[:, 1], KFLIP_Y, 0))
+            self._items, self._klist, r, self._n_items = _items_by_slot(self._store, entries)
             self._direct_r = 1 if r == 1 else (2 if r == 2 else 4)
-            self._n_items = len(groups)
 
     @property
     def mirror_shared(self) -> bool:
         return bool(np.any(self._flips))
+
+    @property
+    def stored_blocks(self) -> list:
+        return [(self.block_size, int(self._fac.shape[0]))]
 
     @property
     def block_size(self) -> int:

@@ -479,6 +479,101 @@ __global__ void __launch_bounds__(256) lub_unfold_kernel(Unfold u, LuGeom g, dou
   }
 }
 
+// Symmetry-sector unfold (sectors.py): slot = kslot * nsec + s holds
+//   B_s[j, j'] = rsc[j] * sum_t cw[j', t] * D_k[rrow[j], ccol[j', t]]
+// with D_k = I - diag(m) N_k evaluated on the fly (reference accel.py:71-91);
+// rows / cols >= the sector's size (rrow / ccol = -1) are identity.
+struct SecUnfold {
+  const double2* __restrict__ lamT;
+  const double2* __restrict__ m;
+  const int* __restrict__ kset;
+  long Ltot;
+  int nzL, nyL, nsec, dmax;
+  const int* __restrict__ rrow;    // [nsec][dmax]
+  const double* __restrict__ rsc;  // [nsec][dmax]
+  const int* __restrict__ ccol;    // [nsec][dmax][4]
+  const double* __restrict__ cw;   // [nsec][dmax][4]
+};
+
+__global__ void __launch_bounds__(256) sec_unfold_kernel(SecUnfold u, LuGeom g, double2* F) {
+  extern __shared__ __align__(16) unsigned char smu[];
+  const int T = g.T, nt = g.nt, npad = g.npad;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int slot = blockIdx.x;
+  const int kslot = slot / u.nsec, sec = slot - kslot * u.nsec;
+  const int k = u.kset ? u.kset[kslot] : kslot;
+  double2* A = F + (long)slot * g.blk;
+  const double2* lam = u.lamT + (long)k * u.Ltot;
+  const int q = u.nzL * u.nyL;
+  const int nyy = 2 * u.nyL - 1, nzz = 2 * u.nzL - 1;
+  const int P = nzz * nyy, base = (u.nzL - 1) * nyy + (u.nyL - 1);
+  double2* rm = reinterpret_cast<double2*>(smu);          // [npad] m at the row's site * rsc
+  double* cwt = reinterpret_cast<double*>(rm + npad);     // [npad][4]
+  int* rkey = reinterpret_cast<int*>(cwt + 4 * npad);     // [npad] (a << 24) | offset, -1 pad
+  int* rid = rkey + npad;                                 // [npad] original row
+  int* ckey = rid + npad;                                 // [npad][4]
+  int* cid = ckey + 4 * npad;                             // [npad][4]
+  const long sb = (long)sec * u.dmax;
+  auto key_of = [&](int o) {
+    const int a = o / q, rr = o - a * q;
+    const int iz = rr / u.nyL, iy = rr - iz * u.nyL;
+    return (a << 24) | (iz * nyy + iy);
+  };
+  for (int j = tid; j < npad; j += 256) {
+    const int r = j < u.dmax ? u.rrow[sb + j] : -1;
+    rid[j] = r;
+    if (r >= 0) {
+      rkey[j] = key_of(r);
+      const double2 mv = __ldg(u.m + (r % q));
+      const double sc = u.rsc[sb + j];
+      rm[j] = cmk(mv.x * sc, mv.y * sc);
+    } else {
+      rkey[j] = -1;
+    }
+    for (int t = 0; t < 4; ++t) {
+      const int c = j < u.dmax ? u.ccol[(sb + j) * 4 + t] : -1;
+      cid[4 * j + t] = c;
+      ckey[4 * j + t] = c >= 0 ? key_of(c) : -1;
+      cwt[4 * j + t] = c >= 0 ? u.cw[(sb + j) * 4 + t] : 0.0;
+    }
+  }
+  __syncthreads();
+  const int ncolw = nt * nt * T;
+  for (int w = warp; w < ncolw; w += 8) {
+    const int tile = w / T, c = w - tile * T;
+    const int it = tile / nt, jt = tile - it * nt;
+    const int col = jt * T + c;
+    if (lane >= T) continue;
+    const int row = it * T + lane;
+    double2 v = cmk(row == col ? 1.0 : 0.0, 0.0);
+    const int rk = rkey[row];
+    if (rk >= 0 && ckey[4 * col] >= 0) {
+      const int a = rk >> 24, r0 = rid[row];
+      const double sc = u.rsc[sb + row];
+      double2 acc = cmk(0.0, 0.0);   // sum_t w_t * N[row, c_t]
+      double dsum = 0.0;             // sum_t w_t * [row == c_t]
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const int ck = ckey[4 * col + t];
+        if (ck < 0) continue;
+        const double wt = cwt[4 * col + t];
+        const int b = ck >> 24;
+        const double2 tv = __ldg(lam + (long)c_pair[3 * a + b] * P + (rk & 0xffffff) - (ck & 0xffffff) + base);
+        acc.x = fma(wt, tv.x, acc.x);
+        acc.y = fma(wt, tv.y, acc.y);
+        if (cid[4 * col + t] == r0) dsum += wt;
+      }
+      const double2 mn = cmul(rm[row], acc);
+      v = cmk(sc * dsum - mn.x, -mn.y);
+    }
+    A[((long)tile * T + c) * T + lane] = v;
+  }
+}
+
+static size_t sec_unfold_smem(const LuGeom& g) {
+  return (size_t)g.npad * (sizeof(double2) + 4 * sizeof(double) + 2 * sizeof(int) + 8 * sizeof(int));
+}
+
 // panel factorisation of tile column kt of every block (one CTA per block),
 // then the diagonal tile's triangular inverses, packed in place.
 __global__ void __launch_bounds__(LU_THREADS) lub_panel_kernel(LuGeom g, double2* F, int kt, int* piv,
@@ -688,14 +783,23 @@ __global__ void lub_perm_kernel(int nslots, int n, const int* piv, int* perm, in
 static int g_lu_monolithic = 0;  // vx_lu_variant(1): single-kernel LU (A/B timing)
 
 static int lu_build_batched(const Unfold& u, const LuGeom& g, int nslots, double2* F, int* perm, int* piv,
-                            int* info, cudaStream_t s) {
+                            int* info, cudaStream_t s, const SecUnfold* su = nullptr) {
   VX_CUDA(cudaMemsetAsync(info, 0, sizeof(int) * nslots, s));
-  const size_t us = (size_t)((g.npad + 3) & ~3) * sizeof(int) + (size_t)g.npad * sizeof(double2);
-  if (us > 48 * 1024)
-    VX_CUDA(cudaFuncSetAttribute(lub_unfold_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)us));
-  VX_REQUIRE((int)us <= device_smem_optin(), "block size %d too large for the unfold tables", g.n);
-  lub_unfold_kernel<<<nslots, 256, us, s>>>(u, g, F);
-  VX_CHECK_LAUNCH("lub_unfold_kernel");
+  if (su) {
+    const size_t us = sec_unfold_smem(g);
+    if (us > 48 * 1024)
+      VX_CUDA(cudaFuncSetAttribute(sec_unfold_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)us));
+    VX_REQUIRE((int)us <= device_smem_optin(), "sector size %d too large for the unfold tables", g.n);
+    sec_unfold_kernel<<<nslots, 256, us, s>>>(*su, g, F);
+    VX_CHECK_LAUNCH("sec_unfold_kernel");
+  } else {
+    const size_t us = (size_t)((g.npad + 3) & ~3) * sizeof(int) + (size_t)g.npad * sizeof(double2);
+    if (us > 48 * 1024)
+      VX_CUDA(cudaFuncSetAttribute(lub_unfold_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)us));
+    VX_REQUIRE((int)us <= device_smem_optin(), "block size %d too large for the unfold tables", g.n);
+    lub_unfold_kernel<<<nslots, 256, us, s>>>(u, g, F);
+    VX_CHECK_LAUNCH("lub_unfold_kernel");
+  }
   for (int kt = 0; kt < g.nt; ++kt) {
     lub_panel_kernel<<<nslots, LU_THREADS, 0, s>>>(g, F, kt, piv, info);
     VX_CHECK_LAUNCH("lub_panel_kernel");
@@ -1086,7 +1190,19 @@ __global__ void __launch_bounds__((PIPE_CONSUMERS + 1) * 32)
           const long tq = t + q;
           const int s = (int)(tq % S);
           mbar_wait(full + s, (uint32_t)(tq / S) & 1);
-          if (q % NWC == warp) {
+          if (!dmma && lane < T) {
+            // every consumer warp takes a column slice of every tile: the
+            // tile GEMV is spread over all warps (short per-tile latency, so
+            // the few ring slots turn over fast); partial sums meet in red
+            const double2* tile = slots + (long)s * T2 + lane;
+            const double2* yj = y + (long)(j0 + q) * T * R;
+            const int cpw = (T + NWC - 1) / NWC, c0 = warp * cpw, c1 = min(T, c0 + cpw);
+            for (int c = c0; c < c1; ++c) {
+              const double2 a = tile[c * T];
+#pragma unroll
+              for (int rr = 0; rr < R; ++rr) cfma(acc[rr], a, yj[c * R + rr]);
+            }
+          } else if (q % NWC == warp) {
             if (dmma) {
               if constexpr (USE_DMMA) {
                 const double2* tile = slots + (long)s * T2;
@@ -1104,15 +1220,6 @@ __global__ void __launch_bounds__((PIPE_CONSUMERS + 1) * 32)
                     dmma884(ci[rb][0], ci[rb][1], a.y, b.x);
                   }
                 }
-              }
-            } else if (lane < T) {
-              const double2* tile = slots + (long)s * T2 + lane;
-              const double2* yj = y + (long)(j0 + q) * T * R;
-#pragma unroll 4
-              for (int c = 0; c < T; ++c) {
-                const double2 a = tile[c * T];
-#pragma unroll
-                for (int rr = 0; rr < R; ++rr) cfma(acc[rr], a, yj[c * R + rr]);
               }
             }
           }
@@ -1250,8 +1357,11 @@ static int launch_solve_pipe(const LuGeom& g, const double2* F, const int* perm,
                        sizeof(double2);
   // two CTAs per SM when the vector state is small, otherwise one
   static const int budget_kb = env_int("VX_PIPE_BUDGET_KB", 0);
-  size_t budget = (fixed < 40 * 1024 ? 112 * 1024 : (size_t)device_smem_optin() - 2048);
-  if (budget_kb > 0 && R == 1) budget = (size_t)budget_kb * 1024;
+  // small blocks (symmetry sectors: <= 8 x 8 tiles) run 3 CTAs per SM -- their
+  // per-block fill / gather / diagonal latencies need more CTAs in flight;
+  // bigger ones 2 (or 1 when the vector state is large)
+  size_t budget = (fixed < 40 * 1024 ? (g.nt <= 8 ? 72 : 112) * 1024 : (size_t)device_smem_optin() - 2048);
+  if (budget_kb > 0 && R <= 2) budget = (size_t)budget_kb * 1024;
   int S = (int)((budget > fixed ? budget - fixed : 0) / tile);
   if (S > 16) S = 16;
   VX_REQUIRE(S >= 2, "block size %d too large for the pipelined solve", g.n);
@@ -1316,6 +1426,77 @@ static int solve_items(const LuGeom& g, const double2* F, const int* perm, const
                                            s_row, s_k, s)
               : launch_solve<MULTI_R, SOLVE_WARPS>(g, F, perm, items, n_single, n_items - n_single, klist, nrhs,
                                                    Y, s_row, s_k, s);
+}
+
+// ------------------------------------------------- symmetry-sector transform
+// One orbit o = (component, site orbit under the reflections) per grid row:
+// forward  u[osec[o][s]] = sum_t ocoef[o][s][t] x[orows[o][t]]   (V^T x)
+// inverse  x[orows[o][t]] = sum_s ocoef[o][s][t] u[osec[o][s]]   (V u)
+// at every spectral column col = k*nrhs + j of the (rows x pitch) arrays;
+// flipk[k] (nullable) applies the x-mirror sign of a shared factor (x rows).
+__global__ void __launch_bounds__(256) sec_xform_kernel(long pitch, int nrhs, const int* __restrict__ orows,
+                                                        const int* __restrict__ osec,
+                                                        const double* __restrict__ ocoef,
+                                                        const unsigned char* __restrict__ flipk, int q,
+                                                        const double2* __restrict__ in, double2* __restrict__ out,
+                                                        int inverse) {
+  const int o = blockIdx.y;
+  int rw[4], sc[4];
+  double cf[4][4];
+#pragma unroll
+  for (int t = 0; t < 4; ++t) {
+    rw[t] = __ldg(orows + 4 * o + t);
+    sc[t] = __ldg(osec + 4 * o + t);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) cf[t][u] = __ldg(ocoef + 16 * o + 4 * t + u);  // [s][t]
+  }
+  const bool xrow = rw[0] < q;
+  for (long col = blockIdx.x * (long)blockDim.x + threadIdx.x; col < pitch; col += (long)gridDim.x * blockDim.x) {
+    const double sg = (flipk && xrow && flipk[col / nrhs]) ? -1.0 : 1.0;
+    if (!inverse) {
+      double2 v[4];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) v[t] = rw[t] >= 0 ? __ldg(in + (long)rw[t] * pitch + col) : cmk(0.0, 0.0);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (sc[u] < 0) continue;
+        double2 a = cmk(0.0, 0.0);
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          a.x = fma(cf[u][t], v[t].x, a.x);
+          a.y = fma(cf[u][t], v[t].y, a.y);
+        }
+        out[(long)sc[u] * pitch + col] = cmk(sg * a.x, sg * a.y);
+      }
+    } else {
+      double2 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = sc[u] >= 0 ? __ldg(in + (long)sc[u] * pitch + col) : cmk(0.0, 0.0);
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        if (rw[t] < 0) continue;
+        double2 a = cmk(0.0, 0.0);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          a.x = fma(cf[u][t], v[u].x, a.x);
+          a.y = fma(cf[u][t], v[u].y, a.y);
+        }
+        out[(long)rw[t] * pitch + col] = cmk(sg * a.x, sg * a.y);
+      }
+    }
+  }
+}
+
+static int sec_xform(long pitch, int nrhs, int norb, const int* orows, const int* osec, const double* ocoef,
+                     const unsigned char* flipk, int q, const double2* in, double2* out, int inverse,
+                     cudaStream_t s) {
+  if (norb <= 0) return VX_OK;
+  long bx = div_up(pitch, 256);
+  if (bx > 64) bx = 64;
+  dim3 grid((unsigned)bx, (unsigned)norb);
+  sec_xform_kernel<<<grid, 256, 0, s>>>(pitch, nrhs, orows, osec, ocoef, flipk, q, in, out, inverse);
+  VX_CHECK_LAUNCH("sec_xform_kernel");
+  return VX_OK;
 }
 
 // ---------------------------------------------------------------- blocked
@@ -1830,5 +2011,65 @@ extern "C" int vx_prec1_apply_reduced(int nx, int ny, int nz, int nrhs, const vx
 
 extern "C" int vx_rep_variant(int sequential) {
   vx::g_rep_sequential = sequential ? 1 : 0;
+  return VX_OK;
+}
+
+// ------------------------------------------------------------ sector entries
+extern "C" int vx_lu1_build_sec(int nx, int ny, int nz, const vx_c128* lamT, const vx_c128* m_yz, const int* kset,
+                                int nk, int nsec, int dmax, const int* rrow, const double* rsc, const int* ccol,
+                                const double* cw, vx_c128* factors, int* perm, int* piv, int* info, void* stream) {
+  VX_REQUIRE(nx >= 1 && ny >= 1 && nz >= 1 && nk >= 0 && nsec >= 1 && nsec <= 4 && dmax >= 1,
+             "bad sector build arguments");
+  const int nslots = nk * nsec;
+  if (nslots == 0) return VX_OK;
+  cudaStream_t s = as_stream(stream);
+  Span span("lu_build", s);
+  Unfold u{reinterpret_cast<const double2*>(lamT), reinterpret_cast<const double2*>(m_yz), kset,
+           6L * (2 * nz - 1) * (2 * ny - 1), nz, ny};
+  SecUnfold su{reinterpret_cast<const double2*>(lamT), reinterpret_cast<const double2*>(m_yz), kset,
+               6L * (2 * nz - 1) * (2 * ny - 1), nz, ny, nsec, dmax, rrow, rsc, ccol, cw};
+  return lu_build_batched(u, lu_geom(dmax), nslots, reinterpret_cast<double2*>(factors), perm, piv, info, s, &su);
+}
+
+extern "C" long vx_prec1_sec_work_elems(int nx, int ny, int nz, int nrhs, int nsec, int dmax) {
+  return (3L * ny * nz + (long)nsec * dmax) * nx * nrhs;
+}
+
+extern "C" int vx_prec1_apply_sec(int nx, int ny, int nz, int nrhs, const vx_c128* factors, const int* perm,
+                                  const int* items, int n_single, int n_items, int direct_r, const int* klist,
+                                  int nsec, int dmax,
+                                  int norb, const int* orows, const int* osec, const double* ocoef,
+                                  const unsigned char* flipk, const vx_c128* x, vx_c128* y, vx_c128* work,
+                                  void* stream) {
+  VX_REQUIRE(nx >= 1 && ny >= 1 && nz >= 1 && nrhs >= 1 && n_single >= 0 && n_items >= n_single && nsec >= 1 &&
+                 dmax >= 1,
+             "bad sector apply arguments");
+  VX_REQUIRE(direct_r == 1 || direct_r == 2, "direct_r must be 1 or 2");
+  VX_REQUIRE((long)nsec * dmax * nx < (1L << 29), "sector layout too large for the work-list encoding");
+  cudaStream_t s = as_stream(stream);
+  Span span("prec_apply", s);
+  FftPlan p;
+  int st = fft_get_plan(nx, &p);
+  if (st) return st;
+  const int q = ny * nz, q3 = 3 * q;
+  double2* S = reinterpret_cast<double2*>(work);
+  double2* U = S + (long)q3 * nx * nrhs;
+  const long pitch = (long)nx * nrhs;
+  {
+    LoadStrided ld{reinterpret_cast<const double2*>(x), {pitch, 1, nrhs, nrhs}};
+    StoreStrided sv{S, {pitch, 1, nrhs, nrhs}, 1.0};
+    if ((st = launch_fft_lines(p, ld, sv, q3 * nrhs, nx, nx, false, nrhs == 1, s))) return st;
+  }
+  VX_CUDA(cudaMemsetAsync(U, 0, sizeof(double2) * (size_t)nsec * dmax * pitch, s));
+  if ((st = sec_xform(pitch, nrhs, norb, orows, osec, ocoef, flipk, q, S, U, 0, s))) return st;
+  if ((st = solve_items(lu_geom(dmax), reinterpret_cast<const double2*>(factors), perm, items, n_single, n_items,
+                        klist, nrhs, U, pitch, nrhs, s, -1, direct_r)))
+    return st;
+  if ((st = sec_xform(pitch, nrhs, norb, orows, osec, ocoef, flipk, q, U, S, 1, s))) return st;
+  {
+    LoadStrided ld{S, {pitch, 1, nrhs, nrhs}};
+    StoreStrided sv{reinterpret_cast<double2*>(y), {pitch, 1, nrhs, nrhs}, 1.0 / nx};
+    if ((st = launch_fft_lines(p, ld, sv, q3 * nrhs, nx, nx, true, nrhs == 1, s))) return st;
+  }
   return VX_OK;
 }

@@ -197,6 +197,38 @@ __device__ __forceinline__ double2 tw_get(const double2* twsm, int t) {
   return cmul(twsm[64 + (t >> 6)], twsm[t & 63]);
 }
 
+// v[r] *= w^(t0*r), r = 1..R-1 (w = e^{sgn 2 pi i / L}): two table lookups
+// (w^t0 and w^(2 t0)), the rest by products of those -- the stage loops are
+// shared-memory-bound and every lookup is two scattered smem loads.
+// VX_TW_EXACT keeps one lookup per twiddle.
+template <int R>
+__device__ __forceinline__ void twiddle_row(double2* v, const double2* twsm, int t0, double sgn) {
+#ifdef VX_TW_EXACT
+#pragma unroll
+  for (int r = 1; r < R; ++r) {
+    double2 t = tw_get(twsm, t0 * r);
+    t.y *= -sgn;
+    v[r] = cmul(v[r], t);
+  }
+#else
+  double2 w1 = tw_get(twsm, t0);
+  w1.y *= -sgn;
+  v[1] = cmul(v[1], w1);
+  if constexpr (R > 2) {
+    double2 w2 = tw_get(twsm, 2 * t0);
+    w2.y *= -sgn;
+    v[2] = cmul(v[2], w2);
+    double2 wo = w1;  // odd powers w^(2k+1) = w^(2k-1) w^2, even ones w^(2k) = w^(2k-2) w^2
+    double2 we = w2;
+#pragma unroll
+    for (int r = 3; r < R; ++r) {
+      if (r & 1) { wo = cmul(wo, w2); v[r] = cmul(v[r], wo); }
+      else       { we = cmul(we, w2); v[r] = cmul(v[r], we); }
+    }
+  }
+#endif
+}
+
 template <int R, bool DIT>
 __device__ __forceinline__ void fft_stage(double2* s, SmemLay lay, int W, const FastDiv& fdW, int n, int m,
                                           const FastDiv& fdm, const FastDiv& fdnb,
@@ -216,23 +248,9 @@ __device__ __forceinline__ void fft_stage(double2* s, SmemLay lay, int W, const 
     double2 v[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) v[r] = q[r * st];
-    if (DIT && j) {
-#pragma unroll
-      for (int r = 1; r < R; ++r) {
-        double2 t = tw_get(tw, j * r * tws);
-        t.y *= -sgn;
-        v[r] = cmul(v[r], t);
-      }
-    }
+    if (DIT && j) twiddle_row<R>(v, tw, j * tws, sgn);
     dft_codelet<R>(v, sgn);
-    if (!DIT && j) {
-#pragma unroll
-      for (int r = 1; r < R; ++r) {
-        double2 t = tw_get(tw, j * r * tws);
-        t.y *= -sgn;
-        v[r] = cmul(v[r], t);
-      }
-    }
+    if (!DIT && j) twiddle_row<R>(v, tw, j * tws, sgn);
 #pragma unroll
     for (int r = 0; r < R; ++r) q[r * st] = v[r];
   }

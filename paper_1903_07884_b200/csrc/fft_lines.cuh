@@ -78,7 +78,7 @@ struct StoreSystem {
 // RMAX = largest radix compiled in: 8 (radices 2..8, 3, 5, 7 -> ~64 registers,
 // two 512-thread CTAs per SM) or 13 (adds the 11/13 codelets).
 template <class Loader, class Storer, int RMAX>
-__global__ void __launch_bounds__(512, (RMAX <= 8 ? 2 : 1))
+__global__ void __launch_bounds__(RMAX <= 8 ? 1024 : 512, 1)
     fft_lines_kernel(FftPlan p, Loader ld, Storer st, int n_lines, int W, FastDiv fdW, int n_in, int n_out,
                      int inv, int contig) {
   extern __shared__ double2 smem[];
@@ -155,9 +155,16 @@ inline int pick_line_launch(const FftPlan& p, bool contig, int n_lines, LineLaun
     while (W > 1 && (size_t)W * p.L * sizeof(double2) > (size_t)strided_kb * 1024) W /= 2;
   }
   if (W > n_lines) W = n_lines > 0 ? n_lines : 1;
+  // a CTA that fills the SM's shared memory alone gets up to 1024 threads
+  // (radix <= 8 kernels fit 64 registers): the stages are smem-latency bound
+  static const int max_thr = env_int("VX_FFT_MAXTHR", 1024);
   for (;;) {
     size_t smem = ((size_t)W * p.L + 64 + p.nhi) * sizeof(double2) + 2 * W * sizeof(long);
     int thr = fft_threads_for(p, W);
+    if (fft_max_radix(p) <= 8 && smem > (size_t)budget / 2 && max_thr > 512) {
+      long t2 = ((long)W * p.L / 4 + 31) / 32 * 32;
+      thr = (int)(t2 < max_thr ? (t2 > thr ? t2 : thr) : max_thr);
+    }
     if (smem <= (size_t)budget) {
       out->W = W;
       out->threads = thr;

@@ -14,7 +14,8 @@ def launches(path):
     h = rows[hi]
     ki, vi, ui = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Unit")
     agg = collections.defaultdict(lambda: [0, 0.0])
-    scale = {"nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0, "second": 1e3}
+    scale = {"nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0, "second": 1e3,
+             "ns": 1e-6, "us": 1e-3, "ms": 1.0, "s": 1e3}
     for r in rows[hi + 1:]:
         if len(r) <= vi:
             continue

@@ -336,6 +336,7 @@ def test_reduced_representative_gemm_path(rng, C, monkeypatch, dims, tol):
     sizes 63, 144, 726 exercise the K/M padding)."""
     from paper_1903_07884_b200 import workloads
 
+    monkeypatch.setenv("VX_SECTORS", "0")  # the GEMM path serves dense (unsectored) blocks
     W = workloads.small(*dims, delta=0.02e-6)
     kern = W.kernel()
     full = C.build_one_level(kern, W.mtilde())

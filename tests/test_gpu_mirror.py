@@ -46,7 +46,7 @@ def test_one_level_mirror_equals_unshared(rng, C, monkeypatch, dims):
     nx = dims[0]
     assert p.mirror_shared == (nx > 2)
     assert not q.mirror_shared
-    assert p._fac.shape[0] == nx // 2 + 1 and q._fac.shape[0] == nx
+    assert p._fac.shape[0] == (nx // 2 + 1) * p.sectors and q._fac.shape[0] == nx * q.sectors
     assert p.bytes == q.bytes  # the reference's accounting is unchanged
     n = W.grid.n_unknowns
     for r in (None, 3):

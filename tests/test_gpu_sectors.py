@@ -1,0 +1,125 @@
+"""Symmetry-sector factorisation of the 1-level blocks (sectors.py): the
+sector path equals the dense-block path (VX_SECTORS=0) and the CPU oracle,
+with and without mirror sharing, for 1 and several right-hand sides."""
+
+import numpy as np
+import pytest
+
+import voxvie_oracle as O
+from conftest import random_field, relerr
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def C():
+    from paper_1903_07884_b200 import circulant
+
+    return circulant
+
+
+def _wl(dims, delta=0.02e-6):
+    from paper_1903_07884_b200 import workloads
+
+    return workloads.small(*dims, delta=delta)
+
+
+def _sym_m(rng, nz, ny, nx, sy, sz):
+    m = 0.6 + 0.3 * rng.random((nz, ny)) - 0.02j * rng.random((nz, ny))
+    if sy:
+        m = 0.5 * (m + m[:, ::-1])
+    if sz:
+        m = 0.5 * (m + m[::-1, :])
+    return np.repeat(m[:, :, None], nx, axis=2)
+
+
+@pytest.mark.parametrize("dims,sy,sz,nsec", [((8, 3, 2), True, True, 4), ((12, 4, 3), True, True, 4),
+                                             ((9, 6, 5), True, False, 2), ((10, 5, 4), False, True, 2),
+                                             ((50, 22, 11), True, True, 4), ((7, 9, 3), False, False, 1)])
+def test_sectors_equal_dense_blocks(rng, C, monkeypatch, dims, sy, sz, nsec):
+    nx, ny, nz = dims
+    W = _wl(dims)
+    kern = W.kernel()
+    m = _sym_m(rng, nz, ny, nx, sy, sz)
+    if not sy and ny > 1:
+        m[:, 0, :] += 0.05
+    if not sz and nz > 1:
+        m[0, :, :] += 0.07
+    p = C.build_one_level(kern, m)
+    assert p.sectors == nsec
+    monkeypatch.setenv("VX_SECTORS", "0")
+    q = C.build_one_level(kern, m)
+    monkeypatch.delenv("VX_SECTORS")
+    assert q.sectors == 1
+    n = W.grid.n_unknowns
+    for r in (None, 3):
+        x = random_field(rng, n, r)
+        assert relerr(p.apply(x), q.apply(x)) < 1e-12
+    if n <= 3 * 12 * 4 * 3:
+        ref = O.build_one_level(kern.tensors, W.grid.dims, m)
+        x = random_field(rng, n)
+        assert relerr(p.apply(x), O.apply_prec(ref, x)) < 1e-10
+        assert np.array_equal(p.piv, q.piv) and relerr(p.lu, q.lu) < 1e-13
+    if nsec > 1:
+        sb = p.stored_blocks
+        assert sum(d for d, _ in sb) == p.block_size
+        assert sum(d * d * c for d, c in sb) < 0.6 * p.block_size ** 2 * q._fac.shape[0]
+
+
+def test_sectors_without_mirror(rng, C, monkeypatch):
+    W = _wl((10, 6, 3))
+    kern, mt = W.kernel(), W.mtilde()
+    p = C.build_one_level(kern, mt)
+    monkeypatch.setenv("VX_MIRROR", "0")
+    q = C.build_one_level(kern, mt)
+    monkeypatch.setenv("VX_SECTORS", "0")
+    d = C.build_one_level(kern, mt)
+    assert p.sectors == 4 and q.sectors == 4 and d.sectors == 1
+    assert p.mirror_shared and not q.mirror_shared
+    x = random_field(rng, W.grid.n_unknowns)
+    assert relerr(p.apply(x), d.apply(x)) < 1e-12
+    assert relerr(q.apply(x), d.apply(x)) < 1e-12
+
+
+def test_sector_reduce_and_classic_solve(rng, C, monkeypatch):
+    from paper_1903_07884_b200 import _native as nv
+
+    W = _wl((40, 12, 4))
+    kern, mt = W.kernel(), W.mtilde()
+    p = C.build_one_level(kern, mt)
+    assert p.sectors == 4
+    ref = O.build_one_level(kern.tensors, W.grid.dims, mt)
+    x = random_field(rng, W.grid.n_unknowns)
+    red = C.reduce_one_level(p, 1e-3)
+    rref = O.reduce_one_level(ref, 1e-3)
+    assert red.sectors == 4
+    assert relerr(red.apply(x), O.apply_prec(rref, x)) < 1e-10
+    red2 = C.build_reduced_one_level(kern, mt, 1e-3)
+    assert red2.sectors == 4 and np.array_equal(red2.kept, rref["kept"])
+    for r in (None, 2):
+        xr = random_field(rng, W.grid.n_unknowns, r)
+        assert relerr(red2.apply(xr), O.apply_prec(rref, xr)) < 1e-10
+    assert np.array_equal(red2.piv, red.piv)
+    nv.call("vx_solve_variant", 1)
+    try:
+        assert relerr(p.apply(x), O.apply_prec(ref, x)) < 1e-10
+    finally:
+        nv.call("vx_solve_variant", 0)
+
+
+def test_sector_singular_block_raises(C):
+    """D_k = (1 - m s) I: singular for m = 1/s in every sector; the message names k."""
+    from paper_1903_07884_b200.errors import PreconditionerBuildError
+    from paper_1903_07884_b200.grid import VoxelGrid
+    from paper_1903_07884_b200.kernel import ToeplitzKernel
+
+    dims = (4, 3, 2)
+    t = np.zeros((6, 3, 5, 7), dtype=complex)
+    t[[0, 3, 5], 1, 2, 3] = 2.0
+    kern = ToeplitzKernel(VoxelGrid(*dims, 0.05), 2 * np.pi, t)
+    with pytest.raises(PreconditionerBuildError, match="k=0"):
+        C.build_one_level(kern, np.full((2, 3, 4), 0.5))
+    ok = C.build_one_level(kern, np.full((2, 3, 4), 0.25))
+    assert ok.sectors == 4
+    x = np.arange(72, dtype=complex)
+    assert relerr(ok.apply(x), 2 * x) < 1e-14
