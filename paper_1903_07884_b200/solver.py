@@ -105,8 +105,12 @@ class _Krylov:
         self.h = nv.empty_c128(m + 2)
         self.stats = self.t.zeros(4, dtype=self.t.float64, device="cuda")
         self.part = nv.empty_c128(int(nv.query("vx_arnoldi_part_elems", n, m + 2)))
-        self.h_host = self.t.empty(m + 2, dtype=self.t.complex128, pin_memory=True)
-        self.s_host = self.t.empty(4, dtype=self.t.float64, pin_memory=True)
+        # double-buffered pinned mirrors of (h column, stats): iteration j
+        # lands in slot j % 2, so the host can read step j while step j+1
+        # (launched speculatively) writes the other slot
+        self.h_host = [self.t.empty(m + 2, dtype=self.t.complex128, pin_memory=True) for _ in range(2)]
+        self.s_host = [self.t.empty(4, dtype=self.t.float64, pin_memory=True) for _ in range(2)]
+        self.ev = [self.t.cuda.Event() for _ in range(2)]
         self.nrm = self.t.zeros(1, dtype=self.t.float64, device="cuda")
         self.nrm_host = self.t.empty(1, dtype=self.t.float64, pin_memory=True)
 
@@ -210,42 +214,74 @@ class GivensQR:
         return np.linalg.solve(r_mat, np.asarray(self.g[:j], dtype=np.complex128))
 
 
+def _speculate(residuals, tol) -> bool:
+    """Launch step j+1 before step j's residual is known, unless the
+    geometric trend of the estimates says step j is likely to converge (the
+    speculative step would then be wasted work)."""
+    if os.environ.get("VX_SPECULATE", "1") == "0":
+        return False
+    if len(residuals) < 3:
+        return True
+    r1, r2 = residuals[-1], residuals[-2]
+    rho = r1 / r2 if r2 > 0 else 1.0
+    return r1 * min(rho, 1.0) > 2.0 * tol
+
+
 def _gmres_cycle(K: _Krylov, op, r0, beta, bnorm, tol, m, residuals, P=None, A=None):
     """One Arnoldi/Givens cycle (reference solver.py:45-111).
 
     With ``K.keep_z`` the preconditioned vectors z_j = P^-1 v_j that the
     operator needs anyway are kept, and the cycle returns u = Z y = P^-1 V y
     (the reference's correction, solver.py:106-110 then 160-161) without the
-    extra preconditioner apply per cycle."""
+    extra preconditioner apply per cycle.
+
+    Steps are pipelined: step j+1 (operator, preconditioner, orthogonalisation
+    -- all device-resident, v_{j+1} = w / h_{j+1,j} is formed on the device)
+    is enqueued before the host reads step j's Hessenberg column, so the GPU
+    never idles while the host runs the reference's Givens arithmetic.  If
+    step j ends the cycle (convergence / breakdown), the speculative step's
+    output is simply never used; _speculate() avoids it near convergence."""
     t = K.t
     if K.keep_z:
-        def op(v):
+        def op(v, j):
             z = P(v)
-            K.Z[op.j].copy_(z)  # row op.j of Z, set by the loop below
+            K.Z[j].copy_(z)
             return A(z)
     else:
         op_base = op
 
-        def op(v):
+        def op(v, j):
             return op_base(v)
     K.row(0)
     K.axpby(1.0 / beta, r0, 0.0, None, out=K.V[0])
-    qr = GivensQR(beta)
-    converged = lucky = False
-    j = 0
-    while j < m:
-        op.j = j
-        w = op(K.V[j])
+
+    def launch(j):
+        w = op(K.V[j], j)
         K.row(j + 1)
         if _aliases(w, K.V) or not w.is_contiguous():
             w = K.axpby(1.0, w, 0.0, None)  # the op returned (a view of) its argument: copy
         nv.call("vx_arnoldi_step", K.n, j + 1, K.V.data_ptr(), K.n, w.data_ptr(), K.V[j + 1].data_ptr(),
                 K.h.data_ptr(), K.stats.data_ptr(), K.part.data_ptr(), nv.stream_ptr())
-        K.h_host[: j + 2].copy_(K.h[: j + 2], non_blocking=True)
-        K.s_host.copy_(K.stats, non_blocking=True)
-        t.cuda.current_stream().synchronize()
-        h = K.h_host[: j + 2].numpy().copy()
-        norm_before = float(K.s_host[0])
+        b = j % 2
+        K.h_host[b][: j + 2].copy_(K.h[: j + 2], non_blocking=True)
+        K.s_host[b].copy_(K.stats, non_blocking=True)
+        K.ev[b].record()
+
+    qr = GivensQR(beta)
+    converged = lucky = False
+    j = 0
+    launched = 0
+    while j < m:
+        if launched <= j:
+            launch(j)
+            launched = j + 1
+        if launched == j + 1 and j + 1 < m and _speculate(residuals, tol):
+            launch(j + 1)
+            launched = j + 2
+        b = j % 2
+        K.ev[b].synchronize()
+        h = K.h_host[b][: j + 2].numpy().copy()
+        norm_before = float(K.s_host[b][0])
         lucky = h[j + 1].real <= 1e-14 * max(norm_before, 1e-300)
         qr.add_column(h, j, residuals, tol)
         j += 1
