@@ -396,6 +396,157 @@ static int op_x_inverse(const FftPlan& fx, int nx, int px, int nlines, long line
   return launch_fft_lines(fx, ld, sv, nlines, px, nx, true, true, s);
 }
 
+// ------------------------------------------------ fused y/z pass (default)
+// Layout "kx-pair-major" A2: x-frequency kx and its mirror px-kx share pair
+// p = min(kx, px-kx) (slot 0: kx <= px/2, slot 1: the mirror); entry
+// (p, line l = (c, z, y), slot) at (p*nl + l)*2 + slot.  K1 writes it, K5
+// reads it, and the fused kernel below reads and writes one contiguous
+// 2*nl-entry block per pair -- the y/z-padded slab never reaches HBM, and
+// the two columns of a pair read the same compact spectra (mirror in x).
+struct StoreKxPair {
+  double2* __restrict__ p;
+  int nl, px;
+  __device__ __forceinline__ long line_base(int l) const { return 2L * l; }
+  __device__ __forceinline__ void operator()(long b, int kx, double2 v) const {
+    const int m = px - kx;
+    const int pr = kx <= m ? kx : m, slot = kx <= m ? 0 : 1;
+    p[(long)pr * 2 * nl + b + slot] = v;
+  }
+};
+struct LoadKxPair {
+  const double2* __restrict__ p;
+  int nl, px;
+  __device__ __forceinline__ long line_base(int l) const { return 2L * l; }
+  __device__ __forceinline__ double2 operator()(long b, int kx) const {
+    const int m = px - kx;
+    const int pr = kx <= m ? kx : m, slot = kx <= m ? 0 : 1;
+    return __ldg(p + (long)pr * 2 * nl + b + slot);
+  }
+};
+
+// One CTA per kx pair: slab S[z][w*3 + c][y] (pz x 6 x py) in shared memory;
+// y-DIF on the nz nonzero z-rows, z-DIF on every (w, c, ky) line, the 9-term
+// spectral multiply at digit-reversed positions, z-DIT, y-DIT on the kept
+// z-rows, crop y < ny, z < nz.  scale = 1/(px py pz).
+template <int RMAX>
+__global__ void __launch_bounds__(512, 2) op_yz_fused_kernel(FftPlan fy, FftPlan fz, double2* __restrict__ A2, SpecView sv,
+                                                          int ny, int nz, double scale, FastDiv fdWy, FastDiv fdWz) {
+  extern __shared__ __align__(16) double2 fsm[];
+  const int py = fy.L, pz = fz.L;
+  const int nl = 3 * nz * ny;
+  const int row6 = 6 * py;            // one z-row of the slab
+  double2* S = fsm;                   // [pz][6][py]
+  double2* twy = S + (long)pz * row6;
+  double2* twz = twy + 64 + fy.nhi;
+  const int pr = blockIdx.x;
+  const int px = sv.Px;
+  const bool two = (pr != 0) && (2 * pr != px);  // slot 1 holds a distinct column
+  fft_load_twiddles(fy, twy);
+  fft_load_twiddles(fz, twz);
+  for (int i = threadIdx.x; i < pz * row6; i += blockDim.x) S[i] = cmk(0.0, 0.0);
+  __syncthreads();
+  const double2* src = A2 + (long)pr * 2 * nl;
+  for (int i = threadIdx.x; i < 2 * nl; i += blockDim.x) {
+    const int slot = i & 1, l = i >> 1;
+    if (slot && !two) continue;
+    const int c = l / (nz * ny), r = l - c * nz * ny;
+    const int z = r / ny, y = r - z * ny;
+    S[(z * 6 + slot * 3 + c) * py + y] = __ldg(src + i);
+  }
+  __syncthreads();
+  const int nw = two ? 2 : 1;
+  {
+    const SmemLay ly{1, py};
+    const int W = 6 * nz;
+    fft_dif<RMAX>(S, ly, W, fdWy, fy, twy, -1.0);
+  }
+  {
+    const SmemLay lz{row6, 1};
+    fft_dif<RMAX>(S, lz, row6, fdWz, fz, twz, -1.0);
+  }
+  // spectral multiply (positions are digit-reversed in y and z)
+  for (int i = threadIdx.x; i < pz * nw * py; i += blockDim.x) {
+    const int zp = i / (nw * py), r = i - zp * nw * py;
+    const int w = r / py, yp = r - w * py;
+    const int kz = __ldg(fz.k_of + zp), ky = __ldg(fy.k_of + yp);
+    const int kx = w ? px - pr : pr;
+    double2 sp[6];
+    if (!sv.compact) {
+      const long so = ((long)kz * sv.Py + ky) * px + kx, sstr = (long)sv.Pz * sv.Py * px;
+#pragma unroll
+      for (int q = 0; q < 6; ++q) sp[q] = ld_stream(sv.S + q * sstr + so);
+    } else {
+      const bool mz = 2 * kz > sv.Pz, my = 2 * ky > sv.Py, mx = 2 * kx > sv.Px;
+      const int kzs = mz ? sv.Pz - kz : kz, kys = my ? sv.Py - ky : ky, kxs = mx ? sv.Px - kx : kx;
+      const long so = ((long)kzs * sv.Hy + kys) * sv.Hx + kxs;
+      const long sstr = (long)sv.Hz * sv.Hy * sv.Hx;
+#pragma unroll
+      for (int q = 0; q < 6; ++q) {
+        const double2 v = __ldg(sv.S + q * sstr + so);
+        const bool neg = (mx && odd_x(q)) ^ (my && odd_y(q)) ^ (mz && odd_z(q));
+        sp[q] = neg ? cmk(-v.x, -v.y) : v;
+      }
+    }
+    double2* qv = S + (zp * 6 + w * 3) * py + yp;
+    const double2 x0 = qv[0], x1 = qv[py], x2 = qv[2 * py];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      double2 acc = cmul(sp[pair_of(a, 0)], x0);
+      cfma(acc, sp[pair_of(a, 1)], x1);
+      cfma(acc, sp[pair_of(a, 2)], x2);
+      qv[a * py] = cscale(acc, scale);
+    }
+  }
+  __syncthreads();
+  {
+    const SmemLay lz{row6, 1};
+    fft_dit<RMAX>(S, lz, row6, fdWz, fz, twz, 1.0);
+  }
+  {
+    const SmemLay ly{1, py};
+    const int W = 6 * nz;
+    fft_dit<RMAX>(S, ly, W, fdWy, fy, twy, 1.0);
+  }
+  double2* dst = A2 + (long)pr * 2 * nl;
+  for (int i = threadIdx.x; i < 2 * nl; i += blockDim.x) {
+    const int slot = i & 1, l = i >> 1;
+    if (slot && !two) continue;
+    const int c = l / (nz * ny), r = l - c * nz * ny;
+    const int z = r / ny, y = r - z * ny;
+    dst[i] = S[(z * 6 + slot * 3 + c) * py + y];
+  }
+}
+
+static size_t yz_fused_smem(const FftPlan& fy, const FftPlan& fz) {
+  return ((size_t)fz.L * 6 * fy.L + 128 + fy.nhi + fz.nhi) * sizeof(double2);
+}
+
+static int op_apply_fused(const FftPlan& fx, const FftPlan& fy, const FftPlan& fz, int nx, int ny, int nz,
+                          const SpecView& sv, const double2* m, const double2* X, double2* Y, double2* A2,
+                          double scale, cudaStream_t s) {
+  int st;
+  const int px = fx.n;
+  const int nl = 3 * nz * ny;
+  {
+    LoadStrided ld{X, {nx, 0, 1, 1}};
+    StoreKxPair sv2{A2, nl, px};
+    if ((st = launch_fft_lines(fx, ld, sv2, nl, nx, px, false, true, s))) return st;
+  }
+  {
+    const size_t smem = yz_fused_smem(fy, fz);
+    const bool hi = fft_max_radix(fy) > 8 || fft_max_radix(fz) > 8;
+    auto kern = hi ? op_yz_fused_kernel<13> : op_yz_fused_kernel<8>;
+    if (smem > 48 * 1024)
+      VX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kern<<<px / 2 + 1, 512, smem, s>>>(fy, fz, A2, sv, ny, nz, scale, FastDiv((unsigned)(6 * nz)),
+                                       FastDiv((unsigned)(6 * fy.L)));
+    VX_CHECK_LAUNCH("op_yz_fused_kernel");
+  }
+  LoadKxPair ld{A2, nl, px};
+  StoreSystem sv3{Y, X, m, nx, (long)nx * ny * nz, 1.0, 0};
+  return launch_fft_lines(fx, ld, sv3, nl, px, nx, true, true, s);
+}
+
 }  // namespace vx
 
 static SpecView spec_view(const vx_c128* spectra, int compact, int px, int py, int pz) {
@@ -422,6 +573,14 @@ extern "C" int vx_op_apply(int nx, int ny, int nz, int px, int py, int pz, const
   double2* A = reinterpret_cast<double2*>(work);
   double2* B = A + 3L * nz * ny * px;
   const int lines_xyz = 3 * nz * ny;
+  // fused y/z pass (VX_OP_FUSED=1) when the padded (6 x pz x py) slab of a kx
+  // pair fits two CTAs per SM (c0-c2); default: the 5-launch path
+  static const int fused_env = env_int("VX_OP_FUSED", 0);  // opt-in: smem-stage bound (0.59 vs 0.52 ms at c1)
+  if (fused_env && !fy.bluestein && !fz.bluestein &&
+      2 * (yz_fused_smem(fy, fz) + 1024) <= (size_t)device_smem_optin() + 1024)
+    return op_apply_fused(fx, fy, fz, nx, ny, nz, spec_view(spectra, compact, px, py, pz),
+                          reinterpret_cast<const double2*>(m), X, reinterpret_cast<double2*>(y), A,
+                          1.0 / ((double)px * py * pz), s);
   if ((st = op_x_forward(fx, nx, px, lines_xyz, X, A, s))) return st;
   if ((st = op_yz(fy, fz, ny, nz, px, py, pz, spec_view(spectra, compact, px, py, pz), A, B,
                   1.0 / ((double)px * py * pz), s)))
