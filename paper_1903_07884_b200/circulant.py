@@ -281,8 +281,21 @@ def _untile(fac_row: np.ndarray, n: int) -> np.ndarray:
     nt = -(-n // T)
     npad = nt * T
     tiles = fac_row.reshape(nt, nt, T, T)            # (it, jt, col, row)
-    full = tiles.transpose(0, 3, 1, 2).reshape(npad, npad)
+    full = tiles.transpose(0, 3, 1, 2).reshape(npad, npad).copy()
     eye = np.eye(T)
+    # diagonal tiles are stored split (csrc/circulant.cu dl_off/du_off):
+    # inv(L) strictly lower packed by columns, then inv(U) upper packed by columns
+    lo_r, lo_c = np.tril_indices(T, -1)
+    up_r, up_c = np.triu_indices(T)
+    lo_order = np.lexsort((lo_r, lo_c))   # column-major order of the packing
+    up_order = np.lexsort((up_r, up_c))
+    nl = T * (T - 1) // 2
+    for i in range(nt if nt > 1 else 0):   # single-tile blocks keep the packed tile
+        flat = fac_row[(i * nt + i) * T * T:(i * nt + i + 1) * T * T]
+        d = np.zeros((T, T), fac_row.dtype)
+        d[lo_r[lo_order], lo_c[lo_order]] = flat[:nl]
+        d[up_r[up_order], up_c[up_order]] = flat[nl:]
+        full[i * T:(i + 1) * T, i * T:(i + 1) * T] = d
     for i in range(nt):
         d = full[i * T:(i + 1) * T, i * T:(i + 1) * T]
         linv = np.tril(d, -1) + eye

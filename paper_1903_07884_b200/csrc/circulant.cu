@@ -49,6 +49,20 @@ __device__ __forceinline__ long lu_off(const LuGeom& g, int row, int col) {
 
 __constant__ int c_pair[9] = {0, 1, 2, 1, 3, 4, 2, 4, 5};
 
+// Stored diagonal tiles of multi-tile blocks (nt > 1) are SPLIT (single-tile
+// blocks keep the column-major packed tile, which their warp kernel stages
+// whole): the first T(T-1)/2 entries hold inv(L_ii)
+// strictly below the diagonal (packed by columns), the next T(T+1)/2 hold
+// inv(U_ii) on and above it (packed by columns), so the forward and backward
+// substitutions each stream only the half they use.
+__host__ __device__ __forceinline__ int dl_n(int T) { return T * (T - 1) / 2; }
+__host__ __device__ __forceinline__ int dl_off(int T, int r, int c) {  // r > c
+  return c * (2 * T - c - 1) / 2 + (r - c - 1);
+}
+__host__ __device__ __forceinline__ int du_off(int T, int r, int c) {  // r <= c, relative to the U half
+  return c * (c + 1) / 2 + r;
+}
+
 // ----------------------------------------------------------------- spectra
 // Generator line l = (p, dz, dy) of a (6, nzz, nyy, *) tensor with strides.
 struct GenLine {
@@ -766,6 +780,30 @@ __global__ void __launch_bounds__(LUB_WARPS * 32, 2) lub_trail_kernel(LuGeom g, 
                           A + (long)(it * nt + jt) * T2, h, lane);
 }
 
+// column-major packed diagonal tile (inv(L) below, inv(U) on/above) -> split layout
+__global__ void __launch_bounds__(256) diag_split_kernel(LuGeom g, double2* F) {
+  extern __shared__ double2 dsm[];
+  const int T = g.T, T2 = T * T;
+  const long slot = blockIdx.x / g.nt;
+  const int i = blockIdx.x - (int)slot * g.nt;
+  double2* D = F + slot * g.blk + (long)(i * g.nt + i) * T2;
+  for (int e = threadIdx.x; e < T2; e += blockDim.x) dsm[e] = D[e];
+  __syncthreads();
+  const int nl = dl_n(T);
+  for (int e = threadIdx.x; e < T2; e += blockDim.x) {
+    const int c = e / T, r = e - c * T;
+    if (r > c) D[dl_off(T, r, c)] = dsm[e];
+    else D[nl + du_off(T, r, c)] = dsm[e];
+  }
+}
+
+static int diag_split(const LuGeom& g, int nslots, double2* F, cudaStream_t s) {
+  if (nslots <= 0 || g.nt == 1) return VX_OK;  // single-tile blocks stay packed (staged whole)
+  diag_split_kernel<<<(unsigned)((long)nslots * g.nt), 256, (size_t)g.T * g.T * sizeof(double2), s>>>(g, F);
+  VX_CHECK_LAUNCH("diag_split_kernel");
+  return VX_OK;
+}
+
 // b_perm[i] = b[perm[i]] from zgetrf's interchange sequence (one thread per block)
 __global__ void lub_perm_kernel(int nslots, int n, const int* piv, int* perm, int* scratch) {
   const int slot = blockIdx.x * blockDim.x + threadIdx.x;
@@ -819,7 +857,7 @@ static int lu_build_batched(const Unfold& u, const LuGeom& g, int nslots, double
   }
   lub_perm_kernel<<<div_up(nslots, 128), 128, 0, s>>>(nslots, g.n, piv, perm, nullptr);
   VX_CHECK_LAUNCH("lub_perm_kernel");
-  return VX_OK;
+  return diag_split(g, nslots, F, s);
 }
 
 static int lu_build(const Unfold& u, int n, int nslots, double2* F, int* perm, int* piv, int* info,
@@ -840,7 +878,7 @@ static int lu_build(const Unfold& u, int n, int nslots, double2* F, int* perm, i
   VX_REQUIRE((int)smem <= device_smem_optin(), "block size %d too large for the LU kernel", n);
   lu_build_kernel<<<nslots, LU_THREADS, smem, s>>>(u, g, F, perm, piv, info);
   VX_CHECK_LAUNCH("lu_build_kernel");
-  return VX_OK;
+  return diag_split(g, nslots, F, s);
 }
 
 // ---------------------------------------------------------------- LU solve
@@ -933,7 +971,8 @@ __global__ void __launch_bounds__(NW * 32) lu_solve_kernel(LuGeom g, const doubl
         for (int rr = 0; rr < R; ++rr) red[(warp * T + lane) * R + rr] = acc[rr];
       }
       const double2* dt = Fb + (long)(i * nt + i) * T2;
-      for (int idx = tid; idx < T2; idx += NT) Ds[idx] = ld_stream(dt + idx);
+      const int dlen = nt > 1 ? dl_n(T) : T2;
+      for (int idx = tid; idx < dlen; idx += NT) Ds[idx] = ld_stream(dt + idx);
       __syncthreads();
       for (int idx = tid; idx < T * R; idx += NT) {
         const int r = idx / R, rr = idx - r * R;
@@ -945,7 +984,7 @@ __global__ void __launch_bounds__(NW * 32) lu_solve_kernel(LuGeom g, const doubl
       for (int idx = tid; idx < T * R; idx += NT) {
         const int r = idx / R, rr = idx - r * R;
         double2 o = zb[idx];
-        for (int c = 0; c < r; ++c) cfma(o, Ds[c * T + r], zb[c * R + rr]);
+        for (int c = 0; c < r; ++c) cfma(o, Ds[nt > 1 ? dl_off(T, r, c) : c * T + r], zb[c * R + rr]);
         y[(long)(i * T + r) * R + rr] = o;
       }
       __syncthreads();
@@ -969,8 +1008,9 @@ __global__ void __launch_bounds__(NW * 32) lu_solve_kernel(LuGeom g, const doubl
 #pragma unroll
         for (int rr = 0; rr < R; ++rr) red[(warp * T + lane) * R + rr] = acc[rr];
       }
-      const double2* dt = Fb + (long)(i * nt + i) * T2;
-      for (int idx = tid; idx < T2; idx += NT) Ds[idx] = ld_stream(dt + idx);
+      const int doff = nt > 1 ? dl_n(T) : 0;
+      const double2* dt = Fb + (long)(i * nt + i) * T2 + doff;
+      for (int idx = tid; idx < T2 - doff; idx += NT) Ds[idx] = ld_stream(dt + idx);
       __syncthreads();
       for (int idx = tid; idx < T * R; idx += NT) {
         const int r = idx / R, rr = idx - r * R;
@@ -982,7 +1022,7 @@ __global__ void __launch_bounds__(NW * 32) lu_solve_kernel(LuGeom g, const doubl
       for (int idx = tid; idx < T * R; idx += NT) {
         const int r = idx / R, rr = idx - r * R;
         double2 o = cmk(0.0, 0.0);
-        for (int c = r; c < T; ++c) cfma(o, Ds[c * T + r], zb[c * R + rr]);
+        for (int c = r; c < T; ++c) cfma(o, Ds[nt > 1 ? du_off(T, r, c) : c * T + r], zb[c * R + rr]);
         y[(long)(i * T + r) * R + rr] = o;
       }
       __syncthreads();
@@ -1122,8 +1162,12 @@ __global__ void __launch_bounds__((PIPE_CONSUMERS + 1) * 32)
               const int s = (int)(t % S);
               const uint32_t use = (uint32_t)(t / S);
               if (use > 0) mbar_wait(empty + s, (use - 1) & 1);
-              mbar_expect_tx(full + s, tile_bytes);
-              bulk_g2s(slots + (long)s * T2, Fb + (long)(i * nt + jj) * T2, tile_bytes, full + s);
+              // the diagonal tile: only the half this phase uses (split layout)
+              const double2* src = Fb + (long)(i * nt + jj) * T2 + ((j == j1 && ph == 1) ? dl_n(T) : 0);
+              const uint32_t bytes = (j == j1) ? (uint32_t)((ph == 0 ? dl_n(T) : T2 - dl_n(T)) * sizeof(double2))
+                                               : tile_bytes;
+              mbar_expect_tx(full + s, bytes);
+              bulk_g2s(slots + (long)s * T2, src, bytes, full + s);
               ++t;
             }
           }
@@ -1257,10 +1301,16 @@ __global__ void __launch_bounds__((PIPE_CONSUMERS + 1) * 32)
             double2 o;
             if (ph == 0) {
               o = zb[idx];
-              for (int c = 0; c < r; ++c) cfma(o, Ds[c * T + r], zb[c * R + rr]);
+              for (int c = 0, oc = r - 1; c < r; ++c) {  // oc = dl_off(T, r, c)
+                cfma(o, Ds[oc], zb[c * R + rr]);
+                oc += T - c - 2;
+              }
             } else {
               o = cmk(0.0, 0.0);
-              for (int c = r; c < T; ++c) cfma(o, Ds[c * T + r], zb[c * R + rr]);
+              for (int c = r, ou = du_off(T, r, r); c < T; ++c) {  // ou = du_off(T, r, c)
+                cfma(o, Ds[ou], zb[c * R + rr]);
+                ou += c + 1;
+              }
             }
             y[(long)(i * T + r) * R + rr] = o;
           }

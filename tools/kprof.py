@@ -14,6 +14,8 @@ ap.add_argument("config", nargs="?", default="c1")
 ap.add_argument("--reps", type=int, default=5)
 ap.add_argument("--env", nargs="*", default=[])
 ap.add_argument("--what", default="op,prec,arnoldi")
+ap.add_argument("--nvec", type=int, default=20)
+ap.add_argument("--seq", action="store_true", help="also list the launches of one step in order")
 a = ap.parse_args()
 for kv in a.env:
     k, v = kv.split("=", 1)
@@ -37,7 +39,7 @@ rng = np.random.default_rng(0)
 n = W.grid.n_unknowns
 x = torch.from_numpy(rng.normal(size=n) + 1j * rng.normal(size=n)).cuda()
 prec = bench.build_prec(W, kern) if "prec" in what else None
-nvec = 20
+nvec = a.nvec
 V = torch.from_numpy(rng.normal(size=(nvec + 1, n)) + 0j).cuda()
 h = torch.zeros(nvec + 2, dtype=torch.complex128, device="cuda")
 stats = torch.zeros(4, dtype=torch.float64, device="cuda")
@@ -79,3 +81,12 @@ tot = sum(r[0] for r in rows)
 print(f"{'ms/step':>9} {'n/step':>6}  kernel   (total {tot:.3f} ms)")
 for t, c, k in rows:
     print(f"{t:9.4f} {c:6.1f}  {k}")
+
+if a.seq:
+    with torch.profiler.profile(activities=[torch.profiler.ProfilerActivity.CUDA]) as prof2:
+        step()
+        torch.cuda.synchronize()
+    evs = [e for e in prof2.events() if e.device_type == torch.autograd.DeviceType.CUDA]
+    print("-- one step in launch order")
+    for e in sorted(evs, key=lambda e: e.time_range.start):
+        print(f"{e.device_time_total / 1e3:9.4f}  {e.name[:110]}")
