@@ -13,7 +13,7 @@
 // Factor storage per block: nt x nt tiles of T x T (T <= 32), tile (i, j) at
 // offset (i*nt + j)*T*T, column-major inside the tile; rows/cols >= n are an
 // identity pad.
-#include "fft_lines.cuh"
+#include "fft_long.cuh"
 
 #include <algorithm>
 #include <vector>
@@ -1751,7 +1751,7 @@ extern "C" int vx_chan_x_spectra(int nx, int ny, int nz, const vx_c128* gen, lon
   const int lines = 6 * nzz * nyy;
   LoadChanGen ld{reinterpret_cast<const double2*>(gen), {g_sp, g_sz, g_sy, nzz, nyy}, g_sx, nx};
   StoreStrided sv{reinterpret_cast<double2*>(lamT), {1, 0, lines, 1}, 1.0};
-  return launch_fft_lines(p, ld, sv, lines, nx, nx, false, false, as_stream(stream));
+  return launch_fft_auto(p, ld, sv, lines, nx, nx, false, false, as_stream(stream));
 }
 
 extern "C" int vx_proxy(int nx, int ny, int nz, const vx_c128* lamT, vx_c128 m00, vx_c128* proxy,
@@ -1799,7 +1799,7 @@ extern "C" int vx_prec1_apply(int nx, int ny, int nz, int nrhs, const vx_c128* f
   {
     LoadStrided ld{reinterpret_cast<const double2*>(x), {pitch, 1, nrhs, nrhs}};
     StoreStrided sv{S, {pitch, 1, nrhs, nrhs}, 1.0};
-    if ((st = launch_fft_lines(p, ld, sv, q3 * nrhs, nx, nx, false, nrhs == 1, s))) return st;
+    if ((st = launch_fft_auto(p, ld, sv, q3 * nrhs, nx, nx, false, nrhs == 1, s))) return st;
   }
   LuGeom g = lu_geom(q3);
   const double2* F = reinterpret_cast<const double2*>(factors);
@@ -1808,7 +1808,7 @@ extern "C" int vx_prec1_apply(int nx, int ny, int nz, int nrhs, const vx_c128* f
   {
     LoadStrided ld{S, {pitch, 1, nrhs, nrhs}};
     StoreStrided sv{reinterpret_cast<double2*>(y), {pitch, 1, nrhs, nrhs}, 1.0 / nx};
-    if ((st = launch_fft_lines(p, ld, sv, q3 * nrhs, nx, nx, true, nrhs == 1, s))) return st;
+    if ((st = launch_fft_auto(p, ld, sv, q3 * nrhs, nx, nx, true, nrhs == 1, s))) return st;
   }
   return VX_OK;
 }
@@ -1830,13 +1830,13 @@ extern "C" int vx_chan_xy_spectra(int nx, int ny, int nz, const vx_c128* gen, lo
   {
     LoadChanGen ld{reinterpret_cast<const double2*>(gen), {g_sp, g_sz, g_sy, nzz, nyy}, g_sx, nx};
     StoreStrided sv{tmp, {nx, 0, 1, 1}, 1.0};
-    if ((st = launch_fft_lines(px, ld, sv, 6 * nzz * nyy, nx, nx, false, g_sx == 1, s))) return st;
+    if ((st = launch_fft_auto(px, ld, sv, 6 * nzz * nyy, nx, nx, false, g_sx == 1, s))) return st;
   }
   {
     // lines (p, dz) x k along dy; Chan along y, DFT length ny, k-major output
     LoadChan ld{tmp, {(long)nyy * nx, 1, nx, nx}, ny};
     StoreStrided sv{reinterpret_cast<double2*>(lam2T), {1, 6L * nzz, 6L * nzz * nx, nx}, 1.0};
-    if ((st = launch_fft_lines(py, ld, sv, 6 * nzz * nx, ny, ny, false, false, s))) return st;
+    if ((st = launch_fft_auto(py, ld, sv, 6 * nzz * nx, ny, ny, false, false, s))) return st;
   }
   return VX_OK;
 }
@@ -1874,12 +1874,12 @@ extern "C" int vx_prec2_apply(int nx, int ny, int nz, int nrhs, const vx_c128* f
   {
     LoadStrided ld{reinterpret_cast<const double2*>(x), {pitch, 1, nrhs, nrhs}};
     StoreStrided sv{S, {pitch, 1, nrhs, nrhs}, 1.0};
-    if ((st = launch_fft_lines(px, ld, sv, q3 * nrhs, nx, nx, false, nrhs == 1, s))) return st;
+    if ((st = launch_fft_auto(px, ld, sv, q3 * nrhs, nx, nx, false, nrhs == 1, s))) return st;
   }
   {
     LoadStrided ld{S, {plane, 1, pitch, (int)pitch}};
     StoreStrided sv{S, {plane, 1, pitch, (int)pitch}, 1.0};
-    if ((st = launch_fft_lines(py, ld, sv, 3 * nz * (int)pitch, ny, ny, false, false, s))) return st;
+    if ((st = launch_fft_auto(py, ld, sv, 3 * nz * (int)pitch, ny, ny, false, false, s))) return st;
   }
   LuGeom g = lu_geom(3 * nz);
   const double2* F = reinterpret_cast<const double2*>(factors);
@@ -1889,12 +1889,12 @@ extern "C" int vx_prec2_apply(int nx, int ny, int nz, int nrhs, const vx_c128* f
   {
     LoadStrided ld{S, {plane, 1, pitch, (int)pitch}};
     StoreStrided sv{S, {plane, 1, pitch, (int)pitch}, 1.0};
-    if ((st = launch_fft_lines(py, ld, sv, 3 * nz * (int)pitch, ny, ny, true, false, s))) return st;
+    if ((st = launch_fft_auto(py, ld, sv, 3 * nz * (int)pitch, ny, ny, true, false, s))) return st;
   }
   {
     LoadStrided ld{S, {pitch, 1, nrhs, nrhs}};
     StoreStrided sv{reinterpret_cast<double2*>(y), {pitch, 1, nrhs, nrhs}, 1.0 / ((double)nx * ny)};
-    if ((st = launch_fft_lines(px, ld, sv, q3 * nrhs, nx, nx, true, nrhs == 1, s))) return st;
+    if ((st = launch_fft_auto(px, ld, sv, q3 * nrhs, nx, nx, true, nrhs == 1, s))) return st;
   }
   return VX_OK;
 }
@@ -2020,7 +2020,7 @@ extern "C" int vx_prec1_apply_reduced(int nx, int ny, int nz, int nrhs, const vx
   {
     LoadStrided ld{reinterpret_cast<const double2*>(x), {pitch, 1, nrhs, nrhs}};
     StoreStrided sv{S, {pitch, 1, nrhs, nrhs}, 1.0};
-    if ((st = launch_fft_lines(p, ld, sv, q3 * nrhs, nx, nx, false, nrhs == 1, s))) return st;
+    if ((st = launch_fft_auto(p, ld, sv, q3 * nrhs, nx, nx, false, nrhs == 1, s))) return st;
   }
   LuGeom g = lu_geom(q3);
   const double2* F = reinterpret_cast<const double2*>(factors);
@@ -2054,7 +2054,7 @@ extern "C" int vx_prec1_apply_reduced(int nx, int ny, int nz, int nrhs, const vx
   {
     LoadStrided ld{S, {pitch, 1, nrhs, nrhs}};
     StoreStrided sv{reinterpret_cast<double2*>(y), {pitch, 1, nrhs, nrhs}, 1.0 / nx};
-    if ((st = launch_fft_lines(p, ld, sv, q3 * nrhs, nx, nx, true, nrhs == 1, s))) return st;
+    if ((st = launch_fft_auto(p, ld, sv, q3 * nrhs, nx, nx, true, nrhs == 1, s))) return st;
   }
   return VX_OK;
 }
@@ -2108,7 +2108,7 @@ extern "C" int vx_prec1_apply_sec(int nx, int ny, int nz, int nrhs, const vx_c12
   {
     LoadStrided ld{reinterpret_cast<const double2*>(x), {pitch, 1, nrhs, nrhs}};
     StoreStrided sv{S, {pitch, 1, nrhs, nrhs}, 1.0};
-    if ((st = launch_fft_lines(p, ld, sv, q3 * nrhs, nx, nx, false, nrhs == 1, s))) return st;
+    if ((st = launch_fft_auto(p, ld, sv, q3 * nrhs, nx, nx, false, nrhs == 1, s))) return st;
   }
   VX_CUDA(cudaMemsetAsync(U, 0, sizeof(double2) * (size_t)nsec * dmax * pitch, s));
   if ((st = sec_xform(pitch, nrhs, norb, orows, osec, ocoef, flipk, q, S, U, 0, s))) return st;
@@ -2119,7 +2119,7 @@ extern "C" int vx_prec1_apply_sec(int nx, int ny, int nz, int nrhs, const vx_c12
   {
     LoadStrided ld{S, {pitch, 1, nrhs, nrhs}};
     StoreStrided sv{reinterpret_cast<double2*>(y), {pitch, 1, nrhs, nrhs}, 1.0 / nx};
-    if ((st = launch_fft_lines(p, ld, sv, q3 * nrhs, nx, nx, true, nrhs == 1, s))) return st;
+    if ((st = launch_fft_auto(p, ld, sv, q3 * nrhs, nx, nx, true, nrhs == 1, s))) return st;
   }
   return VX_OK;
 }

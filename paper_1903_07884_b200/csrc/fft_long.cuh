@@ -1,0 +1,187 @@
+// Long-line FFTs (the x-direction transforms: operator padded lengths 400 ...
+// 10000, preconditioner DFT lengths 200 ... 5000) as two or three register
+// passes instead of 5-6 radix-8 shared-memory stages.
+//
+// L = R1*R2*R3 (R3 = 1 for two factors), decimation in frequency:
+//   pass 1  task m < M1 = L/R1: the R1 inputs x[n1*M1 + m] come straight from
+//           global memory (coalesced across m; zero padding by the loader),
+//           length-R1 register DFT, twiddle w_L^(k1 m), store to smem
+//           position k1*M1 + m.
+//   pass 2  task (k1, m2 < M2 = R3): R2 values at stride M2 inside block k1,
+//           register DFT, twiddle w_L^(R1 k2 m2), back in place.
+//   last    task t = k1 + R1*k2: R3 contiguous values, register DFT, and the
+//           outputs X[t + (L/R3)*k3] go straight to global memory through the
+//           storer (consecutive t -> consecutive addresses: natural order,
+//           coalesced, crop / scale / operator epilogue fused).
+// Only two smem round trips and two barriers per line; the last pass reads
+// with a lane stride of M1 (odd for every factorisation used -> no bank
+// conflicts).  Twiddles: the plan's two-level tables staged in smem, powers
+// by products (twiddle_row).
+#pragma once
+
+#include "fft_lines.cuh"
+#include "fft_reg.cuh"
+
+namespace vx {
+
+template <int R1, int R2, int R3, bool INV, class Loader, class Storer>
+__global__ void __launch_bounds__(512, 1)
+    fft_long_kernel(Loader ld, Storer st, const double2* __restrict__ tw_lo, const double2* __restrict__ tw_hi,
+                    int nhi, int n_lines, int W, int n_in, int n_out) {
+  constexpr int L = R1 * R2 * R3;
+  constexpr int M1 = L / R1;
+  constexpr int M2 = R3;
+  constexpr int RL = R3 > 1 ? R3 : R2;  // last radix
+  constexpr int T = L / RL;             // last-pass tasks per line
+  constexpr double sgn = INV ? 1.0 : -1.0;
+  extern __shared__ double2 lsm[];
+  double2* tw = lsm + (size_t)W * L;
+  for (int i = threadIdx.x; i < 64 + nhi; i += blockDim.x)
+    tw[i] = i < 64 ? __ldg(tw_lo + i) : __ldg(tw_hi + (i - 64));
+  const int l0 = blockIdx.x * W;
+  __syncthreads();
+  // pass 1: global -> registers -> smem
+  for (int i = threadIdx.x; i < W * M1; i += blockDim.x) {
+    const int w = i / M1, m = i - w * M1;
+    const int l = l0 + w;
+    double2 v[R1];
+    if (l < n_lines) {
+      const long b = ld.line_base(l);
+#pragma unroll
+      for (int n1 = 0; n1 < R1; ++n1) {
+        const int e = n1 * M1 + m;
+        v[n1] = e < n_in ? ld(b, e) : cmk(0.0, 0.0);
+      }
+    } else {
+#pragma unroll
+      for (int n1 = 0; n1 < R1; ++n1) v[n1] = cmk(0.0, 0.0);
+    }
+    reg_fft<R1, INV>(v);
+    if (m) twiddle_row<R1>(v, tw, m, sgn);
+    double2* s = lsm + (size_t)w * L + m;
+#pragma unroll
+    for (int k1 = 0; k1 < R1; ++k1) s[k1 * M1] = v[k1];
+  }
+  __syncthreads();
+  if constexpr (R3 > 1) {
+    for (int i = threadIdx.x; i < W * R1 * M2; i += blockDim.x) {
+      const int w = i / (R1 * M2), r = i - w * (R1 * M2);
+      const int k1 = r / M2, m2 = r - k1 * M2;
+      double2* s = lsm + (size_t)w * L + k1 * M1 + m2;
+      double2 v[R2];
+#pragma unroll
+      for (int n2 = 0; n2 < R2; ++n2) v[n2] = s[n2 * M2];
+      reg_fft<R2, INV>(v);
+      if (m2) twiddle_row<R2>(v, tw, R1 * m2, sgn);
+#pragma unroll
+      for (int k2 = 0; k2 < R2; ++k2) s[k2 * M2] = v[k2];
+    }
+    __syncthreads();
+  }
+  // last pass: smem -> registers -> global (natural order)
+  for (int i = threadIdx.x; i < W * T; i += blockDim.x) {
+    const int w = i / T, t = i - w * T;
+    const int l = l0 + w;
+    if (l >= n_lines) continue;
+    int pos;
+    if constexpr (R3 > 1) {
+      const int k2 = t / R1, k1 = t - k2 * R1;
+      pos = k1 * M1 + k2 * M2;
+    } else {
+      pos = t * M1;
+    }
+    const double2* s = lsm + (size_t)w * L + pos;
+    double2 v[RL];
+#pragma unroll
+    for (int n = 0; n < RL; ++n) v[n] = s[n];
+    reg_fft<RL, INV>(v);
+    const long b = st.line_base(l);
+#pragma unroll
+    for (int k = 0; k < RL; ++k) {
+      const int e = t + T * k;
+      if (e < n_out) st(b, e, v[k]);
+    }
+  }
+}
+
+// Factorisations with a register kernel (M1 = L/R1 odd for the conflict-free
+// last pass).  X(L, R1, R2, R3)
+#define VX_LONG_FACTORS(X)                                                                    \
+  X(10000, 16, 25, 25) X(5000, 8, 25, 25) X(2500, 4, 25, 25) X(3000, 8, 15, 25)              \
+  X(1500, 4, 15, 25) X(400, 16, 25, 1) X(200, 8, 25, 1) X(735, 21, 35, 1)
+
+inline bool fft_long_supported(int L) {
+#define VX_LONG_CASE(N, A, B, C) if (L == N) return true;
+  VX_LONG_FACTORS(VX_LONG_CASE)
+#undef VX_LONG_CASE
+  return false;
+}
+
+template <int R1, int R2, int R3, bool INV, class Loader, class Storer>
+int launch_fft_long_t(const FftPlan& p, const Loader& ld, const Storer& st, int n_lines, int n_in, int n_out,
+                      cudaStream_t s) {
+  constexpr int L = R1 * R2 * R3;
+  constexpr int RL = R3 > 1 ? R3 : R2;
+  static const int target = env_int("VX_FFT_LONG_ELEMS", 5000);
+  int W = target / L;
+  if (W < 1) W = 1;
+  if (W > n_lines) W = n_lines;
+  const int tasks = W * (L / R1 > L / RL ? L / R1 : L / RL);
+  // lines that fill the SM alone get up to 640 threads; shorter lines run
+  // 2+ CTAs per SM with fewer threads each
+  const size_t smem = ((size_t)W * L + 64 + p.nhi) * sizeof(double2);
+  const int cap = smem > 100 * 1024 ? 512 : 256;
+  int thr = ((tasks < cap ? tasks : cap) + 31) / 32 * 32;
+  auto kern = fft_long_kernel<R1, R2, R3, INV, Loader, Storer>;
+  if (smem > 48 * 1024)
+    VX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  kern<<<div_up(n_lines, W), thr, smem, s>>>(ld, st, p.tw_lo, p.tw_hi, p.nhi, n_lines, W, n_in, n_out);
+  VX_CHECK_LAUNCH("fft_long_kernel");
+  return VX_OK;
+}
+
+// Contiguous lines of length p.n (direct plan) through the register passes.
+template <class Loader, class Storer>
+int launch_fft_long(const FftPlan& p, const Loader& ld, const Storer& st, int n_lines, int n_in, int n_out,
+                    bool inv, cudaStream_t s) {
+  if (n_lines <= 0) return VX_OK;
+  switch (p.n) {
+#define VX_LONG_LAUNCH(N, A, B, C)                                                              \
+  case N:                                                                                       \
+    return inv ? launch_fft_long_t<A, B, C, true>(p, ld, st, n_lines, n_in, n_out, s)           \
+               : launch_fft_long_t<A, B, C, false>(p, ld, st, n_lines, n_in, n_out, s);
+    VX_LONG_FACTORS(VX_LONG_LAUNCH)
+#undef VX_LONG_LAUNCH
+    default:
+      break;
+  }
+  set_error("no long-line register FFT for length %d", p.n);
+  return VX_EINVAL;
+}
+
+inline bool fft_long_enabled() {
+  static const int on = env_int("VX_FFT_LONG", 1);
+  return on != 0;
+}
+
+// Contiguous line FFT: register passes when the length has a kernel, else the
+// shared-memory stage engine.
+template <class Loader, class Storer>
+int launch_fft_contig(const FftPlan& p, const Loader& ld, const Storer& st, int n_lines, int n_in, int n_out,
+                      bool inv, cudaStream_t s) {
+  if (fft_long_enabled() && !p.bluestein && fft_long_supported(p.n))
+    return launch_fft_long(p, ld, st, n_lines, n_in, n_out, inv, s);
+  return launch_fft_lines(p, ld, st, n_lines, n_in, n_out, inv, true, s);
+}
+
+}  // namespace vx
+
+namespace vx {
+// drop-in for launch_fft_lines: contiguous lines take the register passes
+template <class Loader, class Storer>
+int launch_fft_auto(const FftPlan& p, const Loader& ld, const Storer& st, int n_lines, int n_in, int n_out,
+                    bool inv, bool contig, cudaStream_t s) {
+  if (contig) return launch_fft_contig(p, ld, st, n_lines, n_in, n_out, inv, s);
+  return launch_fft_lines(p, ld, st, n_lines, n_in, n_out, inv, false, s);
+}
+}  // namespace vx

@@ -9,7 +9,7 @@
 //   K5  x-inverse   crop x < nx, epilogue y = x - m .* (N x)          -> y
 // Zero padding and cropping happen in the loaders/storers, so the padded
 // volume is only touched where it carries data.
-#include "fft_lines.cuh"
+#include "fft_long.cuh"
 #include "fft_reg.cuh"
 
 namespace vx {
@@ -53,7 +53,9 @@ __host__ __device__ constexpr bool odd_z(int p) { return p == 2 || p == 4; }
 
 // Compact (symmetry-reduced) spectra: for a parity-symmetric kernel
 // S_p(-k) = +-S_p(k) on every axis, so only k <= P/2 is stored per axis,
-// (6, Hz, Hy, Hx) with H = P/2 + 1 -- 1/8 of the full spectra's bytes.
+// (Hz, Hy, Hx, 6) with H = P/2 + 1 -- 1/8 of the full spectra's bytes; the six
+// components of one frequency are adjacent (96 bytes), so the three lanes of a
+// column that each need three of them share the same L1 lines.
 struct SpecView {
   const double2* S;
   int compact;
@@ -100,8 +102,8 @@ __global__ void __launch_bounds__(512, (RMAX <= 8 ? 2 : 1))
       const int ky = (int)sv.fdPx.div((unsigned)col), kx = (int)(col - (long)ky * sv.Px);
       const bool mz = 2 * kz > sv.Pz, my = 2 * ky > sv.Py, mx = 2 * kx > sv.Px;
       const int kzs = mz ? sv.Pz - kz : kz, kys = my ? sv.Py - ky : ky, kxs = mx ? sv.Px - kx : kx;
-      const long so = ((long)kzs * sv.Hy + kys) * sv.Hx + kxs;
-      const long sstr = (long)sv.Hz * sv.Hy * sv.Hx;
+      const long so = (((long)kzs * sv.Hy + kys) * sv.Hx + kxs) * 6;
+      const long sstr = 1;
 #pragma unroll
       for (int p = 0; p < 6; ++p) {
         double2 v = ld_stream(sv.S + p * sstr + so);
@@ -152,7 +154,7 @@ extern "C" int vx_fft_lines(int n, int n_lines, int n_inner, const vx_c128* in, 
   LoadStrided ld{reinterpret_cast<const double2*>(in), {in_os, in_is, in_es, n_inner}};
   StoreStrided sv{reinterpret_cast<double2*>(out), {out_os, out_is, out_es, n_inner}, scale};
   const bool contig = (in_es == 1 && out_es == 1);
-  return launch_fft_lines(p, ld, sv, n_lines, n_in, n_out, inverse != 0, contig, as_stream(stream));
+  return launch_fft_auto(p, ld, sv, n_lines, n_in, n_out, inverse != 0, contig, as_stream(stream));
 }
 
 extern "C" int vx_op_plan(int nx, int ny, int nz, int px, int py, int pz, const vx_c128* gen,
@@ -169,7 +171,7 @@ extern "C" int vx_op_plan(int nx, int ny, int nz, int px, int py, int pz, const 
   // x pass over every padded (p, z, y) line, generator embedded on load
   LoadEmbed le{reinterpret_cast<const double2*>(gen), g_sp, g_sz, g_sy, g_sx, nx, ny, nz, px, py, pz};
   StoreStrided sx{S, {px, 0, 1, 1}, 1.0};
-  if ((st = launch_fft_lines(fx, le, sx, 6 * pz * py, px, px, false, true, s))) return st;
+  if ((st = launch_fft_auto(fx, le, sx, 6 * pz * py, px, px, false, true, s))) return st;
   // y pass (in place), lines (p,z) x kx
   LoadStrided ly{S, {cols, 1, px, px}};
   StoreStrided sy{S, {cols, 1, px, px}, 1.0};
@@ -239,9 +241,9 @@ __global__ void __launch_bounds__(ZR_T)
     const int ky = (int)sv.fdPx.div((unsigned)col), kx = (int)(col - (long)ky * sv.Px);
     my = 2 * ky > sv.Py;
     mx = 2 * kx > sv.Px;
-    so0 = (long)(my ? sv.Py - ky : ky) * sv.Hx + (mx ? sv.Px - kx : kx);
-    sstr = (long)sv.Hz * sv.Hy * sv.Hx;
-    kstr = (long)sv.Hy * sv.Hx;
+    so0 = ((long)(my ? sv.Py - ky : ky) * sv.Hx + (mx ? sv.Px - kx : kx)) * 6;
+    sstr = 1;
+    kstr = (long)sv.Hy * sv.Hx * 6;
   }
 #pragma unroll 7
   for (int kz = 0; kz < PZ; ++kz) {
@@ -281,6 +283,85 @@ __global__ void __launch_bounds__(ZR_T)
   }
 }
 
+// K3 without shared memory: three lanes per column (ky,kx), one per field
+// component.  Lane (c, j) of a warp (c = lane / 10, j = lane % 10; lanes 30, 31
+// idle) holds component c's z-line of column j in registers, transforms it,
+// and at each kz pulls the other two components' values with warp shuffles
+// for y_c = sum_b S[PAIR_OF[c,b]] x_b.  No smem and ~1/3 of the registers of
+// the one-thread-per-column kernel -> full occupancy; loads of the 3 spectra a
+// lane needs hit L1 for the entries its column partners also use.
+constexpr int ZS_COLS = 10;
+
+__device__ __forceinline__ double2 shfl_c(double2 v, int src) {
+  return cmk(__shfl_sync(0xffffffffu, v.x, src), __shfl_sync(0xffffffffu, v.y, src));
+}
+
+template <int PZ>
+__global__ void __launch_bounds__(256, (PZ <= 16 ? 3 : 2))
+    op_zmul_shfl_kernel(double2* __restrict__ B, SpecView sv, int nz, long cols, double scale) {
+  const int lane = threadIdx.x & 31;
+  const long warp = (blockIdx.x * (long)blockDim.x + threadIdx.x) >> 5;
+  const int c = lane < 3 * ZS_COLS ? lane / ZS_COLS : 2;
+  const int j = lane < 3 * ZS_COLS ? lane - c * ZS_COLS : 0;
+  long col = warp * ZS_COLS + j;
+  const bool active = lane < 3 * ZS_COLS && col < cols;
+  if (!active) col = 0;
+  if (sv.compact) {
+    // rows ky = 0, 1, Py-1, 2, Py-2, ...: a row and its mirror (same compact
+    // spectra) run back to back, so the second read hits L2
+    const int lr = (int)sv.fdPx.div((unsigned)col);
+    const int ky = (lr == 0) ? 0 : ((lr & 1) ? (lr + 1) / 2 : sv.Py - lr / 2);
+    col += (long)(ky - lr) * sv.Px;
+  }
+  double2 v[PZ];
+  const double2* src = B + (long)c * nz * cols + col;
+#pragma unroll
+  for (int e = 0; e < PZ; ++e) v[e] = (active && e < nz) ? __ldg(src + (long)e * cols) : cmk(0.0, 0.0);
+  reg_fft<PZ, false>(v);
+  // spectra this lane needs: PAIR_OF[c][0..2]
+  const int p0 = c == 0 ? 0 : (c == 1 ? 1 : 2);
+  const int p1 = c == 0 ? 1 : (c == 1 ? 3 : 4);
+  const int p2 = c == 0 ? 2 : (c == 1 ? 4 : 5);
+  long so0 = col, sstr = (long)PZ * cols, kstr = cols;
+  bool my = false, mx = false;
+  if (sv.compact) {
+    const int ky = (int)sv.fdPx.div((unsigned)col), kx = (int)(col - (long)ky * sv.Px);
+    my = 2 * ky > sv.Py;
+    mx = 2 * kx > sv.Px;
+    so0 = ((long)(my ? sv.Py - ky : ky) * sv.Hx + (mx ? sv.Px - kx : kx)) * 6;
+    sstr = 1;
+    kstr = (long)sv.Hy * sv.Hx * 6;
+  }
+  // sign of S_p at a mirrored (x, y) index; z mirror added per kz
+  const bool n0 = (mx && odd_x(p0)) ^ (my && odd_y(p0));
+  const bool n1 = (mx && odd_x(p1)) ^ (my && odd_y(p1));
+  const bool n2 = (mx && odd_x(p2)) ^ (my && odd_y(p2));
+  const double2* S0 = sv.S + p0 * sstr + so0;
+  const double2* S1 = sv.S + p1 * sstr + so0;
+  const double2* S2 = sv.S + p2 * sstr + so0;
+#pragma unroll
+  for (int kz = 0; kz < PZ; ++kz) {
+    const bool mz = sv.compact && 2 * kz > PZ;
+    const long ko = (long)(mz ? PZ - kz : kz) * kstr;
+    double2 s0 = __ldg(S0 + ko), s1 = __ldg(S1 + ko), s2 = __ldg(S2 + ko);
+    if (n0 ^ (mz && odd_z(p0))) s0 = cmk(-s0.x, -s0.y);
+    if (n1 ^ (mz && odd_z(p1))) s1 = cmk(-s1.x, -s1.y);
+    if (n2 ^ (mz && odd_z(p2))) s2 = cmk(-s2.x, -s2.y);
+    const double2 x0 = shfl_c(v[kz], j), x1 = shfl_c(v[kz], ZS_COLS + j), x2 = shfl_c(v[kz], 2 * ZS_COLS + j);
+    double2 acc = cmul(s0, x0);
+    cfma(acc, s1, x1);
+    cfma(acc, s2, x2);
+    v[kz] = cscale(acc, scale);
+  }
+  reg_fft<PZ, true>(v);
+  if (active) {
+    double2* dst = B + (long)c * nz * cols + col;
+#pragma unroll
+    for (int e = 0; e < PZ; ++e)
+      if (e < nz) dst[(long)e * cols] = v[e];
+  }
+}
+
 constexpr int REG_ZMUL_MAX = 32;  // longer z-lines spill; they keep the smem kernel
 
 static int g_reg_fft = -1;  // -1: from VX_REG_FFT (default on); vx_op_reg_fft() overrides
@@ -313,6 +394,24 @@ static int launch_reg_cols(int L, const double2* in, long in_os, long in_es, int
 
 static int launch_zmul_reg(int PZ, double2* B, const SpecView& sv, int nz, long cols, double scale,
                            cudaStream_t s) {
+  static const int shfl = env_int("VX_ZMUL_SHFL", 1);
+  if (shfl) {
+    const long warps = (cols + ZS_COLS - 1) / ZS_COLS;
+    const unsigned g = div_up(warps, 8);
+    switch (PZ) {
+#define VX_ZSH_LAUNCH(N)                                                           \
+  case N:                                                                          \
+    if constexpr (N <= REG_ZMUL_MAX) op_zmul_shfl_kernel<N><<<g, 256, 0, s>>>(B, sv, nz, cols, scale); \
+    break;
+      VX_REG_LENGTHS(VX_ZSH_LAUNCH)
+#undef VX_ZSH_LAUNCH
+      default:
+        set_error("no register z-multiply for length %d", PZ);
+        return VX_EINVAL;
+    }
+    VX_CHECK_LAUNCH("op_zmul_shfl_kernel");
+    return VX_OK;
+  }
   const unsigned grid = (unsigned)div_up(cols, ZR_T);
   const size_t smem = (size_t)3 * PZ * ZR_T * sizeof(double2);
   switch (PZ) {
@@ -341,7 +440,231 @@ static int op_x_forward(const FftPlan& fx, int nx, int px, int nlines, const dou
                         cudaStream_t s) {
   LoadStrided ld{X, {nx, 0, 1, 1}};
   StoreStrided sv{A, {px, 0, 1, 1}, 1.0};
-  return launch_fft_lines(fx, ld, sv, nlines, nx, px, false, true, s);
+  return launch_fft_auto(fx, ld, sv, nlines, nx, px, false, true, s);
+}
+
+// ------------------------------------------- fused y/z pass, register FFTs
+// One CTA per G consecutive x-frequencies kx (all c, z, y of them): the y/z
+// padded slab never reaches HBM -- per apply the pass reads A once, the
+// spectra once and writes A once (c1: 353 MB instead of 1.28 GB for the
+// separate y / z+multiply / y passes).
+//   A  y-forward: task (c, z, g): ny values of A -> register DFT (pad to PY)
+//      -> smem S[(c,z)][ky][g]   (only the nz nonzero z-rows are kept)
+//   B  z + multiply: 3 lanes per column (ky, g) (lane = c*10 + j, as in
+//      op_zmul_shfl_kernel): nz values from S -> register DFT (pad to PZ),
+//      y_c = sum_b S[PAIR_OF[c,b]] x_b with the partners' values by shuffle,
+//      inverse DFT, crop z < nz -> back to S
+//   C  y-inverse: task (c, z, g): PY values from S -> register DFT, crop
+//      y < ny -> A (in place: the CTA owns its kx columns)
+// Launch order interleaves kx groups with their mirrors (blockIdx 2i -> group
+// i, 2i+1 -> the last-but-i group) so the compact spectra of kx and px-kx are
+// read from DRAM once.  Row stride of S padded for conflict-free phases A/C.
+template <int G>
+__host__ __device__ constexpr int yzf_row(int py) {
+  // quarter-warp of phase A/C = (G g-values) x (8/G rows): rows must land on
+  // distinct 16-byte bank slots
+  return G == 4 ? (((py * 4) & 7) == 4 ? py * 4 : py * 4 + 4)
+       : G == 2 ? (((py * 2) & 7) == 2 || ((py * 2) & 7) == 6 ? py * 2 : py * 2 + 2)
+                : py + ((py & 1) ? 0 : 1);
+}
+
+// y transforms in two register passes through the slab (PY = R1 * M1, task
+// registers <= max(R1, M1) values): forward n = n1*M1 + m, k = k1 + R1*k2
+// (slab position k1*M1 + k2); inverse = the transpose.
+__host__ __device__ constexpr int yzf_r1(int py) {
+  return py % 5 == 0 ? 5 : py % 4 == 0 ? 4 : py % 3 == 0 ? 3 : py % 2 == 0 ? 2 : 1;
+}
+
+template <int PY, int PZ, int G>
+__global__ void __launch_bounds__(256, 2)
+    op_yz_reg_kernel(double2* __restrict__ A, SpecView sv, int ny, int nz, int nkx, int ngroups, double scale) {
+  extern __shared__ __align__(16) double2 ysm[];
+  constexpr int ROW = yzf_row<G>(PY);
+  constexpr int R1 = yzf_r1(PY), M1 = PY / R1;
+  static_assert(R1 > 1 && M1 > 1, "PY must split into two register lengths");
+  __shared__ double2 twy[PY];  // w_PY^j (forward sign)
+  for (int i = threadIdx.x; i < PY; i += blockDim.x) {
+    constexpr int o = reg_tw_off(PY);
+    twy[i] = cmk(c_rtw[2 * (o + i)], c_rtw[2 * (o + i) + 1]);
+  }
+  const int b = blockIdx.x;
+  const int grp = (b & 1) ? ngroups - 1 - (b >> 1) : (b >> 1);
+  const int kx0 = grp * G;
+  const long cols = nkx;  // A is (3, nz, ny, nkx)
+  const int nlines = 3 * nz;
+  __syncthreads();
+  // ---- A1: y-forward, first factor (global -> slab)
+  for (int i = threadIdx.x; i < nlines * M1 * G; i += blockDim.x) {
+    const int g = i % G, r = i / G;
+    const int m = r % M1, cz = r / M1;
+    const int kx = kx0 + g;
+    double2 v[R1];
+    const double2* src = A + (long)cz * ny * cols + kx;
+#pragma unroll
+    for (int n1 = 0; n1 < R1; ++n1) {
+      const int y = n1 * M1 + m;
+      v[n1] = (y < ny && kx < nkx) ? __ldg(src + (long)y * cols) : cmk(0.0, 0.0);
+    }
+    reg_fft<R1, false>(v);
+    double2* s = ysm + cz * ROW + m * G + g;
+    s[0] = v[0];
+#pragma unroll
+    for (int k1 = 1; k1 < R1; ++k1) s[k1 * M1 * G] = cmul(v[k1], twy[(k1 * m) % PY]);
+  }
+  __syncthreads();
+  // ---- A2: second factor in place (position k1*M1 + k2 = frequency k1 + R1*k2)
+  for (int i = threadIdx.x; i < nlines * R1 * G; i += blockDim.x) {
+    const int g = i % G, r = i / G;
+    const int k1 = r % R1, cz = r / R1;
+    double2* s = ysm + cz * ROW + k1 * M1 * G + g;
+    double2 v[M1];
+#pragma unroll
+    for (int n2 = 0; n2 < M1; ++n2) v[n2] = s[n2 * G];
+    reg_fft<M1, false>(v);
+#pragma unroll
+    for (int k2 = 0; k2 < M1; ++k2) s[k2 * G] = v[k2];
+  }
+  __syncthreads();
+  // ---- B: z-forward, spectral multiply, z-inverse (3 lanes per column)
+  {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int c = lane < 3 * ZS_COLS ? lane / ZS_COLS : 2;
+    const int j = lane < 3 * ZS_COLS ? lane - c * ZS_COLS : 0;
+    const int p0 = c == 0 ? 0 : (c == 1 ? 1 : 2);
+    const int p1 = c == 0 ? 1 : (c == 1 ? 3 : 4);
+    const int p2 = c == 0 ? 2 : (c == 1 ? 4 : 5);
+    constexpr int ncol = PY * G;
+    for (int col0 = wid * ZS_COLS; col0 < ncol; col0 += nw * ZS_COLS) {
+      const int col = col0 + j;
+      const bool act = lane < 3 * ZS_COLS && col < ncol;
+      const int pos = act ? col / G : 0, g = act ? col - (col / G) * G : 0;
+      const int k1 = pos / M1, k2 = pos - (pos / M1) * M1;
+      const int ky = k1 + R1 * k2;
+      const int kx = kx0 + g;
+      const bool live = act && kx < nkx;
+      double2* s = ysm + c * nz * ROW + pos * G + g;
+      double2 v[PZ];
+#pragma unroll
+      for (int z = 0; z < PZ; ++z) v[z] = (live && z < nz) ? s[z * ROW] : cmk(0.0, 0.0);
+      reg_fft<PZ, false>(v);
+      long so0, sstr, kstr;
+      bool my = false, mx = false;
+      if (sv.compact) {
+        my = 2 * ky > sv.Py;
+        mx = 2 * kx > sv.Px;
+        so0 = ((long)(my ? sv.Py - ky : ky) * sv.Hx + (mx ? sv.Px - kx : kx)) * 6;
+        sstr = 1;
+        kstr = (long)sv.Hy * sv.Hx * 6;
+      } else {
+        so0 = (long)ky * nkx + kx;
+        kstr = (long)PY * nkx;
+        sstr = (long)PZ * kstr;
+      }
+      if (!live) so0 = 0;
+      const bool n0 = (mx && odd_x(p0)) ^ (my && odd_y(p0));
+      const bool n1 = (mx && odd_x(p1)) ^ (my && odd_y(p1));
+      const bool n2 = (mx && odd_x(p2)) ^ (my && odd_y(p2));
+      const double2* S0 = sv.S + p0 * sstr + so0;
+      const double2* S1 = sv.S + p1 * sstr + so0;
+      const double2* S2 = sv.S + p2 * sstr + so0;
+#pragma unroll
+      for (int kz = 0; kz < PZ; ++kz) {
+        const bool mz = sv.compact && 2 * kz > PZ;
+        const long ko = (long)(mz ? PZ - kz : kz) * kstr;
+        double2 s0 = __ldg(S0 + ko), s1 = __ldg(S1 + ko), s2 = __ldg(S2 + ko);
+        if (n0 ^ (mz && odd_z(p0))) s0 = cmk(-s0.x, -s0.y);
+        if (n1 ^ (mz && odd_z(p1))) s1 = cmk(-s1.x, -s1.y);
+        if (n2 ^ (mz && odd_z(p2))) s2 = cmk(-s2.x, -s2.y);
+        const double2 x0 = shfl_c(v[kz], j), x1 = shfl_c(v[kz], ZS_COLS + j),
+                      x2 = shfl_c(v[kz], 2 * ZS_COLS + j);
+        double2 acc = cmul(s0, x0);
+        cfma(acc, s1, x1);
+        cfma(acc, s2, x2);
+        v[kz] = cscale(acc, scale);
+      }
+      reg_fft<PZ, true>(v);
+      if (live) {
+#pragma unroll
+        for (int z = 0; z < PZ; ++z)
+          if (z < nz) s[z * ROW] = v[z];
+      }
+    }
+  }
+  __syncthreads();
+  // ---- C1: y-inverse over k2 (-> m), conjugate twiddle, in place
+  for (int i = threadIdx.x; i < nlines * R1 * G; i += blockDim.x) {
+    const int g = i % G, r = i / G;
+    const int k1 = r % R1, cz = r / R1;
+    double2* s = ysm + cz * ROW + k1 * M1 * G + g;
+    double2 v[M1];
+#pragma unroll
+    for (int k2 = 0; k2 < M1; ++k2) v[k2] = s[k2 * G];
+    reg_fft<M1, true>(v);
+    s[0] = v[0];
+#pragma unroll
+    for (int m = 1; m < M1; ++m) s[m * G] = cmulc(v[m], twy[(k1 * m) % PY]);
+  }
+  __syncthreads();
+  // ---- C2: y-inverse over k1 (-> n1), crop y < ny, back to A
+  for (int i = threadIdx.x; i < nlines * M1 * G; i += blockDim.x) {
+    const int g = i % G, r = i / G;
+    const int m = r % M1, cz = r / M1;
+    const int kx = kx0 + g;
+    if (kx >= nkx) continue;
+    const double2* s = ysm + cz * ROW + m * G + g;
+    double2 v[R1];
+#pragma unroll
+    for (int k1 = 0; k1 < R1; ++k1) v[k1] = s[k1 * M1 * G];
+    reg_fft<R1, true>(v);
+    double2* dst = A + (long)cz * ny * cols + kx;
+#pragma unroll
+    for (int n1 = 0; n1 < R1; ++n1) {
+      const int y = n1 * M1 + m;
+      if (y < ny) dst[(long)y * cols] = v[n1];
+    }
+  }
+}
+
+// (PY, PZ) pairs with a fused kernel: the BASELINE grids (c0 20x10, c1 45x21,
+// c2 50x21) and the test grids
+#define VX_YZF_PAIRS(X) X(20, 10) X(45, 21) X(50, 21) X(12, 6) X(16, 8) X(24, 10) X(14, 6)
+
+static int g_yz_fused = -1;  // -1: from VX_YZ_FUSED
+static size_t yzf_smem(int py, int nz, int G) {
+  const int row = G == 4 ? yzf_row<4>(py) : G == 2 ? yzf_row<2>(py) : yzf_row<1>(py);
+  return (size_t)3 * nz * row * sizeof(double2);
+}
+
+// Fused y/z pass when (py, pz) has an instantiation; returns 1 if it ran.
+static int op_yz_fused_reg(int ny, int nz, int nkx, int py, int pz, const SpecView& sv, double2* A, double scale,
+                           cudaStream_t s, int* ran) {
+  *ran = 0;
+  if (g_yz_fused < 0) g_yz_fused = env_int("VX_YZ_FUSED", 0) != 0;  // opt-in: latency-bound (0.51 vs 0.40 ms at c1)
+  if (!g_yz_fused || nkx <= 0) return VX_OK;
+  static const int genv = env_int("VX_YZF_G", 4);
+  const size_t budget = (size_t)device_smem_optin() / 2 - 2048;  // two CTAs per SM
+  int G = genv;
+  while (G > 1 && yzf_smem(py, nz, G) > budget) G /= 2;
+  if (yzf_smem(py, nz, G) > (size_t)device_smem_optin()) return VX_OK;
+  const int ngroups = (nkx + G - 1) / G;
+  const size_t smem = yzf_smem(py, nz, G);
+#define VX_YZF_G(PY_, PZ_, G_)                                                                  \
+  {                                                                                             \
+    auto k = op_yz_reg_kernel<PY_, PZ_, G_>;                                                    \
+    if (smem > 48 * 1024) VX_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+    k<<<ngroups, 256, smem, s>>>(A, sv, ny, nz, nkx, ngroups, scale);                           \
+  }
+#define VX_YZF_CASE(PY_, PZ_)                                                                   \
+  if (py == PY_ && pz == PZ_) {                                                                 \
+    if (G == 4) VX_YZF_G(PY_, PZ_, 4) else if (G == 2) VX_YZF_G(PY_, PZ_, 2) else VX_YZF_G(PY_, PZ_, 1) \
+    VX_CHECK_LAUNCH("op_yz_reg_kernel");                                                        \
+    *ran = 1;                                                                                   \
+    return VX_OK;                                                                               \
+  }
+  VX_YZF_PAIRS(VX_YZF_CASE)
+#undef VX_YZF_CASE
+#undef VX_YZF_G
+  return VX_OK;
 }
 
 // K2-K4 on nkx x-frequency columns held as A (3, nz, ny, nkx): y-DFT (pad ny ->
@@ -350,7 +673,9 @@ static int op_x_forward(const FftPlan& fx, int nx, int px, int nlines, const dou
 // `scale` = 1/(px py pz) of the full transform.
 static int op_yz(const FftPlan& fy, const FftPlan& fz, int ny, int nz, int nkx, int py, int pz,
                  const SpecView& spectra, double2* A, double2* B, double scale, cudaStream_t s) {
-  int st;
+  int st, ran;
+  if ((st = op_yz_fused_reg(ny, nz, nkx, py, pz, spectra, A, scale, s, &ran))) return st;
+  if (ran) return VX_OK;
   const long cols = (long)py * nkx;
   const bool reg_y = reg_fft_enabled() && reg_fft_supported(py);
   const bool reg_z = reg_fft_enabled() && reg_fft_supported(pz) && pz <= REG_ZMUL_MAX;
@@ -393,7 +718,7 @@ static int op_x_inverse(const FftPlan& fx, int nx, int px, int nlines, long line
                         const double2* A, const double2* X, const double2* m, double2* Y, cudaStream_t s) {
   LoadStrided ld{A, {px, 0, 1, 1}};
   StoreSystem sv{Y, X, m, nx, nvox, 1.0, line0 * nx};
-  return launch_fft_lines(fx, ld, sv, nlines, px, nx, true, true, s);
+  return launch_fft_auto(fx, ld, sv, nlines, px, nx, true, true, s);
 }
 
 // ------------------------------------------------ fused y/z pass (default)
@@ -478,8 +803,8 @@ __global__ void __launch_bounds__(512, 2) op_yz_fused_kernel(FftPlan fy, FftPlan
     } else {
       const bool mz = 2 * kz > sv.Pz, my = 2 * ky > sv.Py, mx = 2 * kx > sv.Px;
       const int kzs = mz ? sv.Pz - kz : kz, kys = my ? sv.Py - ky : ky, kxs = mx ? sv.Px - kx : kx;
-      const long so = ((long)kzs * sv.Hy + kys) * sv.Hx + kxs;
-      const long sstr = (long)sv.Hz * sv.Hy * sv.Hx;
+      const long so = (((long)kzs * sv.Hy + kys) * sv.Hx + kxs) * 6;
+      const long sstr = 1;
 #pragma unroll
       for (int q = 0; q < 6; ++q) {
         const double2 v = __ldg(sv.S + q * sstr + so);
@@ -640,7 +965,7 @@ __global__ void spec_compact_kernel(const double2* __restrict__ full, double2* _
     const int ky = (int)(r % hy); r /= hy;
     const int kz = (int)(r % hz);
     const int p = (int)(r / hz);
-    out[i] = full[(((long)p * pz + kz) * py + ky) * px + kx];
+    out[(((long)kz * hy + ky) * hx + kx) * 6 + p] = full[(((long)p * pz + kz) * py + ky) * px + kx];
   }
 }
 

@@ -95,7 +95,7 @@ class OperatorPlan:
         """Host copy of the full spectra (read-only numpy array, made on demand)."""
         h = self.spectra_device.cpu().numpy()
         if self.compact:
-            h = _expand_compact(h, self.padded_shape)
+            h = _expand_compact(np.moveaxis(h, -1, 0), self.padded_shape)
         h.setflags(write=False)
         return h
 
@@ -139,7 +139,7 @@ def plan_operator(kernel: ToeplitzKernel, workers: int = 1, *, compact: bool | N
     if compact is None:
         compact = kernel_asymmetry(kernel) <= SYMMETRY_RTOL
     if compact:
-        comp = nv.empty_c128((6, pz // 2 + 1, py // 2 + 1, px // 2 + 1))
+        comp = nv.empty_c128((pz // 2 + 1, py // 2 + 1, px // 2 + 1, 6))  # component-interleaved
         nv.call("vx_op_compact", px, py, pz, spec.data_ptr(), comp.data_ptr(), nv.stream_ptr())
         del spec
         return OperatorPlan(grid=kernel.grid, k0=float(kernel.k0), spectra_device=comp, workers=workers,

@@ -39,7 +39,7 @@ def _fft_lines(torch, a, axis, inverse, n_out=None, n=None):
 
 
 @pytest.mark.parametrize("n", [1, 2, 3, 4, 5, 7, 8, 11, 13, 16, 17, 24, 31, 45, 64, 97, 200, 367,
-                               400, 734, 735, 1500, 2500, 5000, 10000])
+                               400, 734, 735, 1500, 2500, 3000, 5000, 10000])
 def test_fft_contiguous_lengths(torch, rng, n):
     lines = max(1, min(64, 20000 // n))
     a = random_field(rng, lines * n).reshape(lines, n)
@@ -61,6 +61,18 @@ def test_fft_zero_pad_and_crop(torch, rng):
     assert relerr(got, scipy.fft.fft(a, 16, axis=1)) < 1e-14
     got = _fft_lines(torch, a, 1, True, n=7, n_out=3)
     assert relerr(got, scipy.fft.ifft(a, axis=1)[:, :3]) < 1e-14
+
+
+@pytest.mark.parametrize("n_in,n,n_out", [(5000, 10000, 10000), (200, 400, 400), (1500, 3000, 3000),
+                                          (367, 735, 735)])
+def test_fft_long_pad_and_crop(torch, rng, n_in, n, n_out):
+    # the operator's x passes: zero-pad n_in -> n forward, crop n -> n_in inverse
+    a = random_field(rng, 7 * n_in).reshape(7, n_in)
+    fw = _fft_lines(torch, a, 1, False, n=n)
+    assert relerr(fw, scipy.fft.fft(a, n, axis=1)) < 1e-13
+    got = _fft_lines(torch, fw, 1, True, n=n, n_out=n_in)
+    assert relerr(got, scipy.fft.ifft(fw, axis=1)[:, :n_in]) < 1e-13
+    assert relerr(got, a) < 1e-13
 
 
 OP_TAGS = ["small", "cube", "one", "odd", "prime", "long"]
