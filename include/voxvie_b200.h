@@ -67,6 +67,11 @@ int vx_op_plan(int nx, int ny, int nz, int px, int py, int pz, const vx_c128* ge
  * else the smallest 7-smooth length >= 2n-1. */
 int vx_op_padded_length(int n);
 
+/* Padded z length: vx_op_padded_length(nz), or with VX_ZPAIR=1 (opt-in
+ * paired-parity z kernel, nz <= 16) the reference's own 2 nz
+ * (operator.py:21-41 embeds on 2n). */
+int vx_op_padded_length_z(int nz);
+
 /* Scratch (in vx_c128 elements) needed by vx_op_apply. */
 long vx_op_work_elems(int nx, int ny, int nz, int px, int py, int pz);
 

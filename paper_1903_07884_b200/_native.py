@@ -49,6 +49,7 @@ _SIGS = {
     "vx_op_plan": (c_int, [c_int] * 6 + [P, c_long, c_long, c_long, c_long, P, P]),
     "vx_op_work_elems": (c_long, [c_int] * 6),
     "vx_op_padded_length": (c_int, [c_int]),
+    "vx_op_padded_length_z": (c_int, [c_int]),
     "vx_op_apply": (c_int, [c_int] * 6 + [P, c_int, P, P, P, P, P]),
     "vx_gen_asymmetry": (c_int, [c_int] * 3 + [P, c_long, c_long, c_long, c_long, P, P]),
     "vx_op_compact_elems": (c_long, [c_int] * 3),

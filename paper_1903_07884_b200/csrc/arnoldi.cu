@@ -16,9 +16,10 @@ namespace vx {
 constexpr int AR_THREADS = 256;
 constexpr int AR_GROUP = 4;  // basis vectors per register group
 
+// one resident wave of the dots / update kernels (3 CTAs of 256 per SM)
 static int ar_grid(long n) {
   long g = (n + 2047) / 2048;
-  const long cap = 8L * device_sm_count();
+  const long cap = 3L * device_sm_count();
   if (g > cap) g = cap;
   if (g < 1) g = 1;
   return (int)g;
@@ -53,97 +54,123 @@ __device__ __forceinline__ void chunk(long n, long& beg, long& end) {
 }
 
 // part[i*G + b] = sum_{e in chunk b} conj(V_i[e]) w[e], i < nvec; part[nvec*G+b] = ||w||^2
-__global__ void __launch_bounds__(AR_THREADS) dots_kernel(long n, int nvec, const double2* __restrict__ V,
-                                                          long ldv, const double2* __restrict__ w,
-                                                          double2* __restrict__ part,
-                                                          const double* cond) {
+// Each thread takes two elements per step and a group of AR_DG basis vectors:
+// 2 + 2*AR_DG independent 16-byte loads in flight per thread; the grid is one
+// resident wave (ar_grid), so there is no tail.  ||w||^2 is accumulated in the
+// first group's sweep.
+constexpr int AR_DG = 8;
+constexpr int AR_UG = 4;  // update: basis vectors per load group (register budget)
+
+__global__ void __launch_bounds__(AR_THREADS, 3) dots_kernel(long n, int nvec, const double2* __restrict__ V,
+                                                             long ldv, const double2* __restrict__ w,
+                                                             double2* __restrict__ part,
+                                                             const double* cond) {
   if (cond && cond[2] == 0.0) return;
   __shared__ double2 sh[AR_THREADS / 32];
   long beg, end;
   chunk(n, beg, end);
   const int G = gridDim.x;
-  double2 nrm = cmk(0.0, 0.0);
-  for (long e = beg + threadIdx.x; e < end; e += AR_THREADS) {
-    const double2 x = w[e];
-    nrm.x = fma(x.x, x.x, nrm.x);
-    nrm.x = fma(x.y, x.y, nrm.x);
-  }
-  double2 r = block_sum(nrm, sh);
-  if (threadIdx.x == 0) part[(long)nvec * G + blockIdx.x] = r;
-  for (int i0 = 0; i0 < nvec; i0 += AR_GROUP) {
-    double2 acc[AR_GROUP];
+  double nrm = 0.0;
+  for (int i0 = 0; i0 < (nvec > 0 ? nvec : 1); i0 += AR_DG) {
+    double2 acc[AR_DG];
 #pragma unroll
-    for (int g = 0; g < AR_GROUP; ++g) acc[g] = cmk(0.0, 0.0);
-    for (long e = beg + threadIdx.x; e < end; e += AR_THREADS) {
-      const double2 x = w[e];
+    for (int g = 0; g < AR_DG; ++g) acc[g] = cmk(0.0, 0.0);
+    for (long e = beg + threadIdx.x; e < end; e += 2 * AR_THREADS) {
+      const long e2 = e + AR_THREADS;
+      const bool has2 = e2 < end;
+      const double2 x0 = w[e];
+      const double2 x1 = has2 ? w[e2] : cmk(0.0, 0.0);
+      if (i0 == 0) {
+        nrm = fma(x0.x, x0.x, nrm);
+        nrm = fma(x0.y, x0.y, nrm);
+        nrm = fma(x1.x, x1.x, nrm);
+        nrm = fma(x1.y, x1.y, nrm);
+      }
+      double2 v0[AR_DG], v1[AR_DG];
 #pragma unroll
-      for (int g = 0; g < AR_GROUP; ++g)
-        if (i0 + g < nvec) {
-          const double2 v = ld_stream(V + (long)(i0 + g) * ldv + e);
-          // conj(v) * x
-          acc[g].x = fma(v.x, x.x, acc[g].x);
-          acc[g].x = fma(v.y, x.y, acc[g].x);
-          acc[g].y = fma(v.x, x.y, acc[g].y);
-          acc[g].y = fma(-v.y, x.x, acc[g].y);
-        }
+      for (int g = 0; g < AR_DG; ++g) {
+        const bool ok = i0 + g < nvec;
+        const double2* vp = V + (long)(i0 + g) * ldv;
+        v0[g] = ok ? ld_stream(vp + e) : cmk(0.0, 0.0);
+        v1[g] = (ok && has2) ? ld_stream(vp + e2) : cmk(0.0, 0.0);
+      }
+#pragma unroll
+      for (int g = 0; g < AR_DG; ++g) {  // conj(v) * x
+        acc[g].x = fma(v0[g].x, x0.x, acc[g].x);
+        acc[g].x = fma(v0[g].y, x0.y, acc[g].x);
+        acc[g].y = fma(v0[g].x, x0.y, acc[g].y);
+        acc[g].y = fma(-v0[g].y, x0.x, acc[g].y);
+        acc[g].x = fma(v1[g].x, x1.x, acc[g].x);
+        acc[g].x = fma(v1[g].y, x1.y, acc[g].x);
+        acc[g].y = fma(v1[g].x, x1.y, acc[g].y);
+        acc[g].y = fma(-v1[g].y, x1.x, acc[g].y);
+      }
     }
 #pragma unroll
-    for (int g = 0; g < AR_GROUP; ++g) {
+    for (int g = 0; g < AR_DG; ++g) {
       if (i0 + g < nvec) {
         double2 s = block_sum(acc[g], sh);
         if (threadIdx.x == 0) part[(long)(i0 + g) * G + blockIdx.x] = s;
       }
     }
   }
+  double2 r = block_sum(cmk(nrm, 0.0), sh);
+  if (threadIdx.x == 0) part[(long)nvec * G + blockIdx.x] = r;
 }
 
 // w[e] -= sum_i coef[i] V_i[e]; part[b] = ||w_new||^2 over chunk b
-__global__ void __launch_bounds__(AR_THREADS) update_kernel(long n, int nvec, const double2* __restrict__ V,
-                                                            long ldv, const double2* __restrict__ coef,
-                                                            double2* __restrict__ w,
-                                                            double2* __restrict__ part,
-                                                            const double* cond) {
+// (two elements per thread and step, AR_DG basis loads in flight per element)
+__global__ void __launch_bounds__(AR_THREADS, 3) update_kernel(long n, int nvec, const double2* __restrict__ V,
+                                                               long ldv, const double2* __restrict__ coef,
+                                                               double2* __restrict__ w,
+                                                               double2* __restrict__ part,
+                                                               const double* cond) {
   if (cond && cond[2] == 0.0) return;
   __shared__ double2 sh[AR_THREADS / 32];
   __shared__ double2 cf[128];
   long beg, end;
   chunk(n, beg, end);
-  double2 nrm = cmk(0.0, 0.0);
-  for (int i0 = 0; i0 < nvec; i0 += 128) {
+  double nrm = 0.0;
+  for (int i0 = 0; i0 < (nvec > 0 ? nvec : 1); i0 += 128) {
     const int m = nvec - i0 < 128 ? nvec - i0 : 128;
     __syncthreads();
     for (int i = threadIdx.x; i < m; i += AR_THREADS) cf[i] = coef[i0 + i];
     __syncthreads();
     const bool last = (i0 + 128 >= nvec);
-    for (long e = beg + threadIdx.x; e < end; e += AR_THREADS) {
-      double2 x = w[e];
-      int i = 0;
-      for (; i + 4 <= m; i += 4) {
-        const double2 v0 = ld_stream(V + (long)(i0 + i) * ldv + e);
-        const double2 v1 = ld_stream(V + (long)(i0 + i + 1) * ldv + e);
-        const double2 v2 = ld_stream(V + (long)(i0 + i + 2) * ldv + e);
-        const double2 v3 = ld_stream(V + (long)(i0 + i + 3) * ldv + e);
-        cfms(x, cf[i], v0);
-        cfms(x, cf[i + 1], v1);
-        cfms(x, cf[i + 2], v2);
-        cfms(x, cf[i + 3], v3);
+    for (long e = beg + threadIdx.x; e < end; e += 2 * AR_THREADS) {
+      const long e2 = e + AR_THREADS;
+      const bool has2 = e2 < end;
+      double2 x0 = w[e];
+      double2 x1 = has2 ? w[e2] : cmk(0.0, 0.0);
+      for (int i = 0; i < m; i += AR_UG) {
+        double2 v0[AR_UG], v1[AR_UG];
+#pragma unroll
+        for (int g = 0; g < AR_UG; ++g) {
+          const bool ok = i + g < m;
+          const double2* vp = V + (long)(i0 + i + g) * ldv;
+          v0[g] = ok ? ld_stream(vp + e) : cmk(0.0, 0.0);
+          v1[g] = (ok && has2) ? ld_stream(vp + e2) : cmk(0.0, 0.0);
+        }
+#pragma unroll
+        for (int g = 0; g < AR_UG; ++g) {
+          if (i + g < m) {
+            const double2 c = cf[i + g];
+            cfms(x0, c, v0[g]);
+            cfms(x1, c, v1[g]);
+          }
+        }
       }
-      for (; i < m; ++i) cfms(x, cf[i], ld_stream(V + (long)(i0 + i) * ldv + e));
-      w[e] = x;
+      w[e] = x0;
+      if (has2) w[e2] = x1;
       if (last) {
-        nrm.x = fma(x.x, x.x, nrm.x);
-        nrm.x = fma(x.y, x.y, nrm.x);
+        nrm = fma(x0.x, x0.x, nrm);
+        nrm = fma(x0.y, x0.y, nrm);
+        nrm = fma(x1.x, x1.x, nrm);
+        nrm = fma(x1.y, x1.y, nrm);
       }
     }
   }
-  if (nvec == 0) {
-    for (long e = beg + threadIdx.x; e < end; e += AR_THREADS) {
-      const double2 x = w[e];
-      nrm.x = fma(x.x, x.x, nrm.x);
-      nrm.x = fma(x.y, x.y, nrm.x);
-    }
-  }
-  double2 r = block_sum(nrm, sh);
+  double2 r = block_sum(cmk(nrm, 0.0), sh);
   if (threadIdx.x == 0) part[blockIdx.x] = r;
 }
 

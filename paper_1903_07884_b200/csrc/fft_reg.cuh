@@ -48,7 +48,7 @@ __device__ __forceinline__ void reg_fft(double2* v) {
   constexpr double sgn = INV ? 1.0 : -1.0;
   if constexpr (N == 1) {
     return;
-  } else if constexpr (N == 2 || N == 3 || N == 4 || N == 5 || N == 7 || N == 8) {
+  } else if constexpr (N == 2 || N == 3 || N == 4 || N == 5 || N == 7 || N == 8 || N == 11 || N == 13) {
     dft_codelet<N>(v, sgn);
   } else {
     constexpr int R = reg_radix(N), M = N / R;

@@ -30,6 +30,12 @@ def padded_length(n: int) -> int:
     return int(nv.query("vx_op_padded_length", n))
 
 
+def padded_length_z(nz: int) -> int:
+    """z padding: the reference's 2 nz when the paired-parity z kernel covers nz."""
+    nv.load()
+    return int(nv.query("vx_op_padded_length_z", nz))
+
+
 def upload_tensors(kernel: ToeplitzKernel):
     """Device copy of the generators (cached on the kernel object)."""
     cache = getattr(kernel, "_vx_device_tensors", None)
@@ -130,7 +136,7 @@ def plan_operator(kernel: ToeplitzKernel, workers: int = 1, *, compact: bool | N
     spectra when the generators are parity-symmetric to SYMMETRY_RTOL."""
     nv.require_cuda()
     nx, ny, nz = kernel.grid.dims
-    px, py, pz = padded_length(nx), padded_length(ny), padded_length(nz)
+    px, py, pz = padded_length(nx), padded_length(ny), padded_length_z(nz)
     gen = upload_tensors(kernel)
     spec = nv.empty_c128((6, pz, py, px))
     s = gen.stride()
