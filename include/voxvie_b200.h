@@ -269,6 +269,33 @@ long vx_launch_count(void);
 int vx_timing_enable(int on);
 int vx_timing_read(const char* span, double* total_ms, long* count);
 
+/* ---- ragged ("packed") factor storage for the 1-level block solves.
+ * The build writes every block in the padded tile geometry of dmax (tiles of
+ * 32, reference zgetrf blocks circulant.py:113-118 re-tiled); the repack keeps
+ * only the leading d_s x d_s entries of each sector block (tile (i,j) is
+ * t_i x t_j, t_i = min(32, d_s - 32 i)), so the per-iteration solve streams
+ * sum_s d_s^2 entries per stored frequency instead of nsec * npad^2.
+ * sec_dims: host array of nsec (<= 4) dims, each <= dmax; dense blocks use
+ * nsec = 1, dims = {3 ny nz}.  Ragged storage per frequency slot:
+ * vx_lu_rag_stride(nsec, sec_dims) entries. */
+long vx_lu_rag_stride(int nsec, const int* sec_dims);
+/* 1 while vx_solve_variant(1) selects the synchronous (padded-only) solve. */
+int vx_solve_classic(void);
+int vx_lu_repack(int nkslots, int nsec, int dmax, const int* sec_dims, const vx_c128* padded,
+                 vx_c128* ragged, void* stream);
+int vx_lu_unpack(int nkslots, int nsec, int dmax, const int* sec_dims, const vx_c128* ragged,
+                 vx_c128* padded, void* stream);
+/* vx_prec1_apply / vx_prec1_apply_sec (reference OneLevelPrec.apply,
+ * circulant.py:162-188) on ragged factors (single-RHS work lists only). */
+int vx_prec1_apply_rag(int nx, int ny, int nz, int nrhs, const vx_c128* factors, const int* perm,
+                       const int* items, int n_single, int n_items, int direct_r, const int* klist,
+                       const vx_c128* x, vx_c128* y, vx_c128* work, void* stream);
+int vx_prec1_apply_sec_rag(int nx, int ny, int nz, int nrhs, const vx_c128* factors, const int* perm,
+                           const int* items, int n_single, int n_items, int direct_r, const int* klist,
+                           int nsec, int dmax, const int* sec_dims, int norb, const int* orows,
+                           const int* osec, const double* ocoef, const unsigned char* flipk,
+                           const vx_c128* x, vx_c128* y, vx_c128* work, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

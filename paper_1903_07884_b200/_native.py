@@ -87,6 +87,13 @@ _SIGS = {
     "vx_prec1_sec_work_elems": (c_long, [c_int] * 6),
     "vx_prec1_apply_sec": (c_int, [c_int] * 4 + [P, P, P, c_int, c_int, c_int, P, c_int, c_int, c_int, P, P, P, P,
                                                   P, P, P, P]),
+    "vx_prec1_apply_sec_rag": (c_int, [c_int] * 4 + [P, P, P, c_int, c_int, c_int, P, c_int, c_int, P, c_int,
+                                                      P, P, P, P, P, P, P, P]),
+    "vx_prec1_apply_rag": (c_int, [c_int] * 4 + [P, P, P, c_int, c_int, c_int, P, P, P, P, P]),
+    "vx_lu_rag_stride": (c_long, [c_int, P]),
+    "vx_solve_classic": (c_int, []),
+    "vx_lu_repack": (c_int, [c_int, c_int, c_int, P, P, P, P]),
+    "vx_lu_unpack": (c_int, [c_int, c_int, c_int, P, P, P, P]),
     "vx_rep_variant": (c_int, [c_int]),
     "vx_op_reg_fft": (c_int, [c_int]),
     "vx_prec1_solve": (c_int, [c_int, c_int, P, P, P, c_int, c_int, c_int, P, P, c_long, c_long, P]),

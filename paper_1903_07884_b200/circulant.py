@@ -384,21 +384,74 @@ class _OneLevelBase:
 
     def _apply_dev(self, xd, r):
         nx, ny, nz = self.grid.dims
+        rag = getattr(self, "_rag_dims", None) is not None and r == 1 and not nv.query("vx_solve_classic")
+        if rag:
+            self._padded_fac = None
+        fac = self._fac if (rag or getattr(self, "_rag_dims", None) is None) else self._padded()
         if self._sec is not None:
             sp, sd = self._sec.plan, self._sec
             y = nv.empty_c128((self.grid.n_unknowns, r))
             work = nv.empty_c128(int(nv.query("vx_prec1_sec_work_elems", nx, ny, nz, r, sp.nsec, sp.dmax)))
-            nv.call("vx_prec1_apply_sec", nx, ny, nz, r, self._fac.data_ptr(), self._perm.data_ptr(),
-                    self._items.data_ptr(), self._n_single, self._n_items, self._direct_r, self._klist.data_ptr(),
-                    sp.nsec, sp.dmax, sd.norb, sd.orows.data_ptr(), sd.osec.data_ptr(), sd.ocoef.data_ptr(),
-                    self._flipk.data_ptr(), xd.data_ptr(), y.data_ptr(), work.data_ptr(), nv.stream_ptr())
+            if rag:
+                nv.call("vx_prec1_apply_sec_rag", nx, ny, nz, r, fac.data_ptr(), self._perm.data_ptr(),
+                        self._items.data_ptr(), self._n_single, self._n_items, self._direct_r,
+                        self._klist.data_ptr(), sp.nsec, sp.dmax, self._rag_dims.ctypes.data, sd.norb,
+                        sd.orows.data_ptr(), sd.osec.data_ptr(), sd.ocoef.data_ptr(), self._flipk.data_ptr(),
+                        xd.data_ptr(), y.data_ptr(), work.data_ptr(), nv.stream_ptr())
+            else:
+                nv.call("vx_prec1_apply_sec", nx, ny, nz, r, fac.data_ptr(), self._perm.data_ptr(),
+                        self._items.data_ptr(), self._n_single, self._n_items, self._direct_r,
+                        self._klist.data_ptr(), sp.nsec, sp.dmax, sd.norb, sd.orows.data_ptr(),
+                        sd.osec.data_ptr(), sd.ocoef.data_ptr(), self._flipk.data_ptr(), xd.data_ptr(),
+                        y.data_ptr(), work.data_ptr(), nv.stream_ptr())
             return y
         y = nv.empty_c128((self.grid.n_unknowns, r))
         work = nv.empty_c128(int(nv.query("vx_prec1_work_elems", nx, ny, nz, r)))
-        nv.call("vx_prec1_apply", nx, ny, nz, r, self._fac.data_ptr(), self._perm.data_ptr(),
-                self._items.data_ptr(), self._n_single, self._n_items, self._direct_r, self._klist.data_ptr(),
-                xd.data_ptr(), y.data_ptr(), work.data_ptr(), nv.stream_ptr())
+        nv.call("vx_prec1_apply_rag" if rag else "vx_prec1_apply", nx, ny, nz, r, fac.data_ptr(),
+                self._perm.data_ptr(), self._items.data_ptr(), self._n_single, self._n_items, self._direct_r,
+                self._klist.data_ptr(), xd.data_ptr(), y.data_ptr(), work.data_ptr(), nv.stream_ptr())
         return y
+
+    # ---- ragged factor storage (vx_lu_repack): the per-iteration solve streams
+    # only the d x d entries of every (sector) block, not the 32-padded tiles
+    _rag_dims = None
+    _padded_fac = None
+
+    def _rag_geometry(self):
+        if self._sec is not None:
+            return self._sec.plan.nsec, self._sec.plan.dmax, tuple(self._sec.plan.dims)
+        n = self.block_size
+        return 1, n, (n,)
+
+    def _make_ragged(self):
+        """Repack the padded factors into ragged storage (frees the padded copy)."""
+        nsec, dmax, dims = self._rag_geometry()
+        if dmax <= 32 or os.environ.get("VX_RAGGED", "1") == "0":
+            return
+        dims_a = np.ascontiguousarray(dims, np.int32)
+        nslots = int(self._fac.shape[0])
+        nk = nslots // nsec
+        stride = int(nv.query("vx_lu_rag_stride", nsec, dims_a.ctypes.data))
+        rag = nv.empty_c128((nk, stride))
+        nv.call("vx_lu_repack", nk, nsec, dmax, dims_a.ctypes.data, self._fac.data_ptr(), rag.data_ptr(),
+                nv.stream_ptr())
+        self._fac = rag
+        self._rag_dims = dims_a
+        self._nslots = nslots
+
+    def _padded(self):
+        """Padded-tile factors (nslots, npad^2): the layout the reduced scheme,
+        multi-RHS applies and the LAPACK views read (unpacked on demand)."""
+        if self._rag_dims is None:
+            return self._fac
+        if self._padded_fac is None:
+            nsec, dmax, _ = self._rag_geometry()
+            blk = int(nv.query("vx_lu_block_elems", dmax))
+            pad = nv.empty_c128((self._nslots, blk))
+            nv.call("vx_lu_unpack", self._nslots // nsec, nsec, dmax, self._rag_dims.ctypes.data,
+                    self._fac.data_ptr(), pad.data_ptr(), nv.stream_ptr())
+            self._padded_fac = pad
+        return self._padded_fac
 
     def apply(self, x):
         xd, r, flat, is_t, shape = _as_rhs(x, self.grid.n_unknowns)
@@ -413,15 +466,21 @@ class _OneLevelBase:
         """[(dim, count)] of the factors actually stored (and streamed once per
         apply): mirror sharing halves the count, sectors split each block."""
         sec = getattr(self, "_sec", None)
+        nslots = getattr(self, "_nslots", None) or int(self._fac.shape[0])
         if sec is None:
-            return [(self.block_size, int(self._fac.shape[0]))]
-        nk = int(self._fac.shape[0]) // sec.plan.nsec
+            return [(self.block_size, nslots)]
+        nk = nslots // sec.plan.nsec
         return [(d, nk) for d in sec.plan.dims]
 
     @property
     def storage_bytes(self) -> int:
-        """Bytes actually resident on the device for the factors (padded tiles)."""
+        """Bytes actually resident on the device for the factors (ragged, or padded tiles)."""
         return int(self._fac.numel()) * 16
+
+    @property
+    def stored_slots(self) -> int:
+        """Stored factor blocks (sector blocks count separately)."""
+        return getattr(self, "_nslots", None) or int(self._fac.shape[0])
 
     # per logical block (frequency k for the full scheme, kept index for the
     # reduced one): storage slot and whether it is the x-mirror of that slot
@@ -437,7 +496,7 @@ class _OneLevelBase:
     def lu(self) -> np.ndarray:
         if self._sec is not None:
             return self._dense().lu
-        f = self._fac.cpu().numpy()
+        f = self._padded().cpu().numpy()
         pv = self._piv.cpu().numpy()
         n = self.block_size
         base = [_untile(f[s], n) for s in range(f.shape[0])]
@@ -489,6 +548,7 @@ class OneLevelPrec(_OneLevelBase):
             self._n_single = self._n_items
         else:
             self._sector_items(self._store, np.arange(nx), self._flip)
+        self._make_ragged()
 
     @property
     def proxy(self) -> np.ndarray:
@@ -669,7 +729,7 @@ def reduce_one_level(prec: OneLevelPrec, tol: float = 1e-3) -> ReducedOneLevelPr
     fb = None
     if prec._sec is not None:
         fb = lambda: reduce_one_level(prec._dense(), tol)  # noqa: E731
-    return ReducedOneLevelPrec(prec.grid, kept, slot_of, rep, prec._fac.index_select(0, idx),
+    return ReducedOneLevelPrec(prec.grid, kept, slot_of, rep, prec._padded().index_select(0, idx),
                                prec._perm.index_select(0, idx), prec._piv.index_select(0, idx),
                                proxy.copy(), v_hat, float(tol), store, flip, sec=prec._sec, full_builder=fb)
 

@@ -63,6 +63,33 @@ __host__ __device__ __forceinline__ int du_off(int T, int r, int c) {  // r <= c
   return c * (c + 1) / 2 + r;
 }
 
+// Ragged ("packed") factor storage for the pipelined block solve: a block of
+// dimension d keeps only its d x d entries -- tile (i, j) is t_i x t_j with
+// t_i = min(T, d - T i), column-major (ld t_i), at T i d + t_i T j, diagonal
+// tiles split-packed as above with T -> t_i.  Blocks are grouped per stored
+// frequency slot: nsec sector blocks of dims[s] each (kstride = sum dims^2,
+// soff = prefix sums), so the tile padding of the dmax geometry (c1 sectors
+// 187/187/176/176 -> 192) is never streamed.  on = 0: the padded layout.
+struct RagGeom {
+  int on, nsec;
+  int dims[4];
+  long soff[4];
+  long kstride;
+};
+
+// block of work slot `slot`: base pointer and dimension
+__device__ __forceinline__ const double2* rag_block(const LuGeom& g, const RagGeom& rg, const double2* F, int slot,
+                                                   int& nb) {
+  if (!rg.on) {
+    nb = g.n;
+    return F + (long)slot * g.blk;
+  }
+  const int sec = slot % rg.nsec;  // selects, not a dynamic index (keeps rg in registers)
+  nb = sec == 0 ? rg.dims[0] : sec == 1 ? rg.dims[1] : sec == 2 ? rg.dims[2] : rg.dims[3];
+  const long so = sec == 0 ? rg.soff[0] : sec == 1 ? rg.soff[1] : sec == 2 ? rg.soff[2] : rg.soff[3];
+  return F + (long)(slot / rg.nsec) * rg.kstride + so;
+}
+
 // ----------------------------------------------------------------- spectra
 // Generator line l = (p, dz, dy) of a (6, nzz, nyy, *) tensor with strides.
 struct GenLine {
@@ -1101,7 +1128,7 @@ constexpr int PIPE_CONSUMERS = 8;
 
 template <int R>
 __global__ void __launch_bounds__((PIPE_CONSUMERS + 1) * 32)
-    lu_solve_pipe_kernel(LuGeom g, const double2* __restrict__ F, const int* __restrict__ perm,
+    lu_solve_pipe_kernel(LuGeom g, RagGeom rg, const double2* __restrict__ F, const int* __restrict__ perm,
                          const int* __restrict__ items, int item0, int nwork, const int* __restrict__ klist,
                          int nrhs, double2* Y, long s_row, long s_k, int S) {
   extern __shared__ __align__(128) unsigned char smraw[];
@@ -1150,24 +1177,33 @@ __global__ void __launch_bounds__((PIPE_CONSUMERS + 1) * 32)
       for (int w = blockIdx.x; w < nwork; w += gridDim.x) {
       int slot, beg, cnt;
       decode(w, slot, beg, cnt);
-      const double2* Fb = F + (long)slot * g.blk;
+      int nb;
+      const double2* Fb = rag_block(g, rg, F, slot, nb);
+      const int ntb = rg.on ? (nb + T - 1) / T : nt;
       const int nchunks = (cnt * nrhs + R - 1) / R;
       for (int ch = 0; ch < nchunks; ++ch) {
         for (int ph = 0; ph < 2; ++ph) {
-          for (int ii = 0; ii < nt; ++ii) {
-            const int i = ph == 0 ? ii : nt - 1 - ii;
-            const int j0 = ph == 0 ? 0 : i + 1, j1 = ph == 0 ? i : nt;  // off-diagonal range
+          for (int ii = 0; ii < ntb; ++ii) {
+            const int i = ph == 0 ? ii : ntb - 1 - ii;
+            const int j0 = ph == 0 ? 0 : i + 1, j1 = ph == 0 ? i : ntb;  // off-diagonal range
+            const int ti = rg.on ? min(T, nb - T * i) : T;
             for (int j = j0; j <= j1; ++j) {
               const int jj = (j == j1) ? i : j;  // off-diagonals first, diagonal last
               const int s = (int)(t % S);
               const uint32_t use = (uint32_t)(t / S);
               if (use > 0) mbar_wait(empty + s, (use - 1) & 1);
+              const int tj = rg.on ? min(T, nb - T * jj) : T;
+              const double2* tsrc = rg.on ? Fb + (long)T * i * nb + (long)ti * T * jj : Fb + (long)(i * nt + jj) * T2;
               // the diagonal tile: only the half this phase uses (split layout)
-              const double2* src = Fb + (long)(i * nt + jj) * T2 + ((j == j1 && ph == 1) ? dl_n(T) : 0);
-              const uint32_t bytes = (j == j1) ? (uint32_t)((ph == 0 ? dl_n(T) : T2 - dl_n(T)) * sizeof(double2))
-                                               : tile_bytes;
-              mbar_expect_tx(full + s, bytes);
-              bulk_g2s(slots + (long)s * T2, src, bytes, full + s);
+              const double2* src = tsrc + ((j == j1 && ph == 1) ? dl_n(ti) : 0);
+              const uint32_t bytes = (j == j1) ? (uint32_t)((ph == 0 ? dl_n(ti) : ti * ti - dl_n(ti)) * sizeof(double2))
+                                               : (uint32_t)(ti * tj * sizeof(double2));
+              if (bytes) {
+                mbar_expect_tx(full + s, bytes);
+                bulk_g2s(slots + (long)s * T2, src, bytes, full + s);
+              } else {
+                mbar_arrive(full + s);  // 1x1 diagonal: no strictly-lower half
+              }
               ++t;
             }
           }
@@ -1199,10 +1235,13 @@ __global__ void __launch_bounds__((PIPE_CONSUMERS + 1) * 32)
     }
     consumers_sync(NC);
     const int* pm = perm + (long)slot * n;
+    int nb;
+    (void)rag_block(g, rg, F, slot, nb);
+    const int ntb = rg.on ? (nb + T - 1) / T : nt;
     for (int idx = tid; idx < npad * R; idx += NC) {
       const int row = idx / R, rr = idx - row * R;
       double2 v = cmk(0.0, 0.0);
-      if (row < n && rr < nr) {
+      if (row < nb && rr < nr) {
         const long rb = rbase[rr];
         const int pr = pm[row];
         v = cflip(Y[(long)pr * s_row + (rb & ROFF)], flip_row((int)(rb >> 56), pr, q));
@@ -1211,10 +1250,11 @@ __global__ void __launch_bounds__((PIPE_CONSUMERS + 1) * 32)
     }
     consumers_sync(NC);
     for (int ph = 0; ph < 2; ++ph) {
-      for (int ii = 0; ii < nt; ++ii) {
-        const int i = ph == 0 ? ii : nt - 1 - ii;
-        const int j0 = ph == 0 ? 0 : i + 1, j1 = ph == 0 ? i : nt;
+      for (int ii = 0; ii < ntb; ++ii) {
+        const int i = ph == 0 ? ii : ntb - 1 - ii;
+        const int j0 = ph == 0 ? 0 : i + 1, j1 = ph == 0 ? i : ntb;
         const int noff = j1 - j0;
+        const int ti = rg.on ? min(T, nb - T * i) : T;  // rows of this tile row (= ld of its tiles)
         double2 acc[R];
 #pragma unroll
         for (int rr = 0; rr < R; ++rr) acc[rr] = cmk(0.0, 0.0);
@@ -1234,15 +1274,16 @@ __global__ void __launch_bounds__((PIPE_CONSUMERS + 1) * 32)
           const long tq = t + q;
           const int s = (int)(tq % S);
           mbar_wait(full + s, (uint32_t)(tq / S) & 1);
-          if (!dmma && lane < T) {
+          if (!dmma && lane < ti) {
             // every consumer warp takes a column slice of every tile: the
             // tile GEMV is spread over all warps (short per-tile latency, so
             // the few ring slots turn over fast); partial sums meet in red
             const double2* tile = slots + (long)s * T2 + lane;
             const double2* yj = y + (long)(j0 + q) * T * R;
-            const int cpw = (T + NWC - 1) / NWC, c0 = warp * cpw, c1 = min(T, c0 + cpw);
+            const int tj = rg.on ? min(T, nb - T * (j0 + q)) : T;
+            const int cpw = (tj + NWC - 1) / NWC, c0 = warp * cpw, c1 = min(tj, c0 + cpw);
             for (int c = c0; c < c1; ++c) {
-              const double2 a = tile[c * T];
+              const double2 a = tile[c * ti];
 #pragma unroll
               for (int rr = 0; rr < R; ++rr) cfma(acc[rr], a, yj[c * R + rr]);
             }
@@ -1279,13 +1320,13 @@ __global__ void __launch_bounds__((PIPE_CONSUMERS + 1) * 32)
               for (int e = 0; e < 2; ++e)
                 red[(warp * 32 + rb * 8 + r4) * R + 2 * c4 + e] = cmk(cr[rb][e], ci[rb][e]);
           }
-        } else if (lane < T) {
+        } else if (lane < ti) {
 #pragma unroll
           for (int rr = 0; rr < R; ++rr) red[(warp * T + lane) * R + rr] = acc[rr];
         }
         t += noff;
         consumers_sync(NC);
-        for (int idx = tid; idx < T * R; idx += NC) {
+        for (int idx = tid; idx < ti * R; idx += NC) {
           const int r = idx / R, rr = idx - r * R;
           double2 z = y[(long)(i * T + r) * R + rr];
           for (int w = 0; w < NWC; ++w) z = csub(z, red[(w * T + r) * R + rr]);
@@ -1296,18 +1337,18 @@ __global__ void __launch_bounds__((PIPE_CONSUMERS + 1) * 32)
           const int s = (int)(t % S);
           mbar_wait(full + s, (uint32_t)(t / S) & 1);
           const double2* Ds = slots + (long)s * T2;
-          for (int idx = tid; idx < T * R; idx += NC) {
+          for (int idx = tid; idx < ti * R; idx += NC) {
             const int r = idx / R, rr = idx - r * R;
             double2 o;
             if (ph == 0) {
               o = zb[idx];
-              for (int c = 0, oc = r - 1; c < r; ++c) {  // oc = dl_off(T, r, c)
+              for (int c = 0, oc = r - 1; c < r; ++c) {  // oc = dl_off(ti, r, c)
                 cfma(o, Ds[oc], zb[c * R + rr]);
-                oc += T - c - 2;
+                oc += ti - c - 2;
               }
             } else {
               o = cmk(0.0, 0.0);
-              for (int c = r, ou = du_off(T, r, r); c < T; ++c) {  // ou = du_off(T, r, c)
+              for (int c = r, ou = du_off(ti, r, r); c < ti; ++c) {  // ou = du_off(ti, r, c)
                 cfma(o, Ds[ou], zb[c * R + rr]);
                 ou += c + 1;
               }
@@ -1320,7 +1361,7 @@ __global__ void __launch_bounds__((PIPE_CONSUMERS + 1) * 32)
         }
       }
     }
-    for (int idx = tid; idx < n * R; idx += NC) {
+    for (int idx = tid; idx < nb * R; idx += NC) {
       const int row = idx / R, rr = idx - row * R;
       if (rr < nr) {
         const long rb = rbase[rr];
@@ -1330,6 +1371,87 @@ __global__ void __launch_bounds__((PIPE_CONSUMERS + 1) * 32)
     consumers_sync(NC);
   }
   }
+}
+
+// padded factor blocks (dmax geometry, split diagonal tiles) -> ragged blocks
+// of the sector dimensions (leading d_s x d_s: the identity padding of a
+// smaller sector decouples from its LU, so its leading factors are exact)
+__global__ void __launch_bounds__(256) lu_repack_kernel(LuGeom g, RagGeom rg, const double2* __restrict__ P,
+                                                        double2* __restrict__ Q) {
+  const int slot = blockIdx.y;
+  int nb;
+  double2* dst = const_cast<double2*>(rag_block(g, rg, Q, slot, nb));
+  const double2* src = P + (long)slot * g.blk;
+  const int T = g.T;
+  const long tot = (long)nb * nb;
+  for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < tot; e += (long)gridDim.x * blockDim.x) {
+    const int c = (int)(e / nb), r = (int)(e - (long)c * nb);
+    const int i = r / T, j = c / T, rr = r - i * T, cc = c - j * T;
+    const int ti = min(T, nb - T * i);
+    const long dtile = (long)T * i * nb + (long)ti * T * j;
+    const long stile = (long)(i * g.nt + j) * T * T;
+    long so, d;
+    if (i != j) {
+      so = stile + (long)cc * T + rr;
+      d = dtile + (long)cc * ti + rr;
+    } else if (rr > cc) {
+      so = stile + dl_off(T, rr, cc);
+      d = dtile + dl_off(ti, rr, cc);
+    } else {
+      so = stile + dl_n(T) + du_off(T, rr, cc);
+      d = dtile + dl_n(ti) + du_off(ti, rr, cc);
+    }
+    dst[d] = src[so];
+  }
+}
+
+// inverse of lu_repack_kernel: every entry of the padded block is written
+// (identity factors on the padding: inv(U) diagonal 1, everything else 0)
+__global__ void __launch_bounds__(256) lu_unpack_kernel(LuGeom g, RagGeom rg, const double2* __restrict__ Q,
+                                                        double2* __restrict__ P) {
+  const int slot = blockIdx.y;
+  int nb;
+  const double2* src = rag_block(g, rg, Q, slot, nb);
+  double2* dst = P + (long)slot * g.blk;
+  const int T = g.T, np = g.npad;
+  const long tot = (long)np * np;
+  for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < tot; e += (long)gridDim.x * blockDim.x) {
+    const int c = (int)(e / np), r = (int)(e - (long)c * np);
+    const int i = r / T, j = c / T, rr = r - i * T, cc = c - j * T;
+    const long stile = (long)(i * g.nt + j) * T * T;
+    const bool in = r < nb && c < nb;
+    const int ti = in ? min(T, nb - T * i) : T;
+    const long dtile = (long)T * i * nb + (long)ti * T * j;
+    long po, qo;
+    if (i != j) {
+      po = stile + (long)cc * T + rr;
+      qo = dtile + (long)cc * ti + rr;
+    } else if (rr > cc) {
+      po = stile + dl_off(T, rr, cc);
+      qo = dtile + dl_off(ti, rr, cc);
+    } else {
+      po = stile + dl_n(T) + du_off(T, rr, cc);
+      qo = dtile + dl_n(ti) + du_off(ti, rr, cc);
+    }
+    dst[po] = in ? src[qo] : cmk(r == c ? 1.0 : 0.0, 0.0);
+  }
+}
+
+static int make_rag(int nsec, const int* dims, int dmax, RagGeom* rg) {
+  VX_REQUIRE(nsec >= 1 && nsec <= 4 && dims, "ragged geometry needs 1..4 sector dims");
+  rg->on = 1;
+  rg->nsec = nsec;
+  long off = 0;
+  for (int s = 0; s < 4; ++s) {
+    rg->dims[s] = s < nsec ? dims[s] : 0;
+    rg->soff[s] = off;
+    if (s < nsec) {
+      VX_REQUIRE(dims[s] >= 1 && dims[s] <= dmax, "sector dim %d out of range (dmax %d)", dims[s], dmax);
+      off += (long)dims[s] * dims[s];
+    }
+  }
+  rg->kstride = off;
+  return VX_OK;
 }
 
 // ------------------------------------------------------ single-tile blocks
@@ -1400,7 +1522,10 @@ static int launch_solve_small(const LuGeom& g, const double2* F, const int* perm
 template <int R>
 static int launch_solve_pipe(const LuGeom& g, const double2* F, const int* perm, const int* items,
                              int item0, int nblocks, const int* klist, int nrhs, double2* Y, long s_row,
-                             long s_k, cudaStream_t s, int persist_per_sm = 0) {
+                             long s_k, cudaStream_t s, int persist_per_sm = 0, const RagGeom* rgp = nullptr) {
+  RagGeom rg{};
+  if (rgp) rg = *rgp;
+  VX_REQUIRE(!(rg.on && R == 8), "ragged factor storage has no multi-RHS (DMMA) solve");
   if (nblocks <= 0) return VX_OK;
   const size_t tile = (size_t)g.T * g.T * sizeof(double2);
   const size_t fixed = ((size_t)g.npad * R + (size_t)PIPE_CONSUMERS * g.T * R + (size_t)g.T * R) *
@@ -1421,8 +1546,8 @@ static int launch_solve_pipe(const LuGeom& g, const double2* F, const int* perm,
   VX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int grid = nblocks;
   if (persist_per_sm > 0 && grid > persist_per_sm * device_sm_count()) grid = persist_per_sm * device_sm_count();
-  kern<<<grid, (PIPE_CONSUMERS + 1) * 32, smem, s>>>(g, F, perm, items, item0, nblocks, klist, nrhs, Y, s_row,
-                                                     s_k, S);
+  kern<<<grid, (PIPE_CONSUMERS + 1) * 32, smem, s>>>(g, rg, F, perm, items, item0, nblocks, klist, nrhs, Y,
+                                                     s_row, s_k, S);
   VX_CHECK_LAUNCH("lu_solve_pipe_kernel");
   return VX_OK;
 }
@@ -1451,11 +1576,20 @@ __global__ void cols_copy_kernel(long nrows, double2* A, long lda, int P, const 
 // each, the rest multi-RHS).  vx_solve_variant(1) selects the synchronous kernel.
 static int solve_items(const LuGeom& g, const double2* F, const int* perm, const int* items, int n_single,
                        int n_items, const int* klist, int nrhs, double2* Y, long s_row, long s_k, cudaStream_t s,
-                       int persist = -1, int direct_r = 1) {
+                       int persist = -1, int direct_r = 1, const RagGeom* rg = nullptr) {
   int st;
   Span span("prec_solve", s);
   static const int persist_env = env_int("VX_PIPE_PERSIST", 0);
   if (persist < 0) persist = persist_env;
+  if (rg && rg->on) {
+    VX_REQUIRE(g.nt > 1 && !g_solve_classic && nrhs == 1 && n_items == n_single,
+               "ragged factors: single-RHS pipelined solves only");
+    if (direct_r == 2)
+      return launch_solve_pipe<2>(g, F, perm, items, 0, n_single, klist, 1, Y, s_row, s_k, s, persist, rg);
+    if (direct_r == 4)
+      return launch_solve_pipe<4>(g, F, perm, items, 0, n_single, klist, 1, Y, s_row, s_k, s, persist, rg);
+    return launch_solve_pipe<1>(g, F, perm, items, 0, n_single, klist, 1, Y, s_row, s_k, s, persist, rg);
+  }
   if (g.nt == 1 && !g_solve_classic)
     return launch_solve_small(g, F, perm, items, 0, n_items, klist, nrhs, Y, s_row, s_k, s);
   const bool pipe = g.nt > 1 && !g_solve_classic;
@@ -1781,10 +1915,9 @@ extern "C" long vx_prec1_work_elems(int nx, int ny, int nz, int nrhs) {
   return 3L * nx * ny * nz * nrhs;
 }
 
-extern "C" int vx_prec1_apply(int nx, int ny, int nz, int nrhs, const vx_c128* factors,
-                              const int* perm, const int* items, int n_single, int n_items, int direct_r,
-                              const int* klist, const vx_c128* x, vx_c128* y, vx_c128* work,
-                              void* stream) {
+static int prec1_apply(int nx, int ny, int nz, int nrhs, const vx_c128* factors, const int* perm,
+                       const int* items, int n_single, int n_items, int direct_r, const int* klist,
+                       const vx_c128* x, vx_c128* y, vx_c128* work, void* stream, const RagGeom* rg) {
   VX_REQUIRE(nx >= 1 && ny >= 1 && nz >= 1 && nrhs >= 1, "bad 1-level apply arguments");
   VX_REQUIRE(direct_r == 1 || direct_r == 2, "direct_r must be 1 or 2");
   VX_REQUIRE(n_single >= 0 && n_items >= n_single, "bad work list");
@@ -1803,7 +1936,7 @@ extern "C" int vx_prec1_apply(int nx, int ny, int nz, int nrhs, const vx_c128* f
   }
   LuGeom g = lu_geom(q3);
   const double2* F = reinterpret_cast<const double2*>(factors);
-  if ((st = solve_items(g, F, perm, items, n_single, n_items, klist, nrhs, S, pitch, nrhs, s, -1, direct_r)))
+  if ((st = solve_items(g, F, perm, items, n_single, n_items, klist, nrhs, S, pitch, nrhs, s, -1, direct_r, rg)))
     return st;
   {
     LoadStrided ld{S, {pitch, 1, nrhs, nrhs}};
@@ -2085,12 +2218,12 @@ extern "C" long vx_prec1_sec_work_elems(int nx, int ny, int nz, int nrhs, int ns
   return (3L * ny * nz + (long)nsec * dmax) * nx * nrhs;
 }
 
-extern "C" int vx_prec1_apply_sec(int nx, int ny, int nz, int nrhs, const vx_c128* factors, const int* perm,
-                                  const int* items, int n_single, int n_items, int direct_r, const int* klist,
-                                  int nsec, int dmax,
-                                  int norb, const int* orows, const int* osec, const double* ocoef,
-                                  const unsigned char* flipk, const vx_c128* x, vx_c128* y, vx_c128* work,
-                                  void* stream) {
+static int prec1_apply_sec(int nx, int ny, int nz, int nrhs, const vx_c128* factors, const int* perm,
+                           const int* items, int n_single, int n_items, int direct_r, const int* klist,
+                           int nsec, int dmax,
+                           int norb, const int* orows, const int* osec, const double* ocoef,
+                           const unsigned char* flipk, const vx_c128* x, vx_c128* y, vx_c128* work,
+                           void* stream, const RagGeom* rg) {
   VX_REQUIRE(nx >= 1 && ny >= 1 && nz >= 1 && nrhs >= 1 && n_single >= 0 && n_items >= n_single && nsec >= 1 &&
                  dmax >= 1,
              "bad sector apply arguments");
@@ -2113,7 +2246,7 @@ extern "C" int vx_prec1_apply_sec(int nx, int ny, int nz, int nrhs, const vx_c12
   VX_CUDA(cudaMemsetAsync(U, 0, sizeof(double2) * (size_t)nsec * dmax * pitch, s));
   if ((st = sec_xform(pitch, nrhs, norb, orows, osec, ocoef, flipk, q, S, U, 0, s))) return st;
   if ((st = solve_items(lu_geom(dmax), reinterpret_cast<const double2*>(factors), perm, items, n_single, n_items,
-                        klist, nrhs, U, pitch, nrhs, s, -1, direct_r)))
+                        klist, nrhs, U, pitch, nrhs, s, -1, direct_r, rg)))
     return st;
   if ((st = sec_xform(pitch, nrhs, norb, orows, osec, ocoef, flipk, q, U, S, 1, s))) return st;
   {
@@ -2123,3 +2256,87 @@ extern "C" int vx_prec1_apply_sec(int nx, int ny, int nz, int nrhs, const vx_c12
   }
   return VX_OK;
 }
+
+extern "C" int vx_prec1_apply_sec(int nx, int ny, int nz, int nrhs, const vx_c128* factors, const int* perm,
+                                  const int* items, int n_single, int n_items, int direct_r, const int* klist,
+                                  int nsec, int dmax,
+                                  int norb, const int* orows, const int* osec, const double* ocoef,
+                                  const unsigned char* flipk, const vx_c128* x, vx_c128* y, vx_c128* work,
+                                  void* stream) {
+  return prec1_apply_sec(nx, ny, nz, nrhs, factors, perm, items, n_single, n_items, direct_r, klist, nsec, dmax,
+                         norb, orows, osec, ocoef, flipk, x, y, work, stream, nullptr);
+}
+
+extern "C" int vx_prec1_apply_sec_rag(int nx, int ny, int nz, int nrhs, const vx_c128* factors, const int* perm,
+                                      const int* items, int n_single, int n_items, int direct_r,
+                                      const int* klist, int nsec, int dmax, const int* sec_dims, int norb,
+                                      const int* orows, const int* osec, const double* ocoef,
+                                      const unsigned char* flipk, const vx_c128* x, vx_c128* y, vx_c128* work,
+                                      void* stream) {
+  RagGeom rg;
+  int st = make_rag(nsec, sec_dims, dmax, &rg);
+  if (st) return st;
+  return prec1_apply_sec(nx, ny, nz, nrhs, factors, perm, items, n_single, n_items, direct_r, klist, nsec, dmax,
+                         norb, orows, osec, ocoef, flipk, x, y, work, stream, &rg);
+}
+
+extern "C" long vx_lu_rag_stride(int nsec, const int* sec_dims) {
+  long k = 0;
+  for (int s = 0; s < nsec; ++s) k += (long)sec_dims[s] * sec_dims[s];
+  return k;
+}
+
+extern "C" int vx_lu_repack(int nkslots, int nsec, int dmax, const int* sec_dims, const vx_c128* padded,
+                            vx_c128* ragged, void* stream) {
+  VX_REQUIRE(nkslots >= 0, "bad repack arguments");
+  RagGeom rg;
+  int st = make_rag(nsec, sec_dims, dmax, &rg);
+  if (st) return st;
+  if (nkslots == 0) return VX_OK;
+  const LuGeom g = lu_geom(dmax);
+  VX_REQUIRE(g.nt > 1, "ragged storage is for multi-tile blocks (dmax > 32)");
+  const long per = (long)dmax * dmax;
+  dim3 grid(div_up(per, 256 * 4) > 0 ? div_up(per, 256 * 4) : 1, nkslots * nsec);
+  lu_repack_kernel<<<grid, 256, 0, as_stream(stream)>>>(g, rg, reinterpret_cast<const double2*>(padded),
+                                                        reinterpret_cast<double2*>(ragged));
+  VX_CHECK_LAUNCH("lu_repack_kernel");
+  return VX_OK;
+}
+
+extern "C" int vx_prec1_apply(int nx, int ny, int nz, int nrhs, const vx_c128* factors,
+                              const int* perm, const int* items, int n_single, int n_items, int direct_r,
+                              const int* klist, const vx_c128* x, vx_c128* y, vx_c128* work,
+                              void* stream) {
+  return prec1_apply(nx, ny, nz, nrhs, factors, perm, items, n_single, n_items, direct_r, klist, x, y, work,
+                     stream, nullptr);
+}
+
+extern "C" int vx_prec1_apply_rag(int nx, int ny, int nz, int nrhs, const vx_c128* factors,
+                                  const int* perm, const int* items, int n_single, int n_items, int direct_r,
+                                  const int* klist, const vx_c128* x, vx_c128* y, vx_c128* work,
+                                  void* stream) {
+  RagGeom rg;
+  const int d = 3 * ny * nz;
+  int st = make_rag(1, &d, d, &rg);
+  if (st) return st;
+  return prec1_apply(nx, ny, nz, nrhs, factors, perm, items, n_single, n_items, direct_r, klist, x, y, work,
+                     stream, &rg);
+}
+
+extern "C" int vx_lu_unpack(int nkslots, int nsec, int dmax, const int* sec_dims, const vx_c128* ragged,
+                            vx_c128* padded, void* stream) {
+  VX_REQUIRE(nkslots >= 0, "bad unpack arguments");
+  RagGeom rg;
+  int st = make_rag(nsec, sec_dims, dmax, &rg);
+  if (st) return st;
+  if (nkslots == 0) return VX_OK;
+  const LuGeom g = lu_geom(dmax);
+  VX_REQUIRE(g.nt > 1, "ragged storage is for multi-tile blocks (dmax > 32)");
+  dim3 grid(div_up(g.blk, 256 * 4) > 0 ? div_up(g.blk, 256 * 4) : 1, nkslots * nsec);
+  lu_unpack_kernel<<<grid, 256, 0, as_stream(stream)>>>(g, rg, reinterpret_cast<const double2*>(ragged),
+                                                        reinterpret_cast<double2*>(padded));
+  VX_CHECK_LAUNCH("lu_unpack_kernel");
+  return VX_OK;
+}
+
+extern "C" int vx_solve_classic(void) { return vx::g_solve_classic; }

@@ -46,7 +46,7 @@ def test_one_level_mirror_equals_unshared(rng, C, monkeypatch, dims):
     nx = dims[0]
     assert p.mirror_shared == (nx > 2)
     assert not q.mirror_shared
-    assert p._fac.shape[0] == (nx // 2 + 1) * p.sectors and q._fac.shape[0] == nx * q.sectors
+    assert p.stored_slots == (nx // 2 + 1) * p.sectors and q.stored_slots == nx * q.sectors
     assert p.bytes == q.bytes  # the reference's accounting is unchanged
     n = W.grid.n_unknowns
     for r in (None, 3):
@@ -129,7 +129,7 @@ def test_asymmetric_kernel_is_not_shared(rng, C):
     kern = ToeplitzKernel(VoxelGrid(*dims, 0.05), 2 * np.pi, t)
     m = np.full((2, 3, 6), 0.5 + 0.1j)
     p = C.build_one_level(kern, m)
-    assert not p.mirror_shared and p._fac.shape[0] == 6
+    assert not p.mirror_shared and p.stored_slots == 6
     ref = O.build_one_level(t, dims, m)
     x = random_field(rng, 3 * 36)
     assert relerr(p.apply(x), O.apply_prec(ref, x)) < 1e-10

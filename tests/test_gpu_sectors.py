@@ -63,7 +63,7 @@ def test_sectors_equal_dense_blocks(rng, C, monkeypatch, dims, sy, sz, nsec):
     if nsec > 1:
         sb = p.stored_blocks
         assert sum(d for d, _ in sb) == p.block_size
-        assert sum(d * d * c for d, c in sb) < 0.6 * p.block_size ** 2 * q._fac.shape[0]
+        assert sum(d * d * c for d, c in sb) < 0.6 * p.block_size ** 2 * q.stored_slots
 
 
 def test_sectors_without_mirror(rng, C, monkeypatch):
