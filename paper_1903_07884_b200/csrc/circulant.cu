@@ -62,6 +62,10 @@ __host__ __device__ __forceinline__ int dl_off(int T, int r, int c) {  // r > c
 __host__ __device__ __forceinline__ int du_off(int T, int r, int c) {  // r <= c, relative to the U half
   return c * (c + 1) / 2 + r;
 }
+// row-packed halves of the ragged layout (vx_lu_repack): L row r at r(r-1)/2,
+// U row r (columns r..t-1) at r t - r(r-1)/2
+__host__ __device__ __forceinline__ int lrow_off(int r) { return r * (r - 1) / 2; }           // L half, row r
+__host__ __device__ __forceinline__ int urow_off(int t, int r) { return r * t - r * (r - 1) / 2; }  // U half, row r
 
 // Ragged ("packed") factor storage for the pipelined block solve: a block of
 // dimension d keeps only its d x d entries -- tile (i, j) is t_i x t_j with
@@ -1393,13 +1397,13 @@ __global__ void __launch_bounds__(256) lu_repack_kernel(LuGeom g, RagGeom rg, co
     long so, d;
     if (i != j) {
       so = stile + (long)cc * T + rr;
-      d = dtile + (long)cc * ti + rr;
+      d = dtile + (long)rr * min(T, nb - T * j) + cc;
     } else if (rr > cc) {
       so = stile + dl_off(T, rr, cc);
-      d = dtile + dl_off(ti, rr, cc);
+      d = dtile + lrow_off(rr) + cc;
     } else {
       so = stile + dl_n(T) + du_off(T, rr, cc);
-      d = dtile + dl_n(ti) + du_off(ti, rr, cc);
+      d = dtile + dl_n(ti) + urow_off(ti, rr) + (cc - rr);
     }
     dst[d] = src[so];
   }
@@ -1425,13 +1429,13 @@ __global__ void __launch_bounds__(256) lu_unpack_kernel(LuGeom g, RagGeom rg, co
     long po, qo;
     if (i != j) {
       po = stile + (long)cc * T + rr;
-      qo = dtile + (long)cc * ti + rr;
+      qo = dtile + (long)rr * (in ? min(T, nb - T * j) : T) + cc;
     } else if (rr > cc) {
       po = stile + dl_off(T, rr, cc);
-      qo = dtile + dl_off(ti, rr, cc);
+      qo = dtile + lrow_off(rr) + cc;
     } else {
       po = stile + dl_n(T) + du_off(T, rr, cc);
-      qo = dtile + dl_n(ti) + du_off(ti, rr, cc);
+      qo = dtile + dl_n(ti) + urow_off(ti, rr) + (cc - rr);
     }
     dst[po] = in ? src[qo] : cmk(r == c ? 1.0 : 0.0, 0.0);
   }
@@ -1451,6 +1455,251 @@ static int make_rag(int nsec, const int* dims, int dmax, RagGeom* rg) {
     }
   }
   rg->kstride = off;
+  return VX_OK;
+}
+
+// ------------------------------------------- pipelined solve, ragged blocks
+// The same producer / ring as lu_solve_pipe_kernel, but the ragged tiles are
+// ROW-major (vx_lu_repack) and every consumer warp owns 4 rows of each tile:
+// lane = 8 * row_in_warp + column_group, columns cg, cg + 8, cg + 16, cg + 24
+// (consecutive lanes -> consecutive addresses: conflict-free).  A row's sum is
+// finished with three xor-shuffles inside the warp, so there is no cross-warp
+// reduction buffer; the diagonal products (row-packed inv(L_ii) / inv(U_ii))
+// are spread the same way over all 256 consumer threads.  Two consumer
+// barriers per tile row (the unpadded rows of zb, then of y).
+
+template <int R>
+__global__ void __launch_bounds__((PIPE_CONSUMERS + 1) * 32, 4)
+    lu_solve_rag_kernel(LuGeom g, RagGeom rg, const double2* __restrict__ F, const int* __restrict__ perm,
+                        const int* __restrict__ items, int item0, int nwork, const int* __restrict__ klist,
+                        double2* Y, long s_row, long s_k, int S) {
+  extern __shared__ __align__(128) unsigned char smraw[];
+  constexpr int NWC = PIPE_CONSUMERS;
+  constexpr int NC = NWC * 32;
+  const int T = g.T, T2 = T * T, npad = g.npad, n = g.n, q = n / 3;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smraw);
+  uint64_t* empty = full + S;
+  long* rbase = reinterpret_cast<long*>(empty + S);
+  double2* slots = reinterpret_cast<double2*>(smraw + ((2 * S + R) * 8 + 127) / 128 * 128);
+  double2* y = slots + (long)S * T2;  // [R][npad]
+  double2* zb = y + (long)npad * R;   // [R][T]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  auto decode = [&](int w, int& slot, int& beg, int& cnt) {
+    const int it = item0 + w;
+    slot = items[3 * it];
+    beg = items[3 * it + 1];
+    cnt = items[3 * it + 2];
+  };
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(full + s, 1);
+      mbar_init(empty + s, NWC);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp == NWC) {
+    if (lane == 0) {
+      long t = 0;
+      for (int w = blockIdx.x; w < nwork; w += gridDim.x) {
+        int slot, beg, cnt;
+        decode(w, slot, beg, cnt);
+        int nb;
+        const double2* Fb = rag_block(g, rg, F, slot, nb);
+        const int ntb = (nb + T - 1) / T;
+        const int nchunks = (cnt + R - 1) / R;
+        for (int ch = 0; ch < nchunks; ++ch) {
+          for (int ph = 0; ph < 2; ++ph) {
+            for (int ii = 0; ii < ntb; ++ii) {
+              const int i = ph == 0 ? ii : ntb - 1 - ii;
+              const int j0 = ph == 0 ? 0 : i + 1, j1 = ph == 0 ? i : ntb;
+              const int ti = min(T, nb - T * i);
+              for (int j = j0; j <= j1; ++j) {
+                const int jj = (j == j1) ? i : j;
+                const int s = (int)(t % S);
+                const uint32_t use = (uint32_t)(t / S);
+                if (use > 0) mbar_wait(empty + s, (use - 1) & 1);
+                const int tj = min(T, nb - T * jj);
+                const double2* tsrc = Fb + (long)T * i * nb + (long)ti * T * jj;
+                const double2* src = tsrc + ((j == j1 && ph == 1) ? dl_n(ti) : 0);
+                const uint32_t bytes = (j == j1) ? (uint32_t)((ph == 0 ? dl_n(ti) : ti * ti - dl_n(ti)) * sizeof(double2))
+                                                 : (uint32_t)(ti * tj * sizeof(double2));
+                if (bytes) {
+                  mbar_expect_tx(full + s, bytes);
+                  bulk_g2s(slots + (long)s * T2, src, bytes, full + s);
+                } else {
+                  mbar_arrive(full + s);
+                }
+                ++t;
+              }
+            }
+          }
+        }
+      }
+    }
+    return;
+  }
+
+  long t = 0;
+  const int rw = lane >> 3, cg = lane & 7;
+  const int r = 4 * warp + rw;  // tile row owned by this lane group
+  for (int w = blockIdx.x; w < nwork; w += gridDim.x) {
+    int slot, beg, cnt;
+    decode(w, slot, beg, cnt);
+    int nb;
+    (void)rag_block(g, rg, F, slot, nb);
+    const int ntb = (nb + T - 1) / T;
+    const int* pm = perm + (long)slot * n;
+    const int nchunks = (cnt + R - 1) / R;
+    for (int ch = 0; ch < nchunks; ++ch) {
+      const int rho0 = ch * R;
+      const int nr = min(R, cnt - rho0);
+      if (tid < R) {
+        long b = 0;
+        if (tid < nr) {
+          const int kraw = klist ? klist[beg + rho0 + tid] : beg + rho0 + tid;
+          b = rhs_base(kraw, rho0 + tid, 1, s_k);
+        }
+        rbase[tid] = b;
+      }
+      consumers_sync(NC);
+      for (int idx = tid; idx < npad * R; idx += NC) {
+        const int rr = idx / npad, row = idx - rr * npad;
+        double2 v = cmk(0.0, 0.0);
+        if (row < nb && rr < nr) {
+          const long rb = rbase[rr];
+          const int pr = pm[row];
+          v = cflip(Y[(long)pr * s_row + (rb & ROFF)], flip_row((int)(rb >> 56), pr, q));
+        }
+        y[idx] = v;
+      }
+      consumers_sync(NC);
+      for (int ph = 0; ph < 2; ++ph) {
+        for (int ii = 0; ii < ntb; ++ii) {
+          const int i = ph == 0 ? ii : ntb - 1 - ii;
+          const int j0 = ph == 0 ? 0 : i + 1, j1 = ph == 0 ? i : ntb;
+          const int noff = j1 - j0;
+          const int ti = min(T, nb - T * i);
+          const bool mine = r < ti;
+          double2 acc[R];
+#pragma unroll
+          for (int rr = 0; rr < R; ++rr) acc[rr] = cmk(0.0, 0.0);
+          for (int qq = 0; qq < noff; ++qq) {
+            const long tq = t + qq;
+            const int s = (int)(tq % S);
+            mbar_wait(full + s, (uint32_t)(tq / S) & 1);
+            const int j = j0 + qq;
+            const int tj = min(T, nb - T * j);
+            if (mine) {
+              const double2* arow = slots + (long)s * T2 + r * tj;
+              const double2* yj = y + T * j;
+#pragma unroll
+              for (int m = 0; m < 4; ++m) {
+                const int c = cg + 8 * m;
+                if (c < tj) {
+                  const double2 a = arow[c];
+#pragma unroll
+                  for (int rr = 0; rr < R; ++rr) cfma(acc[rr], a, yj[rr * npad + c]);
+                }
+              }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(empty + s);
+          }
+          t += noff;
+#pragma unroll
+          for (int rr = 0; rr < R; ++rr)
+#pragma unroll
+            for (int o = 1; o < 8; o <<= 1) {
+              acc[rr].x += __shfl_xor_sync(0xffffffffu, acc[rr].x, o);
+              acc[rr].y += __shfl_xor_sync(0xffffffffu, acc[rr].y, o);
+            }
+          if (mine && cg == 0)
+#pragma unroll
+            for (int rr = 0; rr < R; ++rr) zb[rr * T + r] = csub(y[rr * npad + T * i + r], acc[rr]);
+          consumers_sync(NC);
+          {
+            const int s = (int)(t % S);
+            mbar_wait(full + s, (uint32_t)(t / S) & 1);
+            const double2* Ds = slots + (long)s * T2;
+            double2 o[R];
+#pragma unroll
+            for (int rr = 0; rr < R; ++rr) o[rr] = cmk(0.0, 0.0);
+            if (mine) {
+              if (ph == 0) {
+                const double2* Lr = Ds + lrow_off(r);
+#pragma unroll
+                for (int m = 0; m < 4; ++m) {
+                  const int c = cg + 8 * m;
+                  if (c < r) {
+                    const double2 a = Lr[c];
+#pragma unroll
+                    for (int rr = 0; rr < R; ++rr) cfma(o[rr], a, zb[rr * T + c]);
+                  }
+                }
+              } else {
+                const double2* Ur = Ds + urow_off(ti, r) - r;
+#pragma unroll
+                for (int m = 0; m < 4; ++m) {
+                  const int c = cg + 8 * m;
+                  if (c >= r && c < ti) {
+                    const double2 a = Ur[c];
+#pragma unroll
+                    for (int rr = 0; rr < R; ++rr) cfma(o[rr], a, zb[rr * T + c]);
+                  }
+                }
+              }
+            }
+#pragma unroll
+            for (int rr = 0; rr < R; ++rr)
+#pragma unroll
+              for (int o2 = 1; o2 < 8; o2 <<= 1) {
+                o[rr].x += __shfl_xor_sync(0xffffffffu, o[rr].x, o2);
+                o[rr].y += __shfl_xor_sync(0xffffffffu, o[rr].y, o2);
+              }
+            if (mine && cg == 0)
+#pragma unroll
+              for (int rr = 0; rr < R; ++rr)
+                y[rr * npad + T * i + r] = ph == 0 ? cadd(zb[rr * T + r], o[rr]) : o[rr];
+            __syncwarp();
+            if (lane == 0) mbar_arrive(empty + s);
+            consumers_sync(NC);
+            t += 1;
+          }
+        }
+      }
+      for (int idx = tid; idx < nb * R; idx += NC) {
+        const int rr = idx / nb, row = idx - rr * nb;
+        if (rr < nr) {
+          const long rb = rbase[rr];
+          Y[(long)row * s_row + (rb & ROFF)] = cflip(y[rr * npad + row], flip_row((int)(rb >> 56), row, q));
+        }
+      }
+      consumers_sync(NC);
+    }
+  }
+}
+
+template <int R>
+static int launch_solve_rag(const LuGeom& g, const RagGeom& rg, const double2* F, const int* perm, const int* items,
+                            int nblocks, const int* klist, double2* Y, long s_row, long s_k, cudaStream_t s) {
+  if (nblocks <= 0) return VX_OK;
+  const size_t tile = (size_t)g.T * g.T * sizeof(double2);
+  const size_t fixed = ((size_t)g.npad * R + (size_t)g.T * R) * sizeof(double2);
+  // a 2-slot ring and as many CTAs per SM as fit (4 for sector-sized blocks):
+  // more independent blocks in flight beat a deeper ring (c1: 0.93 ms with
+  // 4 CTAs x 2 slots vs 1.01 ms with 3 x 4; c2: 1.10 vs 1.26 ms with 2 x 6)
+  static const int slots_env = env_int("VX_RAG_SLOTS", 2);
+  int S = slots_env;
+  if (S > 16) S = 16;
+  VX_REQUIRE(S >= 2, "block size %d too large for the ragged solve", g.n);
+  const size_t smem = (((size_t)2 * S + R) * 8 + 127) / 128 * 128 + (size_t)S * tile + fixed;
+  auto kern = lu_solve_rag_kernel<R>;
+  VX_REQUIRE((int)smem + 1024 <= device_smem_optin(), "ragged solve smem %zu too large", smem);
+  VX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  kern<<<nblocks, (PIPE_CONSUMERS + 1) * 32, smem, s>>>(g, rg, F, perm, items, 0, nblocks, klist, Y, s_row, s_k, S);
+  VX_CHECK_LAUNCH("lu_solve_rag_kernel");
   return VX_OK;
 }
 
@@ -1584,11 +1833,11 @@ static int solve_items(const LuGeom& g, const double2* F, const int* perm, const
   if (rg && rg->on) {
     VX_REQUIRE(g.nt > 1 && !g_solve_classic && nrhs == 1 && n_items == n_single,
                "ragged factors: single-RHS pipelined solves only");
-    if (direct_r == 2)
-      return launch_solve_pipe<2>(g, F, perm, items, 0, n_single, klist, 1, Y, s_row, s_k, s, persist, rg);
-    if (direct_r == 4)
-      return launch_solve_pipe<4>(g, F, perm, items, 0, n_single, klist, 1, Y, s_row, s_k, s, persist, rg);
-    return launch_solve_pipe<1>(g, F, perm, items, 0, n_single, klist, 1, Y, s_row, s_k, s, persist, rg);
+    (void)persist;
+    VX_REQUIRE(items, "ragged solves take a work list");
+    if (direct_r == 2) return launch_solve_rag<2>(g, *rg, F, perm, items, n_single, klist, Y, s_row, s_k, s);
+    if (direct_r == 4) return launch_solve_rag<4>(g, *rg, F, perm, items, n_single, klist, Y, s_row, s_k, s);
+    return launch_solve_rag<1>(g, *rg, F, perm, items, n_single, klist, Y, s_row, s_k, s);
   }
   if (g.nt == 1 && !g_solve_classic)
     return launch_solve_small(g, F, perm, items, 0, n_items, klist, nrhs, Y, s_row, s_k, s);
