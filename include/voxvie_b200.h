@@ -254,6 +254,10 @@ int vx_arnoldi_step(long n, int nvec, const vx_c128* V, long ldv, vx_c128* w, vx
 /* solver.py:110 -- u = sum_i y_i V_i. */
 int vx_basis_combine(long n, int nvec, const vx_c128* V, long ldv, const vx_c128* y, vx_c128* u,
                      void* stream);
+/* The same with the basis vectors given by a device array of nvec pointers
+ * (each a (n,) complex128 vector): GMRES keeps z_j = P^-1 v_j where the
+ * preconditioner wrote it (reference solver.py:106-110, 160-161). */
+int vx_basis_combine_ptrs(long n, int nvec, const void* zptrs, const vx_c128* y, vx_c128* u, void* stream);
 /* Vector helpers: out = a*x + b*y ; norm2 -> dots[0].re (deterministic). */
 int vx_axpby(long n, vx_c128 a, const vx_c128* x, vx_c128 b, const vx_c128* y, vx_c128* out,
              void* stream);

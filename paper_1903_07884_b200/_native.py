@@ -70,6 +70,7 @@ _SIGS = {
     "vx_box_scatter": (c_int, [c_int] * 10 + [P, P, P]),
     "vx_arnoldi_part_elems": (c_long, [c_long, c_int]),
     "vx_arnoldi_step": (c_int, [c_long, c_int, P, c_long, P, P, P, P, P, P]),
+    "vx_basis_combine_ptrs": (c_int, [c_long, c_int, P, P, P, P]),
     "vx_basis_combine": (c_int, [c_long, c_int, P, c_long, P, P, P]),
     "vx_axpby": (c_int, [c_long, c128, P, c128, P, P, P]),
     "vx_norm2": (c_int, [c_long, P, P, P, P]),

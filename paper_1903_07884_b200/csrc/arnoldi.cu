@@ -250,6 +250,31 @@ __global__ void combine_kernel(long n, int nvec, const double2* __restrict__ V, 
   }
 }
 
+// u = sum_i y[i] Z_i with the basis vectors given by a device pointer array
+// (the preconditioned vectors z_j = P^-1 v_j kept where the preconditioner
+// wrote them, instead of copying each into a basis matrix)
+__global__ void combine_ptrs_kernel(long n, int nvec, const double2* const* __restrict__ Z,
+                                    const double2* __restrict__ y, double2* __restrict__ u) {
+  __shared__ double2 ys[128];
+  __shared__ const double2* zp[128];
+  for (long base = (long)blockIdx.x * blockDim.x; base < n; base += (long)gridDim.x * blockDim.x) {
+    const long e = base + threadIdx.x;
+    double2 acc = cmk(0.0, 0.0);
+    for (int i0 = 0; i0 < nvec; i0 += 128) {
+      const int m = nvec - i0 < 128 ? nvec - i0 : 128;
+      __syncthreads();
+      for (int i = threadIdx.x; i < m; i += blockDim.x) {
+        ys[i] = y[i0 + i];
+        zp[i] = Z[i0 + i];
+      }
+      __syncthreads();
+      if (e < n)
+        for (int i = 0; i < m; ++i) cfma(acc, ys[i], ld_stream(zp[i] + e));
+    }
+    if (e < n) u[e] = acc;
+  }
+}
+
 __global__ void axpby_kernel(long n, double2 a, const double2* __restrict__ x, double2 b,
                              const double2* __restrict__ y, double2* __restrict__ out) {
   for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < n; e += (long)gridDim.x * blockDim.x) {
@@ -384,5 +409,15 @@ extern "C" int vx_cgs_update(long n, int nvec, const vx_c128* V, long ldv, const
   sum_rows_kernel<<<1, AR_THREADS, 0, s>>>(1, G, pd, reinterpret_cast<double2*>(out_norm2));
   count_launch();
   VX_CHECK_LAUNCH("cgs_update");
+  return VX_OK;
+}
+
+extern "C" int vx_basis_combine_ptrs(long n, int nvec, const void* zptrs, const vx_c128* y, vx_c128* u,
+                                     void* stream) {
+  VX_REQUIRE(n >= 1 && nvec >= 0, "bad combine arguments");
+  combine_ptrs_kernel<<<stream_grid(n), 256, 0, as_stream(stream)>>>(
+      n, nvec, reinterpret_cast<const double2* const*>(zptrs), reinterpret_cast<const double2*>(y),
+      reinterpret_cast<double2*>(u));
+  VX_CHECK_LAUNCH("combine_ptrs_kernel");
   return VX_OK;
 }

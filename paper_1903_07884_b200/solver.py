@@ -120,11 +120,6 @@ class _Krylov:
         V = nv.empty_c128((rows, self.n))
         if self.V is not None:
             V[: self.cap].copy_(self.V)
-        if self.keep_z:
-            Z = nv.empty_c128((rows, self.n))
-            if self.Z is not None:
-                Z[: self.cap].copy_(self.Z)
-            self.Z = Z
         self.V, self.cap = V, rows
 
     def row(self, i):
@@ -242,10 +237,18 @@ def _gmres_cycle(K: _Krylov, op, r0, beta, bnorm, tol, m, residuals, P=None, A=N
     step j ends the cycle (convergence / breakdown), the speculative step's
     output is simply never used; _speculate() avoids it near convergence."""
     t = K.t
+    zl = []  # z_j = P^-1 v_j, kept where the preconditioner wrote them (no copy)
     if K.keep_z:
         def op(v, j):
             z = P(v)
-            K.Z[j].copy_(z)
+            if not z.is_contiguous() or z.numel() != K.n:
+                z = z.reshape(-1).contiguous()
+            if _aliases(z, K.V) or any(z.data_ptr() == o.data_ptr() for o in zl[:j]):
+                z = z.clone()  # the callable returned its argument or a reused buffer
+            if len(zl) > j:
+                zl[j] = z
+            else:
+                zl.append(z)
             return A(z)
     else:
         op_base = op
@@ -297,8 +300,11 @@ def _gmres_cycle(K: _Krylov, op, r0, beta, bnorm, tol, m, residuals, P=None, A=N
     y = qr.solve(j)
     yd = nv.device_c128(y)
     u = nv.empty_c128(K.n)
-    basis = K.Z if K.keep_z else K.V
-    nv.call("vx_basis_combine", K.n, j, basis.data_ptr(), K.n, yd.data_ptr(), u.data_ptr(), nv.stream_ptr())
+    if K.keep_z:
+        ptrs = t.tensor([z.data_ptr() for z in zl[:j]] or [0], dtype=t.int64).to("cuda", non_blocking=True)
+        nv.call("vx_basis_combine_ptrs", K.n, j, ptrs.data_ptr(), yd.data_ptr(), u.data_ptr(), nv.stream_ptr())
+    else:
+        nv.call("vx_basis_combine", K.n, j, K.V.data_ptr(), K.n, yd.data_ptr(), u.data_ptr(), nv.stream_ptr())
     return u, j, converged
 
 
