@@ -67,7 +67,9 @@ struct StoreSystem {
     const long i = b + e;
     v = cscale(v, scale);
     if (m) {
-      const double2 mv = __ldg(m + ((moff + i) % nvox));
+      // a line never straddles a component (nvox is a multiple of pitch), so
+      // the modulo depends on the line only (hoisted out of the element loop)
+      const double2 mv = __ldg(m + ((moff + b) % nvox) + e);
       const double2 xv = __ldg(x + i);
       v = csub(xv, cmul(mv, v));
     }

@@ -22,6 +22,8 @@
 #include "fft_lines.cuh"
 #include "fft_reg.cuh"
 
+#include <cooperative_groups.h>
+
 namespace vx {
 
 template <int R1, int R2, int R3, bool INV, class Loader, class Storer>
@@ -104,6 +106,101 @@ __global__ void __launch_bounds__(512, 1)
   }
 }
 
+// Lines too long for two CTAs per SM (L = 10000: 160 KB) are split over a
+// 2-CTA cluster: each CTA holds half of the line's smem (positions
+// [rank L/2, (rank+1) L/2)), so two 80 KB CTAs of different lines share an SM
+// and overlap their load / compute / store phases.  Pass 1 writes its outputs
+// k1 >= R1/2 into the partner's shared memory (DSMEM); after one cluster
+// barrier passes 2 and 3 only touch the CTA's own half (blocks k1 of its
+// half).  Requires R1 even.
+template <int R1, int R2, int R3, bool INV, class Loader, class Storer>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2)
+    fft_long2_kernel(Loader ld, Storer st, const double2* __restrict__ tw_lo, const double2* __restrict__ tw_hi,
+                     int nhi, int n_lines, int n_in, int n_out) {
+  constexpr int L = R1 * R2 * R3;
+  constexpr int M1 = L / R1;
+  constexpr int M2 = R3;
+  constexpr int H1 = R1 / 2;  // k1 blocks per CTA
+  constexpr int HALF = H1 * M1;
+  constexpr double sgn = INV ? 1.0 : -1.0;
+  static_assert(R1 % 2 == 0 && R3 > 1, "cluster split needs an even first radix and three factors");
+  extern __shared__ double2 lsm[];
+  double2* tw = lsm + HALF;
+  namespace cgx = cooperative_groups;
+  cgx::cluster_group cl = cgx::this_cluster();
+  const int rank = (int)cl.block_rank();
+  const int l = blockIdx.x >> 1;
+  for (int i = threadIdx.x; i < 64 + nhi; i += blockDim.x)
+    tw[i] = i < 64 ? __ldg(tw_lo + i) : __ldg(tw_hi + (i - 64));
+  double2* half0 = cl.map_shared_rank(lsm, 0);
+  double2* half1 = cl.map_shared_rank(lsm, 1);
+  __syncthreads();
+  // pass 1: this CTA's share of the M1 tasks; outputs to both halves
+  const int m0 = rank * ((M1 + 1) / 2), m1 = rank ? M1 : (M1 + 1) / 2;
+  if (l < n_lines) {
+    const long b = ld.line_base(l);
+    for (int m = m0 + threadIdx.x; m < m1; m += blockDim.x) {
+      double2 v[R1];
+#pragma unroll
+      for (int n1 = 0; n1 < R1; ++n1) {
+        const int e = n1 * M1 + m;
+        v[n1] = e < n_in ? ld(b, e) : cmk(0.0, 0.0);
+      }
+      reg_fft<R1, INV>(v);
+      if (m) twiddle_row<R1>(v, tw, m, sgn);
+#pragma unroll
+      for (int k1 = 0; k1 < H1; ++k1) half0[k1 * M1 + m] = v[k1];
+#pragma unroll
+      for (int k1 = 0; k1 < H1; ++k1) half1[k1 * M1 + m] = v[H1 + k1];
+    }
+  }
+  cl.sync();
+  if (l >= n_lines) return;
+  // pass 2: blocks k1 = rank H1 + k1l, local
+  for (int i = threadIdx.x; i < H1 * M2; i += blockDim.x) {
+    const int k1l = i / M2, m2 = i - k1l * M2;
+    double2* s = lsm + k1l * M1 + m2;
+    double2 v[R2];
+#pragma unroll
+    for (int n2 = 0; n2 < R2; ++n2) v[n2] = s[n2 * M2];
+    reg_fft<R2, INV>(v);
+    if (m2) twiddle_row<R2>(v, tw, R1 * m2, sgn);
+#pragma unroll
+    for (int k2 = 0; k2 < R2; ++k2) s[k2 * M2] = v[k2];
+  }
+  __syncthreads();
+  // last pass: tasks t = k1 + R1 k2 with k1 in this CTA's half
+  constexpr int T = L / R3;
+  const long bo = st.line_base(l);
+  for (int i = threadIdx.x; i < H1 * R2; i += blockDim.x) {
+    const int k1l = i % H1, k2 = i / H1;
+    const int t = rank * H1 + k1l + R1 * k2;
+    const double2* s = lsm + k1l * M1 + k2 * M2;
+    double2 v[R3];
+#pragma unroll
+    for (int n = 0; n < R3; ++n) v[n] = s[n];
+    reg_fft<R3, INV>(v);
+#pragma unroll
+    for (int k = 0; k < R3; ++k) {
+      const int e = t + T * k;
+      if (e < n_out) st(bo, e, v[k]);
+    }
+  }
+}
+
+template <int R1, int R2, int R3, bool INV, class Loader, class Storer>
+int launch_fft_long2_t(const FftPlan& p, const Loader& ld, const Storer& st, int n_lines, int n_in, int n_out,
+                       cudaStream_t s) {
+  constexpr int L = R1 * R2 * R3;
+  const size_t smem = ((size_t)L / 2 + 64 + p.nhi) * sizeof(double2);
+  auto kern = fft_long2_kernel<R1, R2, R3, INV, Loader, Storer>;
+  VX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  static const int thr_env = env_int("VX_FFT_LONG2_THREADS", 256);
+  kern<<<2 * n_lines, thr_env, smem, s>>>(ld, st, p.tw_lo, p.tw_hi, p.nhi, n_lines, n_in, n_out);
+  VX_CHECK_LAUNCH("fft_long2_kernel");
+  return VX_OK;
+}
+
 // Factorisations with a register kernel (M1 = L/R1 odd for the conflict-free
 // last pass).  X(L, R1, R2, R3)
 #define VX_LONG_FACTORS(X)                                                                    \
@@ -145,6 +242,10 @@ template <class Loader, class Storer>
 int launch_fft_long(const FftPlan& p, const Loader& ld, const Storer& st, int n_lines, int n_in, int n_out,
                     bool inv, cudaStream_t s) {
   if (n_lines <= 0) return VX_OK;
+  static const int split = env_int("VX_FFT_LONG2", 1);
+  if (split && p.n == 10000)
+    return inv ? launch_fft_long2_t<16, 25, 25, true>(p, ld, st, n_lines, n_in, n_out, s)
+               : launch_fft_long2_t<16, 25, 25, false>(p, ld, st, n_lines, n_in, n_out, s);
   switch (p.n) {
 #define VX_LONG_LAUNCH(N, A, B, C)                                                              \
   case N:                                                                                       \
