@@ -77,7 +77,8 @@ def chan_along_axis(gen: np.ndarray, axis: int) -> np.ndarray:
 
 def _constant_along(m: np.ndarray, axis: int, what: str) -> None:
     lead = np.take(m, [0], axis=axis)
-    if not np.allclose(m, lead, rtol=0.0, atol=1e-12 * max(1.0, np.abs(m).max())):
+    # == np.allclose(m, lead, rtol=0, atol) (a NaN fails both), one pass cheaper
+    if not np.abs(m - lead).max() <= 1e-12 * max(1.0, np.abs(m).max()):
         raise ValueError(f"homogenized coefficient must be constant along {what}")
 
 

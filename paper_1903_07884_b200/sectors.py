@@ -33,6 +33,7 @@ Tables (all int32 / float64, padded to dmax = the largest sector):
 
 from __future__ import annotations
 
+import functools
 from dataclasses import dataclass
 
 import numpy as np
@@ -82,6 +83,7 @@ def m_symmetric(m_yz: np.ndarray, axis: str, rtol: float = 1e-13) -> bool:
     return bool(np.abs(m - f).max() <= rtol * scale)
 
 
+@functools.lru_cache(maxsize=16)
 def sector_plan(ny: int, nz: int, sym_y: bool, sym_z: bool) -> SectorPlan | None:
     """Sector tables for the enabled reflections (None if neither)."""
     if not (sym_y or sym_z):

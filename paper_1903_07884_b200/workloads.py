@@ -59,7 +59,10 @@ class Workload:
         """Homogenised map for the whole grid or a box (x0,x1,y0,y1,z0,z1)."""
         strat = self.prec["homogenization"]
         if box is None:
-            return homogenize(self.pmap, strat)
+            # memoised: a pure function of the workload's inputs
+            if getattr(self, "_mtilde", None) is None:
+                object.__setattr__(self, "_mtilde", homogenize(self.pmap, strat))
+            return self._mtilde
         x0, x1, y0, y1, z0, z1 = box
         sub = VoxelGrid(x1 - x0, y1 - y0, z1 - z0, self.grid.delta)
         return homogenize(PermittivityMap(sub, self.pmap.eps_r[z0:z1, y0:y1, x0:x1]), strat)
