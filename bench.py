@@ -89,6 +89,13 @@ class Clocks:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
                  "-lms", "200"], stdout=self.f, stderr=subprocess.DEVNULL)
+            # nvidia-smi's start-up (NVML init) can stall CUDA calls for tens of
+            # ms: wait for its first sample so that happens before the timed region
+            t0 = time.perf_counter()
+            while time.perf_counter() - t0 < 3.0 and self.proc.poll() is None:
+                if os.path.getsize(self.f.name) > 0:
+                    break
+                time.sleep(0.02)
         except Exception:
             self.proc = None
 
@@ -404,18 +411,19 @@ def run_ours(args):
         def solve(b):
             return gmres(A, b, apply_pinv=prec.apply, tol=W.tol, maxit=W.maxit, restart=W.restart)
 
+    # clock sampler runs from before the warm-up until after the timed region
+    clocks = Clocks(local)
+    clocks.start()
     for _ in range(args.warmup):
         _, rep = solve(b_dev)
     torch.cuda.synchronize()
 
     # ---- timed region (device resident)
-    clocks = Clocks(local)
     barrier(torch, world)
     torch.cuda.synchronize()
     nv.timing_enable(True)
     for sp in ("prec_solve", "op_apply", "prec_apply", "arnoldi_step"):
         nv.timing_read(sp)
-    clocks.start()
     l0 = nv.launch_count()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
