@@ -2492,7 +2492,9 @@ static int prec1_apply_sec(int nx, int ny, int nz, int nrhs, const vx_c128* fact
     StoreStrided sv{S, {pitch, 1, nrhs, nrhs}, 1.0};
     if ((st = launch_fft_auto(p, ld, sv, q3 * nrhs, nx, nx, false, nrhs == 1, s))) return st;
   }
-  VX_CUDA(cudaMemsetAsync(U, 0, sizeof(double2) * (size_t)nsec * dmax * pitch, s));
+  // the padding rows of a sector (d_s <= r < dmax) feed the padded solve's
+  // identity rows, so they must be zero; the ragged solve never reads them
+  if (!(rg && rg->on)) VX_CUDA(cudaMemsetAsync(U, 0, sizeof(double2) * (size_t)nsec * dmax * pitch, s));
   if ((st = sec_xform(pitch, nrhs, norb, orows, osec, ocoef, flipk, q, S, U, 0, s))) return st;
   if ((st = solve_items(lu_geom(dmax), reinterpret_cast<const double2*>(factors), perm, items, n_single, n_items,
                         klist, nrhs, U, pitch, nrhs, s, -1, direct_r, rg)))
