@@ -11,6 +11,8 @@
 // CTA summing them in index order): results are bitwise reproducible.
 #include "common.cuh"
 
+#include <cstdlib>
+
 namespace vx {
 
 constexpr int AR_THREADS = 256;
@@ -174,6 +176,81 @@ __global__ void __launch_bounds__(AR_THREADS, 3) update_kernel(long n, int nvec,
   if (threadIdx.x == 0) part[blockIdx.x] = r;
 }
 
+// First-pass update fused with the DGKS second pass's dot products (nvec <=
+// NV): w1 = w - V h is formed element by element as in update_kernel, and the
+// same thread immediately re-reads the basis values it just streamed (L1 /
+// L2 hits) for the partial sums of V^H w1, so the second pass needs no dots
+// sweep over V from HBM.  part[i*G + b] = partial (V_i^H w1) (i < nvec),
+// part[nvec*G + b] = partial ||w1||^2 (the layout of dots_kernel).
+template <int NV>
+__global__ void __launch_bounds__(AR_THREADS, 3)
+    update_dots_kernel(long n, int nvec, const double2* __restrict__ V, long ldv, const double2* __restrict__ coef,
+                       double2* __restrict__ w, double2* __restrict__ part) {
+  __shared__ double2 sh[AR_THREADS / 32];
+  __shared__ double2 cf[NV];
+  long beg, end;
+  chunk(n, beg, end);
+  const int G = gridDim.x;
+  for (int i = threadIdx.x; i < nvec; i += AR_THREADS) cf[i] = coef[i];
+  __syncthreads();
+  double2 acc[NV];
+#pragma unroll
+  for (int i = 0; i < NV; ++i) acc[i] = cmk(0.0, 0.0);
+  double nrm = 0.0;
+  for (long e = beg + threadIdx.x; e < end; e += 2 * AR_THREADS) {
+    const long e2 = e + AR_THREADS;
+    const bool has2 = e2 < end;
+    double2 x0 = w[e];
+    double2 x1 = has2 ? w[e2] : cmk(0.0, 0.0);
+#pragma unroll
+    for (int i = 0; i < NV; i += AR_UG) {
+      double2 v0[AR_UG], v1[AR_UG];
+#pragma unroll
+      for (int g = 0; g < AR_UG; ++g) {
+        const bool ok = i + g < nvec;
+        const double2* vp = V + (long)(i + g) * ldv;
+        v0[g] = ok ? __ldg(vp + e) : cmk(0.0, 0.0);
+        v1[g] = (ok && has2) ? __ldg(vp + e2) : cmk(0.0, 0.0);
+      }
+#pragma unroll
+      for (int g = 0; g < AR_UG; ++g)
+        if (i + g < nvec) {
+          cfms(x0, cf[i + g], v0[g]);
+          cfms(x1, cf[i + g], v1[g]);
+        }
+    }
+    w[e] = x0;
+    if (has2) w[e2] = x1;
+    nrm = fma(x0.x, x0.x, nrm);
+    nrm = fma(x0.y, x0.y, nrm);
+    nrm = fma(x1.x, x1.x, nrm);
+    nrm = fma(x1.y, x1.y, nrm);
+#pragma unroll
+    for (int i = 0; i < NV; ++i)
+      if (i < nvec) {
+        const double2* vp = V + (long)i * ldv;
+        const double2 v0 = __ldg(vp + e);
+        const double2 v1 = has2 ? __ldg(vp + e2) : cmk(0.0, 0.0);
+        acc[i].x = fma(v0.x, x0.x, acc[i].x);
+        acc[i].x = fma(v0.y, x0.y, acc[i].x);
+        acc[i].y = fma(v0.x, x0.y, acc[i].y);
+        acc[i].y = fma(-v0.y, x0.x, acc[i].y);
+        acc[i].x = fma(v1.x, x1.x, acc[i].x);
+        acc[i].x = fma(v1.y, x1.y, acc[i].x);
+        acc[i].y = fma(v1.x, x1.y, acc[i].y);
+        acc[i].y = fma(-v1.y, x1.x, acc[i].y);
+      }
+  }
+#pragma unroll
+  for (int i = 0; i < NV; ++i)
+    if (i < nvec) {
+      const double2 r = block_sum(acc[i], sh);
+      if (threadIdx.x == 0) part[(long)i * G + blockIdx.x] = r;
+    }
+  const double2 r = block_sum(cmk(nrm, 0.0), sh);
+  if (threadIdx.x == 0) part[(long)nvec * G + blockIdx.x] = r;
+}
+
 // Fixed-order finalisation of the partial sums (single CTA).
 //  mode 0: h[i] = sum part_i (i<nvec); stats[0] = sqrt(sum part_nvec)
 //  mode 1: stats[1] = sqrt(sum part_0); stats[2] = stats[1] < 0.7071 stats[0]; h[nvec] = stats[1]
@@ -186,10 +263,12 @@ __global__ void __launch_bounds__(AR_THREADS) finalize_kernel(int nvec, int G, c
   if ((mode == 2 || mode == 3) && stats[2] == 0.0) return;
   __shared__ double2 sh[AR_THREADS / 32];
   const int rows = (mode == 0) ? nvec + 1 : (mode == 2 ? nvec : 1);
+  const int row0 = (mode == 5) ? nvec : 0;  // mode 5: mode 1 on the norm row of update_dots_kernel
+  if (mode == 5) mode = 1;
   // one CTA per row (grid-strided): each row is summed in the same fixed order
   for (int i = blockIdx.x; i < rows; i += gridDim.x) {
     double2 v = cmk(0.0, 0.0);
-    for (int b = threadIdx.x; b < G; b += AR_THREADS) v = cadd(v, part[(long)i * G + b]);
+    for (int b = threadIdx.x; b < G; b += AR_THREADS) v = cadd(v, part[(long)(row0 + i) * G + b]);
     v = block_sum(v, sh);
     if (threadIdx.x == 0) {
       if (mode == 0) {
@@ -336,11 +415,24 @@ extern "C" int vx_arnoldi_step(long n, int nvec, const vx_c128* V, long ldv, vx_
   double2* cd = pd + (long)(nvec + 2) * G;  // second-pass coefficients
   dots_kernel<<<G, AR_THREADS, 0, s>>>(n, nvec, Vd, ldv, wd, pd, nullptr);
   finalize_kernel<<<nvec + 1, AR_THREADS, 0, s>>>(nvec, G, pd, hd, cd, stats, 0);
-  update_kernel<<<G, AR_THREADS, 0, s>>>(n, nvec, Vd, ldv, hd, wd, pd, nullptr);
-  finalize_kernel<<<1, AR_THREADS, 0, s>>>(nvec, G, pd, hd, cd, stats, 1);
-  // DGKS second pass, executed only if the device flag stats[2] is set
-  dots_kernel<<<G, AR_THREADS, 0, s>>>(n, nvec, Vd, ldv, wd, pd, stats);
-  finalize_kernel<<<nvec > 0 ? nvec : 1, AR_THREADS, 0, s>>>(nvec, G, pd, hd, cd, stats, 2);
+  static const int fuse = [] { const char* v = getenv("VX_AR_FUSE"); return v ? atoi(v) : 1; }();
+  // fused only while the re-read basis values are still in L1 (measured at
+  // c1: nvec <= 8 saves the second dots sweep; at 9..16 the re-read goes to
+  // L2/HBM and the fused kernel costs as much as the two passes)
+  if (fuse && nvec >= 1 && nvec <= 8) {
+    // first update + the second pass's dots in one sweep (partials for the
+    // conditional DGKS pass are ready whether or not it fires)
+    const int Gf = G;
+    update_dots_kernel<8><<<Gf, AR_THREADS, 0, s>>>(n, nvec, Vd, ldv, hd, wd, pd);
+    finalize_kernel<<<1, AR_THREADS, 0, s>>>(nvec, Gf, pd, hd, cd, stats, 5);
+    finalize_kernel<<<nvec, AR_THREADS, 0, s>>>(nvec, Gf, pd, hd, cd, stats, 2);
+  } else {
+    update_kernel<<<G, AR_THREADS, 0, s>>>(n, nvec, Vd, ldv, hd, wd, pd, nullptr);
+    finalize_kernel<<<1, AR_THREADS, 0, s>>>(nvec, G, pd, hd, cd, stats, 1);
+    // DGKS second pass, executed only if the device flag stats[2] is set
+    dots_kernel<<<G, AR_THREADS, 0, s>>>(n, nvec, Vd, ldv, wd, pd, stats);
+    finalize_kernel<<<nvec > 0 ? nvec : 1, AR_THREADS, 0, s>>>(nvec, G, pd, hd, cd, stats, 2);
+  }
   update_kernel<<<G, AR_THREADS, 0, s>>>(n, nvec, Vd, ldv, cd, wd, pd, stats);
   finalize_kernel<<<1, AR_THREADS, 0, s>>>(nvec, G, pd, hd, cd, stats, 3);
   if (vnext)
