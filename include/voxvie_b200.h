@@ -273,6 +273,21 @@ long vx_launch_count(void);
 int vx_timing_enable(int on);
 int vx_timing_read(const char* span, double* total_ms, long* count);
 
+/* Host -> device upload of a PAGEABLE host buffer (the numpy field vectors /
+ * coefficient maps callers pass to apply_n, apply_system and gmres:
+ * reference operator.py:82-105, solver.py:114-174).  A persistent pool of
+ * host threads copies 2 MB chunks into a ring of pinned slots and each issues
+ * its chunk's DMA on `stream`.  Returns once `src` has been consumed (same
+ * contract as cudaMemcpy from pageable memory); the DMA is ordered on
+ * `stream`.  vx_h2d_threads() = host threads used (pool + caller). */
+int vx_h2d_staged(void* dst, const void* src, size_t bytes, void* stream);
+int vx_h2d_threads(void);
+/* Pinned host blocks for results (pooled by the host side) and a synchronous
+ * device -> pinned-host copy ordered on `stream`. */
+int vx_host_alloc(size_t bytes, void** out);
+int vx_host_free(void* p);
+int vx_d2h_pinned(void* dst, const void* src, size_t bytes, void* stream);
+
 /* ---- ragged ("packed") factor storage for the 1-level block solves.
  * The build writes every block in the padded tile geometry of dmax (tiles of
  * 32, reference zgetrf blocks circulant.py:113-118 re-tiled); the repack keeps

@@ -101,6 +101,11 @@ _SIGS = {
     "vx_cgs_dots": (c_int, [c_long, c_int, P, c_long, P, P, P, P]),
     "vx_cgs_update": (c_int, [c_long, c_int, P, c_long, P, P, P, P, P]),
     "vx_launch_count": (c_long, []),
+    "vx_h2d_staged": (c_int, [P, P, c_size_t, P]),
+    "vx_h2d_threads": (c_int, []),
+    "vx_host_alloc": (c_int, [c_size_t, C.POINTER(C.c_void_p)]),
+    "vx_host_free": (c_int, [P]),
+    "vx_d2h_pinned": (c_int, [P, P, c_size_t, P]),
     "vx_solve_variant": (c_int, [c_int]),
     "vx_lu_variant": (c_int, [c_int]),
     "vx_timing_enable": (c_int, [c_int]),
@@ -188,6 +193,9 @@ def ptr(t) -> int | None:
     return None if t is None else t.data_ptr()
 
 
+H2D_STAGED_MIN = int(os.environ.get("VX_H2D_STAGED_MIN", 4 << 20))
+
+
 def device_c128(a, device=None):
     """Host array-like / tensor -> contiguous complex128 CUDA tensor."""
     t = require_cuda()
@@ -196,6 +204,11 @@ def device_c128(a, device=None):
             a = a.to("cuda" if device is None else device, non_blocking=False)
         return a.to(t.complex128).contiguous()
     arr = np.ascontiguousarray(np.asarray(a, dtype=np.complex128))
+    if arr.nbytes >= H2D_STAGED_MIN and device is None:
+        # large pageable upload: threaded copy through the library's pinned ring
+        out = t.empty(arr.shape, dtype=t.complex128, device="cuda")
+        call("vx_h2d_staged", out.data_ptr(), arr.ctypes.data, arr.nbytes, stream_ptr())
+        return out
     if not arr.flags.writeable:
         arr = arr.copy()
     host = t.from_numpy(arr)
@@ -231,13 +244,64 @@ def launch_count() -> int:
     return int(query("vx_launch_count"))
 
 
+class _PinnedBlock:
+    """One pooled pinned host block, exposed to numpy through the array
+    interface; when the last numpy view dies the block returns to the pool."""
+
+    __slots__ = ("ptr", "nbytes", "__weakref__")
+
+    def __init__(self, ptr: int, nbytes: int):
+        self.ptr = ptr
+        self.nbytes = nbytes
+
+    @property
+    def __array_interface__(self):
+        return {"shape": (self.nbytes,), "typestr": "|u1", "data": (self.ptr, False), "version": 3}
+
+    def __del__(self):
+        try:
+            _pinned_release(self.ptr, self.nbytes)
+        except Exception:  # pragma: no cover - interpreter shutdown
+            pass
+
+
+_pin_lock = threading.Lock()
+_pin_free: dict[int, list[int]] = {}
+_PIN_KEEP = 4            # free blocks kept per size
+
+
+def _pinned_acquire(nbytes: int) -> _PinnedBlock:
+    with _pin_lock:
+        lst = _pin_free.get(nbytes)
+        if lst:
+            return _PinnedBlock(lst.pop(), nbytes)
+    out = C.c_void_p()
+    call("vx_host_alloc", nbytes, C.byref(out))
+    return _PinnedBlock(out.value, nbytes)
+
+
+def _pinned_release(ptr: int, nbytes: int):
+    with _pin_lock:
+        lst = _pin_free.setdefault(nbytes, [])
+        if len(lst) < _PIN_KEEP:
+            lst.append(ptr)
+            return
+    query("vx_host_free", ptr)
+
+
 def to_host(t):
-    """Device tensor -> numpy through pinned memory (pageable D2H of large
-    vectors runs at ~2 GB/s; pinned at link speed)."""
+    """Device tensor -> numpy.  Large results land in a pooled pinned block
+    (DMA at link speed, no page faults on a fresh allocation); the returned
+    array owns its block until it is garbage collected."""
     if t.numel() * t.element_size() < (1 << 20) or not t.is_cuda:
         return t.cpu().numpy()
-    tt = torch()
-    h = tt.empty(t.shape, dtype=t.dtype, pin_memory=True)
-    h.copy_(t, non_blocking=True)
-    tt.cuda.current_stream().synchronize()
-    return h.numpy()
+    t = t.contiguous()
+    nbytes = t.numel() * t.element_size()
+    blk = _pinned_acquire(nbytes)
+    call("vx_d2h_pinned", blk.ptr, t.data_ptr(), nbytes, stream_ptr())
+    raw = np.asarray(blk)
+    np_dtype = {torch().complex128: np.complex128, torch().float64: np.float64,
+                torch().complex64: np.complex64, torch().float32: np.float32}.get(t.dtype)
+    if np_dtype is None:
+        return t.cpu().numpy()
+    return raw.view(np_dtype).reshape(tuple(t.shape))

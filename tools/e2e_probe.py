@@ -43,3 +43,10 @@ timed("D2H x", lambda: b_dev.cpu().numpy())
 timed("apply_system host m", lambda: apply_system(plan, m_host, b_dev))
 timed("apply_system dev m", lambda: apply_system(plan, m_dev, b_dev))
 timed("prec.apply dev", lambda: prec.apply(b_dev))
+from paper_1903_07884_b200 import _native as nv  # noqa: E402
+
+print("h2d threads", nv.query("vx_h2d_threads"))
+timed("H2D b (staged ring)", lambda: nv.device_c128(b_host))
+timed("H2D m (staged ring)", lambda: nv.device_c128(m_host))
+timed("H2D m (pageable)", lambda: torch.from_numpy(m_host).cuda())
+timed("D2H x (to_host pinned)", lambda: nv.to_host(b_dev))
