@@ -458,7 +458,7 @@ def run_ours(args):
         nvec = W.grid.n_unknowns
         if W.prec["kind"] == "blocked":   # one solve launch per box: per-launch bytes of one box
             x0, x1, y0, y1, z0, z1 = W.prec["boxes"][0]
-            stored = stored[:1]
+            stored = list(prec.box_precs[0].stored_blocks)   # every (sector) block of box 0
             nvec = 3 * (x1 - x0) * (y1 - y0) * (z1 - z0)
     sol_ms, sol_n = spans["prec_solve"]
     solve_bytes = 16 * sum(n * n * c for n, c in stored) + 2 * 16 * nvec
@@ -515,15 +515,19 @@ def run_ours(args):
         barrier(torch, world)
         t0 = time.perf_counter()
         its_e = 0
+        step_wall = []
         for _ in range(args.steps):
+            ts = time.perf_counter()
             x_h, rep = e2e_step()
             its_e += rep.iterations
+            step_wall.append((time.perf_counter() - ts) * 1e3)
         torch.cuda.synchronize()
         te = reduce_max(torch, world, time.perf_counter() - t0)
         its_e_all = its_e if sharded else reduce_sum(torch, world, its_e)
         nb_loc = b_host.nbytes // world if sharded else b_host.nbytes
         e2e = {"value": its_e_all / te, "unit": "it/s", "h2d_bytes_per_step": int(nb_loc + m_host.nbytes),
                "d2h_bytes_per_step": int(nb_loc), "ms_per_step": te / args.steps * 1e3,
+               "step_wall_ms": [round(v, 2) for v in step_wall],
                "tts_s": build_s + te / args.steps,
                "note": "numpy b and m in (threaded pinned-ring upload, vx_h2d_staged), numpy x out (pooled pinned block); plan+factors resident (setup)"}
 

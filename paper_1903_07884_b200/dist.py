@@ -325,7 +325,17 @@ def _norm(B, C, x, part):
 def gmres_sharded(apply_a, b_loc, backend, comm: _Comm, *, apply_pinv=None, tol=1e-4, maxit=2000,
                   restart=None):
     """Right-preconditioned restarted GMRES on line-sharded vectors (reference
-    solver.py:114-174 control flow; see module docstring for the exchanges)."""
+    solver.py:114-174 control flow; see module docstring for the exchanges).
+    The garbage collector is paused during the solve (solver.gc_paused)."""
+    from .solver import gc_paused
+
+    with gc_paused():
+        return _gmres_sharded(apply_a, b_loc, backend, comm, apply_pinv=apply_pinv, tol=tol, maxit=maxit,
+                              restart=restart)
+
+
+def _gmres_sharded(apply_a, b_loc, backend, comm: _Comm, *, apply_pinv=None, tol=1e-4, maxit=2000,
+                   restart=None):
     if not tol > 0:
         raise ValueError("tol must be positive")
     if maxit < 1:

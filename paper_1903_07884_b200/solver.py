@@ -21,6 +21,8 @@ a CUDA tensor -> ``x`` as a CUDA tensor.
 
 from __future__ import annotations
 
+import contextlib
+import gc
 import os
 import threading
 import time
@@ -310,7 +312,30 @@ def _gmres_cycle(K: _Krylov, op, r0, beta, bnorm, tol, m, residuals, P=None, A=N
 
 def gmres(apply_a, b, *, apply_pinv=None, tol: float = 1e-4, maxit: int = 2000,
           restart: int | None = None):
-    """Right-preconditioned (restarted) GMRES from x0 = 0 (reference solver.py:114-174)."""
+    """Right-preconditioned (restarted) GMRES from x0 = 0 (reference solver.py:114-174).
+
+    Python's cyclic garbage collector is paused for the duration of the solve
+    (and restored afterwards): a full collection with torch loaded walks ~10^6
+    objects (tens of ms), long enough to drain the one-iteration-deep device
+    queue of the pipelined Arnoldi loop; the solve itself creates no cycles."""
+    with gc_paused():
+        return _gmres(apply_a, b, apply_pinv=apply_pinv, tol=tol, maxit=maxit, restart=restart)
+
+
+@contextlib.contextmanager
+def gc_paused():
+    """Pause the cyclic garbage collector inside a solve, restoring its state."""
+    gc_on = gc.isenabled()
+    gc.disable()
+    try:
+        yield
+    finally:
+        if gc_on:
+            gc.enable()
+
+
+def _gmres(apply_a, b, *, apply_pinv=None, tol: float = 1e-4, maxit: int = 2000,
+           restart: int | None = None):
     if not tol > 0:
         raise ValueError("tol must be positive")
     if maxit < 1:

@@ -11,7 +11,7 @@ import torch
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 from paper_1903_07884_b200 import _native as nv  # noqa: E402
 from paper_1903_07884_b200 import workloads  # noqa: E402
-from paper_1903_07884_b200.circulant import build_one_level  # noqa: E402
+import bench  # noqa: E402
 from paper_1903_07884_b200.operator import apply_system, plan_operator  # noqa: E402
 from paper_1903_07884_b200.solver import gmres  # noqa: E402
 
@@ -19,7 +19,7 @@ name = sys.argv[1] if len(sys.argv) > 1 else "c1"
 W = workloads.make(name)
 kern = W.kernel()
 plan = plan_operator(kern)
-prec = build_one_level(kern, W.mtilde(), cap_bytes=2 ** 62)
+prec = bench.build_prec(W, kern)
 m_host, b_host = W.m, W.b
 m_copies = [np.array(m_host, copy=True), np.array(m_host, copy=True)]
 print("staged min", nv.H2D_STAGED_MIN, "threads env", os.environ.get("VX_H2D_THREADS"), flush=True)
