@@ -273,6 +273,14 @@ long vx_launch_count(void);
 int vx_timing_enable(int on);
 int vx_timing_read(const char* span, double* total_ms, long* count);
 
+/* Generating tensors assembled on the device (replaces the host assembly of
+ * reference kernel.py:152-198 / accel.py:131-155): out = (6, 2nz-1, 2ny-1,
+ * 2nx-1) complex128, component order xx, xy, xz, yy, yz, zz, entry at offset d
+ * = vol * G(delta d) (centroid rule), the zero offset = self_val on xx/yy/zz
+ * and 0 elsewhere (self term from the host quadrature, kernel.py:101-116). */
+int vx_assemble_green(int nx, int ny, int nz, double delta, double k0, double vol, vx_c128 self_val,
+                      vx_c128* out, void* stream);
+
 /* Host -> device upload of a PAGEABLE host buffer (the numpy field vectors /
  * coefficient maps callers pass to apply_n, apply_system and gmres:
  * reference operator.py:82-105, solver.py:114-174).  A persistent pool of

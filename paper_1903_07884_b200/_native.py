@@ -102,6 +102,7 @@ _SIGS = {
     "vx_cgs_update": (c_int, [c_long, c_int, P, c_long, P, P, P, P, P]),
     "vx_launch_count": (c_long, []),
     "vx_h2d_staged": (c_int, [P, P, c_size_t, P]),
+    "vx_assemble_green": (c_int, [c_int] * 3 + [c_double] * 3 + [c128, P, P]),
     "vx_h2d_threads": (c_int, []),
     "vx_host_alloc": (c_int, [c_size_t, C.POINTER(C.c_void_p)]),
     "vx_host_free": (c_int, [P]),

@@ -177,23 +177,92 @@ def assemble_kernel(grid: VoxelGrid, k0: float, *, near_gauss: bool = False) -> 
     for p, name in enumerate(PAIRS):
         t[(p,) + c] = s if name in ("xx", "yy", "zz") else 0.0
     if near_gauss:
-        pts, wts = _gauss_cube(d, 3)
-        for ddz in (-1, 0, 1):
-            for ddy in (-1, 0, 1):
-                for ddx in (-1, 0, 1):
-                    if (ddx, ddy, ddz) == (0, 0, 0):
-                        continue
-                    if abs(ddx) >= nx or abs(ddy) >= ny or abs(ddz) >= nz:
-                        continue
-                    rc = d * np.array([ddx, ddy, ddz], dtype=float)
-                    acc = np.zeros((3, 3), dtype=np.complex128)
-                    for ps, ws in zip(rc - pts, wts):
-                        acc += ws * dyadic_green(ps, k0)
-                    loc = (c[0] + ddz, c[1] + ddy, c[2] + ddx)
-                    for p, name in enumerate(PAIRS):
-                        t[(p,) + loc] = acc["xyz".index(name[0]), "xyz".index(name[1])]
+        for loc, vals in _near_gauss_entries(grid, k0):
+            for p in range(6):
+                t[(p,) + loc] = vals[p]
     t.setflags(write=False)
     return ToeplitzKernel(grid=grid, k0=float(k0), tensors=t)
+
+
+def _near_gauss_entries(grid: VoxelGrid, k0: float):
+    """3x3x3-point Gauss cube integrals for the 26 face/edge/corner neighbours
+    (reference kernel.py:180-196): [(index (z, y, x) into the generator, six values)]."""
+    nx, ny, nz = grid.dims
+    d = grid.delta
+    c = (nz - 1, ny - 1, nx - 1)
+    pts, wts = _gauss_cube(d, 3)
+    out = []
+    for ddz in (-1, 0, 1):
+        for ddy in (-1, 0, 1):
+            for ddx in (-1, 0, 1):
+                if (ddx, ddy, ddz) == (0, 0, 0):
+                    continue
+                if abs(ddx) >= nx or abs(ddy) >= ny or abs(ddz) >= nz:
+                    continue
+                rc = d * np.array([ddx, ddy, ddz], dtype=float)
+                acc = np.zeros((3, 3), dtype=np.complex128)
+                for ps, ws in zip(rc - pts, wts):
+                    acc += ws * dyadic_green(ps, k0)
+                loc = (c[0] + ddz, c[1] + ddy, c[2] + ddx)
+                out.append((loc, [acc["xyz".index(nm[0]), "xyz".index(nm[1])] for nm in PAIRS]))
+    return out
+
+
+class DeviceToeplitzKernel:
+    """ToeplitzKernel whose generators live in HBM (assembled by
+    ``assemble_kernel_device``).  Same attributes as ToeplitzKernel; ``tensors``
+    is a lazily downloaded read-only host copy (only host-side helpers such as
+    the blocked preconditioner's box slicing read it)."""
+
+    def __init__(self, grid: VoxelGrid, k0: float, device_tensors):
+        self.grid = grid
+        self.k0 = float(k0)
+        self._vx_device_tensors = device_tensors
+        self._host = None
+
+    @property
+    def tensors(self) -> np.ndarray:
+        if self._host is None:
+            from . import _native as nv
+
+            h = np.array(nv.to_host(self._vx_device_tensors), copy=True)
+            h.setflags(write=False)
+            self._host = h
+        return self._host
+
+    def storage_entries(self) -> int:
+        nx, ny, nz = self.grid.dims
+        return 6 * (2 * nx - 1) * (2 * ny - 1) * (2 * nz - 1)
+
+    def storage_bytes(self) -> int:
+        return 16 * self.storage_entries()
+
+    def component(self, name: str) -> np.ndarray:
+        return self.tensors[PAIRS.index(name)]
+
+
+def assemble_kernel_device(grid: VoxelGrid, k0: float, *, near_gauss: bool = False) -> DeviceToeplitzKernel:
+    """assemble_kernel (reference kernel.py:152-198) evaluated on the GPU
+    (vx_assemble_green): the generators are written straight into HBM; the
+    self term (and the optional 26 near-neighbour Gauss integrals) come from
+    the host quadrature as in the reference."""
+    from . import _native as nv
+
+    if not k0 * grid.delta < 2.0:
+        raise ValueError(f"k0*delta = {k0 * grid.delta:.3f} too coarse; need k0*delta < 2")
+    t = nv.require_cuda()
+    nx, ny, nz = grid.dims
+    s = complex(self_term(grid.delta, k0)[0, 0])
+    out = t.empty((6, 2 * nz - 1, 2 * ny - 1, 2 * nx - 1), dtype=t.complex128, device="cuda")
+    nv.call("vx_assemble_green", nx, ny, nz, float(grid.delta), float(k0), float(grid.voxel_volume),
+            nv.c128(s.real, s.imag), out.data_ptr(), nv.stream_ptr())
+    if near_gauss:
+        ent = _near_gauss_entries(grid, k0)
+        if ent:
+            idx = t.tensor([loc for loc, _ in ent], dtype=t.long)
+            vals = t.tensor(np.array([v for _, v in ent], dtype=np.complex128).T.copy()).cuda()  # (6, m)
+            out[:, idx[:, 0], idx[:, 1], idx[:, 2]] = vals
+    return DeviceToeplitzKernel(grid, k0, out)
 
 
 def check_dense_guard(n_unknowns: int, guard: int = DENSE_GUARD):
