@@ -16,7 +16,6 @@
 namespace vx {
 
 constexpr int AR_THREADS = 256;
-constexpr int AR_GROUP = 4;  // basis vectors per register group
 
 // one resident wave of the dots / update kernels (3 CTAs of 256 per SM)
 static int ar_grid(long n) {

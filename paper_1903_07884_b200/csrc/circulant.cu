@@ -133,7 +133,6 @@ __global__ void proxy_kernel(int nx, long Ltot, const double2* __restrict__ lamT
 // ---------------------------------------------------------------- LU build
 constexpr int LU_WARPS = 4;
 constexpr int LU_THREADS = LU_WARPS * 32;
-constexpr int LU_CW = 8;  // output columns per register chunk
 
 // unfold parameters: rows/cols ordered a*q + iz*nyL + iy (reference accel.py:71-91);
 // the 2-level (3nz)^2 block is the nyL = 1 case (accel.py:94-111).
@@ -918,7 +917,8 @@ static int lu_build(const Unfold& u, int n, int nslots, double2* F, int* perm, i
 // y-mirror S = -1 on the y-component rows [q, 2q); so the mirror block's
 // solve is y = S D_k^-1 S b with D_k's stored factors.  A klist entry carries
 // the frequency in its low 29 bits and the flips in bits 30 (x) / 29 (y).
-constexpr int KFLIP_X = 1 << 30, KFLIP_Y = 1 << 29, KIDX = KFLIP_Y - 1;
+[[maybe_unused]] constexpr int KFLIP_X = 1 << 30;  // documents the encoding (x flip = bit 30)
+constexpr int KFLIP_Y = 1 << 29, KIDX = KFLIP_Y - 1;
 constexpr long ROFF = (1L << 56) - 1;  // rbase: offset in the low 56 bits, flips (kraw >> 29) above
 __device__ __forceinline__ bool flip_row(int f2, int row, int q) {
   return ((f2 & 2) && row < q) || ((f2 & 1) && row >= q && row < 2 * q);
@@ -1139,7 +1139,6 @@ __global__ void __launch_bounds__((PIPE_CONSUMERS + 1) * 32)
   constexpr int NWC = PIPE_CONSUMERS;
   constexpr int NC = NWC * 32;
   const int T = g.T, T2 = T * T, nt = g.nt, npad = g.npad, n = g.n, q = n / 3;
-  const uint32_t tile_bytes = (uint32_t)T2 * sizeof(double2);
   uint64_t* full = reinterpret_cast<uint64_t*>(smraw);
   uint64_t* empty = full + S;
   long* rbase = reinterpret_cast<long*>(empty + S);
