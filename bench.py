@@ -376,8 +376,10 @@ def run_ours(args):
     torch.cuda.synchronize()
     # N > 1: the 1-level configs run ONE sharded solve across all ranks (strong
     # scaling: line-sharded vectors, k-sharded factors, NCCL all-to-all);
-    # blocked / 2-level configs run one replica per rank (weak scaling).
-    sharded = world > 1 and W.prec["kind"] in ("one-level", "reduced-one-level") and not args.replicas
+    # 2-level config (c4) too, with kx-sharded factors; blocked configs run one
+    # replica per rank (weak scaling).
+    sharded = (world > 1 and W.prec["kind"] in ("one-level", "reduced-one-level", "two-level")
+               and not args.replicas)
     mode = "sharded" if sharded else ("replicas" if world > 1 else "single-gpu")
 
     # ---- setup (time-to-solution part 1): plan + preconditioner build
@@ -385,8 +387,8 @@ def run_ours(args):
     t0 = time.perf_counter()
     ev_a, ev_b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     if sharded:
-        from paper_1903_07884_b200.dist import (CudaBackend, DistOneLevelPrec, DistOperator, Layout, _Comm,
-                                                gmres_sharded)
+        from paper_1903_07884_b200.dist import (CudaBackend, DistOneLevelPrec, DistOperator, DistTwoLevelPrec,
+                                                Layout, _Comm, gmres_sharded)
         from paper_1903_07884_b200.operator import padded_length
 
         Bk, Cm = CudaBackend(), _Comm()
@@ -395,12 +397,18 @@ def run_ours(args):
         torch.cuda.synchronize()
         plan_s = time.perf_counter() - t0
         ptol = W.prec.get("tol") if W.prec["kind"] == "reduced-one-level" else None
-        prec = DistOneLevelPrec(kern, W.mtilde(), L, Bk, Cm, tol=ptol)   # warm build
+
+        def dist_prec():
+            if W.prec["kind"] == "two-level":
+                return DistTwoLevelPrec(kern, W.mtilde(), L, Bk, Cm)
+            return DistOneLevelPrec(kern, W.mtilde(), L, Bk, Cm, tol=ptol)
+
+        prec = dist_prec()   # warm build
         del prec
         torch.cuda.synchronize()
         torch.cuda.empty_cache()
         ev_a.record()
-        prec = DistOneLevelPrec(kern, W.mtilde(), L, Bk, Cm, tol=ptol)
+        prec = dist_prec()
         ev_b.record()
         torch.cuda.synchronize()
         build_s = ev_a.elapsed_time(ev_b) / 1e3
@@ -470,8 +478,8 @@ def run_ours(args):
     # ---- roofline of the dominant kernel (factor-streaming block solve)
     peak, peak_kind = peaks()
     if sharded:
-        stored_global = [(3 * W.grid.ny * W.grid.nz, prec.n_stored_global)]
-        stored = [(3 * W.grid.ny * W.grid.nz, prec.bytes_local // (16 * (3 * W.grid.ny * W.grid.nz) ** 2))]
+        stored_global = [(prec.n, prec.n_stored_global)]
+        stored = [(prec.n, prec.bytes_local // (16 * prec.n ** 2))]
         nvec = W.grid.n_unknowns // world
     else:
         stored = stored_global = stored_blocks_of(W, prec)

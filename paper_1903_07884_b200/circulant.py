@@ -817,20 +817,26 @@ class TwoLevelPrec:
                 "block_size": int(self.block_size), "bytes": int(self.bytes)}
 
 
-def _build_two_level_dev(grid, gen, mtilde, cap_bytes):
-    t = _torch()
-    nx, ny, nz = grid.dims
+def _coerce_mz(grid, mtilde) -> np.ndarray:
+    """m~ for the 2-level scheme: (nz, ny, nx) constant in x and y, (nz,), or a
+    scalar (reference circulant.py:405-433) -> (nz,)."""
+    nz = grid.nz
     m = np.asarray(mtilde, dtype=np.complex128)
     if m.shape == grid.shape:
         _constant_along(m, 2, "x")
         _constant_along(m, 1, "y")
-        m_z = m[:, 0, 0]
-    elif m.shape == (nz,):
-        m_z = m
-    elif m.ndim == 0:
-        m_z = np.full(nz, m, dtype=np.complex128)
-    else:
-        raise ValueError(f"mtilde shape {m.shape} not usable for a 2-level build")
+        return m[:, 0, 0]
+    if m.shape == (nz,):
+        return m
+    if m.ndim == 0:
+        return np.full(nz, m, dtype=np.complex128)
+    raise ValueError(f"mtilde shape {m.shape} not usable for a 2-level build")
+
+
+def _build_two_level_dev(grid, gen, mtilde, cap_bytes):
+    t = _torch()
+    nx, ny, nz = grid.dims
+    m_z = _coerce_mz(grid, mtilde)
     _check_cap(nx * ny * (3 * nz) ** 2 * BYTES_PER_ENTRY, cap_bytes, "reduce the box size or cross-section")
     share_x, share_y = mirror_axes(gen, grid.dims)
     work = nv.empty_c128(int(nv.query("vx_chan_xy_work_elems", nx, ny, nz)))

@@ -35,7 +35,7 @@ import time
 import numpy as np
 
 from . import _native as nv
-from .circulant import _coerce_mtilde, _select_kept
+from .circulant import _check_cap, _coerce_mtilde, _coerce_mz, _select_kept
 from .errors import BreakdownError, PreconditionerBuildError
 from .solver import GivensQR, SolveReport
 
@@ -178,6 +178,46 @@ class CudaBackend:
             raise PreconditionerBuildError(f"1-level build failed: singular frequency block k={int(kset[bad])}")
         return fac, perm
 
+    def chan_xy(self, kernel):
+        from .circulant import _gen_strides
+        from .operator import upload_tensors
+
+        nx, ny, nz = kernel.grid.dims
+        gen = upload_tensors(kernel)
+        work = self.empty(int(nv.query("vx_chan_xy_work_elems", nx, ny, nz)))
+        lam2 = self.empty((nx * ny, 6 * (2 * nz - 1)))
+        nv.call("vx_chan_xy_spectra", nx, ny, nz, gen.data_ptr(), *_gen_strides(gen), lam2.data_ptr(),
+                work.data_ptr(), nv.stream_ptr())
+        return lam2
+
+    def build_factors2(self, lam2, dims, m_z, kset):
+        from .circulant import _first_bad
+
+        nx, ny, nz = dims
+        n, nb = 3 * nz, len(kset)
+        fac = self.t.empty((max(1, nb), int(nv.query("vx_lu_block_elems", n))), dtype=self.t.complex128,
+                           device="cuda")
+        perm = self.t.empty((max(1, nb), n), dtype=self.t.int32, device="cuda")
+        piv = self.t.empty((max(1, nb), n), dtype=self.t.int32, device="cuda")
+        info = self.t.zeros((max(1, nb),), dtype=self.t.int32, device="cuda")
+        if nb:
+            # keep the argument tensors referenced until the launch is ordered
+            m_dev, k_dev = nv.device_c128(np.ascontiguousarray(m_z)), self.ints(kset)
+            nv.call("vx_lu2_build", nx, ny, nz, lam2.data_ptr(), m_dev.data_ptr(), k_dev.data_ptr(), nb,
+                    fac.data_ptr(), perm.data_ptr(), piv.data_ptr(), info.data_ptr(), nv.stream_ptr())
+        bad = _first_bad(info[:nb]) if nb else -1
+        if bad >= 0:
+            l, k = divmod(int(kset[bad]), nx)
+            raise PreconditionerBuildError(f"2-level build failed: singular block (k={k}, l={l})")
+        return fac, perm
+
+    def dft_y(self, Y, nplanes, ny, nk, inverse):
+        """In-place DFT along y of Y laid out (plane, y, kx_local)."""
+        if nplanes * nk == 0:
+            return
+        nv.call("vx_fft_lines", ny, nplanes * nk, nk, Y.data_ptr(), ny * nk, 1, nk, ny, Y.data_ptr(), ny * nk, 1,
+                nk, ny, 1 if inverse else 0, (1.0 / ny) if inverse else 1.0, nv.stream_ptr())
+
     def solve(self, Y, n, factors, perm, items, n_single, n_items, klist, s_row):
         nv.call("vx_prec1_solve", n, 1, factors.data_ptr(), perm.data_ptr(), items.data_ptr(), n_single, n_items,
                 1, klist.data_ptr(), Y.data_ptr(), s_row, 1, nv.stream_ptr())
@@ -307,6 +347,61 @@ class DistOneLevelPrec:
                      [L.nl * L.kown[s].size for s in range(L.P)])
         if self.n_items:
             B.solve(recv, self.n, self.factors, self.perm, self.items, self.n_single, self.n_items, self.klist, nk)
+        back = B.empty(max(1, L.nl * nx))
+        C.all_to_all(back[:L.nl * nx], recv[:L.nlines * nk],
+                     [L.nl * L.kown[s].size for s in range(L.P)],
+                     [L.lines_of(r) * nk for r in range(L.P)])
+        B.scatter_cols(back, S, L.nl, nx, self.col_off, self.colmap, nx)
+        return B.dft_lines(S, L.nl, nx, True).reshape(-1)
+
+
+class DistTwoLevelPrec:
+    """Frequency-sharded 2-level preconditioner (reference circulant.py:362-447,
+    SURVEY 8(e) "2-level"): local x-DFT of the owned lines, one all-to-all to
+    kx ownership (kx dealt cyclically, as for the 1-level scheme), the y-DFT
+    and the (3nz)^2 block solves of every (ky, owned kx) locally -- the rank
+    stores only the factors of its kx columns (1/P of them) -- then the
+    inverse path.  Two all-to-alls of one vector per apply."""
+
+    def __init__(self, kernel, mtilde, layout: Layout, backend, comm: _Comm, cap_bytes=2 ** 62):
+        self.L, self.B, self.C = layout, backend, comm
+        grid = kernel.grid
+        nx, ny, nz = grid.dims
+        m_z = _coerce_mz(grid, mtilde)
+        self.n = 3 * nz
+        _check_cap(nx * ny * self.n ** 2 * 16, cap_bytes, "reduce the box size or cross-section")
+        lam2 = backend.chan_xy(kernel)
+        owned = layout.kown[layout.rank]
+        nk = owned.size
+        # slot l*nk + kl factors block (l, owned[kl]); its right-hand side is
+        # column l*nk + kl of the (3nz, ny*nk) received array
+        kset = (np.arange(ny)[:, None] * nx + owned[None, :]).reshape(-1).astype(np.int64)
+        self.n_slots = int(kset.size)
+        self.n_stored_global = nx * ny
+        self.bytes_local = self.n_slots * self.n ** 2 * 16
+        self.factors, self.perm = backend.build_factors2(lam2, grid.dims, m_z, kset)
+        del lam2
+        items = np.stack([np.arange(self.n_slots)] * 2 + [np.ones(self.n_slots, np.int64)], 1)
+        self.items = backend.ints(items.reshape(-1) if self.n_slots else np.zeros(3, np.int32))
+        self.klist = backend.ints(np.arange(max(1, self.n_slots)))
+        off, cmap = layout.prec_cols()
+        self.col_off, self.colmap = backend.ints(off), backend.ints(cmap)
+
+    def apply(self, x_loc):
+        L, B, C = self.L, self.B, self.C
+        nx, ny, nz = L.dims
+        S = B.dft_lines(x_loc, L.nl, nx, False)
+        send = B.gather_cols(S, L.nl, nx, self.col_off, self.colmap, nx)
+        nk = L.nk
+        recv = B.empty(max(1, L.nlines * nk))
+        C.all_to_all(recv[:L.nlines * nk], send[:L.nl * nx],
+                     [L.lines_of(r) * nk for r in range(L.P)],
+                     [L.nl * L.kown[s].size for s in range(L.P)])
+        if self.n_slots:
+            B.dft_y(recv, 3 * nz, ny, nk, False)
+            B.solve(recv, self.n, self.factors, self.perm, self.items, self.n_slots, self.n_slots, self.klist,
+                    ny * nk)
+            B.dft_y(recv, 3 * nz, ny, nk, True)
         back = B.empty(max(1, L.nl * nx))
         C.all_to_all(back[:L.nl * nx], recv[:L.nlines * nk],
                      [L.nl * L.kown[s].size for s in range(L.P)],

@@ -81,6 +81,22 @@ class NumpyBackend:
         facs = [O.lu_checked(O.unfold_block_yz(lam[:, :, :, int(k)], m_yz)) for k in kset]
         return facs, None
 
+    def chan_xy(self, kernel):
+        # (6, 2nz-1, ny, nx): Chan along x then y, 2-D DFT (oracle build_two_level)
+        return scipy.fft.fftn(O.chan_along_axis(O.chan_along_axis(kernel.tensors, 3), 2), axes=(2, 3))
+
+    def build_factors2(self, lam2, dims, m_z, kset):
+        nx, ny, nz = dims
+        facs = []
+        for key in kset:
+            l, k = divmod(int(key), nx)
+            facs.append(O.lu_checked(O.unfold_block_z(lam2[:, :, l, k], m_z)))
+        return facs, None
+
+    def dft_y(self, Y, nplanes, ny, nk, inverse):
+        a = Y.numpy()[: nplanes * ny * nk].reshape(nplanes, ny, nk)
+        a[...] = (scipy.fft.ifft if inverse else scipy.fft.fft)(a, axis=1)
+
     def solve(self, Y, n, factors, perm, items, n_single, n_items, klist, s_row):
         y = Y.numpy()[: n * s_row].reshape(n, s_row)
         it = items.numpy().reshape(-1, 3)

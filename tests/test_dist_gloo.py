@@ -91,3 +91,64 @@ def test_sharded_solve_world2_matches_oracle(tmp_path, tol):
     assert abs(int(parts[0]["its"]) - ro["iterations"]) <= 2
     assert np.linalg.norm(xs - xo) / np.linalg.norm(xo) < 1e-7
     assert nx * 36 == xs.size
+
+
+def _worker2(rank, world, port, out_dir):
+    sys.path.insert(0, str(ROOT))
+    sys.path.insert(0, str(ROOT / "oracle"))
+    sys.path.insert(0, str(ROOT / "tests"))
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    import torch.distributed as dist
+
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from dist_numpy_backend import NumpyBackend
+    from paper_1903_07884_b200 import workloads
+    from paper_1903_07884_b200.dist import DistOperator, DistTwoLevelPrec, Layout, _Comm, gmres_sharded
+
+    W = workloads.small(12, 6, 3, delta=0.045e-6)
+    kern = W.kernel()
+    B, C = NumpyBackend(), _Comm()
+    L = Layout(W.grid.dims, world, rank, 2 * W.grid.nx)
+    op = DistOperator(kern, L, B, C)
+    m_full = torch.from_numpy(W.m.reshape(-1).copy())
+    mt = complex(np.mean(W.m))
+    prec = DistTwoLevelPrec(kern, mt, L, B, C)
+    rng = np.random.default_rng(11)
+    x = rng.normal(size=W.grid.n_unknowns) + 1j * rng.normal(size=W.grid.n_unknowns)
+    results = {"prec": prec.apply(torch.from_numpy(L.local_slice(x).copy())).numpy(), "nk": L.nk}
+    b_loc = torch.from_numpy(L.local_slice(W.b).copy())
+    xs, rep = gmres_sharded(lambda v: op.apply(m_full, v), b_loc, B, C, apply_pinv=prec.apply, tol=1e-8,
+                            maxit=200, restart=9)
+    results["x"] = xs.numpy()
+    results["its"] = rep.iterations
+    np.savez(os.path.join(out_dir, f"r{rank}.npz"), **results)
+    dist.destroy_process_group()
+
+
+def test_sharded_two_level_world2_matches_oracle(tmp_path):
+    """kx-sharded factors, y-DFT + (3nz)^2 solves per rank."""
+    world = 2
+    mp.spawn(_worker2, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import voxvie_oracle as O
+    from paper_1903_07884_b200 import workloads
+
+    W = workloads.small(12, 6, 3, delta=0.045e-6)
+    dims = W.grid.dims
+    t = W.kernel().tensors
+    spec = O.plan_spectra(t, dims)
+    p = O.build_two_level(t, dims, complex(np.mean(W.m)))
+    rng = np.random.default_rng(11)
+    x = rng.normal(size=W.grid.n_unknowns) + 1j * rng.normal(size=W.grid.n_unknowns)
+    parts = [dict(np.load(tmp_path / f"r{r}.npz")) for r in range(world)]
+    assert [int(q["nk"]) for q in parts] == [6, 6]
+    pr = np.concatenate([q["prec"] for q in parts])
+    ref = O.apply_prec(p, x)
+    assert np.linalg.norm(pr - ref) / np.linalg.norm(ref) < 1e-12
+    xo, ro = O.gmres(lambda v: O.apply_system(spec, dims, W.m, v), W.b,
+                     apply_pinv=lambda v: O.apply_prec(p, v), tol=1e-8, maxit=200, restart=9)
+    xs = np.concatenate([q["x"] for q in parts])
+    assert int(parts[0]["its"]) == int(parts[1]["its"])
+    assert abs(int(parts[0]["its"]) - ro["iterations"]) <= 2
+    assert np.linalg.norm(xs - xo) / np.linalg.norm(xo) < 1e-7
