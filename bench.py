@@ -374,12 +374,11 @@ def run_ours(args):
     m_host = W.m
     b_host = W.b
     torch.cuda.synchronize()
-    # N > 1: the 1-level configs run ONE sharded solve across all ranks (strong
-    # scaling: line-sharded vectors, k-sharded factors, NCCL all-to-all);
-    # 2-level config (c4) too, with kx-sharded factors; blocked configs run one
-    # replica per rank (weak scaling).
-    sharded = (world > 1 and W.prec["kind"] in ("one-level", "reduced-one-level", "two-level")
-               and not args.replicas)
+    # N > 1: every config runs ONE sharded solve across all ranks (strong
+    # scaling: line-sharded vectors, k-sharded factors, NCCL all-to-all; the
+    # blocked config redistributes each box's lines to the box's own layout);
+    # --replicas runs one independent solve per rank instead (weak scaling).
+    sharded = world > 1 and not args.replicas
     mode = "sharded" if sharded else ("replicas" if world > 1 else "single-gpu")
 
     # ---- setup (time-to-solution part 1): plan + preconditioner build
@@ -401,6 +400,15 @@ def run_ours(args):
         def dist_prec():
             if W.prec["kind"] == "two-level":
                 return DistTwoLevelPrec(kern, W.mtilde(), L, Bk, Cm)
+            if W.prec["kind"] == "blocked":
+                from paper_1903_07884_b200 import circulant as CC
+                from paper_1903_07884_b200.dist import DistBlockedPrec
+
+                boxes = [CC.Box(lbl, *b) for lbl, b in zip(W.prec["labels"], W.prec["boxes"])]
+                homog = ({lbl: W.prec["homogenization"] for lbl in W.prec["labels"]}
+                         if W.prec.get("homogenization") else None)
+                return DistBlockedPrec(kern, W.pmap, CC.partition_boxes(W.grid, boxes),
+                                       dict(zip(W.prec["labels"], W.prec["levels"])), L, Bk, Cm, homog=homog)
             return DistOneLevelPrec(kern, W.mtilde(), L, Bk, Cm, tol=ptol)
 
         prec = dist_prec()   # warm build
@@ -478,9 +486,10 @@ def run_ours(args):
     # ---- roofline of the dominant kernel (factor-streaming block solve)
     peak, peak_kind = peaks()
     if sharded:
-        stored_global = [(prec.n, prec.n_stored_global)]
-        stored = [(prec.n, prec.bytes_local // (16 * prec.n ** 2))]
-        nvec = W.grid.n_unknowns // world
+        pl = prec.box_precs if W.prec["kind"] == "blocked" else [prec]
+        stored_global = [(q.n, q.n_stored_global) for q in pl]
+        stored = [(pl[0].n, pl[0].bytes_local // (16 * pl[0].n ** 2))]   # per launch: first box / whole prec
+        nvec = prec.boxes[0]["n_loc"] if W.prec["kind"] == "blocked" else W.grid.n_unknowns // world
     else:
         stored = stored_global = stored_blocks_of(W, prec)
         nvec = W.grid.n_unknowns

@@ -410,6 +410,98 @@ class DistTwoLevelPrec:
         return B.dft_lines(S, L.nl, nx, True).reshape(-1)
 
 
+class DistBlockedPrec:
+    """Sharded blocked preconditioner (reference circulant.py:540-651; SURVEY
+    8(e) "Blocked": each box's frequency blocks spread over all ranks).  Per
+    box: the box's lines (c, z in box, y in box; x range [x0, x1)) move from
+    the global line ownership to the box's own line Layout (one all-to-all),
+    the box's sharded 1-level / reduced / 2-level preconditioner runs on them
+    (built on the box's generators and homogenised map, as build_blocked
+    does), and the result moves back (second all-to-all) into the box's x
+    range; identity outside the boxes."""
+
+    def __init__(self, kernel, pmap, partition, levels: dict, layout: Layout, backend, comm: _Comm, *,
+                 homog: dict | None = None, reduce_tol: float = 1e-3, cap_bytes=2 ** 62):
+        from .circulant import _DEFAULT_HOMOG, _slice_kernel, _sub_grid
+        from .grid import PermittivityMap, homogenize
+
+        self.L, self.B, self.C = layout, backend, comm
+        homog = homog or {}
+        grid = kernel.grid
+        nx, ny, nz = grid.dims
+        P, rank = layout.P, layout.rank
+        self.boxes, self.box_precs = [], []
+        self.bytes_local = 0
+        for box in partition.boxes:
+            choice = levels[box.label]
+            sgrid = _sub_grid(grid, box)
+            smap = PermittivityMap(sgrid, pmap.eps_r[box.z0:box.z1, box.y0:box.y1, box.x0:box.x1])
+            mt = homogenize(smap, homog.get(box.label, _DEFAULT_HOMOG.get(choice, "real_mean_x")))
+            skern = _slice_kernel(kernel, box)
+            bx, by, bz = box.dims
+            bL = Layout(sgrid.dims, P, rank, 2 * bx)
+            if choice == "one-level":
+                prec = DistOneLevelPrec(skern, mt, bL, backend, comm, cap_bytes=cap_bytes)
+            elif choice == "reduced-one-level":
+                if not 0.0 <= reduce_tol <= 1.0:
+                    raise ValueError(f"reduction tolerance must lie in [0, 1], got {reduce_tol}")
+                prec = DistOneLevelPrec(skern, mt, bL, backend, comm, tol=reduce_tol, cap_bytes=cap_bytes)
+            elif choice == "two-level":
+                prec = DistTwoLevelPrec(skern, mt, bL, backend, comm, cap_bytes=cap_bytes)
+            else:
+                raise ValueError(f"unknown per-box level {choice!r} for {box.label!r}")
+            self.bytes_local += prec.bytes_local
+            # global line and box line of every box line, in box-line order
+            c, z, y = np.meshgrid(np.arange(3), np.arange(box.z0, box.z1), np.arange(box.y0, box.y1),
+                                  indexing="ij")
+            gline = ((c * nz + z) * ny + y).reshape(-1)
+            bline = np.arange(gline.size)
+            og = np.searchsorted(layout.lb, gline, side="right") - 1
+            ob = np.searchsorted(bL.lb, bline, side="right") - 1
+            xr = np.arange(box.x0, box.x1)
+            send_idx, send_splits = [], []
+            for d in range(P):   # my global lines, grouped by their box owner
+                sel = gline[(og == rank) & (ob == d)]
+                send_idx.append(((sel - layout.line0)[:, None] * nx + xr[None, :]).reshape(-1))
+                send_splits.append(sel.size * bx)
+            recv_pos, recv_splits = [], []
+            for src in range(P):  # my box lines, grouped by their global owner
+                sel = bline[(ob == rank) & (og == src)]
+                recv_pos.append(((sel - bL.line0)[:, None] * bx + np.arange(bx)[None, :]).reshape(-1))
+                recv_splits.append(sel.size * bx)
+            self.box_precs.append(prec)
+            self.boxes.append(dict(prec=prec, n_loc=bL.nloc,
+                                   send_idx=np.concatenate(send_idx).astype(np.int64),
+                                   recv_pos=np.concatenate(recv_pos).astype(np.int64),
+                                   send_splits=send_splits, recv_splits=recv_splits, idx_dev={}))
+
+    @staticmethod
+    def _idx(bx_, key, dev):
+        import torch
+
+        t = bx_["idx_dev"].get((key, str(dev)))
+        if t is None:
+            t = torch.as_tensor(bx_[key], dtype=torch.long, device=dev)
+            bx_["idx_dev"][(key, str(dev))] = t
+        return t
+
+    def apply(self, x_loc):
+        B, C = self.B, self.C
+        y = x_loc.clone()
+        for bx_ in self.boxes:
+            si, rp = self._idx(bx_, "send_idx", x_loc.device), self._idx(bx_, "recv_pos", x_loc.device)
+            sendbuf = x_loc.reshape(-1)[si]
+            recv = B.empty(max(1, int(sum(bx_["recv_splits"]))))
+            C.all_to_all(recv[:rp.numel()], sendbuf, bx_["recv_splits"], bx_["send_splits"])
+            xb = B.empty(max(1, bx_["n_loc"]))
+            xb[rp] = recv[:rp.numel()]
+            yb = bx_["prec"].apply(xb[:bx_["n_loc"]])
+            back = B.empty(max(1, si.numel()))
+            C.all_to_all(back[:si.numel()], yb.reshape(-1)[rp], bx_["send_splits"], bx_["recv_splits"])
+            y.reshape(-1)[si] = back[:si.numel()]
+        return y
+
+
 # ------------------------------------------------------------------- GMRES
 def _norm(B, C, x, part):
     d = B.cgs_dots(x.reshape(1, -1), 0, x, part)

@@ -152,3 +152,60 @@ def test_sharded_two_level_world2_matches_oracle(tmp_path):
     assert int(parts[0]["its"]) == int(parts[1]["its"])
     assert abs(int(parts[0]["its"]) - ro["iterations"]) <= 2
     assert np.linalg.norm(xs - xo) / np.linalg.norm(xo) < 1e-7
+
+
+_BOXES = [("a", (0, 14, 0, 4, 0, 3), "one-level"), ("b", (2, 12, 4, 8, 0, 2), "reduced-one-level"),
+          ("c", (0, 9, 4, 8, 2, 3), "two-level")]
+
+
+def _worker3(rank, world, port, out_dir):
+    sys.path.insert(0, str(ROOT))
+    sys.path.insert(0, str(ROOT / "oracle"))
+    sys.path.insert(0, str(ROOT / "tests"))
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    import torch.distributed as dist
+
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from dist_numpy_backend import NumpyBackend
+    from paper_1903_07884_b200 import workloads
+    from paper_1903_07884_b200.circulant import Box, partition_boxes
+    from paper_1903_07884_b200.dist import DistBlockedPrec, Layout, _Comm
+
+    W = workloads.small(14, 8, 3, delta=0.045e-6)
+    kern = W.kernel()
+    B, C = NumpyBackend(), _Comm()
+    L = Layout(W.grid.dims, world, rank, 2 * W.grid.nx)
+    part = partition_boxes(W.grid, [Box(lbl, *b) for lbl, b, _ in _BOXES])
+    prec = DistBlockedPrec(kern, W.pmap, part, {lbl: lv for lbl, _, lv in _BOXES}, L, B, C, reduce_tol=0.3)
+    rng = np.random.default_rng(13)
+    x = rng.normal(size=W.grid.n_unknowns) + 1j * rng.normal(size=W.grid.n_unknowns)
+    np.savez(os.path.join(out_dir, f"r{rank}.npz"),
+             prec=prec.apply(torch.from_numpy(L.local_slice(x).copy())).numpy())
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_blocked_matches_oracle(tmp_path, world):
+    """SURVEY 8(e) blocked: per-box line redistribution + sharded box preconditioners."""
+    mp.spawn(_worker3, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import voxvie_oracle as O
+    from paper_1903_07884_b200 import workloads
+    from paper_1903_07884_b200.circulant import _DEFAULT_HOMOG, Box, _sub_grid
+    from paper_1903_07884_b200.grid import PermittivityMap, homogenize
+
+    W = workloads.small(14, 8, 3, delta=0.045e-6)
+    dims = W.grid.dims
+    mts = []
+    for lbl, b, lv in _BOXES:
+        bb = Box(lbl, *b)
+        smap = PermittivityMap(_sub_grid(W.grid, bb), W.pmap.eps_r[bb.z0:bb.z1, bb.y0:bb.y1, bb.x0:bb.x1])
+        mts.append(homogenize(smap, _DEFAULT_HOMOG[lv]))
+    p = O.build_blocked(W.kernel().tensors, dims, [b for _, b, _ in _BOXES], [lv for _, _, lv in _BOXES], mts,
+                        reduce_tol=0.3)
+    rng = np.random.default_rng(13)
+    x = rng.normal(size=W.grid.n_unknowns) + 1j * rng.normal(size=W.grid.n_unknowns)
+    pr = np.concatenate([dict(np.load(tmp_path / f"r{r}.npz"))["prec"] for r in range(world)])
+    ref = O.apply_prec(p, x)
+    assert np.linalg.norm(pr - ref) / np.linalg.norm(ref) < 1e-12

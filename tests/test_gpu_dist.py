@@ -262,3 +262,52 @@ def test_sharded_two_level_loopback(P):
     assert all(r[2] == results[0][2] for r in results)
     assert abs(results[0][2] - rep1.iterations) <= 2
     assert relerr(xs, x1) < 1e-6
+
+
+@pytest.mark.parametrize("P", [1, 2, 3])
+def test_sharded_blocked_loopback(P):
+    """SURVEY 8(e) blocked: per-box line redistribution and sharded box
+    preconditioners (1-level, reduced, 2-level boxes) on the CUDA backend
+    reproduce the single-GPU BlockedPrec (identity outside the boxes)."""
+    import threading
+
+    import torch
+
+    from paper_1903_07884_b200 import workloads
+    from paper_1903_07884_b200.circulant import Box, build_blocked, partition_boxes
+    from paper_1903_07884_b200.dist import CudaBackend, DistBlockedPrec, Layout
+    from paper_1903_07884_b200.operator import padded_length
+
+    W = workloads.small(30, 9, 4, delta=0.03e-6)
+    kern = W.kernel()
+    dims = W.grid.dims
+    spec = [("a", (0, 30, 0, 4, 0, 4), "one-level"), ("b", (3, 25, 4, 9, 0, 2), "reduced-one-level"),
+            ("c", (0, 17, 5, 9, 2, 4), "two-level")]
+    part = partition_boxes(W.grid, [Box(lbl, *b) for lbl, b, _ in spec])
+    levels = {lbl: lv for lbl, _, lv in spec}
+    comm = LoopbackComm(P)
+    rng = np.random.default_rng(17)
+    x = random_field(rng, W.grid.n_unknowns)
+    results = [None] * P
+    errors = []
+
+    def run(rank):
+        try:
+            torch.cuda.set_device(0)
+            B, C = CudaBackend(), comm.view(rank)
+            L = Layout(dims, P, rank, padded_length(dims[0]))
+            prec = DistBlockedPrec(kern, W.pmap, part, levels, L, B, C, reduce_tol=0.3)
+            xl = torch.from_numpy(L.local_slice(x).copy()).cuda()
+            results[rank] = prec.apply(xl).cpu().numpy()
+        except Exception as e:  # surface worker failures in the main thread
+            errors.append(e)
+            comm.bar.abort()
+
+    th = [threading.Thread(target=run, args=(r,)) for r in range(P)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errors, errors
+    p = build_blocked(kern, W.pmap, part, levels, reduce_tol=0.3, cap_bytes=2 ** 40)
+    assert relerr(np.concatenate(results), p.apply(x)) < 1e-11
