@@ -56,6 +56,8 @@ def parse():
     ap.add_argument("--config", default="c1", choices=["c0", "c1", "c1r", "c2", "c3", "c4", "c4b"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--shard", action="store_true",
+                    help="run the sharded (multi-GPU) code path even at N=1 (1-rank NCCL group)")
     ap.add_argument("--host-kernel", action="store_true",
                     help="assemble the generators on the host (numpy) instead of vx_assemble_green")
     ap.add_argument("--cpu-sample-blocks", type=int, default=24)
@@ -131,11 +133,25 @@ class Clocks:
 
 
 # ------------------------------------------------------------ dist helpers
-def dist_setup(torch):
+def dist_setup(torch, force=False):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
+    if world == 1 and force:
+        # --shard on one GPU: a 1-rank NCCL group drives the sharded code path
+        import socket
+
+        import torch.distributed as dist
+
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        if "MASTER_PORT" not in os.environ:
+            sk = socket.socket()
+            sk.bind(("127.0.0.1", 0))
+            os.environ["MASTER_PORT"] = str(sk.getsockname()[1])
+            sk.close()
+        torch.cuda.set_device(0)
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    elif world > 1:
         import torch.distributed as dist
 
         torch.cuda.set_device(local)
@@ -347,7 +363,7 @@ def run_ours(args):
     from paper_1903_07884_b200.operator import apply_system, plan_operator
     from paper_1903_07884_b200.solver import gmres
 
-    world, rank, local = dist_setup(torch)
+    world, rank, local = dist_setup(torch, force=args.shard)
     nv.load()
     nv.query("vx_solve_variant", 1 if args.solve_classic else 0)
     name = args.config
@@ -378,7 +394,7 @@ def run_ours(args):
     # scaling: line-sharded vectors, k-sharded factors, NCCL all-to-all; the
     # blocked config redistributes each box's lines to the box's own layout);
     # --replicas runs one independent solve per rank instead (weak scaling).
-    sharded = world > 1 and not args.replicas
+    sharded = (world > 1 or args.shard) and not args.replicas
     mode = "sharded" if sharded else ("replicas" if world > 1 else "single-gpu")
 
     # ---- setup (time-to-solution part 1): plan + preconditioner build
@@ -618,7 +634,7 @@ def run_ours(args):
     }
     if rank == 0:
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if world > 1 or args.shard:
         torch.distributed.destroy_process_group()
 
 
