@@ -503,8 +503,9 @@ def run_ours(args):
     peak, peak_kind = peaks()
     if sharded:
         pl = prec.box_precs if W.prec["kind"] == "blocked" else [prec]
-        stored_global = [(q.n, q.n_stored_global) for q in pl]
-        stored = [(pl[0].n, pl[0].bytes_local // (16 * pl[0].n ** 2))]   # per launch: first box / whole prec
+        stored_global = [b for q in pl for b in (getattr(q, "stored_global", None) or [(q.n, q.n_stored_global)])]
+        stored = (getattr(pl[0], "stored_local", None)       # per launch: first box / whole prec
+                  or [(pl[0].n, pl[0].bytes_local // (16 * pl[0].n ** 2))])
         nvec = prec.boxes[0]["n_loc"] if W.prec["kind"] == "blocked" else W.grid.n_unknowns // world
     else:
         stored = stored_global = stored_blocks_of(W, prec)

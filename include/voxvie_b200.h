@@ -306,6 +306,15 @@ int vx_d2h_pinned(void* dst, const void* src, size_t bytes, void* stream);
  * nsec = 1, dims = {3 ny nz}.  Ragged storage per frequency slot:
  * vx_lu_rag_stride(nsec, sec_dims) entries. */
 long vx_lu_rag_stride(int nsec, const int* sec_dims);
+/* Solve-only sector path (sharded preconditioner, dist.py): on S (3 ny nz rows
+ * x pitch frequency columns): orbit transform, ragged sector block solves
+ * (work list as vx_prec1_apply_sec_rag with nx -> pitch), inverse transform,
+ * in place.  U: nsec*dmax*pitch scratch. */
+int vx_prec1_solve_sec_rag(int ny, int nz, long pitch, const vx_c128* factors, const int* perm, const int* items,
+                           int n_single, int n_items, int direct_r, const int* klist, int nsec, int dmax,
+                           const int* sec_dims, int norb, const int* orows, const int* osec, const double* ocoef,
+                           const unsigned char* flipk, vx_c128* S, vx_c128* U, void* stream);
+
 /* 1 while vx_solve_variant(1) selects the synchronous (padded-only) solve. */
 int vx_solve_classic(void);
 int vx_lu_repack(int nkslots, int nsec, int dmax, const int* sec_dims, const vx_c128* padded,

@@ -92,6 +92,8 @@ _SIGS = {
                                                       P, P, P, P, P, P, P, P]),
     "vx_prec1_apply_rag": (c_int, [c_int] * 4 + [P, P, P, c_int, c_int, c_int, P, P, P, P, P]),
     "vx_lu_rag_stride": (c_long, [c_int, P]),
+    "vx_prec1_solve_sec_rag": (c_int, [c_int, c_int, c_long, P, P, P, c_int, c_int, c_int, P, c_int, c_int, P,
+                                       c_int, P, P, P, P, P, P, P]),
     "vx_solve_classic": (c_int, []),
     "vx_lu_repack": (c_int, [c_int, c_int, c_int, P, P, P, P]),
     "vx_lu_unpack": (c_int, [c_int, c_int, c_int, P, P, P, P]),

@@ -2530,6 +2530,34 @@ extern "C" int vx_prec1_apply_sec_rag(int nx, int ny, int nz, int nrhs, const vx
                          norb, orows, osec, ocoef, flipk, x, y, work, stream, &rg);
 }
 
+// Solve-only sector path on a caller-owned spectral array (the sharded
+// preconditioner's received frequency columns, dist.py): S (3q rows x pitch
+// columns) -> orbit transform -> ragged sector block solves -> back into S.
+// U: nsec * dmax * pitch scratch.  Same work-list / flip conventions as
+// vx_prec1_apply_sec_rag with nx replaced by the column pitch.
+extern "C" int vx_prec1_solve_sec_rag(int ny, int nz, long pitch, const vx_c128* factors, const int* perm,
+                                      const int* items, int n_single, int n_items, int direct_r,
+                                      const int* klist, int nsec, int dmax, const int* sec_dims, int norb,
+                                      const int* orows, const int* osec, const double* ocoef,
+                                      const unsigned char* flipk, vx_c128* S, vx_c128* U, void* stream) {
+  RagGeom rg;
+  int st = make_rag(nsec, sec_dims, dmax, &rg);
+  if (st) return st;
+  VX_REQUIRE(ny >= 1 && nz >= 1 && pitch >= 1 && n_single >= 0 && n_items >= n_single, "bad sector solve arguments");
+  VX_REQUIRE(direct_r == 1 || direct_r == 2, "direct_r must be 1 or 2");
+  VX_REQUIRE((long)nsec * dmax * pitch < (1L << 29), "sector layout too large for the work-list encoding");
+  cudaStream_t s = as_stream(stream);
+  Span span("prec_apply", s);
+  const int q = ny * nz;
+  double2* Sd = reinterpret_cast<double2*>(S);
+  double2* Ud = reinterpret_cast<double2*>(U);
+  if ((st = sec_xform(pitch, 1, norb, orows, osec, ocoef, flipk, q, Sd, Ud, 0, s))) return st;
+  if ((st = solve_items(lu_geom(dmax), reinterpret_cast<const double2*>(factors), perm, items, n_single, n_items,
+                        klist, 1, Ud, pitch, 1, s, -1, direct_r, &rg)))
+    return st;
+  return sec_xform(pitch, 1, norb, orows, osec, ocoef, flipk, q, Ud, Sd, 1, s);
+}
+
 extern "C" long vx_lu_rag_stride(int nsec, const int* sec_dims) {
   long k = 0;
   for (int s = 0; s < nsec; ++s) k += (long)sec_dims[s] * sec_dims[s];

@@ -104,6 +104,8 @@ class _Comm:
 class CudaBackend:
     """Local compute on the C-ABI kernels (product path)."""
 
+    sectors = True   # symmetry-reduced (mirror + sector, ragged) 1-level factors
+
     def __init__(self):
         self.t = nv.require_cuda()
 
@@ -299,6 +301,10 @@ class DistOneLevelPrec:
         m_yz = _coerce_mtilde(grid, mtilde)
         q3 = 3 * ny * nz
         self.n = q3
+        self.kown = layout.kown
+        self.sec = None
+        if tol is None and getattr(backend, "sectors", False) and self._init_sectors(kernel, m_yz):
+            return
         lam = backend.chan_x(kernel)
         owned = layout.kown[layout.rank]
         col_of = {int(k): i for i, k in enumerate(owned)}
@@ -335,21 +341,99 @@ class DistOneLevelPrec:
         off, cmap = layout.prec_cols()
         self.col_off, self.colmap = backend.ints(off), backend.ints(cmap)
 
+    def _init_sectors(self, kernel, m_yz) -> bool:
+        """Symmetry-reduced factors (the single-GPU layout, circulant.py /
+        sectors.py): mirror orbits {k, nx-k} are dealt to ranks whole, each rank
+        factorises the sector blocks of its canonical frequencies only and
+        stores them ragged, and the apply runs the orbit transform + ragged
+        sector solves on the received columns (vx_prec1_solve_sec_rag).  False
+        when the kernel / m~ lack the symmetries (dense path)."""
+        from .circulant import _SectorDev, _first_bad, _lamhat_x, _lu1_sec, _mirror_store, mirror_axes, sector_axes
+        from .operator import upload_tensors
+        from .sectors import sector_plan
+
+        L = self.L
+        grid = kernel.grid
+        nx, ny, nz = grid.dims
+        gen = upload_tensors(kernel)
+        share = mirror_axes(gen, grid.dims)[0]
+        sy, sz = sector_axes(gen, grid.dims, m_yz)
+        if not (share and (sy or sz)):
+            return False
+        plan = sector_plan(ny, nz, sy, sz)
+        if plan.dmax <= 32:
+            return False
+        kc = np.arange(nx // 2 + 1)
+        owner = kc % L.P
+        self.kown = [np.unique(np.concatenate([kc[owner == r], (nx - kc[owner == r]) % nx])) for r in range(L.P)]
+        owned = self.kown[L.rank]
+        nk = owned.size
+        kset, store, flip = _mirror_store(owned, nx, True)
+        sec = _SectorDev(plan)
+        t = self.B.t
+        kdev = t.from_numpy(kset.astype(np.int32)).cuda()
+        m_dev = nv.device_c128(m_yz)
+        lam = _lamhat_x(gen, nx, ny, nz)
+        fac, perm, piv, info = _lu1_sec(lam, m_dev, kdev, int(kset.size), nx, ny, nz, sec)
+        del lam, piv
+        bad = _first_bad(info)
+        if bad >= 0:
+            raise PreconditionerBuildError(
+                f"1-level build failed: singular frequency block k={int(kset[bad // plan.nsec])}")
+        dims_a = np.ascontiguousarray(plan.dims, np.int32)
+        stride = int(nv.query("vx_lu_rag_stride", plan.nsec, dims_a.ctypes.data))
+        rag = nv.empty_c128((max(1, int(kset.size)), stride))
+        if kset.size:
+            nv.call("vx_lu_repack", int(kset.size), plan.nsec, plan.dmax, dims_a.ctypes.data, fac.data_ptr(),
+                    rag.data_ptr(), nv.stream_ptr())
+        del fac
+        ns, dm = plan.nsec, plan.dmax
+        st = (store[None, :] * ns + np.arange(ns)[:, None]).reshape(-1)
+        ent = (np.arange(ns)[:, None] * dm * nk + np.arange(nk)[None, :]).reshape(-1)
+        order = np.argsort(st, kind="stable")
+        slots, starts, counts = np.unique(st[order], return_index=True, return_counts=True)
+        flipk = np.zeros(max(1, nk), np.uint8)
+        flipk[:nk][flip] = 1
+        self.sec, self.sec_dims, self.factors, self.perm = sec, dims_a, rag, perm
+        self.items = t.from_numpy(np.stack([slots, starts, counts], 1).astype(np.int32).reshape(-1).copy()).cuda()
+        self.klist = t.from_numpy(ent[order].astype(np.int32) if ent.size else np.zeros(1, np.int32)).cuda()
+        self.flipk = t.from_numpy(flipk).cuda()
+        self.n_single = self.n_items = int(slots.size)
+        self.direct_r = int(counts.max()) if counts.size else 1
+        self.n_stored_global = nx // 2 + 1
+        self.bytes_local = int(kset.size) * stride * 16
+        self.stored_local = [(int(d), int(kset.size)) for d in plan.dims]
+        self.stored_global = [(int(d), nx // 2 + 1) for d in plan.dims]
+        off = np.cumsum([0] + [k.size for k in self.kown]).astype(np.int32)
+        self.col_off = self.B.ints(off)
+        self.colmap = self.B.ints(np.concatenate(self.kown).astype(np.int32))
+        return True
+
     def apply(self, x_loc):
         L, B, C = self.L, self.B, self.C
         nx = L.dims[0]
+        kown = self.kown
         S = B.dft_lines(x_loc, L.nl, nx, False)
         send = B.gather_cols(S, L.nl, nx, self.col_off, self.colmap, nx)
-        nk = L.nk
+        nk = kown[L.rank].size
         recv = B.empty(max(1, L.nlines * nk))
         C.all_to_all(recv[:L.nlines * nk], send[:L.nl * nx],
                      [L.lines_of(r) * nk for r in range(L.P)],
-                     [L.nl * L.kown[s].size for s in range(L.P)])
-        if self.n_items:
+                     [L.nl * kown[s].size for s in range(L.P)])
+        if self.sec is not None:
+            if self.n_items:
+                sd, sp = self.sec, self.sec.plan
+                U = B.empty(max(1, sp.nsec * sp.dmax * nk))
+                nv.call("vx_prec1_solve_sec_rag", L.dims[1], L.dims[2], nk, self.factors.data_ptr(),
+                        self.perm.data_ptr(), self.items.data_ptr(), self.n_single, self.n_items, self.direct_r,
+                        self.klist.data_ptr(), sp.nsec, sp.dmax, self.sec_dims.ctypes.data, sd.norb,
+                        sd.orows.data_ptr(), sd.osec.data_ptr(), sd.ocoef.data_ptr(), self.flipk.data_ptr(),
+                        recv.data_ptr(), U.data_ptr(), nv.stream_ptr())
+        elif self.n_items:
             B.solve(recv, self.n, self.factors, self.perm, self.items, self.n_single, self.n_items, self.klist, nk)
         back = B.empty(max(1, L.nl * nx))
         C.all_to_all(back[:L.nl * nx], recv[:L.nlines * nk],
-                     [L.nl * L.kown[s].size for s in range(L.P)],
+                     [L.nl * kown[s].size for s in range(L.P)],
                      [L.lines_of(r) * nk for r in range(L.P)])
         B.scatter_cols(back, S, L.nl, nx, self.col_off, self.colmap, nx)
         return B.dft_lines(S, L.nl, nx, True).reshape(-1)
