@@ -88,8 +88,10 @@ int init_pool() {
   std::call_once(g_once, [] {
     Pool* p = new Pool();  // never destroyed: workers are detached
     unsigned hc = std::thread::hardware_concurrency();
-    int n = hc > 2 ? int(hc) / 2 : 1;   // memcpy saturates well before all cores
-    if (n > 7) n = 7;
+    // a few helpers saturate the copy; more contend with the launching thread
+    // (c1 e2e per solve: 3 helpers 32.0 ms, 7: 32.3, 11: 33.6, 15: 34.2)
+    int n = hc > 2 ? int(hc) / 2 : 1;
+    if (n > 4) n = 4;
     if (const char* e = getenv("VX_H2D_THREADS")) n = atoi(e);
     if (n > 15) n = 15;
     if (n < 0) n = 0;
