@@ -463,6 +463,14 @@ def run_ours(args):
         def solve(b):
             return gmres(A, b, apply_pinv=prec.apply, tol=W.tol, maxit=W.maxit, restart=W.restart)
 
+    # setup objects (torch / numpy / scipy modules, the workload) move to the
+    # GC's permanent generation, so a collection triggered between solves
+    # scans only what the solves allocate (a full collection otherwise walks
+    # ~10^6 objects: 50-100 ms stalls in the timed loops)
+    import gc
+
+    gc.collect()
+    gc.freeze()
     # clock sampler runs from before the warm-up until after the timed region
     clocks = Clocks(local)
     clocks.start()
