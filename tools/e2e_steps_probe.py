@@ -14,7 +14,7 @@ from paper_1903_07884_b200.kernel import assemble_kernel_device  # noqa: E402
 from paper_1903_07884_b200.operator import apply_system, plan_operator  # noqa: E402
 from paper_1903_07884_b200.solver import gmres  # noqa: E402
 
-W = workloads.make("c1")
+W = workloads.make(sys.argv[1] if len(sys.argv) > 1 else "c1")
 kern = assemble_kernel_device(W.grid, W.physics.k0)
 plan = plan_operator(kern)
 prec = bench.build_prec(W, kern)
@@ -39,3 +39,11 @@ for i in range(10):
     x, rep = step()
     t1 = time.perf_counter()
     print(f"step {i}: {(t1 - t0) * 1e3:.2f} ms  (solve_seconds {rep.solve_seconds * 1e3:.2f})", flush=True)
+bd, md = torch.from_numpy(b_host.copy()).cuda(), torch.from_numpy(W.m.reshape(-1).copy()).cuda()
+for i in range(3):
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    xd, rep = gmres(lambda v: apply_system(plan, md, v), bd, apply_pinv=prec.apply, tol=W.tol, maxit=W.maxit,
+                    restart=W.restart)
+    torch.cuda.synchronize()
+    print(f"device-resident solve {i}: {(time.perf_counter() - t0) * 1e3:.2f} ms, its {rep.iterations}", flush=True)
