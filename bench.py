@@ -546,15 +546,11 @@ def run_ours(args):
     # ---- e2e through the public API with host numpy buffers
     e2e = None
     if not args.no_e2e:
-        # two host copies of m used alternately: each step's m is a different
-        # array, so the API uploads it (no device-side cache hit), without a
-        # fresh allocation (page faults) inside the timed region
-        m_copies = [np.array(m_host, copy=True), np.array(m_host, copy=True)]
-        e2e_count = [0]
+        # m is a writeable host array: the API uploads it once per solve (its
+        # device copy lives only for the solve's scope, operator._medium_in)
+        m_step = m_host
 
         def e2e_step():
-            m_step = m_copies[e2e_count[0] % 2]                # forces the H2D copy of m
-            e2e_count[0] += 1
             if sharded:
                 # host buffers through the sharded API: local slice of b in, local x out
                 m_d = torch.from_numpy(m_step.reshape(-1)).cuda()

@@ -8,6 +8,7 @@ and the current CUDA stream.
 
 from __future__ import annotations
 
+import contextlib
 import ctypes as C
 import os
 import threading
@@ -222,6 +223,37 @@ def empty_c128(n, device=None):
     t = require_cuda()
     shape = (n,) if isinstance(n, int) else tuple(n)
     return t.empty(shape, dtype=t.complex128, device="cuda" if device is None else device)
+
+
+_scope = threading.local()
+
+
+@contextlib.contextmanager
+def solve_scope():
+    """A solve in progress on this thread: host inputs that the caller passes
+    unchanged to every operator call of the solve (the medium map m) may be
+    uploaded once per scope instead of once per call.  Nested scopes share the
+    outermost token."""
+    outer = getattr(_scope, "token", None)
+    if outer is None:
+        _scope.token = object()
+    try:
+        yield
+    finally:
+        if outer is None:
+            _scope.token = None
+
+
+def scope_token():
+    """The active solve scope's token on this thread (None outside a solve)."""
+    return getattr(_scope, "token", None)
+
+
+def fresh_output(f):
+    """Mark a callable whose every result is a newly allocated buffer (the
+    GMRES Z basis may then keep the result itself instead of a copy)."""
+    f._vx_fresh_output = True
+    return f
 
 
 def is_tensor(a) -> bool:

@@ -317,9 +317,12 @@ def _as_rhs(x, nunk):
         a = np.asarray(x, dtype=np.complex128)
         shape = a.shape
         xd = nv.device_c128(a)
+    # reference circulant.py:176-188: any array whose size is a multiple of
+    # the unknown count is read as x.reshape(n_unknowns, -1) (C order) and the
+    # result returned in the input's shape (flat for 1-D input)
     flat = len(shape) == 1
-    if xd.numel() % nunk != 0 or (not flat and shape[0] != nunk) or (flat and shape[0] != nunk):
-        raise ValueError(f"vector has {xd.numel()} entries, expected {nunk} x r")
+    if xd.numel() % nunk != 0:
+        raise ValueError(f"cannot reshape array of size {xd.numel()} into shape ({nunk},newaxis)")
     r = xd.numel() // nunk
     return xd.reshape(nunk, r).contiguous(), r, flat, is_t, shape
 
@@ -454,8 +457,11 @@ class _OneLevelBase:
             self._padded_fac = pad
         return self._padded_fac
 
+    @nv.fresh_output
     def apply(self, x):
         xd, r, flat, is_t, shape = _as_rhs(x, self.grid.n_unknowns)
+        if r == 0:
+            return _ret(xd.clone(), flat, is_t, shape)
         return _ret(self._apply_dev(xd, r), flat, is_t, shape)
 
     @property
@@ -808,8 +814,11 @@ class TwoLevelPrec:
                 xd.data_ptr(), y.data_ptr(), work.data_ptr(), nv.stream_ptr())
         return y
 
+    @nv.fresh_output
     def apply(self, x):
         xd, r, flat, is_t, shape = _as_rhs(x, self.grid.n_unknowns)
+        if r == 0:
+            return _ret(xd.clone(), flat, is_t, shape)
         return _ret(self._apply_dev(xd, r), flat, is_t, shape)
 
     def summary(self) -> dict:
@@ -1008,8 +1017,11 @@ class BlockedPrec:
                     ys.data_ptr(), y.data_ptr(), nv.stream_ptr())
         return y
 
+    @nv.fresh_output
     def apply(self, x):
         xd, r, flat, is_t, shape = _as_rhs(x, self.grid.n_unknowns)
+        if r == 0:
+            return _ret(xd.clone(), flat, is_t, shape)
         return _ret(self._apply_dev(xd, r), flat, is_t, shape)
 
     def summary(self) -> dict:

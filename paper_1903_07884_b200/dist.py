@@ -593,6 +593,27 @@ def _norm(B, C, x, part):
     return float(np.sqrt(B.to_host(d)[0].real))
 
 
+class _Basis:
+    """Krylov basis rows on the backend, grown geometrically (as the
+    single-GPU solver._Krylov): a solve that converges in a few iterations
+    never allocates the (mmax + 1) x n basis of the worst case."""
+
+    def __init__(self, B, n, maxrows):
+        self.B, self.n, self.maxrows = B, n, maxrows
+        self.V, self.cap = None, 0
+        self.ensure(min(maxrows, 32))
+
+    def ensure(self, rows):
+        if rows <= self.cap:
+            return self.V
+        rows = min(max(rows, 2 * self.cap), max(self.maxrows, rows))
+        V = self.B.empty((rows, self.n))
+        if self.V is not None:
+            V[: self.cap].copy_(self.V[: self.cap])
+        self.V, self.cap = V, rows
+        return V
+
+
 def gmres_sharded(apply_a, b_loc, backend, comm: _Comm, *, apply_pinv=None, tol=1e-4, maxit=2000,
                   restart=None):
     """Right-preconditioned restarted GMRES on line-sharded vectors (reference
@@ -623,7 +644,7 @@ def _gmres_sharded(apply_a, b_loc, backend, comm: _Comm, *, apply_pinv=None, tol
                                                            true_residual=0.0)
     op = apply_a if apply_pinv is None else (lambda v: apply_a(apply_pinv(v)))
     x = B.axpby(0.0, b_loc, 0.0, None)
-    V = B.empty((mmax + 1, n))
+    basis = _Basis(B, n, mmax + 1)
     residuals = [1.0]
     total = 0
     converged = False
@@ -634,6 +655,7 @@ def _gmres_sharded(apply_a, b_loc, backend, comm: _Comm, *, apply_pinv=None, tol
             converged = True
             break
         m = maxit - total if restart is None else min(restart, maxit - total)
+        V = basis.V
         B.axpby(1.0 / beta, r0, 0.0, None, out=V[0])
         qr = GivensQR(beta)
         j = 0
@@ -652,6 +674,7 @@ def _gmres_sharded(apply_a, b_loc, backend, comm: _Comm, *, apply_pinv=None, tol
                 n1 = float(np.sqrt(B.to_host(C.all_reduce(B.cgs_update(V, j + 1, c, w, part)))[0].real))
             h[j + 1] = n1
             lucky = n1 <= 1e-14 * max(n0, 1e-300)
+            V = basis.ensure(j + 2)
             B.axpby(1.0 / n1 if n1 > 0 else 0.0, w, 0.0, None, out=V[j + 1])
             qr.add_column(h, j, residuals, tol)
             j += 1

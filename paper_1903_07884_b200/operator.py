@@ -173,14 +173,23 @@ def _medium_in(plan: OperatorPlan, m):
         if m.numel() != plan.grid.n_voxels:
             raise ValueError("coefficient map size does not match grid")
         return nv.device_c128(m.reshape(-1))
+    # The reference re-reads m on every call (operator.py:101-105), so a host
+    # m may change between calls.  Its device copy is reused only while it
+    # provably cannot have: inside one solve (gmres opens a solve scope; the
+    # caller's code does not run between the solve's operator calls), or for
+    # a frozen array that owns its data (setflags(write=False), as the
+    # reference does for its own immutable inputs).  Callers that want
+    # zero-copy reuse across solves pass a CUDA tensor.
+    tok = nv.scope_token()
+    frozen = isinstance(m, np.ndarray) and not m.flags.writeable and m.flags.owndata
     cached = getattr(plan, "_m_cache", None)
-    if cached is not None and cached[0] is m:
+    if cached is not None and cached[0] is m and (frozen or (tok is not None and cached[2] is tok)):
         return cached[1]
     a = np.asarray(m, dtype=np.complex128)
     if a.size != plan.grid.n_voxels:
         raise ValueError("coefficient map size does not match grid")
     d = nv.device_c128(a.reshape(-1))
-    object.__setattr__(plan, "_m_cache", (m, d))
+    object.__setattr__(plan, "_m_cache", (m, d, tok))
     return d
 
 

@@ -68,6 +68,15 @@ class _Callable:
         self.f = f
         self.n = n
         self.mode = None
+        # our preconditioners / operators allocate a new output every call
+        # (marked by _native.fresh_output); anything else may hand back a
+        # buffer it reuses on the next call
+        self.declared_fresh = bool(getattr(f, "_vx_fresh_output", False))
+
+    @property
+    def fresh(self) -> bool:
+        """True when every result is a new buffer (host-mode copies always are)."""
+        return self.mode == "host" or self.declared_fresh
 
     def __call__(self, v):
         if self.mode != "host":
@@ -101,7 +110,8 @@ class _Krylov:
         self.cap = 0
         self.maxrows = m + 1
         self.V = None
-        self.Z = None
+        self.Z = None      # copies of z_j for callables that may reuse their output buffer
+        self.zcap = 0
         self.keep_z = keep_z
         self._grow(min(m + 1, 32))
         self.h = nv.empty_c128(m + 2)
@@ -129,6 +139,17 @@ class _Krylov:
         if i >= self.cap:
             self._grow(min(max(i + 1, 2 * self.cap), max(self.maxrows, i + 1)))
         return self.V[i]
+
+    def zrow(self, i):
+        """Row i of the Z basis (grown geometrically like V, allocated only
+        when the preconditioner may reuse its output buffer)."""
+        if i >= self.zcap:
+            rows = min(max(i + 1, 2 * self.zcap, min(self.maxrows, 32)), max(self.maxrows, i + 1))
+            Z = nv.empty_c128((rows, self.n))
+            if self.Z is not None:
+                Z[: self.zcap].copy_(self.Z)
+            self.Z, self.zcap = Z, rows
+        return self.Z[i]
 
     def norm(self, x) -> float:
         nv.call("vx_norm2", self.n, x.data_ptr(), self.nrm.data_ptr(), self.part.data_ptr(),
@@ -245,8 +266,13 @@ def _gmres_cycle(K: _Krylov, op, r0, beta, bnorm, tol, m, residuals, P=None, A=N
             z = P(v)
             if not z.is_contiguous() or z.numel() != K.n:
                 z = z.reshape(-1).contiguous()
-            if _aliases(z, K.V) or any(z.data_ptr() == o.data_ptr() for o in zl[:j]):
-                z = z.clone()  # the callable returned its argument or a reused buffer
+            if not P.fresh or _aliases(z, K.V):
+                # the callable may hand the same buffer back next call (or
+                # returned a view of its argument): keep a private copy, or
+                # z_j would be overwritten before u = Z y is formed
+                zr = K.zrow(j)
+                zr.copy_(z)
+                z = zr
             if len(zl) > j:
                 zl[j] = z
             else:
@@ -318,7 +344,7 @@ def gmres(apply_a, b, *, apply_pinv=None, tol: float = 1e-4, maxit: int = 2000,
     (and restored afterwards): a full collection with torch loaded walks ~10^6
     objects (tens of ms), long enough to drain the one-iteration-deep device
     queue of the pipelined Arnoldi loop; the solve itself creates no cycles."""
-    with gc_paused():
+    with gc_paused(), nv.solve_scope():
         return _gmres(apply_a, b, apply_pinv=apply_pinv, tol=tol, maxit=maxit, restart=restart)
 
 
