@@ -337,7 +337,7 @@ def solve_kernel_traffic(name, W, world):
     if W.prec["kind"] == "two-level":
         kname = "lu_solve_small_kernel"
     elif W.prec["kind"] == "reduced-one-level":
-        kname = "lu_solve_pipe_kernel<2>/<8>"
+        kname = "lu_solve_rag_kernel<2> + rep_gemm_kernel"
     traffic = None
     f = ROOT / "profiles" / "r01_solve_traffic.json"
     if world == 1 and f.exists():

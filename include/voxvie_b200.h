@@ -332,6 +332,22 @@ int vx_prec1_apply_sec_rag(int nx, int ny, int nz, int nrhs, const vx_c128* fact
                            const int* osec, const double* ocoef, const unsigned char* flipk,
                            const vx_c128* x, vx_c128* y, vx_c128* work, void* stream);
 
+/* Reduced scheme on sector factors (ReducedOneLevelPrec.apply,
+ * circulant.py:264-269, with the symmetry sectors above): items [0, n_single)
+ * are the kept blocks' sector solves (ragged factors when sec_dims is given,
+ * else the padded dmax geometry); the n_rep discarded frequencies rep_ks are,
+ * per sector s, one FP64 tensor-core GEMM with the representative sector
+ * block's explicit inverse rep_inv + s * vx_rep_inverse_elems(dmax) (formed
+ * by vx_rep_inverse on the padded sector factor), on a side stream
+ * concurrently with the single-block solves.  work holds
+ * vx_prec1_sec_reduced_work_elems entries. */
+long vx_prec1_sec_reduced_work_elems(int nx, int ny, int nz, int nrhs, int nsec, int dmax, int n_rep);
+int vx_prec1_apply_sec_reduced(int nx, int ny, int nz, int nrhs, const vx_c128* factors, const int* perm,
+                               const int* items, int n_single, int direct_r, const int* klist, int nsec, int dmax,
+                               const int* sec_dims, int norb, const int* orows, const int* osec, const double* ocoef,
+                               const unsigned char* flipk, const vx_c128* rep_inv, const int* rep_ks, int n_rep,
+                               const vx_c128* x, vx_c128* y, vx_c128* work, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

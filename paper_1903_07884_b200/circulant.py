@@ -667,6 +667,22 @@ class ReducedOneLevelPrec(_OneLevelBase):
         if self._sec is not None:
             keep = np.arange(self.kept.size) != rep_idx
             rep_ks = np.flatnonzero(self.slot_of == rep_idx)
+            ns, dm = self._sec.plan.nsec, self._sec.plan.dmax
+            if dm > 32 and rep_ks.size >= 8 and os.environ.get("VX_REP_GEMM", "1") != "0":
+                # the discarded frequencies: per sector ONE GEMM with the
+                # representative sector block's explicit inverse (side stream);
+                # the kept blocks' sector solves stream ragged factors
+                self._sector_items(self._store[keep], self.kept[keep], self._flip[keep])
+                per = int(nv.query("vx_rep_inverse_elems", dm))
+                inv = nv.empty_c128(ns * per)
+                for sc in range(ns):
+                    sl = rep_slot * ns + sc
+                    nv.call("vx_rep_inverse", dm, self._fac[sl].data_ptr(), self._perm[sl].data_ptr(),
+                            inv[sc * per:].data_ptr(), nv.stream_ptr())
+                self._inv = inv
+                self._rep_ks = t.from_numpy(rep_ks.astype(np.int32)).cuda()
+                self._make_ragged()
+                return
             self._sector_items(self._store[keep], self.kept[keep], self._flip[keep], rep=(rep_slot, rep_ks))
             return
         groups = {}
@@ -694,6 +710,8 @@ class ReducedOneLevelPrec(_OneLevelBase):
             self._rep_ks = t.from_numpy(rep_ks.astype(np.int32)).cuda()
 
     def _apply_dev(self, xd, r):
+        if self._inv is not None and self._sec is not None:
+            return self._apply_sec_rep(xd, r)
         if self._inv is None or self._sec is not None:
             return super()._apply_dev(xd, r)
         nx, ny, nz = self.grid.dims
@@ -703,6 +721,21 @@ class ReducedOneLevelPrec(_OneLevelBase):
         nv.call("vx_prec1_apply_reduced", nx, ny, nz, r, self._fac.data_ptr(), self._perm.data_ptr(),
                 self._items.data_ptr(), self._n_single, self._direct_r, self._klist.data_ptr(), self._inv.data_ptr(),
                 self._rep_ks.data_ptr(), n_rep, xd.data_ptr(), y.data_ptr(), work.data_ptr(), nv.stream_ptr())
+        return y
+
+    def _apply_sec_rep(self, xd, r):
+        nx, ny, nz = self.grid.dims
+        sp, sd = self._sec.plan, self._sec
+        rag = self._rag_dims is not None and r == 1 and not nv.query("vx_solve_classic")
+        fac = self._fac if (rag or self._rag_dims is None) else self._padded()
+        n_rep = int(self._rep_ks.numel())
+        y = nv.empty_c128((self.grid.n_unknowns, r))
+        work = nv.empty_c128(int(nv.query("vx_prec1_sec_reduced_work_elems", nx, ny, nz, r, sp.nsec, sp.dmax, n_rep)))
+        nv.call("vx_prec1_apply_sec_reduced", nx, ny, nz, r, fac.data_ptr(), self._perm.data_ptr(),
+                self._items.data_ptr(), self._n_single, self._direct_r, self._klist.data_ptr(), sp.nsec, sp.dmax,
+                self._rag_dims.ctypes.data if rag else None, sd.norb, sd.orows.data_ptr(), sd.osec.data_ptr(),
+                sd.ocoef.data_ptr(), self._flipk.data_ptr(), self._inv.data_ptr(), self._rep_ks.data_ptr(), n_rep,
+                xd.data_ptr(), y.data_ptr(), work.data_ptr(), nv.stream_ptr())
         return y
 
     @property

@@ -2096,9 +2096,14 @@ static SideStream* side_stream() {
   return &ss;
 }
 
+// lda: leading dimension of the k-major inverse (rep_mp(n) for an inverse of
+// exactly n rows; a sector inverse formed in the dmax geometry keeps
+// rep_mp(dmax) -- its rows / columns beyond n are the identity padding, so the
+// leading n x n part is the sector block's inverse).
 static int rep_gemm(int n, const double2* inv, int ncols, int nrhs, const int* ks, double2* S, long s_row,
-                    long s_k, double2* Bt, cudaStream_t s) {
+                    long s_k, double2* Bt, cudaStream_t s, long lda = -1) {
   const int Kp = rep_kp(n), Mp = rep_mp(n);
+  if (lda < 0) lda = Mp;
   const int Np = (ncols + RG_N - 1) / RG_N * RG_N;
   const long total = (long)Kp * Np;
   {
@@ -2114,7 +2119,7 @@ static int rep_gemm(int n, const double2* inv, int ncols, int nrhs, const int* k
     attr = true;
   }
   dim3 grid(Np / RG_N, Mp / RG_M);
-  rep_gemm_kernel<<<grid, RG_THREADS, smem, s>>>(n, Kp, inv, Mp, Bt, Np, ncols, nrhs, ks, S, s_row, s_k, stages);
+  rep_gemm_kernel<<<grid, RG_THREADS, smem, s>>>(n, Kp, inv, lda, Bt, Np, ncols, nrhs, ks, S, s_row, s_k, stages);
   VX_CHECK_LAUNCH("rep_gemm_kernel");
   return VX_OK;
 }
@@ -2466,12 +2471,23 @@ extern "C" long vx_prec1_sec_work_elems(int nx, int ny, int nz, int nrhs, int ns
   return (3L * ny * nz + (long)nsec * dmax) * nx * nrhs;
 }
 
+// Representative block of the reduced scheme on sector factors: per sector s
+// the frequencies rep_ks are ONE GEMM with the sector block's explicit inverse
+// (rep_inv + s * inv_stride, dmax geometry, k-major) on a side stream,
+// concurrently with the single-block solves (disjoint spectral columns).
+struct SecRep {
+  const double2* inv = nullptr;
+  long inv_stride = 0;
+  const int* ks = nullptr;
+  int n = 0;
+};
+
 static int prec1_apply_sec(int nx, int ny, int nz, int nrhs, const vx_c128* factors, const int* perm,
                            const int* items, int n_single, int n_items, int direct_r, const int* klist,
                            int nsec, int dmax,
                            int norb, const int* orows, const int* osec, const double* ocoef,
                            const unsigned char* flipk, const vx_c128* x, vx_c128* y, vx_c128* work,
-                           void* stream, const RagGeom* rg) {
+                           void* stream, const RagGeom* rg, const SecRep* rep = nullptr) {
   VX_REQUIRE(nx >= 1 && ny >= 1 && nz >= 1 && nrhs >= 1 && n_single >= 0 && n_items >= n_single && nsec >= 1 &&
                  dmax >= 1,
              "bad sector apply arguments");
@@ -2495,9 +2511,33 @@ static int prec1_apply_sec(int nx, int ny, int nz, int nrhs, const vx_c128* fact
   // identity rows, so they must be zero; the ragged solve never reads them
   if (!(rg && rg->on)) VX_CUDA(cudaMemsetAsync(U, 0, sizeof(double2) * (size_t)nsec * dmax * pitch, s));
   if ((st = sec_xform(pitch, nrhs, norb, orows, osec, ocoef, flipk, q, S, U, 0, s))) return st;
-  if ((st = solve_items(lu_geom(dmax), reinterpret_cast<const double2*>(factors), perm, items, n_single, n_items,
-                        klist, nrhs, U, pitch, nrhs, s, -1, direct_r, rg)))
+  if (rep && rep->n > 0) {
+    Span span2("prec_solve", s);
+    SideStream* ss = g_rep_sequential ? nullptr : side_stream();
+    cudaStream_t sr = ss ? ss->s : s;
+    if (ss) {
+      VX_CUDA(cudaEventRecord(ss->fork, s));
+      VX_CUDA(cudaStreamWaitEvent(sr, ss->fork, 0));
+    }
+    double2* Bt = U + (long)nsec * dmax * pitch;
+    const long lda = rep_mp(dmax);
+    for (int sc = 0; sc < nsec; ++sc) {
+      const int d = rg && rg->on ? rg->dims[sc] : dmax;
+      if ((st = rep_gemm(d, rep->inv + sc * rep->inv_stride, rep->n * nrhs, nrhs, rep->ks, U + (long)sc * dmax * pitch,
+                         pitch, nrhs, Bt, sr, lda)))
+        return st;
+    }
+    if (n_single > 0 && (st = solve_items(lu_geom(dmax), reinterpret_cast<const double2*>(factors), perm, items,
+                                          n_single, n_single, klist, nrhs, U, pitch, nrhs, s, -1, direct_r, rg)))
+      return st;
+    if (ss) {
+      VX_CUDA(cudaEventRecord(ss->join, sr));
+      VX_CUDA(cudaStreamWaitEvent(s, ss->join, 0));
+    }
+  } else if ((st = solve_items(lu_geom(dmax), reinterpret_cast<const double2*>(factors), perm, items, n_single,
+                               n_items, klist, nrhs, U, pitch, nrhs, s, -1, direct_r, rg))) {
     return st;
+  }
   if ((st = sec_xform(pitch, nrhs, norb, orows, osec, ocoef, flipk, q, U, S, 1, s))) return st;
   {
     LoadStrided ld{S, {pitch, 1, nrhs, nrhs}};
@@ -2528,6 +2568,33 @@ extern "C" int vx_prec1_apply_sec_rag(int nx, int ny, int nz, int nrhs, const vx
   if (st) return st;
   return prec1_apply_sec(nx, ny, nz, nrhs, factors, perm, items, n_single, n_items, direct_r, klist, nsec, dmax,
                          norb, orows, osec, ocoef, flipk, x, y, work, stream, &rg);
+}
+
+extern "C" long vx_prec1_sec_reduced_work_elems(int nx, int ny, int nz, int nrhs, int nsec, int dmax, int n_rep) {
+  const long np = ((long)n_rep * nrhs + RG_N - 1) / RG_N * RG_N;
+  return vx_prec1_sec_work_elems(nx, ny, nz, nrhs, nsec, dmax) + (long)rep_kp(dmax) * np;
+}
+
+extern "C" int vx_prec1_apply_sec_reduced(int nx, int ny, int nz, int nrhs, const vx_c128* factors, const int* perm,
+                                          const int* items, int n_single, int direct_r, const int* klist, int nsec,
+                                          int dmax, const int* sec_dims, int norb, const int* orows, const int* osec,
+                                          const double* ocoef, const unsigned char* flipk, const vx_c128* rep_inv,
+                                          const int* rep_ks, int n_rep, const vx_c128* x, vx_c128* y, vx_c128* work,
+                                          void* stream) {
+  VX_REQUIRE(n_rep >= 0 && (n_rep == 0 || (rep_inv && rep_ks)), "bad representative arguments");
+  RagGeom rg;
+  rg.on = 0;
+  if (sec_dims) {
+    int st = make_rag(nsec, sec_dims, dmax, &rg);
+    if (st) return st;
+  }
+  SecRep rep;
+  rep.inv = reinterpret_cast<const double2*>(rep_inv);
+  rep.inv_stride = vx_rep_inverse_elems(dmax);
+  rep.ks = rep_ks;
+  rep.n = n_rep;
+  return prec1_apply_sec(nx, ny, nz, nrhs, factors, perm, items, n_single, n_single, direct_r, klist, nsec, dmax,
+                         norb, orows, osec, ocoef, flipk, x, y, work, stream, rg.on ? &rg : nullptr, &rep);
 }
 
 // Solve-only sector path on a caller-owned spectral array (the sharded

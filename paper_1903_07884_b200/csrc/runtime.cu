@@ -22,14 +22,23 @@ static std::vector<SpanLog> g_spans;
 
 void count_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
+// names of the spans open on this thread: a span nested inside one of the
+// same name (an entry point that times its whole solve phase around helpers
+// that time their own) records nothing, so each phase is counted once
+static thread_local std::vector<const char*> t_open;
+
 Span::Span(const char* name, cudaStream_t s) : nm(name), st(s), a(nullptr), on(g_timing.load() != 0) {
   if (!on) return;
+  for (const char* o : t_open)
+    if (std::strcmp(o, name) == 0) { on = false; return; }
   if (cudaEventCreate(&a) != cudaSuccess) { on = false; return; }
   cudaEventRecord(a, st);
+  t_open.push_back(nm);
 }
 
 Span::~Span() {
   if (!on) return;
+  if (!t_open.empty()) t_open.pop_back();
   cudaEvent_t b;
   if (cudaEventCreate(&b) != cudaSuccess) return;
   cudaEventRecord(b, st);

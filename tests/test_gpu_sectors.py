@@ -123,3 +123,27 @@ def test_sector_singular_block_raises(C):
     assert ok.sectors == 4
     x = np.arange(72, dtype=complex)
     assert relerr(ok.apply(x), 2 * x) < 1e-14
+
+
+@pytest.mark.parametrize("tol", [1e-3, 0.3])
+def test_sector_reduced_representative_gemm(rng, C, monkeypatch, tol):
+    """Reduced scheme on sector factors: the discarded frequencies go through
+    one GEMM per sector with the representative sector block's explicit
+    inverse (side stream), the kept ones through the ragged sector solves;
+    equal to the chunked representative solves (VX_REP_GEMM=0) and the oracle."""
+    W = _wl((64, 10, 6))          # 3q = 180: sectors of 45 rows (> one tile)
+    kern, mt = W.kernel(), W.mtilde()
+    red = C.build_reduced_one_level(kern, mt, tol)
+    assert red.sectors == 4 and red._inv is not None and red._rag_dims is not None
+    assert int(red._rep_ks.numel()) >= 8
+    monkeypatch.setenv("VX_REP_GEMM", "0")
+    chunked = C.build_reduced_one_level(kern, mt, tol)
+    monkeypatch.delenv("VX_REP_GEMM")
+    assert chunked._inv is None
+    ref = O.build_reduced_one_level(kern.tensors, W.grid.dims, mt, tol)
+    assert np.array_equal(red.kept, ref["kept"])
+    for r in (None, 3):
+        x = random_field(rng, W.grid.n_unknowns, r)
+        y = red.apply(x)
+        assert relerr(y, O.apply_prec(ref, x)) < 1e-10
+        assert relerr(y, chunked.apply(x)) < 1e-12
