@@ -326,7 +326,7 @@ def build_prec(W, kern):
     raise ValueError(kind)
 
 
-def solve_kernel_traffic(name, W, world):
+def solve_kernel_traffic(name, W, world, layout=None):
     """(kernel name, DRAM bytes per launch) of the dominant block-solve kernel:
     the name from the factor layout in use, the traffic from the committed ncu
     capture (dram__bytes_read.sum + dram__bytes_write.sum of one launch,
@@ -338,6 +338,8 @@ def solve_kernel_traffic(name, W, world):
         kname = "lu_solve_small_kernel"
     elif W.prec["kind"] == "reduced-one-level":
         kname = "lu_solve_rag_kernel<2> + rep_gemm_kernel"
+    if layout == "symmetric":
+        kname = "lu_solve_sym_kernel<2>" + (" + rep_gemm_kernel" if W.prec["kind"] == "reduced-one-level" else "")
     traffic = None
     f = ROOT / "profiles" / "r01_solve_traffic.json"
     if world == 1 and f.exists():
@@ -524,11 +526,14 @@ def run_ours(args):
             nvec = 3 * (x1 - x0) * (y1 - y0) * (z1 - z0)
     sol_ms, sol_n = spans["prec_solve"]
     solve_bytes = 16 * sum(n * n * c for n, c in stored) + 2 * 16 * nvec
+    fb = None if sharded or W.prec["kind"] == "blocked" else getattr(prec, "factor_bytes_per_apply", None)
+    if fb is not None:   # symmetric layout: the stored lower triangles, read once per apply
+        solve_bytes = fb + 2 * 16 * nvec
     roof = None
     if sol_n:
         avg = sol_ms / sol_n / 1e3
         ach = solve_bytes / avg / 1e9
-        kname, traffic = solve_kernel_traffic(name, W, world)
+        kname, traffic = solve_kernel_traffic(name, W, world, getattr(prec, "factor_layout", None))
         roof = {"kernel": kname + " (prec_solve span)", "bound": "hbm", "achieved": ach,
                 "peak": peak, "unit": "GB/s", "frac": ach / peak, "peak_source": peak_kind,
                 "traffic": traffic, "bytes_per_launch": solve_bytes, "avg_launch_ms": avg * 1e3,
@@ -536,7 +541,7 @@ def run_ours(args):
     its_per_solve = its / args.steps
     restart_eff = min(W.restart, its_per_solve)
     b_it, b_mv, b_pc, b_ar = iteration_bytes(W, stored_global, restart_eff)
-    b_pc = 2 * 48 * W.grid.n_voxels + 16 * sum(n * n * c for n, c in stored_global)
+    b_pc = 2 * 48 * W.grid.n_voxels + (fb if fb is not None else 16 * sum(n * n * c for n, c in stored_global))
     b_it = b_mv + b_pc + b_ar
     it_roof = {"bytes_per_iteration": b_it, "B_mv": b_mv, "B_pc": b_pc, "B_ar": b_ar,
                "achieved": b_it * its_all / t_max / 1e9, "peak": peak * (world if sharded else 1),

@@ -348,6 +348,36 @@ int vx_prec1_apply_sec_reduced(int nx, int ny, int nz, int nrhs, const vx_c128* 
                                const unsigned char* flipk, const vx_c128* rep_inv, const int* rep_ks, int n_rep,
                                const vx_c128* x, vx_c128* y, vx_c128* work, void* stream);
 
+/* ---- symmetric factors (csrc/lu_sym.cuh).  S M^-1 D_k is complex symmetric
+ * (the Green's tensor is even under d -> -d; S = -1 on the x-component rows,
+ * M = diag(m~)), so when m~ has no zero entry an UNPIVOTED factorisation
+ * D_k = L U has U = diag(u) W L^T W^-1 with W = S M on the (sector) rows and
+ * only L is stored: half the factor bytes of the LU layout (reference
+ * circulant.py:113-118 stores the full zgetrf LU).
+ * vx_lu1_build_opts: vx_lu1_build (nsec == 0 or rrow == NULL) or
+ *   vx_lu1_build_sec with flags bit 0 = eliminate without row interchanges.
+ * vx_lu_sym_pack: padded unpivoted sector factors -> symmetric layout
+ *   (vx_lu_sym_stride entries per frequency slot), h = 1/(u W) per row
+ *   ([slot][dmax]) and per slot dev[2 slot] = max |U - diag(u) W L^T W^-1| /
+ *   max |U|, dev[2 slot + 1] = min |u| / max |u| (the caller keeps the
+ *   symmetric layout only when every block passes).  w: [sector][dmax] W.
+ * vx_lu_sym_unpack: back to the padded LU layout (multi-RHS applies, views).
+ * vx_prec1_apply_sym: vx_prec1_apply_sec_reduced on symmetric factors
+ *   (single RHS; n_rep = 0 for the full 1-level scheme); sector dims up to 256. */
+int vx_lu1_build_opts(int nx, int ny, int nz, const vx_c128* lamT, const vx_c128* m_yz, const int* kset, int nk,
+                      int nsec, int dmax, const int* rrow, const double* rsc, const int* ccol, const double* cw,
+                      vx_c128* factors, int* perm, int* piv, int* info, int flags, void* stream);
+long vx_lu_sym_stride(int nsec, const int* sec_dims);
+int vx_lu_sym_pack(int nkslots, int nsec, int dmax, const int* sec_dims, const vx_c128* padded, const vx_c128* w,
+                   vx_c128* sym, vx_c128* h, double* dev, void* stream);
+int vx_lu_sym_unpack(int nkslots, int nsec, int dmax, const int* sec_dims, const vx_c128* sym, const vx_c128* h,
+                     const vx_c128* w, vx_c128* padded, void* stream);
+int vx_prec1_apply_sym(int nx, int ny, int nz, const vx_c128* factors, const vx_c128* h, const vx_c128* w,
+                       const int* items, int n_single, int direct_r, const int* klist, int nsec, int dmax,
+                       const int* sec_dims, int norb, const int* orows, const int* osec, const double* ocoef,
+                       const unsigned char* flipk, const vx_c128* rep_inv, const int* rep_ks, int n_rep,
+                       const vx_c128* x, vx_c128* y, vx_c128* work, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

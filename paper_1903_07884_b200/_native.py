@@ -98,6 +98,12 @@ _SIGS = {
     "vx_prec1_sec_reduced_work_elems": (c_long, [c_int] * 7),
     "vx_prec1_apply_sec_reduced": (c_int, [c_int] * 4 + [P, P, P, c_int, c_int, P, c_int, c_int, P, c_int, P, P, P,
                                                       P, P, P, c_int, P, P, P, P]),
+    "vx_lu1_build_opts": (c_int, [c_int] * 3 + [P, P, P, c_int, c_int, c_int, P, P, P, P, P, P, P, P, c_int, P]),
+    "vx_lu_sym_stride": (c_long, [c_int, P]),
+    "vx_lu_sym_pack": (c_int, [c_int, c_int, c_int, P, P, P, P, P, P, P]),
+    "vx_lu_sym_unpack": (c_int, [c_int, c_int, c_int, P, P, P, P, P, P]),
+    "vx_prec1_apply_sym": (c_int, [c_int] * 3 + [P, P, P, P, c_int, c_int, P, c_int, c_int, P, c_int, P, P, P, P,
+                                                  P, P, c_int, P, P, P, P]),
     "vx_solve_classic": (c_int, []),
     "vx_lu_repack": (c_int, [c_int, c_int, c_int, P, P, P, P]),
     "vx_lu_unpack": (c_int, [c_int, c_int, c_int, P, P, P, P]),

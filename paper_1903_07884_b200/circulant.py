@@ -159,8 +159,9 @@ def _lu1(lam, m_yz_dev, kset_dev, nslots, nx, ny, nz):
     return fac, perm, piv, info
 
 
-def _lu1_sec(lam, m_yz_dev, kset_dev, nk, nx, ny, nz, sec):
-    """Sector factorisation (vx_lu1_build_sec): nk * nsec blocks of dmax rows."""
+def _lu1_sec(lam, m_yz_dev, kset_dev, nk, nx, ny, nz, sec, nopiv=False):
+    """Sector factorisation (vx_lu1_build_opts): nk * nsec blocks of dmax rows
+    (nopiv: elimination without row interchanges, for the symmetric layout)."""
     t = _torch()
     sp = sec.plan
     nslots = nk * sp.nsec
@@ -169,10 +170,81 @@ def _lu1_sec(lam, m_yz_dev, kset_dev, nk, nx, ny, nz, sec):
     perm = t.empty((nslots, sp.dmax), dtype=t.int32, device="cuda")
     piv = t.empty((nslots, sp.dmax), dtype=t.int32, device="cuda")
     info = t.empty((nslots,), dtype=t.int32, device="cuda")
-    nv.call("vx_lu1_build_sec", nx, ny, nz, lam.data_ptr(), m_yz_dev.data_ptr(), kset_dev.data_ptr(), nk,
+    nv.call("vx_lu1_build_opts", nx, ny, nz, lam.data_ptr(), m_yz_dev.data_ptr(), kset_dev.data_ptr(), nk,
             sp.nsec, sp.dmax, sec.rrow.data_ptr(), sec.rsc.data_ptr(), sec.ccol.data_ptr(), sec.cw.data_ptr(),
-            fac.data_ptr(), perm.data_ptr(), piv.data_ptr(), info.data_ptr(), nv.stream_ptr())
+            fac.data_ptr(), perm.data_ptr(), piv.data_ptr(), info.data_ptr(), 1 if nopiv else 0, nv.stream_ptr())
     return fac, perm, piv, info
+
+
+# ---------------------------------------------------------------------------
+# symmetric factors (csrc/lu_sym.cuh): S M^-1 D_k is complex symmetric (the
+# Green's tensor is even under d -> -d), so an unpivoted factorisation D = L U
+# has U = diag(u) W L^T W^-1 with W = S M restricted to the (sector) rows, and
+# only L is stored -- half the bytes every apply streams.  Used when m~ has no
+# zero entry and the blocks fit the register-resident solve (<= 256 rows); the
+# pack kernel verifies the relation per block, else the pivoted LU is kept.
+SYM_TOL = 1e-11        # max |U - diag(u) W L^T W^-1| / max |U| per block
+SYM_MIN_PIVOT = 1e-8   # min |u| / max |u| per block
+
+
+def _sym_eligible(m_yz: np.ndarray, dmax: int) -> bool:
+    if os.environ.get("VX_SYM", "1") == "0":
+        return False
+    a = np.abs(np.asarray(m_yz))
+    return 32 < dmax <= 256 and bool(np.all(np.isfinite(a))) and bool(a.min() > 0.0)
+
+
+def _sym_weights(plan, m_yz: np.ndarray) -> np.ndarray:
+    """W (nsec, dmax): S M on the sector rows -- -m~ on x-component rows, +m~
+    on the others, at the orbit's representative site (m~ is equal on every
+    site of an orbit when the sectors exist)."""
+    q = m_yz.size
+    mf = np.asarray(m_yz, np.complex128).reshape(-1)
+    W = np.ones((plan.nsec, plan.dmax), np.complex128)
+    rr = plan.rrow
+    ok = rr >= 0
+    a, site = rr // q, rr % q
+    W[ok] = np.where(a[ok] == 0, -1.0, 1.0) * mf[site[ok]]
+    return W
+
+
+class _SymFactors:
+    """Device symmetric factors: packed lower triangles, h = 1/(u W) per row, W."""
+
+    def __init__(self, fac, h, w, dims):
+        self.fac, self.h, self.w, self.dims = fac, h, w, dims
+
+
+def _sym_pack(fac, sec, m_yz, nk):
+    """Pack unpivoted sector factors into the symmetric layout; None when a
+    block fails the symmetric-reconstruction or pivot-size check."""
+    sp = sec.plan
+    dims_a = np.ascontiguousarray(sp.dims, np.int32)
+    w = nv.device_c128(_sym_weights(sp, m_yz))
+    stride = int(nv.query("vx_lu_sym_stride", sp.nsec, dims_a.ctypes.data))
+    t = _torch()
+    sym = nv.empty_c128((max(1, nk), stride))
+    h = nv.empty_c128((max(1, nk * sp.nsec), sp.dmax))
+    dev = t.zeros((max(1, nk * sp.nsec), 2), dtype=t.float64, device="cuda")
+    nv.call("vx_lu_sym_pack", nk, sp.nsec, sp.dmax, dims_a.ctypes.data, fac.data_ptr(), w.data_ptr(),
+            sym.data_ptr(), h.data_ptr(), dev.data_ptr(), nv.stream_ptr())
+    d = dev[: nk * sp.nsec].cpu().numpy()
+    if d.size and not (d[:, 0].max() <= SYM_TOL and d[:, 1].min() >= SYM_MIN_PIVOT):
+        return None
+    return _SymFactors(sym, h, w, dims_a)
+
+
+def _lu1_sec_auto(lam, m_dev, kdev, nk, nx, ny, nz, sec, m_yz):
+    """Sector factorisation: symmetric (unpivoted, verified) when eligible,
+    else zgetrf's partial pivoting -> (fac, perm, piv, info, sym or None)."""
+    if _sym_eligible(m_yz, sec.plan.dmax):
+        fac, perm, piv, info = _lu1_sec(lam, m_dev, kdev, nk, nx, ny, nz, sec, nopiv=True)
+        if _first_bad(info) < 0:
+            sym = _sym_pack(fac, sec, m_yz, nk)
+            if sym is not None:
+                return fac, perm, piv, info, sym
+        del fac, perm, piv, info
+    return _lu1_sec(lam, m_dev, kdev, nk, nx, ny, nz, sec) + (None,)
 
 
 def _first_bad(info) -> int:
@@ -341,6 +413,7 @@ class _OneLevelBase:
     _sec = None            # _SectorDev when the blocks are stored as symmetry sectors
     _full_builder = None   # builds the plain dense-block preconditioner (for .lu / .piv)
     _full = None
+    _sym = None            # _SymFactors when the sector factors are stored symmetric
 
     @property
     def sectors(self) -> int:
@@ -386,12 +459,30 @@ class _OneLevelBase:
         self._flipk = t.from_numpy(flipk).cuda()
         self._n_single, self._n_items, self._direct_r = n_single, int(items.shape[0]), direct_r
 
+    def _apply_sym(self, xd, rep_inv=None, rep_ks=None):
+        """Single-RHS apply on symmetric sector factors (optionally with the
+        reduced scheme's representative GEMM)."""
+        nx, ny, nz = self.grid.dims
+        sp, sd, sy = self._sec.plan, self._sec, self._sym
+        n_rep = 0 if rep_ks is None else int(rep_ks.numel())
+        y = nv.empty_c128((self.grid.n_unknowns, 1))
+        work = nv.empty_c128(int(nv.query("vx_prec1_sec_reduced_work_elems", nx, ny, nz, 1, sp.nsec, sp.dmax, n_rep)))
+        nv.call("vx_prec1_apply_sym", nx, ny, nz, sy.fac.data_ptr(), sy.h.data_ptr(), sy.w.data_ptr(),
+                self._items.data_ptr(), self._n_single, self._direct_r, self._klist.data_ptr(), sp.nsec, sp.dmax,
+                sy.dims.ctypes.data, sd.norb, sd.orows.data_ptr(), sd.osec.data_ptr(), sd.ocoef.data_ptr(),
+                self._flipk.data_ptr(), nv.ptr(rep_inv), nv.ptr(rep_ks), n_rep, xd.data_ptr(), y.data_ptr(),
+                work.data_ptr(), nv.stream_ptr())
+        return y
+
     def _apply_dev(self, xd, r):
         nx, ny, nz = self.grid.dims
+        if self._sym is not None and r == 1 and not nv.query("vx_solve_classic"):
+            return self._apply_sym(xd)
         rag = getattr(self, "_rag_dims", None) is not None and r == 1 and not nv.query("vx_solve_classic")
         if rag:
             self._padded_fac = None
-        fac = self._fac if (rag or getattr(self, "_rag_dims", None) is None) else self._padded()
+        fac = (self._fac if (rag or getattr(self, "_rag_dims", None) is None) and self._sym is None
+               else self._padded())
         if self._sec is not None:
             sp, sd = self._sec.plan, self._sec
             y = nv.empty_c128((self.grid.n_unknowns, r))
@@ -428,7 +519,12 @@ class _OneLevelBase:
         return 1, n, (n,)
 
     def _make_ragged(self):
-        """Repack the padded factors into ragged storage (frees the padded copy)."""
+        """Repack the padded factors into ragged storage (frees the padded copy);
+        symmetric factors replace them by the packed lower triangles."""
+        if self._sym is not None:
+            self._nslots = int(self._fac.shape[0])
+            self._fac = self._sym.fac
+            return
         nsec, dmax, dims = self._rag_geometry()
         if dmax <= 32 or os.environ.get("VX_RAGGED", "1") == "0":
             return
@@ -446,6 +542,16 @@ class _OneLevelBase:
     def _padded(self):
         """Padded-tile factors (nslots, npad^2): the layout the reduced scheme,
         multi-RHS applies and the LAPACK views read (unpacked on demand)."""
+        if self._sym is not None:
+            if self._padded_fac is None:
+                nsec, dmax, _ = self._rag_geometry()
+                blk = int(nv.query("vx_lu_block_elems", dmax))
+                pad = nv.empty_c128((self._nslots, blk))
+                sy = self._sym
+                nv.call("vx_lu_sym_unpack", self._nslots // nsec, nsec, dmax, sy.dims.ctypes.data, sy.fac.data_ptr(),
+                        sy.h.data_ptr(), sy.w.data_ptr(), pad.data_ptr(), nv.stream_ptr())
+                self._padded_fac = pad
+            return self._padded_fac
         if self._rag_dims is None:
             return self._fac
         if self._padded_fac is None:
@@ -481,8 +587,23 @@ class _OneLevelBase:
 
     @property
     def storage_bytes(self) -> int:
-        """Bytes actually resident on the device for the factors (ragged, or padded tiles)."""
+        """Bytes actually resident on the device for the factors (symmetric,
+        ragged, or padded tiles)."""
         return int(self._fac.numel()) * 16
+
+    @property
+    def factor_bytes_per_apply(self) -> int:
+        """Compulsory factor bytes of one single-RHS apply: every stored factor
+        entry read once (symmetric layout: the lower triangles only)."""
+        if self._sym is not None:
+            return int(self._sym.fac.numel()) * 16
+        return 16 * sum(d * d * c for d, c in self.stored_blocks)
+
+    @property
+    def factor_layout(self) -> str:
+        if self._sym is not None:
+            return "symmetric"
+        return "ragged" if getattr(self, "_rag_dims", None) is not None else "padded"
 
     @property
     def stored_slots(self) -> int:
@@ -541,9 +662,10 @@ class OneLevelPrec(_OneLevelBase):
 
     level = "one-level"
 
-    def __init__(self, grid, fac, perm, piv, proxy, store=None, flip=None, sec=None, full_builder=None):
+    def __init__(self, grid, fac, perm, piv, proxy, store=None, flip=None, sec=None, full_builder=None, sym=None):
         self.grid = grid
         self._fac, self._perm, self._piv, self._proxy = fac, perm, piv, proxy
+        self._sym = sym
         nx = grid.nx
         self._store = np.arange(nx) if store is None else np.asarray(store)
         self._flip = np.zeros(nx, bool) if flip is None else np.asarray(flip, bool)
@@ -589,14 +711,14 @@ def _build_one_level_dev(grid, gen, m_yz, cap_bytes, tol=None, sectors=True):
             from .sectors import sector_plan
 
             sec = _SectorDev(sector_plan(ny, nz, sy, sz))
-            fac, perm, piv, info = _lu1_sec(lam, m_dev, kdev, int(kset.size), nx, ny, nz, sec)
+            fac, perm, piv, info, sym = _lu1_sec_auto(lam, m_dev, kdev, int(kset.size), nx, ny, nz, sec, m_yz)
             bad = _first_bad(info)
             if bad >= 0:
                 raise PreconditionerBuildError(
                     f"1-level build failed: singular frequency block k={int(kset[bad // sec.plan.nsec])}")
             return OneLevelPrec(grid, fac, perm, piv, proxy, store, flip, sec=sec,
                                 full_builder=lambda: _build_one_level_dev(grid, gen, m_yz, cap_bytes,
-                                                                          sectors=False))
+                                                                          sectors=False), sym=sym)
         fac, perm, piv, info = _lu1(lam, m_dev, kdev, int(kset.size), nx, ny, nz)
         bad = _first_bad(info)
         if bad >= 0:
@@ -612,13 +734,14 @@ def _build_one_level_dev(grid, gen, m_yz, cap_bytes, tol=None, sectors=True):
         from .sectors import sector_plan
 
         sec = _SectorDev(sector_plan(ny, nz, sy, sz))
-        fac, perm, piv, info = _lu1_sec(lam, m_dev, kdev, int(kset.size), nx, ny, nz, sec)
+        fac, perm, piv, info, sym = _lu1_sec_auto(lam, m_dev, kdev, int(kset.size), nx, ny, nz, sec, m_yz)
         bad = _first_bad(info)
         if bad >= 0:
             raise PreconditionerBuildError(f"singular frequency block k={int(kset[bad // sec.plan.nsec])}")
         return ReducedOneLevelPrec(grid, kept, slot_of, rep, fac, perm, piv, ph, v_hat, float(tol), store, flip,
                                    sec=sec, full_builder=lambda: _build_one_level_dev(grid, gen, m_yz, cap_bytes,
-                                                                                      tol=tol, sectors=False))
+                                                                                      tol=tol, sectors=False),
+                                   sym=sym)
     fac, perm, piv, info = _lu1(lam, m_dev, kdev, int(kset.size), nx, ny, nz)
     bad = _first_bad(info)
     if bad >= 0:
@@ -645,8 +768,9 @@ class ReducedOneLevelPrec(_OneLevelBase):
     level = "reduced-one-level"
 
     def __init__(self, grid, kept, slot_of, representative, fac, perm, piv, proxy, v_hat, tol,
-                 store=None, flip=None, sec=None, full_builder=None):
+                 store=None, flip=None, sec=None, full_builder=None, sym=None):
         self.grid = grid
+        self._sym = sym
         self.kept = np.asarray(kept)
         self.slot_of = np.asarray(slot_of)
         self.representative = int(representative)
@@ -683,6 +807,7 @@ class ReducedOneLevelPrec(_OneLevelBase):
                 self._rep_ks = t.from_numpy(rep_ks.astype(np.int32)).cuda()
                 self._make_ragged()
                 return
+            self._sym = None   # representative chunks are multi-RHS items: padded pivot-free LU factors
             self._sector_items(self._store[keep], self.kept[keep], self._flip[keep], rep=(rep_slot, rep_ks))
             return
         groups = {}
@@ -724,10 +849,12 @@ class ReducedOneLevelPrec(_OneLevelBase):
         return y
 
     def _apply_sec_rep(self, xd, r):
+        if self._sym is not None and r == 1 and not nv.query("vx_solve_classic"):
+            return self._apply_sym(xd, self._inv, self._rep_ks)
         nx, ny, nz = self.grid.dims
         sp, sd = self._sec.plan, self._sec
         rag = self._rag_dims is not None and r == 1 and not nv.query("vx_solve_classic")
-        fac = self._fac if (rag or self._rag_dims is None) else self._padded()
+        fac = self._fac if (rag or self._rag_dims is None) and self._sym is None else self._padded()
         n_rep = int(self._rep_ks.numel())
         y = nv.empty_c128((self.grid.n_unknowns, r))
         work = nv.empty_c128(int(nv.query("vx_prec1_sec_reduced_work_elems", nx, ny, nz, r, sp.nsec, sp.dmax, n_rep)))

@@ -621,7 +621,7 @@ static size_t sec_unfold_smem(const LuGeom& g) {
 // panel factorisation of tile column kt of every block (one CTA per block),
 // then the diagonal tile's triangular inverses, packed in place.
 __global__ void __launch_bounds__(LU_THREADS) lub_panel_kernel(LuGeom g, double2* F, int kt, int* piv,
-                                                               int* info) {
+                                                               int* info, int nopiv) {
   __shared__ double redv[LU_WARPS];
   __shared__ int redi[LU_WARPS];
   __shared__ int pivs[32];
@@ -656,7 +656,7 @@ __global__ void __launch_bounds__(LU_THREADS) lub_panel_kernel(LuGeom g, double2
       for (int w = 1; w < LU_WARPS; ++w)
         if (redv[w] > bb || (redv[w] == bb && redi[w] < ii)) { bb = redv[w]; ii = redi[w]; }
       if (!(bb > 0.0) && bb != 0.0) ii = j;  // all NaN
-      if (j >= n) ii = j;                    // identity pad never pivots
+      if (j >= n || nopiv) ii = j;           // identity pad never pivots; nopiv: elimination in order
       pivs[jj] = ii;
       if (j < n) piv[(long)slot * n + j] = ii;
     }
@@ -851,7 +851,7 @@ __global__ void lub_perm_kernel(int nslots, int n, const int* piv, int* perm, in
 static int g_lu_monolithic = 0;  // vx_lu_variant(1): single-kernel LU (A/B timing)
 
 static int lu_build_batched(const Unfold& u, const LuGeom& g, int nslots, double2* F, int* perm, int* piv,
-                            int* info, cudaStream_t s, const SecUnfold* su = nullptr) {
+                            int* info, cudaStream_t s, const SecUnfold* su = nullptr, int nopiv = 0) {
   VX_CUDA(cudaMemsetAsync(info, 0, sizeof(int) * nslots, s));
   if (su) {
     const size_t us = sec_unfold_smem(g);
@@ -869,7 +869,7 @@ static int lu_build_batched(const Unfold& u, const LuGeom& g, int nslots, double
     VX_CHECK_LAUNCH("lub_unfold_kernel");
   }
   for (int kt = 0; kt < g.nt; ++kt) {
-    lub_panel_kernel<<<nslots, LU_THREADS, 0, s>>>(g, F, kt, piv, info);
+    lub_panel_kernel<<<nslots, LU_THREADS, 0, s>>>(g, F, kt, piv, info, nopiv);
     VX_CHECK_LAUNCH("lub_panel_kernel");
     if (g.nt > 1) {
       dim3 sg(div_up(g.npad, 256), nslots);
@@ -1702,6 +1702,8 @@ static int launch_solve_rag(const LuGeom& g, const RagGeom& rg, const double2* F
   return VX_OK;
 }
 
+#include "lu_sym.cuh"
+
 // ------------------------------------------------------ single-tile blocks
 // n <= 32 (the 2-level scheme's (3nz)^2 blocks): one warp per work item, lane
 // = row; the packed diagonal tile holds inv(L) below and inv(U) on/above the
@@ -2487,7 +2489,8 @@ static int prec1_apply_sec(int nx, int ny, int nz, int nrhs, const vx_c128* fact
                            int nsec, int dmax,
                            int norb, const int* orows, const int* osec, const double* ocoef,
                            const unsigned char* flipk, const vx_c128* x, vx_c128* y, vx_c128* work,
-                           void* stream, const RagGeom* rg, const SecRep* rep = nullptr) {
+                           void* stream, const RagGeom* rg, const SecRep* rep = nullptr,
+                           const SymGeom* sym = nullptr) {
   VX_REQUIRE(nx >= 1 && ny >= 1 && nz >= 1 && nrhs >= 1 && n_single >= 0 && n_items >= n_single && nsec >= 1 &&
                  dmax >= 1,
              "bad sector apply arguments");
@@ -2499,8 +2502,12 @@ static int prec1_apply_sec(int nx, int ny, int nz, int nrhs, const vx_c128* fact
   int st = fft_get_plan(nx, &p);
   if (st) return st;
   const int q = ny * nz, q3 = 3 * q;
+  // norb == 0 (symmetric factors of dense blocks only): no orbit transform,
+  // the solves run on the x-DFT output itself
+  const bool xf = norb > 0;
+  VX_REQUIRE(xf || (sym && nsec == 1), "sector apply without orbit tables");
   double2* S = reinterpret_cast<double2*>(work);
-  double2* U = S + (long)q3 * nx * nrhs;
+  double2* U = xf ? S + (long)q3 * nx * nrhs : S;
   const long pitch = (long)nx * nrhs;
   {
     LoadStrided ld{reinterpret_cast<const double2*>(x), {pitch, 1, nrhs, nrhs}};
@@ -2508,9 +2515,19 @@ static int prec1_apply_sec(int nx, int ny, int nz, int nrhs, const vx_c128* fact
     if ((st = launch_fft_auto(p, ld, sv, q3 * nrhs, nx, nx, false, nrhs == 1, s))) return st;
   }
   // the padding rows of a sector (d_s <= r < dmax) feed the padded solve's
-  // identity rows, so they must be zero; the ragged solve never reads them
-  if (!(rg && rg->on)) VX_CUDA(cudaMemsetAsync(U, 0, sizeof(double2) * (size_t)nsec * dmax * pitch, s));
-  if ((st = sec_xform(pitch, nrhs, norb, orows, osec, ocoef, flipk, q, S, U, 0, s))) return st;
+  // identity rows, so they must be zero; the ragged / symmetric solves never read them
+  if (!(rg && rg->on) && !sym) VX_CUDA(cudaMemsetAsync(U, 0, sizeof(double2) * (size_t)nsec * dmax * pitch, s));
+  if (xf && (st = sec_xform(pitch, nrhs, norb, orows, osec, ocoef, flipk, q, S, U, 0, s))) return st;
+  auto singles = [&](int n_it) -> int {
+    if (sym) {
+      VX_REQUIRE(nrhs == 1, "symmetric factors: single-RHS work lists only");
+      Span sp("prec_solve", s);
+      return launch_solve_sym(*sym, reinterpret_cast<const double2*>(factors), items, n_it, direct_r, klist, U,
+                              pitch, nrhs, q, s);
+    }
+    return solve_items(lu_geom(dmax), reinterpret_cast<const double2*>(factors), perm, items, n_it, n_it, klist,
+                       nrhs, U, pitch, nrhs, s, -1, direct_r, rg);
+  };
   if (rep && rep->n > 0) {
     Span span2("prec_solve", s);
     SideStream* ss = g_rep_sequential ? nullptr : side_stream();
@@ -2519,26 +2536,27 @@ static int prec1_apply_sec(int nx, int ny, int nz, int nrhs, const vx_c128* fact
       VX_CUDA(cudaEventRecord(ss->fork, s));
       VX_CUDA(cudaStreamWaitEvent(sr, ss->fork, 0));
     }
-    double2* Bt = U + (long)nsec * dmax * pitch;
+    double2* Bt = S + (long)q3 * nx * nrhs + (long)nsec * dmax * pitch;
     const long lda = rep_mp(dmax);
     for (int sc = 0; sc < nsec; ++sc) {
-      const int d = rg && rg->on ? rg->dims[sc] : dmax;
+      const int d = sym ? sym->dims[sc] : (rg && rg->on ? rg->dims[sc] : dmax);
       if ((st = rep_gemm(d, rep->inv + sc * rep->inv_stride, rep->n * nrhs, nrhs, rep->ks, U + (long)sc * dmax * pitch,
                          pitch, nrhs, Bt, sr, lda)))
         return st;
     }
-    if (n_single > 0 && (st = solve_items(lu_geom(dmax), reinterpret_cast<const double2*>(factors), perm, items,
-                                          n_single, n_single, klist, nrhs, U, pitch, nrhs, s, -1, direct_r, rg)))
-      return st;
+    if (n_single > 0 && (st = singles(n_single))) return st;
     if (ss) {
       VX_CUDA(cudaEventRecord(ss->join, sr));
       VX_CUDA(cudaStreamWaitEvent(s, ss->join, 0));
     }
+  } else if (sym) {
+    VX_REQUIRE(n_items == n_single, "symmetric factors: direct items only");
+    if ((st = singles(n_single))) return st;
   } else if ((st = solve_items(lu_geom(dmax), reinterpret_cast<const double2*>(factors), perm, items, n_single,
                                n_items, klist, nrhs, U, pitch, nrhs, s, -1, direct_r, rg))) {
     return st;
   }
-  if ((st = sec_xform(pitch, nrhs, norb, orows, osec, ocoef, flipk, q, U, S, 1, s))) return st;
+  if (xf && (st = sec_xform(pitch, nrhs, norb, orows, osec, ocoef, flipk, q, U, S, 1, s))) return st;
   {
     LoadStrided ld{S, {pitch, 1, nrhs, nrhs}};
     StoreStrided sv{reinterpret_cast<double2*>(y), {pitch, 1, nrhs, nrhs}, 1.0 / nx};
@@ -2595,6 +2613,87 @@ extern "C" int vx_prec1_apply_sec_reduced(int nx, int ny, int nz, int nrhs, cons
   rep.n = n_rep;
   return prec1_apply_sec(nx, ny, nz, nrhs, factors, perm, items, n_single, n_single, direct_r, klist, nsec, dmax,
                          norb, orows, osec, ocoef, flipk, x, y, work, stream, rg.on ? &rg : nullptr, &rep);
+}
+
+// ------------------------------------------------------ symmetric factors
+extern "C" int vx_lu1_build_opts(int nx, int ny, int nz, const vx_c128* lamT, const vx_c128* m_yz, const int* kset,
+                                 int nk, int nsec, int dmax, const int* rrow, const double* rsc, const int* ccol,
+                                 const double* cw, vx_c128* factors, int* perm, int* piv, int* info, int flags,
+                                 void* stream) {
+  VX_REQUIRE(nx >= 1 && ny >= 1 && nz >= 1 && nk >= 0 && (flags & ~1) == 0, "bad 1-level build arguments");
+  cudaStream_t s = as_stream(stream);
+  Unfold u{reinterpret_cast<const double2*>(lamT), reinterpret_cast<const double2*>(m_yz), kset,
+           6L * (2 * nz - 1) * (2 * ny - 1), nz, ny};
+  const int nopiv = flags & 1;
+  if (nsec == 0 || !rrow) {
+    if (nk == 0) return VX_OK;
+    Span span("lu_build", s);
+    return lu_build_batched(u, lu_geom(3 * ny * nz), nk, reinterpret_cast<double2*>(factors), perm, piv, info, s,
+                            nullptr, nopiv);
+  }
+  VX_REQUIRE(nsec >= 1 && nsec <= 4 && dmax >= 1, "bad sector build arguments");
+  const int nslots = nk * nsec;
+  if (nslots == 0) return VX_OK;
+  Span span("lu_build", s);
+  SecUnfold su{reinterpret_cast<const double2*>(lamT), reinterpret_cast<const double2*>(m_yz), kset,
+               6L * (2 * nz - 1) * (2 * ny - 1), nz, ny, nsec, dmax, rrow, rsc, ccol, cw};
+  return lu_build_batched(u, lu_geom(dmax), nslots, reinterpret_cast<double2*>(factors), perm, piv, info, s, &su,
+                          nopiv);
+}
+
+extern "C" long vx_lu_sym_stride(int nsec, const int* sec_dims) {
+  long k = 0;
+  for (int s = 0; s < nsec; ++s) k += sym_size(sec_dims[s]);
+  return k;
+}
+
+extern "C" int vx_lu_sym_pack(int nkslots, int nsec, int dmax, const int* sec_dims, const vx_c128* padded,
+                              const vx_c128* w, vx_c128* sym, vx_c128* h, double* dev, void* stream) {
+  VX_REQUIRE(nkslots >= 0, "bad symmetric pack arguments");
+  SymGeom sg;
+  int st = make_sym(nsec, sec_dims, dmax, h, w, &sg);
+  if (st) return st;
+  if (nkslots == 0) return VX_OK;
+  const LuGeom g = lu_geom(dmax);
+  lu_sym_pack_kernel<<<nkslots * nsec, 256, 0, as_stream(stream)>>>(g, sg, reinterpret_cast<const double2*>(padded),
+                                                                   reinterpret_cast<double2*>(sym),
+                                                                   reinterpret_cast<double2*>(h), dev);
+  VX_CHECK_LAUNCH("lu_sym_pack_kernel");
+  return VX_OK;
+}
+
+extern "C" int vx_lu_sym_unpack(int nkslots, int nsec, int dmax, const int* sec_dims, const vx_c128* sym,
+                                const vx_c128* h, const vx_c128* w, vx_c128* padded, void* stream) {
+  VX_REQUIRE(nkslots >= 0, "bad symmetric unpack arguments");
+  SymGeom sg;
+  int st = make_sym(nsec, sec_dims, dmax, h, w, &sg);
+  if (st) return st;
+  if (nkslots == 0) return VX_OK;
+  const LuGeom g = lu_geom(dmax);
+  dim3 grid(div_up(g.blk, 256 * 4) > 0 ? div_up(g.blk, 256 * 4) : 1, nkslots * nsec);
+  lu_sym_unpack_kernel<<<grid, 256, 0, as_stream(stream)>>>(g, sg, reinterpret_cast<const double2*>(sym),
+                                                            reinterpret_cast<double2*>(padded));
+  VX_CHECK_LAUNCH("lu_sym_unpack_kernel");
+  return VX_OK;
+}
+
+extern "C" int vx_prec1_apply_sym(int nx, int ny, int nz, const vx_c128* factors, const vx_c128* h,
+                                  const vx_c128* w, const int* items, int n_single, int direct_r, const int* klist,
+                                  int nsec, int dmax, const int* sec_dims, int norb, const int* orows,
+                                  const int* osec, const double* ocoef, const unsigned char* flipk,
+                                  const vx_c128* rep_inv, const int* rep_ks, int n_rep, const vx_c128* x,
+                                  vx_c128* y, vx_c128* work, void* stream) {
+  VX_REQUIRE(n_rep >= 0 && (n_rep == 0 || (rep_inv && rep_ks)), "bad representative arguments");
+  SymGeom sg;
+  int st = make_sym(nsec, sec_dims, dmax, h, w, &sg);
+  if (st) return st;
+  SecRep rep;
+  rep.inv = reinterpret_cast<const double2*>(rep_inv);
+  rep.inv_stride = vx_rep_inverse_elems(dmax);
+  rep.ks = rep_ks;
+  rep.n = n_rep;
+  return prec1_apply_sec(nx, ny, nz, 1, factors, nullptr, items, n_single, n_single, direct_r, klist, nsec, dmax,
+                         norb, orows, osec, ocoef, flipk, x, y, work, stream, nullptr, n_rep ? &rep : nullptr, &sg);
 }
 
 // Solve-only sector path on a caller-owned spectral array (the sharded

@@ -134,7 +134,7 @@ def test_sector_reduced_representative_gemm(rng, C, monkeypatch, tol):
     W = _wl((64, 10, 6))          # 3q = 180: sectors of 45 rows (> one tile)
     kern, mt = W.kernel(), W.mtilde()
     red = C.build_reduced_one_level(kern, mt, tol)
-    assert red.sectors == 4 and red._inv is not None and red._rag_dims is not None
+    assert red.sectors == 4 and red._inv is not None and red.factor_layout in ("ragged", "symmetric")
     assert int(red._rep_ks.numel()) >= 8
     monkeypatch.setenv("VX_REP_GEMM", "0")
     chunked = C.build_reduced_one_level(kern, mt, tol)
@@ -147,3 +147,67 @@ def test_sector_reduced_representative_gemm(rng, C, monkeypatch, tol):
         y = red.apply(x)
         assert relerr(y, O.apply_prec(ref, x)) < 1e-10
         assert relerr(y, chunked.apply(x)) < 1e-12
+
+
+@pytest.mark.parametrize("dims", [(50, 22, 11), (40, 12, 4), (64, 10, 6), (30, 16, 9)])
+def test_symmetric_factors_equal_pivoted(rng, C, monkeypatch, dims):
+    """Symmetric sector factors (unpivoted L, U = diag(u) W L^T W^-1; half the
+    stored bytes) give the same P^-1 x as the pivoted LU factors (VX_SYM=0),
+    for one right-hand side (symmetric solve kernel) and several (unpacked
+    padded layout); the LAPACK views are the pivoted dense ones."""
+    W = _wl(dims)
+    kern, mt = W.kernel(), W.mtilde()
+    p = C.build_one_level(kern, mt)
+    monkeypatch.setenv("VX_SYM", "0")
+    q = C.build_one_level(kern, mt)
+    monkeypatch.delenv("VX_SYM")
+    assert p.factor_layout == "symmetric" and q.factor_layout == "ragged"
+    assert p.storage_bytes < 0.53 * q.storage_bytes
+    assert p.factor_bytes_per_apply == p.storage_bytes
+    n = W.grid.n_unknowns
+    for r in (None, 2):
+        x = random_field(rng, n, r)
+        assert relerr(p.apply(x), q.apply(x)) < 1e-12
+    if n <= 3 * 40 * 12 * 4:
+        ref = O.build_one_level(kern.tensors, W.grid.dims, mt)
+        x = random_field(rng, n)
+        assert relerr(p.apply(x), O.apply_prec(ref, x)) < 1e-10
+        assert np.array_equal(p.piv, q.piv)
+
+
+def test_symmetric_factors_not_used_with_zero_coefficients(rng, C):
+    """m~ with a zero row (cladding with eps = 1 in interpretation B) breaks
+    S M^-1 D symmetry: the pivoted ragged layout is kept."""
+    W = _wl((40, 12, 4))
+    m = np.repeat(W.mtilde()[:, :, :1], 40, axis=2).copy()
+    m[:, 0, :] = 0.0
+    m[:, -1, :] = 0.0
+    p = C.build_one_level(W.kernel(), m)
+    assert p.sectors > 1 and p.factor_layout == "ragged"
+    ref = O.build_one_level(W.kernel().tensors, W.grid.dims, m)
+    x = random_field(rng, W.grid.n_unknowns)
+    assert relerr(p.apply(x), O.apply_prec(ref, x)) < 1e-10
+
+
+def test_symmetric_reduced_and_solve(rng, C, monkeypatch):
+    """Reduced scheme with symmetric kept factors + representative GEMM, and a
+    full GMRES solve on symmetric factors vs the pivoted layout."""
+    from paper_1903_07884_b200.operator import apply_system, plan_operator
+    from paper_1903_07884_b200.solver import gmres
+
+    W = _wl((64, 10, 6))
+    kern, mt = W.kernel(), W.mtilde()
+    red = C.build_reduced_one_level(kern, mt, 0.3)
+    assert red.factor_layout == "symmetric" and red._inv is not None
+    ref = O.build_reduced_one_level(kern.tensors, W.grid.dims, mt, 0.3)
+    x = random_field(rng, W.grid.n_unknowns)
+    assert relerr(red.apply(x), O.apply_prec(ref, x)) < 1e-10
+    plan = plan_operator(kern)
+    p = C.build_one_level(kern, mt)
+    monkeypatch.setenv("VX_SYM", "0")
+    q = C.build_one_level(kern, mt)
+    monkeypatch.delenv("VX_SYM")
+    A = lambda v: apply_system(plan, W.m, v)  # noqa: E731
+    x1, r1 = gmres(A, W.b, apply_pinv=p.apply, tol=1e-10, maxit=300)
+    x2, r2 = gmres(A, W.b, apply_pinv=q.apply, tol=1e-10, maxit=300)
+    assert r1.iterations == r2.iterations and relerr(x1, x2) < 1e-9
