@@ -88,6 +88,8 @@ class Clocks:
         self.f = None
 
     def start(self):
+        if os.environ.get("VX_BENCH_CLOCKS", "1") == "0":   # A/B: host-jitter experiments only
+            return
         try:
             self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
             self.proc = subprocess.Popen(
@@ -105,7 +107,7 @@ class Clocks:
 
     def stop(self):
         if self.proc is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable or disabled"]}
         self.proc.terminate()
         try:
             self.proc.wait(timeout=5)
@@ -488,15 +490,19 @@ def run_ours(args):
         nv.timing_read(sp)
     l0 = nv.launch_count()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev_steps = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     e0.record()
     its = 0
     reports = []
-    for _ in range(args.steps):
+    for k in range(args.steps):
         x, rep = solve(b_dev)
         its += rep.iterations
         reports.append(rep)
+        ev_steps[k].record()
     e1.record()
     torch.cuda.synchronize()
+    step_ms = [round(e0.elapsed_time(ev_steps[0]), 2)] + [round(ev_steps[k - 1].elapsed_time(ev_steps[k]), 2)
+                                                           for k in range(1, args.steps)]
     launches = nv.launch_count() - l0
     clk = clocks.stop()
     barrier(torch, world)
@@ -626,6 +632,7 @@ def run_ours(args):
                        16 * sum(n * n * c for n, c in stored) / 1e9),
                    "parallelism": mode},
         "iterations_per_solve": its_per_solve,
+        "step_ms": step_ms,
         "build_s": build_s,
         "build_note": "warm build (second in process): Chan + x-DFT spectra, proxies, unfold + LU of all blocks",
         "plan_s": plan_s,

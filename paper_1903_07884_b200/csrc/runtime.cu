@@ -19,6 +19,21 @@ struct SpanLog {
 };
 static std::mutex g_tmu;
 static std::vector<SpanLog> g_spans;
+static std::vector<cudaEvent_t> g_evpool;  // recycled span events (creation is a driver call)
+
+static cudaEvent_t ev_get() {
+  {
+    std::lock_guard<std::mutex> lock(g_tmu);
+    if (!g_evpool.empty()) {
+      cudaEvent_t e = g_evpool.back();
+      g_evpool.pop_back();
+      return e;
+    }
+  }
+  cudaEvent_t e = nullptr;
+  if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
+  return e;
+}
 
 void count_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
@@ -31,7 +46,8 @@ Span::Span(const char* name, cudaStream_t s) : nm(name), st(s), a(nullptr), on(g
   if (!on) return;
   for (const char* o : t_open)
     if (std::strcmp(o, name) == 0) { on = false; return; }
-  if (cudaEventCreate(&a) != cudaSuccess) { on = false; return; }
+  a = ev_get();
+  if (!a) { on = false; return; }
   cudaEventRecord(a, st);
   t_open.push_back(nm);
 }
@@ -39,8 +55,8 @@ Span::Span(const char* name, cudaStream_t s) : nm(name), st(s), a(nullptr), on(g
 Span::~Span() {
   if (!on) return;
   if (!t_open.empty()) t_open.pop_back();
-  cudaEvent_t b;
-  if (cudaEventCreate(&b) != cudaSuccess) return;
+  cudaEvent_t b = ev_get();
+  if (!b) return;
   cudaEventRecord(b, st);
   std::lock_guard<std::mutex> lock(g_tmu);
   for (auto& s : g_spans)
@@ -69,8 +85,8 @@ extern "C" int vx_timing_read(const char* span, double* total_ms, long* count) {
       VX_CUDA(cudaEventElapsedTime(&ms, e.first, e.second));
       *total_ms += ms;
       *count += 1;
-      cudaEventDestroy(e.first);
-      cudaEventDestroy(e.second);
+      vx::g_evpool.push_back(e.first);
+      vx::g_evpool.push_back(e.second);
     }
     s.ev.clear();
   }
