@@ -376,4 +376,5 @@ def test_sharded_sector_factors_loopback(P):
     assert relerr(xs, x1) < 1e-6
     # every rank holds a share of the symmetry-reduced factors
     assert all(r[3] > 0 for r in results)
-    assert sum(r[3] for r in results) <= 1.5 * p.storage_bytes
+    # (ragged LU sector factors per rank; the single-GPU object may store the symmetric half)
+    assert sum(r[3] for r in results) <= 1.5 * 16 * sum(d * d * c for d, c in p.stored_blocks)
