@@ -2670,8 +2670,7 @@ extern "C" int vx_lu_sym_unpack(int nkslots, int nsec, int dmax, const int* sec_
   if (st) return st;
   if (nkslots == 0) return VX_OK;
   const LuGeom g = lu_geom(dmax);
-  dim3 grid(div_up(g.blk, 256 * 4) > 0 ? div_up(g.blk, 256 * 4) : 1, nkslots * nsec);
-  lu_sym_unpack_kernel<<<grid, 256, 0, as_stream(stream)>>>(g, sg, reinterpret_cast<const double2*>(sym),
+  lu_sym_unpack_kernel<<<nkslots * nsec, 256, 0, as_stream(stream)>>>(g, sg, reinterpret_cast<const double2*>(sym),
                                                             reinterpret_cast<double2*>(padded));
   VX_CHECK_LAUNCH("lu_sym_unpack_kernel");
   return VX_OK;
