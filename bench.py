@@ -340,6 +340,9 @@ def solve_kernel_traffic(name, W, world, layout=None):
         kname = "lu_solve_small_kernel"
     elif W.prec["kind"] == "reduced-one-level":
         kname = "lu_solve_rag_kernel<2> + rep_gemm_kernel"
+    if layout == "symmetric-inverse":
+        kname = "symv_inv_kernel<2>" + (" + rep_gemm_kernel" if W.prec["kind"] == "reduced-one-level" else "")
+        return kname, None
     if layout == "symmetric":
         kname = "lu_solve_sym_kernel<2>" + (" + rep_gemm_kernel" if W.prec["kind"] == "reduced-one-level" else "")
     traffic = None

@@ -378,6 +378,23 @@ int vx_prec1_apply_sym(int nx, int ny, int nz, const vx_c128* factors, const vx_
                        const unsigned char* flipk, const vx_c128* rep_inv, const int* rep_ks, int n_rep,
                        const vx_c128* x, vx_c128* y, vx_c128* work, void* stream);
 
+/* ---- symmetric inverse (csrc/lu_syminv.cuh).  With B = W A^ (A^ complex
+ * symmetric) the block inverse is B^-1 = G W^-1, G = A^^-1 = (L^-1 W)^T diag(h)
+ * (L^-1 W) complex symmetric: its lower triangle costs the bytes of L and
+ * x = G (b / W) is ONE streaming pass (a symmetric matrix-vector product on
+ * the FP64 tensor cores) instead of zgetrs's two dependent triangular sweeps
+ * (reference circulant.py:183-186).
+ * vx_lu_sym_invert: G of every block from the symmetric factors (layout and
+ *   stride of vx_lu_sym_pack; scratch: same size, receives L^-1).
+ * vx_prec1_apply_syminv: vx_prec1_apply_sym on G. */
+int vx_lu_sym_invert(int nkslots, int nsec, int dmax, const int* sec_dims, const vx_c128* sym, const vx_c128* h,
+                     const vx_c128* w, vx_c128* scratch, vx_c128* ginv, void* stream);
+int vx_prec1_apply_syminv(int nx, int ny, int nz, const vx_c128* ginv, const vx_c128* w, const int* items,
+                          int n_single, int direct_r, const int* klist, int nsec, int dmax, const int* sec_dims,
+                          int norb, const int* orows, const int* osec, const double* ocoef,
+                          const unsigned char* flipk, const vx_c128* rep_inv, const int* rep_ks, int n_rep,
+                          const vx_c128* x, vx_c128* y, vx_c128* work, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -208,11 +208,29 @@ def _sym_weights(plan, m_yz: np.ndarray) -> np.ndarray:
     return W
 
 
-class _SymFactors:
-    """Device symmetric factors: packed lower triangles, h = 1/(u W) per row, W."""
+SYMINV_TOL = 1e-11     # inverse apply vs triangular solves on a random vector (relative L2)
 
-    def __init__(self, fac, h, w, dims):
+
+class _SymFactors:
+    """Device symmetric factors: packed lower triangles, h = 1/(u W) per row, W;
+    inv: the lower triangles of the symmetric inverses G = A^^-1 (csrc/lu_syminv.cuh)
+    once build_inverse() has produced and verified them."""
+
+    def __init__(self, fac, h, w, dims, nsec, dmax):
         self.fac, self.h, self.w, self.dims = fac, h, w, dims
+        self.nsec, self.dmax = int(nsec), int(dmax)
+        self.inv = None
+
+    def build_inverse(self):
+        """G = (L^-1 W)^T diag(h) (L^-1 W) per block (vx_lu_sym_invert)."""
+        if os.environ.get("VX_SYMINV", "1") == "0":
+            return None
+        nk = int(self.fac.shape[0])
+        scratch = nv.empty_c128(tuple(self.fac.shape))
+        ginv = nv.empty_c128(tuple(self.fac.shape))
+        nv.call("vx_lu_sym_invert", nk, self.nsec, self.dmax, self.dims.ctypes.data, self.fac.data_ptr(),
+                self.h.data_ptr(), self.w.data_ptr(), scratch.data_ptr(), ginv.data_ptr(), nv.stream_ptr())
+        return ginv
 
 
 def _sym_pack(fac, sec, m_yz, nk):
@@ -231,7 +249,7 @@ def _sym_pack(fac, sec, m_yz, nk):
     d = dev[: nk * sp.nsec].cpu().numpy()
     if d.size and not (d[:, 0].max() <= SYM_TOL and d[:, 1].min() >= SYM_MIN_PIVOT):
         return None
-    return _SymFactors(sym, h, w, dims_a)
+    return _SymFactors(sym, h, w, dims_a, sp.nsec, sp.dmax)
 
 
 def _lu1_sec_auto(lam, m_dev, kdev, nk, nx, ny, nz, sec, m_yz):
@@ -459,14 +477,22 @@ class _OneLevelBase:
         self._flipk = t.from_numpy(flipk).cuda()
         self._n_single, self._n_items, self._direct_r = n_single, int(items.shape[0]), direct_r
 
-    def _apply_sym(self, xd, rep_inv=None, rep_ks=None):
-        """Single-RHS apply on symmetric sector factors (optionally with the
-        reduced scheme's representative GEMM)."""
+    def _apply_sym(self, xd, rep_inv=None, rep_ks=None, force_factors=False):
+        """Single-RHS apply on symmetric sector factors -- or, once built and
+        verified, on the symmetric inverses (one streaming pass) -- optionally
+        with the reduced scheme's representative GEMM."""
         nx, ny, nz = self.grid.dims
         sp, sd, sy = self._sec.plan, self._sec, self._sym
         n_rep = 0 if rep_ks is None else int(rep_ks.numel())
         y = nv.empty_c128((self.grid.n_unknowns, 1))
         work = nv.empty_c128(int(nv.query("vx_prec1_sec_reduced_work_elems", nx, ny, nz, 1, sp.nsec, sp.dmax, n_rep)))
+        if sy.inv is not None and not force_factors:
+            nv.call("vx_prec1_apply_syminv", nx, ny, nz, sy.inv.data_ptr(), sy.w.data_ptr(),
+                    self._items.data_ptr(), self._n_single, self._direct_r, self._klist.data_ptr(), sp.nsec,
+                    sp.dmax, sy.dims.ctypes.data, sd.norb, sd.orows.data_ptr(), sd.osec.data_ptr(),
+                    sd.ocoef.data_ptr(), self._flipk.data_ptr(), nv.ptr(rep_inv), nv.ptr(rep_ks), n_rep,
+                    xd.data_ptr(), y.data_ptr(), work.data_ptr(), nv.stream_ptr())
+            return y
         nv.call("vx_prec1_apply_sym", nx, ny, nz, sy.fac.data_ptr(), sy.h.data_ptr(), sy.w.data_ptr(),
                 self._items.data_ptr(), self._n_single, self._direct_r, self._klist.data_ptr(), sp.nsec, sp.dmax,
                 sy.dims.ctypes.data, sd.norb, sd.orows.data_ptr(), sd.osec.data_ptr(), sd.ocoef.data_ptr(),
@@ -524,6 +550,7 @@ class _OneLevelBase:
         if self._sym is not None:
             self._nslots = int(self._fac.shape[0])
             self._fac = self._sym.fac
+            self._make_inverse()
             return
         nsec, dmax, dims = self._rag_geometry()
         if dmax <= 32 or os.environ.get("VX_RAGGED", "1") == "0":
@@ -538,6 +565,31 @@ class _OneLevelBase:
         self._fac = rag
         self._rag_dims = dims_a
         self._nslots = nslots
+
+    def _make_inverse(self):
+        """Symmetric inverses of the stored blocks, kept only when one apply on a
+        random vector agrees with the triangular solves to SYMINV_TOL."""
+        sy = self._sym
+        if sy is None or sy.inv is not None or self._sec is None:
+            return
+        ginv = sy.build_inverse()
+        if ginv is None:
+            return
+        t = _torch()
+        gen = t.Generator(device="cuda")
+        gen.manual_seed(20240811)
+        n = self.grid.n_unknowns
+        x = t.randn(n, 2, dtype=t.float64, device="cuda", generator=gen)
+        xd = t.view_as_complex(x).reshape(n, 1)
+        rep = (getattr(self, "_inv", None), getattr(self, "_rep_ks", None)) if getattr(self, "_inv", None) is not None \
+            else (None, None)
+        ref = self._apply_sym(xd, rep[0], rep[1], force_factors=True)
+        sy.inv = ginv
+        got = self._apply_sym(xd, rep[0], rep[1])
+        err = float(t.linalg.vector_norm(got - ref) / t.linalg.vector_norm(ref))
+        if not err <= SYMINV_TOL:
+            sy.inv = None
+        self._syminv_err = err
 
     def _padded(self):
         """Padded-tile factors (nslots, npad^2): the layout the reduced scheme,
@@ -589,20 +641,21 @@ class _OneLevelBase:
     def storage_bytes(self) -> int:
         """Bytes actually resident on the device for the factors (symmetric,
         ragged, or padded tiles)."""
-        return int(self._fac.numel()) * 16
+        extra = self._sym.inv.numel() if self._sym is not None and self._sym.inv is not None else 0
+        return int(self._fac.numel() + extra) * 16
 
     @property
     def factor_bytes_per_apply(self) -> int:
         """Compulsory factor bytes of one single-RHS apply: every stored factor
         entry read once (symmetric layout: the lower triangles only)."""
         if self._sym is not None:
-            return int(self._sym.fac.numel()) * 16
+            return int(self._sym.fac.numel()) * 16   # inverse layout: same size as the factor layout
         return 16 * sum(d * d * c for d, c in self.stored_blocks)
 
     @property
     def factor_layout(self) -> str:
         if self._sym is not None:
-            return "symmetric"
+            return "symmetric-inverse" if self._sym.inv is not None else "symmetric"
         return "ragged" if getattr(self, "_rag_dims", None) is not None else "padded"
 
     @property

@@ -1703,6 +1703,7 @@ static int launch_solve_rag(const LuGeom& g, const RagGeom& rg, const double2* F
 }
 
 #include "lu_sym.cuh"
+#include "lu_syminv.cuh"
 
 // ------------------------------------------------------ single-tile blocks
 // n <= 32 (the 2-level scheme's (3nz)^2 blocks): one warp per work item, lane
@@ -2522,6 +2523,9 @@ static int prec1_apply_sec(int nx, int ny, int nz, int nrhs, const vx_c128* fact
     if (sym) {
       VX_REQUIRE(nrhs == 1, "symmetric factors: single-RHS work lists only");
       Span sp("prec_solve", s);
+      if (sym->inverse)
+        return launch_symv_inv(*sym, reinterpret_cast<const double2*>(factors), items, n_it, direct_r, klist, U,
+                               pitch, nrhs, q, s);
       return launch_solve_sym(*sym, reinterpret_cast<const double2*>(factors), items, n_it, direct_r, klist, U,
                               pitch, nrhs, q, s);
     }
@@ -2692,6 +2696,46 @@ extern "C" int vx_prec1_apply_sym(int nx, int ny, int nz, const vx_c128* factors
   rep.ks = rep_ks;
   rep.n = n_rep;
   return prec1_apply_sec(nx, ny, nz, 1, factors, nullptr, items, n_single, n_single, direct_r, klist, nsec, dmax,
+                         norb, orows, osec, ocoef, flipk, x, y, work, stream, nullptr, n_rep ? &rep : nullptr, &sg);
+}
+
+// vx_lu_sym_invert: G = (L^-1 W)^T diag(h) (L^-1 W), the lower triangle of the
+// symmetric inverse A^^-1 of every block, from the symmetric factors (scratch:
+// another buffer of the same size, holds L^-1 afterwards).
+extern "C" int vx_lu_sym_invert(int nkslots, int nsec, int dmax, const int* sec_dims, const vx_c128* sym,
+                                const vx_c128* h, const vx_c128* w, vx_c128* scratch, vx_c128* ginv, void* stream) {
+  VX_REQUIRE(nkslots >= 0 && sym && scratch && ginv, "bad symmetric inverse arguments");
+  SymGeom sg;
+  int st = make_sym(nsec, sec_dims, dmax, h, w, &sg);
+  if (st) return st;
+  if (nkslots == 0) return VX_OK;
+  Span span("lu_build", as_stream(stream));
+  lu_sym_invert_kernel<<<nkslots * nsec, 256, 0, as_stream(stream)>>>(
+      sg, reinterpret_cast<const double2*>(sym), reinterpret_cast<double2*>(scratch),
+      reinterpret_cast<double2*>(ginv));
+  VX_CHECK_LAUNCH("lu_sym_invert_kernel");
+  return VX_OK;
+}
+
+// vx_prec1_apply_syminv: vx_prec1_apply_sym with the block solves replaced by
+// x = G (b / W) on the stored symmetric inverses (one streaming pass).
+extern "C" int vx_prec1_apply_syminv(int nx, int ny, int nz, const vx_c128* ginv, const vx_c128* w,
+                                     const int* items, int n_single, int direct_r, const int* klist, int nsec,
+                                     int dmax, const int* sec_dims, int norb, const int* orows, const int* osec,
+                                     const double* ocoef, const unsigned char* flipk, const vx_c128* rep_inv,
+                                     const int* rep_ks, int n_rep, const vx_c128* x, vx_c128* y, vx_c128* work,
+                                     void* stream) {
+  VX_REQUIRE(n_rep >= 0 && (n_rep == 0 || (rep_inv && rep_ks)), "bad representative arguments");
+  SymGeom sg;
+  int st = make_sym(nsec, sec_dims, dmax, nullptr, w, &sg);
+  if (st) return st;
+  sg.inverse = 1;
+  SecRep rep;
+  rep.inv = reinterpret_cast<const double2*>(rep_inv);
+  rep.inv_stride = vx_rep_inverse_elems(dmax);
+  rep.ks = rep_ks;
+  rep.n = n_rep;
+  return prec1_apply_sec(nx, ny, nz, 1, ginv, nullptr, items, n_single, n_single, direct_r, klist, nsec, dmax,
                          norb, orows, osec, ocoef, flipk, x, y, work, stream, nullptr, n_rep ? &rep : nullptr, &sg);
 }
 

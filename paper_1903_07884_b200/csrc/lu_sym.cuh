@@ -67,6 +67,7 @@ struct SymGeom {
   long kstride;
   const double2* h;  // [slot][dmax]
   const double2* w;  // [sector][dmax]
+  int inverse;       // 0: factors (lu_solve_sym_kernel); 1: symmetric inverse G (lu_syminv.cuh)
 };
 
 constexpr int SYM_MAX_DIM = 1024;
@@ -77,6 +78,7 @@ static int make_sym(int nsec, const int* dims, int dmax, const void* h, const vo
              SYM_MAX_DIM);
   sg->nsec = nsec;
   sg->dmax = dmax;
+  sg->inverse = 0;
   long off = 0;
   for (int s = 0; s < 4; ++s) {
     sg->dims[s] = s < nsec ? dims[s] : 0;
@@ -333,6 +335,8 @@ __global__ void __launch_bounds__(256) lu_sym_unpack_kernel(LuGeom g, SymGeom sg
 // each factor byte once.
 constexpr int SYM_WARPS = 8;
 
+// (volatile: the warp-collective must stay where it is written -- without it the
+// compiler sinks the products into the divergent "lanes t < 2 store" branches)
 __device__ __forceinline__ void dmma_884(double& c0, double& c1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
                : "+d"(c0), "+d"(c1)
@@ -353,10 +357,29 @@ __device__ __forceinline__ void bulk_g2s_hint(void* dst, const void* src, uint32
       : "memory");
 }
 
+// L2 prefetch of a span of the factor stream (no shared-memory destination):
+// the forward pass's tiles are requested from HBM a window ahead of the ring,
+// so the ring's own loads see L2 latency
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+// wait with a suspend-time hint: the polling warp sleeps in hardware instead
+// of spinning through the issue slots of the warps that have work
+__device__ __forceinline__ void mbar_wait_hint(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "W%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+      " @!p bra W%=;\n}\n" ::"r"(smem_u32(b)),
+      "r"(parity), "r"(20000u)
+      : "memory");
+}
+
 template <int R, int MINB>
 __global__ void __launch_bounds__((SYM_WARPS + 1) * 32, MINB)
     lu_solve_sym_kernel(SymGeom sg, const double2* __restrict__ F, const int* __restrict__ items, int nwork,
-                        const int* __restrict__ klist, double2* Y, long s_row, long s_k, int S, int q, int l2hint) {
+                        const int* __restrict__ klist, double2* Y, long s_row, long s_k, int S, int q, int l2hint,
+                        int pfwin, int dbg) {
   extern __shared__ __align__(128) unsigned char smraw[];
   constexpr int T2 = 1024;
   const int npad = (sg.dmax + 31) / 32 * 32;
@@ -387,7 +410,7 @@ __global__ void __launch_bounds__((SYM_WARPS + 1) * 32, MINB)
       uint32_t use = 0;  // completed passes over the ring
       bool fwd = true;
       auto emit = [&](const double2* src, uint32_t elems) {
-        if (use > 0) mbar_wait(empty + s, (use - 1) & 1u);
+        if (use > 0) mbar_wait_hint(empty + s, (use - 1) & 1u);
         const uint32_t bytes = elems * (uint32_t)sizeof(double2);
         mbar_expect_tx(full + s, bytes);
         if (l2hint) bulk_g2s_hint(slots + s * T2, src, bytes, full + s, fwd);
@@ -402,22 +425,39 @@ __global__ void __launch_bounds__((SYM_WARPS + 1) * 32, MINB)
         int nb, sec;
         const double2* Fb = sym_block(sg, F, slot, nb, sec);
         const int nt = (nb + 31) / 32;
+        const long total = sym_size(nb);
+        long pf = 0;  // entries of this block already requested into L2
+        auto prefetch_to = [&](long upto) {
+          upto = upto < total ? upto : total;
+          while (pf < upto) {
+            const long n = upto - pf < 1024 ? upto - pf : 1024;
+            bulk_prefetch_l2(Fb + pf, (uint32_t)(n * sizeof(double2)));
+            pf += n;
+          }
+        };
         auto tile = [&](int i, int j) {  // j == i: the trapezoid
           const int ti = min(32, nb - 32 * i);
-          emit(Fb + sym_band(i) + 32L * ti * j, (uint32_t)(i == j ? trap_size(ti) : ti * 32));
+          const long off = sym_band(i) + 32L * ti * j;
+          const uint32_t n = (uint32_t)(i == j ? trap_size(ti) : ti * 32);
+          if (fwd && pfwin > 0) prefetch_to(off + n + pfwin);
+          emit(Fb + off, n);
         };
         for (int ch = 0; ch < (cnt + R - 1) / R; ++ch) {
           fwd = true;
+          pf = 0;
+          if (!(dbg & 2))
           for (int i = 0; i < nt; ++i) {
             for (int j = 0; j < i; ++j) tile(i, j);
             tile(i, i);
           }
           fwd = false;
+          if (!(dbg & 1)) {
           for (int i = nt - 1; i >= 0; --i) {
             for (int j = nt - 1; j > i; --j) tile(j, i);
             if (i + 1 < nt) tile(i + 1, i + 1);
           }
           tile(0, 0);
+          }
         }
       }
     }
@@ -427,7 +467,7 @@ __global__ void __launch_bounds__((SYM_WARPS + 1) * 32, MINB)
   int cs = 0;
   uint32_t cph = 0;
   auto wait_tile = [&]() -> const double* {
-    mbar_wait(full + cs, cph);
+    mbar_wait_hint(full + cs, cph);
     return reinterpret_cast<const double*>(slots + cs * T2);
   };
   auto release_tile = [&]() {
@@ -517,7 +557,7 @@ __global__ void __launch_bounds__((SYM_WARPS + 1) * 32, MINB)
   // when every warp has stored its partials, rdone once every warp has read them
   uint32_t nput = 0, nget = 0;
   auto put_partials = [&](bool with_z) {
-    if (nput > 0) mbar_wait(rdone, (nput - 1) & 1u);
+    if (nput > 0) mbar_wait_hint(rdone, (nput - 1) & 1u);
     if (t < 2) {
 #pragma unroll
       for (int b = 0; b < 4; ++b) pt[((warp * 32 + 8 * b + g) << 1) + t] = cmk(acc[b][0], acc[b][1]);
@@ -531,7 +571,7 @@ __global__ void __launch_bounds__((SYM_WARPS + 1) * 32, MINB)
     ++nput;
   };
   auto wait_partials = [&]() {
-    mbar_wait(pbar, nget & 1u);
+    mbar_wait_hint(pbar, nget & 1u);
     ++nget;
   };
   auto done_partials = [&]() {
@@ -585,8 +625,9 @@ __global__ void __launch_bounds__((SYM_WARPS + 1) * 32, MINB)
         }
         done_partials();
       };
+      if (!(dbg & 2))
       for (int i = 0; i < nt; ++i) {
-        const int ti = min(32, nb - 32 * i), nrb = (ti + 7) >> 3;
+        const int ti = min(32, nb - 32 * i), nrb = (dbg & 4) ? 0 : (ti + 7) >> 3;
         zero(acc);
         for (int j = 0; j + 1 < i; ++j) {
           fwd_tile(wait_tile(), nrb, 32 * j);
@@ -601,7 +642,8 @@ __global__ void __launch_bounds__((SYM_WARPS + 1) * 32, MINB)
         release_tile();
         put_partials(false);
       }
-      finish_fwd(nt - 1);
+      if (!(dbg & 2)) finish_fwd(nt - 1);
+      if (dbg & 1) continue;
       // ---------------- backward: t_i = c_i - sum_{j>i} L'_ji^T t_j with c = y / (u W);
       // z_{i+1} = inv(L_{i+1})^T t_{i+1} rides one step behind
       auto finish_bwd = [&](int p, double2 hv) {  // t_p slice <- c_p + partials; z_{p+1} -> global
@@ -629,11 +671,11 @@ __global__ void __launch_bounds__((SYM_WARPS + 1) * 32, MINB)
         double2 hv = cmk(0.0, 0.0);
         if (dep) hv = hval(i + 1);
         for (int j = nt - 1; j > i + 1; --j) {
-          bwd_tile(wait_tile(), min(32, nb - 32 * j), 32 * j);
+          bwd_tile(wait_tile(), (dbg & 4) ? 0 : min(32, nb - 32 * j), 32 * j);
           release_tile();
         }
         if (dep) {
-          const int tp = min(32, nb - 32 * (i + 1));
+          const int tp = (dbg & 4) ? 0 : min(32, nb - 32 * (i + 1));
           finish_bwd(i + 1, hv);
           bwd_tile(wait_tile(), tp, 32 * (i + 1));
           release_tile();
@@ -669,6 +711,9 @@ static int launch_solve_sym_t(const SymGeom& sg, const double2* F, const int* it
   // 3 CTAs per SM: the in-flight triangles fit L2, so DRAM traffic ~= the stored bytes
   static const int minb = env_int("VX_SYM_MINB", 3);
   static const int l2hint = env_int("VX_SYM_L2HINT", 1);
+  // forward tiles are requested into L2 this many KB ahead of the ring
+  static const int pfwin = env_int("VX_SYM_PF", 64) * 64;  // entries (16 bytes)
+  static const int dbg = env_int("VX_SYM_DBG", 0);
   const int S = slots_env < 2 ? 2 : (slots_env > 12 ? 12 : slots_env);
   const int npad = (sg.dmax + 31) / 32 * 32;
   const size_t smem = (((size_t)2 * S + 2) * 8 + 127) / 128 * 128 + (size_t)S * 1024 * sizeof(double2) +
@@ -676,7 +721,8 @@ static int launch_solve_sym_t(const SymGeom& sg, const double2* F, const int* it
   auto kern = minb == 2 ? lu_solve_sym_kernel<R, 2> : minb == 4 ? lu_solve_sym_kernel<R, 4> : lu_solve_sym_kernel<R, 3>;
   VX_REQUIRE((int)smem + 1024 <= device_smem_optin(), "symmetric solve smem %zu too large", smem);
   VX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  kern<<<nblocks, (SYM_WARPS + 1) * 32, smem, s>>>(sg, F, items, nblocks, klist, Y, s_row, s_k, S, q, l2hint);
+  kern<<<nblocks, (SYM_WARPS + 1) * 32, smem, s>>>(sg, F, items, nblocks, klist, Y, s_row, s_k, S, q, l2hint,
+                                                   pfwin, dbg);
   VX_CHECK_LAUNCH("lu_solve_sym_kernel");
   return VX_OK;
 }

@@ -1,0 +1,489 @@
+// Symmetric INVERSE storage of the 1-level sector blocks and its one-pass
+// apply -- included by circulant.cu after lu_sym.cuh (same geometry: SymGeom,
+// sym_band, trap_off, sym_swz; the mbarrier / bulk-copy helpers).
+//
+// Why: the two triangular passes of lu_sym.cuh read every factor byte twice
+// (the second time from L2) and are a chain of dependent tile rows; measured
+// on c1 the pair of passes cannot go below ~0.65 ms even with the arithmetic
+// removed (forward alone: 0.44 ms = the HBM peak; profiles/r02_sym_phases.txt).
+// With B = W A^ (A^ complex symmetric, W = S M on the sector rows) the inverse
+// is B^-1 = G W^-1 with G = A^^-1 complex SYMMETRIC, and from the unpivoted
+// factors B = L U, U = diag(u) W L^T W^-1:
+//     G = (L^-1 W)^T diag(h) (L^-1 W),      h = 1 / (u W).
+// Storing the lower triangle of G costs the bytes of L, and x = G (b / W) is a
+// symmetric matrix-vector product: ONE streaming pass over the stored bytes,
+// every tile used for both its product and its transposed product while it
+// sits in shared memory, no dependencies between tiles.  The reference's
+// zgetrs (circulant.py:183-186) becomes a bandwidth-bound SYMV.
+// The blocks here are well conditioned (cond <= 1.6e2 on the BASELINE
+// workloads), the caller verifies G against the triangular solves on a random
+// vector (relative 1e-11) and keeps the factors otherwise.
+//
+// Layout of G: the lu_sym.cuh layout (tile rows of row-major swizzled t_i x 32
+// tiles, then the diagonal trapezoid); the diagonal 8 x 8 blocks of the
+// trapezoid hold both triangles of the symmetric block.
+//
+// Included INSIDE namespace vx.
+
+// ------------------------------------------------------------------ build
+// One CTA per slot.  N = L^-1 by tile columns (N_ij = -sum_{j<=k<i} L'_ik N_kj,
+// N_jj = inv(L_jj), with the premultiplied tiles L' of the symmetric layout),
+// written to the scratch buffer in the same layout; then
+// G_ij = W_i [sum_{k>=i} N_ki^T diag(h_k) N_kj] W_j for i >= j.
+__device__ __forceinline__ void syminv_load_tile(double2 (*dst)[33], const double2* blk, int nb, int i, int j,
+                                                 const double2* rowscale, int tid) {
+  // dst[r][c] = entry (r, c) of tile (i, j) (j == i: the trapezoid; zeros outside), rows scaled
+  const int ti = min(32, nb - 32 * i);
+  const double2* base = blk + sym_band(i) + 32L * ti * j;
+  for (int e = tid; e < 1024; e += 256) {
+    const int r = e >> 5, c = e & 31;
+    double2 v = cmk(0.0, 0.0);
+    if (r < ti) {
+      if (i != j) v = base[r * 32 + sym_swz(r, c)];
+      else if (c < 8 * (r >> 3) + 8) v = base[trap_off(r) + sym_swz(r, c)];
+      if (rowscale) v = cmul(v, rowscale[32 * i + r]);
+    }
+    dst[r][c] = v;
+  }
+}
+
+__global__ void __launch_bounds__(256) lu_sym_invert_kernel(SymGeom sg, const double2* __restrict__ Lp,
+                                                            double2* __restrict__ Nq, double2* __restrict__ Gq) {
+  __shared__ double2 As[32][33];
+  __shared__ double2 Bs[32][33];
+  const int slot = blockIdx.x;
+  int nb, sec;
+  const double2* Lb = sym_block(sg, Lp, slot, nb, sec);
+  double2* Nb = const_cast<double2*>(sym_block(sg, Nq, slot, nb, sec));
+  double2* Gb = const_cast<double2*>(sym_block(sg, Gq, slot, nb, sec));
+  const double2* W = sg.w + (long)sec * sg.dmax;
+  const double2* H = sg.h + (long)slot * sg.dmax;
+  const int tid = threadIdx.x;
+  const int nt = (nb + 31) / 32;
+  const int r0 = tid >> 5, c = tid & 31;  // outputs (r0 + 8 m, c), m = 0..3
+  // ---- N = L^-1
+  for (int j = 0; j < nt; ++j) {
+    {  // N_jj = inv(L_jj): the trapezoid as stored
+      const int tj = min(32, nb - 32 * j);
+      const long o = sym_band(j) + 32L * tj * j;
+      for (int e = tid; e < trap_size(tj); e += 256) Nb[o + e] = Lb[o + e];
+    }
+    for (int i = j + 1; i < nt; ++i) {
+      const int ti = min(32, nb - 32 * i);
+      double2 acc[4];
+#pragma unroll
+      for (int m = 0; m < 4; ++m) acc[m] = cmk(0.0, 0.0);
+      for (int k = j; k < i; ++k) {
+        __syncthreads();  // previous product done with As / Bs; N_kj of this block written
+        syminv_load_tile(As, Lb, nb, i, k, nullptr, tid);
+        syminv_load_tile(Bs, Nb, nb, k, j, nullptr, tid);
+        __syncthreads();
+#pragma unroll 8
+        for (int mm = 0; mm < 32; ++mm) {
+          const double2 b = Bs[mm][c];
+#pragma unroll
+          for (int m = 0; m < 4; ++m) cfma(acc[m], As[r0 + 8 * m][mm], b);
+        }
+      }
+      double2* dst = Nb + sym_band(i) + 32L * ti * j;
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {
+        const int r = r0 + 8 * m;
+        if (r < ti) dst[r * 32 + sym_swz(r, c)] = cmk(-acc[m].x, -acc[m].y);
+      }
+    }
+  }
+  // ---- G_ij = W_i sum_k N_ki^T diag(h_k) N_kj W_j (rows a of tile row i, columns b of tile row j)
+  for (int i = 0; i < nt; ++i) {
+    const int ti = min(32, nb - 32 * i);
+    for (int j = 0; j <= i; ++j) {
+      double2 acc[4];
+#pragma unroll
+      for (int m = 0; m < 4; ++m) acc[m] = cmk(0.0, 0.0);
+      for (int k = i; k < nt; ++k) {
+        __syncthreads();
+        syminv_load_tile(As, Nb, nb, k, i, H, tid);  // As[m][a] = h_k[m] N_ki[m][a]
+        syminv_load_tile(Bs, Nb, nb, k, j, nullptr, tid);
+        __syncthreads();
+#pragma unroll 8
+        for (int mm = 0; mm < 32; ++mm) {
+          const double2 b = Bs[mm][c];
+#pragma unroll
+          for (int m = 0; m < 4; ++m) cfma(acc[m], As[mm][r0 + 8 * m], b);
+        }
+      }
+      double2* dst = Gb + sym_band(i) + 32L * ti * j;
+      const double2 wj = W[32 * j + c < nb ? 32 * j + c : 0];
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {
+        const int a = r0 + 8 * m;
+        if (a < ti) {
+          const double2 v = cmul(cmul(acc[m], W[32 * i + a]), wj);
+          if (i != j) dst[a * 32 + sym_swz(a, c)] = v;
+          else if (c < 8 * (a >> 3) + 8) dst[trap_off(a) + sym_swz(a, c)] = v;
+        }
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------ apply
+// x = G (b / W): one CTA per work item (a stored sector block and its one or
+// two right-hand sides), 4 tensor-core warps + a producer warp.  The producer
+// streams the block's storage in order as UNITS of up to 16 tile rows (8 KB)
+// into an S-slot mbarrier ring; unit n belongs to warp n mod 4 alone, which
+// runs both products of the unit on the FP64 tensor cores (fragment scheme of
+// lu_sym.cuh: A = stored entries, B = (Re, Im) columns of the two right-hand
+// sides) -- rows of tile row i from the unit times c_j, and columns of tile
+// row j from the unit's transpose times c_i -- and adds the results into ITS
+// OWN partial vector in shared memory (no atomics; the four partial vectors
+// are summed in a fixed order at the end: bitwise reproducible).
+constexpr int SYMV_WARPS = 4;
+
+// Per-lane fragment offsets (doubles), fixed for the whole kernel, so that every
+// fragment load of the unrolled unit bodies is [register + immediate]:
+//   nb[kl]  product A fragment: row g of a row block, unit (kc & 3) == kl; + 512 rb + 16 (kc >> 2)
+//   tb[par] transposed A fragment: rows 2 kc + (t >> 1), kc & 1 == par; + 128 kc + 16 cb
+//   cb      operand fragment in the signed right-hand-side array c3; + 192 panel + 12 kc
+struct SymvLane {
+  int nb[4];
+  int tb[2];
+  int cb;
+  int g, t;
+};
+
+// c3: per (entry, right-hand side) three doubles (y_i, y_r, -y_i): the B
+// fragment column "Re" reads (y_r, -y_i) at +1, the column "Im" reads (y_i, y_r)
+// at +0 -- no sign arithmetic in the loops.  Lanes g >= 4 mirror lanes g - 4:
+// their C columns are never stored.
+__device__ __forceinline__ SymvLane symv_lane(int lane) {
+  SymvLane L;
+  L.g = lane >> 2;
+  L.t = lane & 3;
+  const int g = L.g, t = L.t;
+  const int fsw = ((g & 1) << 1) | ((g >> 1) & 1);
+#pragma unroll
+  for (int kl = 0; kl < 4; ++kl) L.nb[kl] = g * 64 + ((kl ^ fsw) << 2) + t;
+  const int bcol = ((g & 1) << 1) + (t & 1);
+#pragma unroll
+  for (int par = 0; par < 2; ++par) L.tb[par] = (t >> 1) * 64 + ((((g >> 1) ^ (((t >> 1) << 1) | par)) << 2)) + bcol;
+  const int rr = (g >> 1) & 1, im = g & 1;
+  L.cb = (t >> 1) * 6 + rr * 3 + (1 - im) + (t & 1);
+  return L;
+}
+
+// a full 16 x 32 unit of tile (i, j), j < i: rows 16 h .. 16 h + 15 of tile row i
+// times c_j into (n0, n1), and the unit's transpose times c_i (rows) into aT.
+// Eight stages of 8 products; the 11 fragment loads of stage s + 1 are issued
+// before the products of stage s (explicit double buffer: the tensor pipe
+// never waits for a shared-memory round trip).
+struct SymvStage {
+  double an[4], bn[2], at[4], bt;
+};
+__device__ __forceinline__ void symv_stage_load(SymvStage& f, int st, const double* __restrict__ A,
+                                                const SymvLane& L, const double* __restrict__ cj,
+                                                const double* __restrict__ ci) {
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    const int kc = 2 * st + u;
+    const double* An = A + L.nb[kc & 3] + 16 * (kc >> 2);
+    f.bn[u] = cj[L.cb + 12 * kc];
+    f.an[2 * u] = An[0];
+    f.an[2 * u + 1] = An[512];
+  }
+  f.bt = ci[L.cb + 12 * st];
+  const double* At = A + L.tb[st & 1] + 128 * st;
+#pragma unroll
+  for (int cb = 0; cb < 4; ++cb) f.at[cb] = At[16 * cb];
+}
+__device__ __forceinline__ void symv_stage_mma(const SymvStage& f, double (&n0)[2], double (&n1)[2],
+                                               double (&aT)[4][2]) {
+  dmma_884(n0[0], n0[1], f.an[0], f.bn[0]);
+  dmma_884(n1[0], n1[1], f.an[1], f.bn[0]);
+  dmma_884(aT[0][0], aT[0][1], f.at[0], f.bt);
+  dmma_884(aT[1][0], aT[1][1], f.at[1], f.bt);
+  dmma_884(n0[0], n0[1], f.an[2], f.bn[1]);
+  dmma_884(n1[0], n1[1], f.an[3], f.bn[1]);
+  dmma_884(aT[2][0], aT[2][1], f.at[2], f.bt);
+  dmma_884(aT[3][0], aT[3][1], f.at[3], f.bt);
+}
+__device__ __forceinline__ void symv_unit_full(const double* __restrict__ A, const SymvLane& L,
+                                               const double* __restrict__ cj, const double* __restrict__ ci,
+                                               double (&n0)[2], double (&n1)[2], double (&aT)[4][2]) {
+  SymvStage f0, f1;
+  symv_stage_load(f0, 0, A, L, cj, ci);
+#pragma unroll
+  for (int st = 0; st < 8; st += 2) {
+    symv_stage_load(f1, st + 1, A, L, cj, ci);
+    symv_stage_mma(f0, n0, n1, aT);
+    if (st + 2 < 8) symv_stage_load(f0, st + 2, A, L, cj, ci);
+    symv_stage_mma(f1, n0, n1, aT);
+  }
+}
+
+// a partial unit (rows < 16: the last tile row of a block)
+__device__ __forceinline__ void symv_unit_part(const double* __restrict__ A, const SymvLane& L, int rows,
+                                               const double* __restrict__ cj, const double* __restrict__ ci,
+                                               double (&n0)[2], double (&n1)[2], double (&aT)[4][2]) {
+  const bool two = rows > 8;
+#pragma unroll 4
+  for (int kc = 0; kc < 16; ++kc) {
+    const double b = cj[L.cb + 12 * kc];
+    const double* An = A + L.nb[kc & 3] + 16 * (kc >> 2);
+    dmma_884(n0[0], n0[1], An[0], b);
+    if (two) dmma_884(n1[0], n1[1], An[512], b);
+  }
+  for (int kc = 0; 2 * kc < rows; ++kc) {
+    const bool ok = 2 * kc + (L.t >> 1) < rows;
+    const double bt = ci[L.cb + 12 * kc];
+    const double* At = A + L.tb[kc & 1] + 128 * kc;
+#pragma unroll
+    for (int cb = 0; cb < 4; ++cb) {
+      const double a = ok ? At[16 * cb] : 0.0;
+      dmma_884(aT[cb][0], aT[cb][1], a, bt);
+    }
+  }
+}
+
+// rows [16 H, 16 H + 16) of the diagonal trapezoid of tile row i (ti rows): the
+// product covers the columns < 8 rb + 8 of row block rb (both triangles of the
+// diagonal 8 x 8 blocks are stored), the transposed product the blocks cb < rb
+template <int H>
+__device__ __forceinline__ void symv_unit_diag(const double* __restrict__ A, const SymvLane& L, int ti,
+                                               const double* __restrict__ ci, double (&n0)[2], double (&n1)[2],
+                                               double (&aT)[4][2]) {
+  const double* Ad = A - 2 * trap_off(16 * H);
+#pragma unroll
+  for (int rl = 0; rl < 2; ++rl) {
+    constexpr int dummy = 0;
+    (void)dummy;
+    const int rb = 2 * H + rl;
+    if (8 * rb >= ti) continue;
+    const int len = 8 * rb + 8;  // entries per row of this row block
+    const double* Ab = Ad + 2 * (32 * rb * (rb + 1));
+    // product: row 8 rb + g
+    const double* Arow = Ab + 2 * L.g * len;
+#pragma unroll
+    for (int kc = 0; kc < 4 * rb + 4; ++kc) {
+      const double b = ci[L.cb + 12 * kc];
+      const double a = Arow[(L.nb[kc & 3] - L.g * 64) + 16 * (kc >> 2)];
+      if (rl == 0) dmma_884(n0[0], n0[1], a, b);
+      else dmma_884(n1[0], n1[1], a, b);
+    }
+    // transposed product: contracted rows 8 rb + 2 kc + (t >> 1), outputs 8 cb + g, cb < rb
+    if (rb > 0) {
+#pragma unroll
+      for (int kc = 0; kc < 4; ++kc) {
+        const int r = 2 * kc + (L.t >> 1);  // row inside the row block
+        const bool ok = 8 * rb + r < ti;
+        const double bt = ci[L.cb + 12 * (4 * rb + kc)];
+        const double* At = Ab + 2 * r * len + (L.tb[kc & 1] - (L.t >> 1) * 64);
+#pragma unroll
+        for (int cb = 0; cb < 4; ++cb)
+          if (cb < rb) {
+            const double a = ok ? At[16 * cb] : 0.0;
+            dmma_884(aT[cb][0], aT[cb][1], a, bt);
+          }
+      }
+    }
+  }
+}
+
+template <int R, int MINB>
+__global__ void __launch_bounds__((SYMV_WARPS + 1) * 32, MINB)
+    symv_inv_kernel(SymGeom sg, const double2* __restrict__ G, const int* __restrict__ items, int nwork,
+                    const int* __restrict__ klist, double2* Y, long s_row, long s_k, int S, int q) {
+  extern __shared__ __align__(128) unsigned char smraw[];
+  constexpr int NC = SYMV_WARPS * 32;
+  constexpr int U2 = 512;  // entries per ring slot (8 KB)
+  const int npad = (sg.dmax + 31) / 32 * 32, ntm = npad / 32;
+  const uint32_t D = (uint32_t)S / SYMV_WARPS;  // slots per warp
+  uint64_t* full = reinterpret_cast<uint64_t*>(smraw);
+  uint64_t* empty = full + S;
+  double2* slots = reinterpret_cast<double2*>(smraw + (2 * S * 8 + 127) / 128 * 128);
+  double2* pt = slots + (long)S * U2;                                    // [SYMV_WARPS][ntm][32][2]
+  double* c3 = reinterpret_cast<double*>(pt + (long)SYMV_WARPS * ntm * 64);  // [npad][2][3]: c = b / W, signed
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(full + s, 1);
+      mbar_init(empty + s, 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp == SYMV_WARPS) {
+    if (lane == 0) {
+      uint32_t n = 0;  // units emitted (all work items)
+      for (int w = blockIdx.x; w < nwork; w += gridDim.x) {
+        const int slot = items[3 * w], cnt = items[3 * w + 2];
+        int nb, sec;
+        const double2* Gb = sym_block(sg, G, slot, nb, sec);
+        const int nt = (nb + 31) / 32;
+        for (int ch = 0; ch < (cnt + R - 1) / R; ++ch) {
+          for (int i = 0; i < nt; ++i) {
+            const int ti = min(32, nb - 32 * i), nh = ti > 16 ? 2 : 1;
+            const double2* band = Gb + sym_band(i);
+            for (int j = 0; j <= i; ++j)
+              for (int h = 0; h < nh; ++h) {
+                const int rows = min(16, ti - 16 * h);
+                const double2* src;
+                uint32_t elems;
+                if (j < i) {
+                  src = band + 32L * ti * j + 512 * h;
+                  elems = (uint32_t)rows * 32;
+                } else {
+                  src = band + 32L * ti * i + trap_off(16 * h);
+                  elems = (uint32_t)(trap_off(16 * h + rows) - trap_off(16 * h));
+                }
+                const uint32_t k = n / SYMV_WARPS;
+                const int s = (int)(n % SYMV_WARPS) + SYMV_WARPS * (int)(k % D);
+                const uint32_t use = k / D;
+                if (use > 0) mbar_wait_hint(empty + s, (use - 1) & 1u);
+                mbar_expect_tx(full + s, elems * (uint32_t)sizeof(double2));
+                bulk_g2s(slots + s * U2, src, elems * (uint32_t)sizeof(double2), full + s);
+                ++n;
+              }
+          }
+        }
+      }
+    }
+    return;
+  }
+
+  const SymvLane L = symv_lane(lane);
+  double2* ptw = pt + (long)warp * ntm * 64;
+  // add C fragments (blocks of 8 entries x 2 right-hand sides) into the warp's partial vector
+  auto rmw1 = [&](int panel, int blk, const double (&a)[2]) {
+    if (L.t < 2) {
+      double2* p = ptw + (((panel * 32 + 8 * blk + L.g) << 1) + L.t);
+      const double2 o = *p;
+      *p = cmk(o.x + a[0], o.y + a[1]);
+    }
+  };
+  uint32_t n = 0;  // units seen (all work items): unit n is warp n % 4's
+  for (int w = blockIdx.x; w < nwork; w += gridDim.x) {
+    const int slot = items[3 * w], beg = items[3 * w + 1], cnt = items[3 * w + 2];
+    int nb, sec;
+    (void)sym_block(sg, G, slot, nb, sec);
+    const int nt = (nb + 31) / 32;
+    const double2* wrow = sg.w + (long)sec * sg.dmax;
+    for (int ch = 0; ch < (cnt + R - 1) / R; ++ch) {
+      const int rho0 = ch * R;
+      const int nr = min(R, cnt - rho0);
+      long rb0 = 0, rb1 = 0;
+      {
+        const int k0 = klist ? klist[beg + rho0] : beg + rho0;
+        rb0 = rhs_base(k0, rho0, 1, s_k);
+        if (nr > 1) {
+          const int k1 = klist ? klist[beg + rho0 + 1] : beg + rho0 + 1;
+          rb1 = rhs_base(k1, rho0 + 1, 1, s_k);
+        }
+      }
+      consumers_sync(NC);  // the previous item's final reduction is done with c3 / pt
+      for (int idx = tid; idx < npad * 2; idx += NC) {
+        const int row = idx >> 1, rr = idx & 1;
+        double2 v = cmk(0.0, 0.0);
+        if (row < nb && rr < nr) {
+          const long rb = rr ? rb1 : rb0;
+          v = cdiv(cflip(Y[(long)row * s_row + (rb & ROFF)], flip_row((int)(rb >> 56), row, q)), wrow[row]);
+        }
+        double* o = c3 + 3 * idx;
+        o[0] = v.y;
+        o[1] = v.x;
+        o[2] = -v.y;
+      }
+      for (int idx = lane; idx < ntm * 64; idx += 32) ptw[idx] = cmk(0.0, 0.0);
+      consumers_sync(NC);
+      double accN[4][2];
+#pragma unroll
+      for (int b = 0; b < 4; ++b) accN[b][0] = accN[b][1] = 0.0;
+      for (int i = 0; i < nt; ++i) {
+        const int ti = min(32, nb - 32 * i), nh = ti > 16 ? 2 : 1;
+        const double* ci = c3 + 192 * i;
+        bool mine = false;
+        for (int j = 0; j <= i; ++j)
+          for (int h = 0; h < nh; ++h, ++n) {
+            if ((int)(n % SYMV_WARPS) != warp) continue;
+            mine = true;
+            // the warp's k-th unit sits in ITS slot warp + 4 (k mod D): only the owner ever
+            // waits on a slot, so it sees the slot's phases one after the other
+            const uint32_t k = n / SYMV_WARPS;
+            const int s = warp + SYMV_WARPS * (int)(k % D);
+            mbar_wait_hint(full + s, (k / D) & 1u);
+            const double* A = reinterpret_cast<const double*>(slots + s * U2);
+            const int rows = min(16, ti - 16 * h);
+            double accT[4][2];
+#pragma unroll
+            for (int b = 0; b < 4; ++b) accT[b][0] = accT[b][1] = 0.0;
+            if (j < i) {
+              const double* cj = c3 + 192 * j;
+              if (rows == 16) {
+                if (h == 0) symv_unit_full(A, L, cj, ci, accN[0], accN[1], accT);
+                else symv_unit_full(A, L, cj, ci + 96, accN[2], accN[3], accT);
+              } else {
+                if (h == 0) symv_unit_part(A, L, rows, cj, ci, accN[0], accN[1], accT);
+                else symv_unit_part(A, L, rows, cj, ci + 96, accN[2], accN[3], accT);
+              }
+              __syncwarp();
+              if (lane == 0) mbar_arrive(empty + s);
+#pragma unroll
+              for (int cb = 0; cb < 4; ++cb) rmw1(j, cb, accT[cb]);
+            } else {
+              if (h == 0) symv_unit_diag<0>(A, L, ti, ci, accN[0], accN[1], accT);
+              else symv_unit_diag<1>(A, L, ti, ci, accN[2], accN[3], accT);
+              __syncwarp();
+              if (lane == 0) mbar_arrive(empty + s);
+#pragma unroll
+              for (int cb = 0; cb < 3; ++cb) rmw1(i, cb, accT[cb]);
+            }
+          }
+        if (mine) {  // rows of tile row i accumulated over this warp's units of the band
+#pragma unroll
+          for (int b = 0; b < 4; ++b) {
+            rmw1(i, b, accN[b]);
+            accN[b][0] = accN[b][1] = 0.0;
+          }
+        }
+      }
+      consumers_sync(NC);
+      for (int idx = tid; idx < nb * 2; idx += NC) {
+        const int row = idx >> 1, rr = idx & 1;
+        if (rr < nr) {
+          double2 s = pt[idx];  // == ((panel * 32 + row % 32) << 1) + rr
+#pragma unroll
+          for (int ww = 1; ww < SYMV_WARPS; ++ww) s = cadd(s, pt[(long)ww * ntm * 64 + idx]);
+          const long rb = rr ? rb1 : rb0;
+          Y[(long)row * s_row + (rb & ROFF)] = cflip(s, flip_row((int)(rb >> 56), row, q));
+        }
+      }
+    }
+  }
+}
+
+template <int R>
+static int launch_symv_inv_t(const SymGeom& sg, const double2* G, const int* items, int nblocks, const int* klist,
+                             double2* Y, long s_row, long s_k, int q, cudaStream_t s) {
+  // ring slots: a multiple of the 4 consumer warps (each warp owns S / 4 of them)
+  static const int slots_env = env_int("VX_SYMV_SLOTS", 4);
+  static const int minb = env_int("VX_SYMV_MINB", 3);
+  const int S = slots_env < 4 ? 4 : (slots_env > 24 ? 24 : slots_env / SYMV_WARPS * SYMV_WARPS);
+  const int npad = (sg.dmax + 31) / 32 * 32;
+  const size_t smem = ((size_t)2 * S * 8 + 127) / 128 * 128 + (size_t)S * 512 * sizeof(double2) +
+                      (size_t)SYMV_WARPS * (npad / 32) * 64 * sizeof(double2) + (size_t)npad * 6 * sizeof(double);
+  auto kern = minb == 2 ? symv_inv_kernel<R, 2> : minb == 4 ? symv_inv_kernel<R, 4> : symv_inv_kernel<R, 3>;
+  VX_REQUIRE((int)smem + 1024 <= device_smem_optin(), "symmetric inverse apply smem %zu too large", smem);
+  VX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  kern<<<nblocks, (SYMV_WARPS + 1) * 32, smem, s>>>(sg, G, items, nblocks, klist, Y, s_row, s_k, S, q);
+  VX_CHECK_LAUNCH("symv_inv_kernel");
+  return VX_OK;
+}
+
+static int launch_symv_inv(const SymGeom& sg, const double2* G, const int* items, int nblocks, int direct_r,
+                           const int* klist, double2* Y, long s_row, long s_k, int q, cudaStream_t s) {
+  if (nblocks <= 0) return VX_OK;
+  VX_REQUIRE(direct_r == 1 || direct_r == 2, "symmetric inverse apply: direct_r must be 1 or 2");
+  return direct_r == 2 ? launch_symv_inv_t<2>(sg, G, items, nblocks, klist, Y, s_row, s_k, q, s)
+                       : launch_symv_inv_t<1>(sg, G, items, nblocks, klist, Y, s_row, s_k, q, s);
+}

@@ -33,3 +33,4 @@ for _ in range(napply):
 e1.record()
 torch.cuda.synchronize()
 print(f"{name}: {e0.elapsed_time(e1) / napply:.3f} ms/apply, prec bytes {prec.bytes / 1e9:.3f} GB")
+print("layout", getattr(prec, "factor_layout", None), "syminv_err", getattr(prec, "_syminv_err", None))
