@@ -292,7 +292,7 @@ __device__ __forceinline__ void symv_unit_diag(const double* __restrict__ A, con
 template <int R, int MINB>
 __global__ void __launch_bounds__((SYMV_WARPS + 1) * 32, MINB)
     symv_inv_kernel(SymGeom sg, const double2* __restrict__ G, const int* __restrict__ items, int nwork,
-                    const int* __restrict__ klist, double2* Y, long s_row, long s_k, int S, int q) {
+                    const int* __restrict__ klist, double2* Y, long s_row, long s_k, int S, int q, int pfwin) {
   extern __shared__ __align__(128) unsigned char smraw[];
   constexpr int NC = SYMV_WARPS * 32;
   constexpr int U2 = 512;  // entries per ring slot (8 KB)
@@ -321,7 +321,20 @@ __global__ void __launch_bounds__((SYMV_WARPS + 1) * 32, MINB)
         int nb, sec;
         const double2* Gb = sym_block(sg, G, slot, nb, sec);
         const int nt = (nb + 31) / 32;
+        // the block's storage is one contiguous stream in unit order: request it from
+        // HBM into L2 a window ahead of the ring (each warp owns few slots, so the
+        // ring's own loads should only see L2 latency)
+        const long total = sym_size(nb);
         for (int ch = 0; ch < (cnt + R - 1) / R; ++ch) {
+          long pf = 0;
+          auto prefetch_to = [&](long upto) {
+            upto = upto < total ? upto : total;
+            while (pf < upto) {
+              const long m = upto - pf < 1024 ? upto - pf : 1024;
+              bulk_prefetch_l2(Gb + pf, (uint32_t)(m * sizeof(double2)));
+              pf += m;
+            }
+          };
           for (int i = 0; i < nt; ++i) {
             const int ti = min(32, nb - 32 * i), nh = ti > 16 ? 2 : 1;
             const double2* band = Gb + sym_band(i);
@@ -337,6 +350,7 @@ __global__ void __launch_bounds__((SYMV_WARPS + 1) * 32, MINB)
                   src = band + 32L * ti * i + trap_off(16 * h);
                   elems = (uint32_t)(trap_off(16 * h + rows) - trap_off(16 * h));
                 }
+                if (pfwin > 0) prefetch_to((src - Gb) + elems + pfwin);
                 const uint32_t k = n / SYMV_WARPS;
                 const int s = (int)(n % SYMV_WARPS) + SYMV_WARPS * (int)(k % D);
                 const uint32_t use = k / D;
@@ -468,6 +482,7 @@ static int launch_symv_inv_t(const SymGeom& sg, const double2* G, const int* ite
   // ring slots: a multiple of the 4 consumer warps (each warp owns S / 4 of them)
   static const int slots_env = env_int("VX_SYMV_SLOTS", 4);
   static const int minb = env_int("VX_SYMV_MINB", 3);
+  static const int pfwin = env_int("VX_SYMV_PF", 24) * 64;  // L2 prefetch window, entries
   const int S = slots_env < 4 ? 4 : (slots_env > 24 ? 24 : slots_env / SYMV_WARPS * SYMV_WARPS);
   const int npad = (sg.dmax + 31) / 32 * 32;
   const size_t smem = ((size_t)2 * S * 8 + 127) / 128 * 128 + (size_t)S * 512 * sizeof(double2) +
@@ -475,7 +490,7 @@ static int launch_symv_inv_t(const SymGeom& sg, const double2* G, const int* ite
   auto kern = minb == 2 ? symv_inv_kernel<R, 2> : minb == 4 ? symv_inv_kernel<R, 4> : symv_inv_kernel<R, 3>;
   VX_REQUIRE((int)smem + 1024 <= device_smem_optin(), "symmetric inverse apply smem %zu too large", smem);
   VX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  kern<<<nblocks, (SYMV_WARPS + 1) * 32, smem, s>>>(sg, G, items, nblocks, klist, Y, s_row, s_k, S, q);
+  kern<<<nblocks, (SYMV_WARPS + 1) * 32, smem, s>>>(sg, G, items, nblocks, klist, Y, s_row, s_k, S, q, pfwin);
   VX_CHECK_LAUNCH("symv_inv_kernel");
   return VX_OK;
 }

@@ -214,3 +214,46 @@ def test_symmetric_reduced_and_solve(rng, C, monkeypatch):
     x1, r1 = gmres(A, W.b, apply_pinv=p.apply, tol=1e-10, maxit=300)
     x2, r2 = gmres(A, W.b, apply_pinv=q.apply, tol=1e-10, maxit=300)
     assert r1.iterations == r2.iterations and relerr(x1, x2) < 1e-9
+
+
+@pytest.mark.parametrize("dims", [(50, 22, 11), (40, 12, 4), (30, 16, 9), (33, 14, 12)])
+def test_symmetric_inverse_equals_factors(rng, C, monkeypatch, dims):
+    """The one-pass symmetric-inverse apply (G = A^^-1, x = G (b / W), csrc/lu_syminv.cuh)
+    equals the two triangular sweeps on the symmetric factors (VX_SYMINV=0) and the
+    pivoted LU (VX_SYM=0); it is bitwise reproducible; several right-hand sides still
+    go through the factors; block sizes with full and ragged last tile rows
+    (sector dims 176..187, 36, 108, 126)."""
+    W = _wl(dims)
+    kern, mt = W.kernel(), W.mtilde()
+    p = C.build_one_level(kern, mt)
+    monkeypatch.setenv("VX_SYMINV", "0")
+    f = C.build_one_level(kern, mt)
+    monkeypatch.delenv("VX_SYMINV")
+    monkeypatch.setenv("VX_SYM", "0")
+    q = C.build_one_level(kern, mt)
+    monkeypatch.delenv("VX_SYM")
+    assert (p.factor_layout, f.factor_layout, q.factor_layout) == ("symmetric-inverse", "symmetric", "ragged")
+    assert p._syminv_err < 1e-12
+    n = W.grid.n_unknowns
+    x = random_field(rng, n)
+    y = p.apply(x)
+    assert np.array_equal(y, p.apply(x))
+    assert relerr(y, f.apply(x)) < 1e-12
+    assert relerr(y, q.apply(x)) < 1e-12
+    x3 = random_field(rng, n, 3)
+    assert relerr(p.apply(x3), q.apply(x3)) < 1e-12
+    if n <= 3 * 40 * 12 * 4:
+        ref = O.build_one_level(kern.tensors, W.grid.dims, mt)
+        assert relerr(y, O.apply_prec(ref, x)) < 1e-10
+
+
+def test_symmetric_inverse_rejected_when_inaccurate(rng, C, monkeypatch):
+    """The inverses are kept only if one apply agrees with the triangular solves:
+    with an impossible tolerance the factors stay in use."""
+    W = _wl((40, 12, 4))
+    monkeypatch.setattr(C, "SYMINV_TOL", 0.0)
+    p = C.build_one_level(W.kernel(), W.mtilde())
+    assert p.factor_layout == "symmetric" and p._sym.inv is None
+    ref = O.build_one_level(W.kernel().tensors, W.grid.dims, W.mtilde())
+    x = random_field(rng, W.grid.n_unknowns)
+    assert relerr(p.apply(x), O.apply_prec(ref, x)) < 1e-10
