@@ -551,14 +551,24 @@ def run_ours(args):
             nvec = 3 * (x1 - x0) * (y1 - y0) * (z1 - z0)
     sol_ms, sol_n = spans["prec_solve"]
     solve_bytes = 16 * sum(n * n * c for n, c in stored) + 2 * 16 * nvec
-    fb = None if sharded or W.prec["kind"] == "blocked" else getattr(prec, "factor_bytes_per_apply", None)
-    if fb is not None:   # symmetric layout: the stored lower triangles, read once per apply
-        solve_bytes = fb + 2 * 16 * nvec
+    # compulsory factor bytes: per launch (one box of the blocked scheme) and per iteration (all boxes)
+    fb = fb_launch = None
+    layout = getattr(prec, "factor_layout", None)
+    if not sharded:
+        if W.prec["kind"] == "blocked":
+            per_box = [getattr(q, "factor_bytes_per_apply", None) for q in prec.box_precs]
+            if all(v is not None for v in per_box):
+                fb, fb_launch = sum(per_box), per_box[0]
+            layout = getattr(prec.box_precs[0], "factor_layout", None)
+        else:
+            fb = fb_launch = getattr(prec, "factor_bytes_per_apply", None)
+    if fb_launch is not None:   # symmetric layouts: the stored lower triangles, read once per apply
+        solve_bytes = fb_launch + 2 * 16 * nvec
     roof = None
     if sol_n:
         avg = sol_ms / sol_n / 1e3
         ach = solve_bytes / avg / 1e9
-        kname, traffic = solve_kernel_traffic(name, W, world, getattr(prec, "factor_layout", None))
+        kname, traffic = solve_kernel_traffic(name, W, world, layout)
         roof = {"kernel": kname + " (prec_solve span)", "bound": "hbm", "achieved": ach,
                 "peak": peak, "unit": "GB/s", "frac": ach / peak, "peak_source": peak_kind,
                 "traffic": traffic, "bytes_per_launch": solve_bytes, "avg_launch_ms": avg * 1e3,

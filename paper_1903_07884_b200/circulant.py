@@ -181,17 +181,18 @@ def _lu1_sec(lam, m_yz_dev, kset_dev, nk, nx, ny, nz, sec, nopiv=False):
 # Green's tensor is even under d -> -d), so an unpivoted factorisation D = L U
 # has U = diag(u) W L^T W^-1 with W = S M restricted to the (sector) rows, and
 # only L is stored -- half the bytes every apply streams.  Used when m~ has no
-# zero entry and the blocks fit the register-resident solve (<= 256 rows); the
-# pack kernel verifies the relation per block, else the pivoted LU is kept.
+# zero entry (sector blocks of up to SYM_MAX_DIM rows); the pack kernel verifies
+# the relation per block, else the pivoted LU is kept.
 SYM_TOL = 1e-11        # max |U - diag(u) W L^T W^-1| / max |U| per block
 SYM_MIN_PIVOT = 1e-8   # min |u| / max |u| per block
+SYM_MAX_DIM = int(os.environ.get("VX_SYM_MAX_DIM", "1024"))   # csrc/lu_sym.cuh SYM_MAX_DIM
 
 
 def _sym_eligible(m_yz: np.ndarray, dmax: int) -> bool:
     if os.environ.get("VX_SYM", "1") == "0":
         return False
     a = np.abs(np.asarray(m_yz))
-    return 32 < dmax <= 256 and bool(np.all(np.isfinite(a))) and bool(a.min() > 0.0)
+    return 32 < dmax <= SYM_MAX_DIM and bool(np.all(np.isfinite(a))) and bool(a.min() > 0.0)
 
 
 def _sym_weights(plan, m_yz: np.ndarray) -> np.ndarray:

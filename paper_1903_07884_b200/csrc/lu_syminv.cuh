@@ -476,9 +476,254 @@ __global__ void __launch_bounds__((SYMV_WARPS + 1) * 32, MINB)
   }
 }
 
+// ------------------------------------------------------------------ apply, output-owned variant
+// Same stream, different split of the work: every tile (16 KB) is consumed by
+// all four warps; warp w OWNS entries 8w .. 8w+7 of every tile row of the
+// result, i.e. it computes rows 8w.. of (tile x c_j) and columns 8w.. of
+// (tile^T x c_i).  The result vector therefore exists once (no per-warp partial
+// vectors, no final reduction), the ring is a plain in-order ring shared by the
+// warps (1 tile in use + S - 1 in flight per CTA), and the c_i fragments of the
+// transposed products stay in registers for a whole tile row.
+struct Symv2Stage {
+  double an[2], bn[2], at[2];
+};
+
+template <int R, int MINB>
+__global__ void __launch_bounds__((SYMV_WARPS + 1) * 32, MINB)
+    symv2_inv_kernel(SymGeom sg, const double2* __restrict__ G, const int* __restrict__ items, int nwork,
+                     const int* __restrict__ klist, double2* Y, long s_row, long s_k, int S, int q, int pfwin) {
+  extern __shared__ __align__(128) unsigned char smraw[];
+  constexpr int NC = SYMV_WARPS * 32;
+  constexpr int T2 = 1024;  // entries per ring slot (16 KB)
+  const int npad = (sg.dmax + 31) / 32 * 32;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smraw);
+  uint64_t* empty = full + S;
+  double2* slots = reinterpret_cast<double2*>(smraw + (2 * S * 8 + 127) / 128 * 128);
+  double2* out = slots + (long)S * T2;                       // [npad][2]: the result
+  double* c3 = reinterpret_cast<double*>(out + 2L * npad);   // [npad][2][3]: c = b / W, signed
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(full + s, 1);
+      mbar_init(empty + s, SYMV_WARPS);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp == SYMV_WARPS) {
+    if (lane == 0) {
+      uint32_t n = 0;  // tiles emitted (all work items)
+      for (int w = blockIdx.x; w < nwork; w += gridDim.x) {
+        const int slot = items[3 * w], cnt = items[3 * w + 2];
+        int nb, sec;
+        const double2* Gb = sym_block(sg, G, slot, nb, sec);
+        const int nt = (nb + 31) / 32;
+        const long total = sym_size(nb);
+        for (int ch = 0; ch < (cnt + R - 1) / R; ++ch) {
+          long pf = 0;
+          auto prefetch_to = [&](long upto) {
+            upto = upto < total ? upto : total;
+            while (pf < upto) {
+              const long m = upto - pf < 1024 ? upto - pf : 1024;
+              bulk_prefetch_l2(Gb + pf, (uint32_t)(m * sizeof(double2)));
+              pf += m;
+            }
+          };
+          for (int i = 0; i < nt; ++i) {
+            const int ti = min(32, nb - 32 * i);
+            const double2* band = Gb + sym_band(i);
+            for (int j = 0; j <= i; ++j, ++n) {
+              const double2* src = band + 32L * ti * j;
+              const uint32_t elems = (uint32_t)(j < i ? ti * 32 : trap_size(ti));
+              if (pfwin > 0) prefetch_to((src - Gb) + elems + pfwin);
+              const int s = n % S;
+              const uint32_t use = n / S;
+              if (use > 0) mbar_wait_hint(empty + s, (use - 1) & 1u);
+              mbar_expect_tx(full + s, elems * (uint32_t)sizeof(double2));
+              bulk_g2s(slots + s * T2, src, elems * (uint32_t)sizeof(double2), full + s);
+            }
+          }
+        }
+      }
+    }
+    return;
+  }
+
+  const SymvLane L = symv_lane(lane);
+  const int g = L.g, t = L.t;
+  // this warp's fragment bases inside a tile: product rows 8w + g; transposed columns 8w + g
+  const int nbw[4] = {L.nb[0] + 512 * warp, L.nb[1] + 512 * warp, L.nb[2] + 512 * warp, L.nb[3] + 512 * warp};
+  const int tbw[2] = {L.tb[0] + 16 * warp, L.tb[1] + 16 * warp};
+  // C fragment owner: lanes t < 2 hold (entry 8w + g, right-hand side t)
+  auto add_out = [&](int panel, double c0, double c1) {
+    if (t < 2) {
+      double2* p = out + (((panel * 32 + 8 * warp + g) << 1) + t);
+      const double2 o = *p;
+      *p = cmk(o.x + c0, o.y + c1);
+    }
+  };
+  uint32_t n = 0;
+  for (int w = blockIdx.x; w < nwork; w += gridDim.x) {
+    const int slot = items[3 * w], beg = items[3 * w + 1], cnt = items[3 * w + 2];
+    int nb, sec;
+    (void)sym_block(sg, G, slot, nb, sec);
+    const int nt = (nb + 31) / 32;
+    const double2* wrow = sg.w + (long)sec * sg.dmax;
+    for (int ch = 0; ch < (cnt + R - 1) / R; ++ch) {
+      const int rho0 = ch * R;
+      const int nr = min(R, cnt - rho0);
+      long rb0 = 0, rb1 = 0;
+      {
+        const int k0 = klist ? klist[beg + rho0] : beg + rho0;
+        rb0 = rhs_base(k0, rho0, 1, s_k);
+        if (nr > 1) {
+          const int k1 = klist ? klist[beg + rho0 + 1] : beg + rho0 + 1;
+          rb1 = rhs_base(k1, rho0 + 1, 1, s_k);
+        }
+      }
+      consumers_sync(NC);  // the previous item's result has been written out
+      for (int idx = tid; idx < npad * 2; idx += NC) {
+        const int row = idx >> 1, rr = idx & 1;
+        double2 v = cmk(0.0, 0.0);
+        if (row < nb && rr < nr) {
+          const long rb = rr ? rb1 : rb0;
+          v = cdiv(cflip(Y[(long)row * s_row + (rb & ROFF)], flip_row((int)(rb >> 56), row, q)), wrow[row]);
+        }
+        double* o = c3 + 3 * idx;
+        o[0] = v.y;
+        o[1] = v.x;
+        o[2] = -v.y;
+        out[idx] = cmk(0.0, 0.0);
+      }
+      consumers_sync(NC);
+      for (int i = 0; i < nt; ++i) {
+        const int ti = min(32, nb - 32 * i);
+        const double* ci = c3 + 192 * i + L.cb;
+        double bi[16];  // c_i fragments: operands of every transposed product of this tile row
+#pragma unroll
+        for (int k = 0; k < 16; ++k) bi[k] = ci[12 * k];
+        double aN[4][2];
+#pragma unroll
+        for (int b = 0; b < 4; ++b) aN[b][0] = aN[b][1] = 0.0;
+        for (int j = 0; j < i; ++j, ++n) {
+          const int s = n % S;
+          mbar_wait_hint(full + s, (n / S) & 1u);
+          const double* A = reinterpret_cast<const double*>(slots + s * T2);
+          const double* cj = c3 + 192 * j + L.cb;
+          double aT[4][2];
+#pragma unroll
+          for (int b = 0; b < 4; ++b) aT[b][0] = aT[b][1] = 0.0;
+          if (ti == 32) {
+            // 8 stages of (2 product + 2 transposed) tensor-core products, fragment loads one stage ahead
+            Symv2Stage f0, f1;
+            auto load = [&](Symv2Stage& f, int st) {
+#pragma unroll
+              for (int u = 0; u < 2; ++u) {
+                const int kc = 2 * st + u;
+                f.bn[u] = cj[12 * kc];
+                f.an[u] = A[nbw[kc & 3] + 16 * (kc >> 2)];
+                f.at[u] = A[tbw[kc & 1] + 128 * kc];
+              }
+            };
+            load(f0, 0);
+#pragma unroll
+            for (int st = 0; st < 8; st += 2) {
+              load(f1, st + 1);
+              dmma_884(aN[0][0], aN[0][1], f0.an[0], f0.bn[0]);
+              dmma_884(aT[0][0], aT[0][1], f0.at[0], bi[2 * st]);
+              dmma_884(aN[1][0], aN[1][1], f0.an[1], f0.bn[1]);
+              dmma_884(aT[1][0], aT[1][1], f0.at[1], bi[2 * st + 1]);
+              if (st + 2 < 8) load(f0, st + 2);
+              dmma_884(aN[2][0], aN[2][1], f1.an[0], f1.bn[0]);
+              dmma_884(aT[2][0], aT[2][1], f1.at[0], bi[2 * st + 2]);
+              dmma_884(aN[3][0], aN[3][1], f1.an[1], f1.bn[1]);
+              dmma_884(aT[3][0], aT[3][1], f1.at[1], bi[2 * st + 3]);
+            }
+          } else {
+            // last tile row of the block: ti < 32 rows
+            if (8 * warp < ti) {
+#pragma unroll 4
+              for (int kc = 0; kc < 16; ++kc)
+                dmma_884(aN[kc & 3][0], aN[kc & 3][1], A[nbw[kc & 3] + 16 * (kc >> 2)], cj[12 * kc]);
+            }
+#pragma unroll
+            for (int kc = 0; kc < 16; ++kc)
+              if (2 * kc < ti) {
+                const bool ok = 2 * kc + (t >> 1) < ti;
+                const double a = ok ? A[tbw[kc & 1] + 128 * kc] : 0.0;
+                dmma_884(aT[kc & 3][0], aT[kc & 3][1], a, bi[kc]);
+              }
+          }
+          __syncwarp();
+          if (lane == 0) mbar_arrive(empty + s);
+          add_out(j, (aT[0][0] + aT[1][0]) + (aT[2][0] + aT[3][0]), (aT[0][1] + aT[1][1]) + (aT[2][1] + aT[3][1]));
+        }
+        {
+          // diagonal trapezoid: row block w times c_i (columns < 8w + 8) and column block w of
+          // the row blocks below it, transposed, times c_i -- both land on entries 8w + g of tile row i
+          const int s = n % S;
+          mbar_wait_hint(full + s, (n / S) & 1u);
+          const double* A = reinterpret_cast<const double*>(slots + s * T2);
+          if (8 * warp < ti) {
+            const double* Arow = A + 2 * (32 * warp * (warp + 1) + g * (8 * warp + 8)) - g * 64;
+#pragma unroll
+            for (int kc = 0; kc < 16; ++kc)
+              if (kc < 4 * warp + 4) dmma_884(aN[kc & 3][0], aN[kc & 3][1], Arow[L.nb[kc & 3] + 16 * (kc >> 2)], bi[kc]);
+#pragma unroll
+            for (int rb = 1; rb < 4; ++rb)
+              if (rb > warp && 8 * rb < ti) {
+                const double* Ab = A + 2 * (32 * rb * (rb + 1)) - (t >> 1) * 64;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                  const int r = 2 * k + (t >> 1);
+                  const bool ok = 8 * rb + r < ti;
+                  const double a = ok ? Ab[2 * r * (8 * rb + 8) + tbw[k & 1]] : 0.0;
+                  dmma_884(aN[k][0], aN[k][1], a, bi[4 * rb + k]);
+                }
+              }
+          }
+          __syncwarp();
+          if (lane == 0) mbar_arrive(empty + s);
+          ++n;
+        }
+        add_out(i, (aN[0][0] + aN[1][0]) + (aN[2][0] + aN[3][0]), (aN[0][1] + aN[1][1]) + (aN[2][1] + aN[3][1]));
+      }
+      consumers_sync(NC);
+      for (int idx = tid; idx < nb * 2; idx += NC) {
+        const int row = idx >> 1, rr = idx & 1;
+        if (rr < nr) {
+          const long rb = rr ? rb1 : rb0;
+          Y[(long)row * s_row + (rb & ROFF)] = cflip(out[idx], flip_row((int)(rb >> 56), row, q));
+        }
+      }
+    }
+  }
+}
+
+template <int R>
+static int launch_symv2_inv_t(const SymGeom& sg, const double2* G, const int* items, int nblocks, const int* klist,
+                              double2* Y, long s_row, long s_k, int q, cudaStream_t s) {
+  static const int slots_env = env_int("VX_SYMV2_SLOTS", 3);
+  static const int minb = env_int("VX_SYMV_MINB", 3);
+  static const int pfwin = env_int("VX_SYMV_PF", 24) * 64;  // L2 prefetch window, entries
+  const int S = slots_env < 2 ? 2 : (slots_env > 12 ? 12 : slots_env);
+  const int npad = (sg.dmax + 31) / 32 * 32;
+  const size_t smem = ((size_t)2 * S * 8 + 127) / 128 * 128 + (size_t)S * 1024 * sizeof(double2) +
+                      (size_t)npad * 2 * sizeof(double2) + (size_t)npad * 6 * sizeof(double);
+  auto kern = minb == 2 ? symv2_inv_kernel<R, 2> : minb == 4 ? symv2_inv_kernel<R, 4> : symv2_inv_kernel<R, 3>;
+  VX_REQUIRE((int)smem + 1024 <= device_smem_optin(), "symmetric inverse apply smem %zu too large", smem);
+  VX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  kern<<<nblocks, (SYMV_WARPS + 1) * 32, smem, s>>>(sg, G, items, nblocks, klist, Y, s_row, s_k, S, q, pfwin);
+  VX_CHECK_LAUNCH("symv2_inv_kernel");
+  return VX_OK;
+}
+
 template <int R>
 static int launch_symv_inv_t(const SymGeom& sg, const double2* G, const int* items, int nblocks, const int* klist,
                              double2* Y, long s_row, long s_k, int q, cudaStream_t s) {
+  static const int variant = env_int("VX_SYMV_VARIANT", 2);
+  if (variant == 2) return launch_symv2_inv_t<R>(sg, G, items, nblocks, klist, Y, s_row, s_k, q, s);
   // ring slots: a multiple of the 4 consumer warps (each warp owns S / 4 of them)
   static const int slots_env = env_int("VX_SYMV_SLOTS", 4);
   static const int minb = env_int("VX_SYMV_MINB", 3);

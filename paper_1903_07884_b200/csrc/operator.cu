@@ -345,19 +345,48 @@ __global__ void __launch_bounds__(256, (PZ <= 16 ? 3 : 2))
   const double2* S0 = sv.S + p0 * sstr + so0;
   const double2* S1 = sv.S + p1 * sstr + so0;
   const double2* S2 = sv.S + p2 * sstr + so0;
+  if (sv.compact) {
+    // compact spectra: S(PZ - kz) = +-S(kz) (sign by the z parity of the
+    // component), so kz and its mirror share ONE load of the three spectra --
+    // the loads, not the arithmetic, fill the L1 data pipe of this kernel
+    const bool z0 = odd_z(p0), z1 = odd_z(p1), z2 = odd_z(p2);
 #pragma unroll
-  for (int kz = 0; kz < PZ; ++kz) {
-    const bool mz = sv.compact && 2 * kz > PZ;
-    const long ko = (long)(mz ? PZ - kz : kz) * kstr;
-    double2 s0 = __ldg(S0 + ko), s1 = __ldg(S1 + ko), s2 = __ldg(S2 + ko);
-    if (n0 ^ (mz && odd_z(p0))) s0 = cmk(-s0.x, -s0.y);
-    if (n1 ^ (mz && odd_z(p1))) s1 = cmk(-s1.x, -s1.y);
-    if (n2 ^ (mz && odd_z(p2))) s2 = cmk(-s2.x, -s2.y);
-    const double2 x0 = shfl_c(v[kz], j), x1 = shfl_c(v[kz], ZS_COLS + j), x2 = shfl_c(v[kz], 2 * ZS_COLS + j);
-    double2 acc = cmul(s0, x0);
-    cfma(acc, s1, x1);
-    cfma(acc, s2, x2);
-    v[kz] = cscale(acc, scale);
+    for (int kz = 0; kz <= PZ / 2; ++kz) {
+      const long ko = (long)kz * kstr;
+      double2 s0 = __ldg(S0 + ko), s1 = __ldg(S1 + ko), s2 = __ldg(S2 + ko);
+      if (n0) s0 = cmk(-s0.x, -s0.y);
+      if (n1) s1 = cmk(-s1.x, -s1.y);
+      if (n2) s2 = cmk(-s2.x, -s2.y);
+      {
+        const double2 x0 = shfl_c(v[kz], j), x1 = shfl_c(v[kz], ZS_COLS + j), x2 = shfl_c(v[kz], 2 * ZS_COLS + j);
+        double2 acc = cmul(s0, x0);
+        cfma(acc, s1, x1);
+        cfma(acc, s2, x2);
+        v[kz] = cscale(acc, scale);
+      }
+      const int km = PZ - kz;
+      if (kz > 0 && km > kz && km < PZ) {
+        if (z0) s0 = cmk(-s0.x, -s0.y);
+        if (z1) s1 = cmk(-s1.x, -s1.y);
+        if (z2) s2 = cmk(-s2.x, -s2.y);
+        const double2 x0 = shfl_c(v[km], j), x1 = shfl_c(v[km], ZS_COLS + j), x2 = shfl_c(v[km], 2 * ZS_COLS + j);
+        double2 acc = cmul(s0, x0);
+        cfma(acc, s1, x1);
+        cfma(acc, s2, x2);
+        v[km] = cscale(acc, scale);
+      }
+    }
+  } else {
+#pragma unroll
+    for (int kz = 0; kz < PZ; ++kz) {
+      const long ko = (long)kz * kstr;
+      const double2 s0 = __ldg(S0 + ko), s1 = __ldg(S1 + ko), s2 = __ldg(S2 + ko);
+      const double2 x0 = shfl_c(v[kz], j), x1 = shfl_c(v[kz], ZS_COLS + j), x2 = shfl_c(v[kz], 2 * ZS_COLS + j);
+      double2 acc = cmul(s0, x0);
+      cfma(acc, s1, x1);
+      cfma(acc, s2, x2);
+      v[kz] = cscale(acc, scale);
+    }
   }
   reg_fft<PZ, true>(v);
   if (active) {
