@@ -77,6 +77,9 @@ def chan_along_axis(gen: np.ndarray, axis: int) -> np.ndarray:
 
 def _constant_along(m: np.ndarray, axis: int, what: str) -> None:
     lead = np.take(m, [0], axis=axis)
+    # exactly constant (what homogenize() returns): one comparison pass, no temporaries of m's size
+    if np.array_equal(m, np.broadcast_to(lead, m.shape)):
+        return
     # == np.allclose(m, lead, rtol=0, atol) (a NaN fails both), one pass cheaper
     if not np.abs(m - lead).max() <= 1e-12 * max(1.0, np.abs(m).max()):
         raise ValueError(f"homogenized coefficient must be constant along {what}")
@@ -696,19 +699,17 @@ class _OneLevelBase:
 def _mirror_store(ks: np.ndarray, nx: int, share: bool):
     """Storage plan for the logical blocks ks (sorted frequencies): the blocks
     to factorise (kset), and per block its storage slot and x-flip."""
-    pos = {int(k): i for i, k in enumerate(ks)}
+    ks = np.asarray(ks, np.int64)
+    km = (nx - ks) % nx
+    # position of each block's mirror frequency in ks (ks is sorted), if present
+    pos = np.searchsorted(ks, km)
+    pos_c = np.minimum(pos, ks.size - 1)
+    flip = (km < ks) & (ks[pos_c] == km) if share else np.zeros(ks.size, bool)
+    own = ~flip
     store = np.empty(ks.size, np.int64)
-    flip = np.zeros(ks.size, bool)
-    kset = []
-    for i, k in enumerate(ks):
-        km = (nx - int(k)) % nx
-        if share and km < k and km in pos:
-            store[i] = store[pos[km]]
-            flip[i] = True
-        else:
-            store[i] = len(kset)
-            kset.append(int(k))
-    return np.asarray(kset, np.int64), store, flip
+    store[own] = np.arange(int(own.sum()))
+    store[flip] = store[pos_c[flip]]      # the mirror has the smaller frequency: it owns its factor
+    return ks[own].copy(), store, flip
 
 
 class OneLevelPrec(_OneLevelBase):

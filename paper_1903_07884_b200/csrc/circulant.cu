@@ -739,6 +739,88 @@ __global__ void __launch_bounds__(LU_THREADS) lub_panel_kernel(LuGeom g, double2
   }
 }
 
+// panel step WITHOUT row interchanges (symmetric factors, lu_sym.cuh): the
+// diagonal tile is factorised in shared memory (one barrier per column instead
+// of three plus a global-memory rank-1 sweep of the whole panel), and the tiles
+// below it become L(it, kt) = A(it, kt) inv(U_kk) -- tensor-core tile products
+// with no dependency between them.  T = 32 only (multi-tile blocks).
+__global__ void __launch_bounds__(LU_THREADS) lub_panel_nopiv_kernel(LuGeom g, double2* F, int kt, int* piv,
+                                                                     int* info) {
+  extern __shared__ double2 pnsm[];
+  double2* D = pnsm;             // diagonal tile (column-major, ld 33); later a staged A tile
+  double2* Ls = D + 32 * 33;     // inv(L_kk); later a second staged A tile
+  double2* Ub = Ls + 32 * 33;    // inv(U_kk), ld 32: also the B operand of the tile products
+  constexpr int T = 32, T2 = 1024, LD = 33;
+  const int nt = g.nt, n = g.n;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int slot = blockIdx.x;
+  double2* A = F + (long)slot * g.blk;
+  double2* Dg = A + (long)(kt * nt + kt) * T2;
+  const int c0 = kt * T;
+  for (int i = tid; i < T2; i += LU_THREADS) D[(i >> 5) * LD + (i & 31)] = Dg[i];
+  if (tid < T && c0 + tid < n) piv[(long)slot * n + c0 + tid] = c0 + tid;
+  __syncthreads();
+  for (int jj = 0; jj < T; ++jj) {
+    const double2 d = D[jj * LD + jj];
+    const bool bad = (d.x == 0.0 && d.y == 0.0) || !isfinite(d.x) || !isfinite(d.y);
+    if (bad && tid == 0 && c0 + jj < n && info[slot] == 0) info[slot] = c0 + jj + 1;
+    const double2 dinv = bad ? cmk(0.0, 0.0) : cinv(d);
+    const int r = lane;
+    double2 l = cmk(0.0, 0.0);
+    if (r > jj) {
+      l = D[jj * LD + r];
+      if (!bad) {
+        l = cmul(l, dinv);
+        for (int c = jj + 1 + warp; c < T; c += LU_WARPS) cfms(D[c * LD + r], l, D[c * LD + jj]);
+      }
+    }
+    __syncthreads();
+    if (warp == 0 && r > jj) D[jj * LD + r] = l;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    const int c = lane;
+    for (int r = 0; r < T; ++r) {
+      double2 x = cmk(r == c ? 1.0 : 0.0, 0.0);
+      if (r > c) {
+        for (int i = c; i < r; ++i) cfms(x, D[i * LD + r], Ls[c * LD + i]);
+      } else if (r < c) {
+        x = cmk(0.0, 0.0);
+      }
+      Ls[c * LD + r] = x;
+    }
+  } else if (warp == 1) {
+    const int c = lane;
+    for (int r = T - 1; r >= 0; --r) {
+      double2 x = cmk(0.0, 0.0);
+      if (r <= c) {
+        x = cmk(r == c ? 1.0 : 0.0, 0.0);
+        for (int i = r + 1; i <= c; ++i) cfms(x, D[i * LD + r], Ub[c * 32 + i]);
+        x = cdiv(x, D[r * LD + r]);
+      }
+      Ub[c * 32 + r] = x;
+    }
+  }
+  __syncthreads();
+  for (int i = tid; i < T2; i += LU_THREADS) {
+    const int c = i >> 5, r = i & 31;
+    Dg[i] = (r > c) ? Ls[c * LD + r] : Ub[i];
+  }
+  // L(it, kt) = A(it, kt) inv(U_kk): two tiles at a time (a warp pair per tile, 16 columns each)
+  for (int it0 = kt + 1; it0 < nt; it0 += 2) {
+    __syncthreads();  // D / Ls free (inverses written out; previous products done)
+    for (int q2 = 0; q2 < 2; ++q2) {
+      if (it0 + q2 >= nt) break;
+      const double2* src = A + (long)((it0 + q2) * nt + kt) * T2;
+      double2* dst = q2 ? Ls : D;
+      for (int i = tid; i < T2; i += LU_THREADS) dst[(i >> 5) * LD + (i & 31)] = src[i];
+    }
+    __syncthreads();
+    const int it = it0 + (warp >> 1);
+    if (it < nt) tile_mma_half<false>((warp >> 1) ? Ls : D, Ub, A + (long)(it * nt + kt) * T2, warp & 1, lane);
+  }
+}
+
 // the step's row interchanges on every column outside the panel (zlaswp)
 __global__ void __launch_bounds__(256) lub_swap_kernel(LuGeom g, double2* F, int kt, const int* piv) {
   __shared__ int pv[32];
@@ -869,9 +951,14 @@ static int lu_build_batched(const Unfold& u, const LuGeom& g, int nslots, double
     VX_CHECK_LAUNCH("lub_unfold_kernel");
   }
   for (int kt = 0; kt < g.nt; ++kt) {
-    lub_panel_kernel<<<nslots, LU_THREADS, 0, s>>>(g, F, kt, piv, info, nopiv);
+    const bool fast = nopiv && g.T == 32 && env_int("VX_PANEL_FAST", 1);
+    constexpr int pn_smem = (2 * 32 * 33 + 32 * 32) * (int)sizeof(double2);
+    if (fast && kt == 0)
+      VX_CUDA(cudaFuncSetAttribute(lub_panel_nopiv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, pn_smem));
+    if (fast) lub_panel_nopiv_kernel<<<nslots, LU_THREADS, pn_smem, s>>>(g, F, kt, piv, info);
+    else lub_panel_kernel<<<nslots, LU_THREADS, 0, s>>>(g, F, kt, piv, info, nopiv);
     VX_CHECK_LAUNCH("lub_panel_kernel");
-    if (g.nt > 1) {
+    if (g.nt > 1 && !fast) {
       dim3 sg(div_up(g.npad, 256), nslots);
       lub_swap_kernel<<<sg, 256, 0, s>>>(g, F, kt, piv);
       VX_CHECK_LAUNCH("lub_swap_kernel");
