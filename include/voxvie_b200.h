@@ -386,7 +386,13 @@ int vx_prec1_apply_sym(int nx, int ny, int nz, const vx_c128* factors, const vx_
  * (reference circulant.py:183-186).
  * vx_lu_sym_invert: G of every block from the symmetric factors (layout and
  *   stride of vx_lu_sym_pack; scratch: same size, receives L^-1).
- * vx_prec1_apply_syminv: vx_prec1_apply_sym on G. */
+ * vx_prec1_apply_syminv: vx_prec1_apply_sym on G.
+ * vx_prec1_solve_syminv: vx_prec1_solve_sec_rag on G (the sharded
+ *   preconditioner's received frequency columns, dist.py). */
+int vx_prec1_solve_syminv(int ny, int nz, long pitch, const vx_c128* ginv, const vx_c128* w, const int* items,
+                          int n_single, int direct_r, const int* klist, int nsec, int dmax, const int* sec_dims,
+                          int norb, const int* orows, const int* osec, const double* ocoef,
+                          const unsigned char* flipk, vx_c128* S, vx_c128* U, void* stream);
 int vx_lu_sym_invert(int nkslots, int nsec, int dmax, const int* sec_dims, const vx_c128* sym, const vx_c128* h,
                      const vx_c128* w, vx_c128* scratch, vx_c128* ginv, void* stream);
 int vx_prec1_apply_syminv(int nx, int ny, int nz, const vx_c128* ginv, const vx_c128* w, const int* items,

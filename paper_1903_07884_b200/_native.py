@@ -107,6 +107,8 @@ _SIGS = {
     "vx_lu_sym_invert": (c_int, [c_int, c_int, c_int, P, P, P, P, P, P, P]),
     "vx_prec1_apply_syminv": (c_int, [c_int] * 3 + [P, P, P, c_int, c_int, P, c_int, c_int, P, c_int, P, P, P, P,
                                                      P, P, c_int, P, P, P, P]),
+    "vx_prec1_solve_syminv": (c_int, [c_int, c_int, c_long, P, P, P, c_int, c_int, P, c_int, c_int, P, c_int, P, P,
+                                       P, P, P, P, P]),
     "vx_solve_classic": (c_int, []),
     "vx_lu_repack": (c_int, [c_int, c_int, c_int, P, P, P, P]),
     "vx_lu_unpack": (c_int, [c_int, c_int, c_int, P, P, P, P]),

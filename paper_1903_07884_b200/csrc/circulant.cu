@@ -2854,6 +2854,35 @@ extern "C" int vx_prec1_solve_sec_rag(int ny, int nz, long pitch, const vx_c128*
   return sec_xform(pitch, 1, norb, orows, osec, ocoef, flipk, q, Ud, Sd, 1, s);
 }
 
+// vx_prec1_solve_syminv: the same solve-only path on the symmetric inverses
+// (vx_lu_sym_invert): orbit transform -> x = G (b / W) per sector block -> back.
+extern "C" int vx_prec1_solve_syminv(int ny, int nz, long pitch, const vx_c128* ginv, const vx_c128* w,
+                                     const int* items, int n_single, int direct_r, const int* klist, int nsec,
+                                     int dmax, const int* sec_dims, int norb, const int* orows, const int* osec,
+                                     const double* ocoef, const unsigned char* flipk, vx_c128* S, vx_c128* U,
+                                     void* stream) {
+  SymGeom sg;
+  int st = make_sym(nsec, sec_dims, dmax, nullptr, w, &sg);
+  if (st) return st;
+  sg.inverse = 1;
+  VX_REQUIRE(ny >= 1 && nz >= 1 && pitch >= 1 && n_single >= 0, "bad sector solve arguments");
+  VX_REQUIRE(direct_r == 1 || direct_r == 2, "direct_r must be 1 or 2");
+  VX_REQUIRE((long)nsec * dmax * pitch < (1L << 29), "sector layout too large for the work-list encoding");
+  cudaStream_t s = as_stream(stream);
+  Span span("prec_apply", s);
+  const int q = ny * nz;
+  double2* Sd = reinterpret_cast<double2*>(S);
+  double2* Ud = reinterpret_cast<double2*>(U);
+  if ((st = sec_xform(pitch, 1, norb, orows, osec, ocoef, flipk, q, Sd, Ud, 0, s))) return st;
+  {
+    Span sp("prec_solve", s);
+    if ((st = launch_symv_inv(sg, reinterpret_cast<const double2*>(ginv), items, n_single, direct_r, klist, Ud, pitch,
+                              1, q, s)))
+      return st;
+  }
+  return sec_xform(pitch, 1, norb, orows, osec, ocoef, flipk, q, Ud, Sd, 1, s);
+}
+
 extern "C" long vx_lu_rag_stride(int nsec, const int* sec_dims) {
   long k = 0;
   for (int s = 0; s < nsec; ++s) k += (long)sec_dims[s] * sec_dims[s];

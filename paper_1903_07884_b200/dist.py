@@ -348,7 +348,8 @@ class DistOneLevelPrec:
         stores them ragged, and the apply runs the orbit transform + ragged
         sector solves on the received columns (vx_prec1_solve_sec_rag).  False
         when the kernel / m~ lack the symmetries (dense path)."""
-        from .circulant import _SectorDev, _first_bad, _lamhat_x, _lu1_sec, _mirror_store, mirror_axes, sector_axes
+        from .circulant import (SYMINV_TOL, _SectorDev, _first_bad, _lamhat_x, _lu1_sec_auto, _mirror_store,
+                                mirror_axes, sector_axes)
         from .operator import upload_tensors
         from .sectors import sector_plan
 
@@ -374,7 +375,8 @@ class DistOneLevelPrec:
         kdev = t.from_numpy(kset.astype(np.int32)).cuda()
         m_dev = nv.device_c128(m_yz)
         lam = _lamhat_x(gen, nx, ny, nz)
-        fac, perm, piv, info = _lu1_sec(lam, m_dev, kdev, int(kset.size), nx, ny, nz, sec)
+        # unpivoted + symmetric when eligible (circulant._lu1_sec_auto), else zgetrf's pivoting
+        fac, perm, piv, info, sym = _lu1_sec_auto(lam, m_dev, kdev, int(kset.size), nx, ny, nz, sec, m_yz)
         del lam, piv
         bad = _first_bad(info)
         if bad >= 0:
@@ -407,7 +409,45 @@ class DistOneLevelPrec:
         off = np.cumsum([0] + [k.size for k in self.kown]).astype(np.int32)
         self.col_off = self.B.ints(off)
         self.colmap = self.B.ints(np.concatenate(self.kown).astype(np.int32))
+        # symmetric inverses of this rank's blocks (csrc/lu_syminv.cuh): kept when one solve on
+        # seeded random columns agrees with the ragged factors; then they are what the applies stream
+        self.sym = self.ginv = None
+        if sym is not None and self.n_items:
+            ginv = sym.build_inverse()
+            if ginv is not None:
+                gen_ = t.Generator(device="cuda")
+                gen_.manual_seed(20240811 + L.rank)
+                S0 = t.view_as_complex(t.randn(3 * ny * nz * nk, 2, dtype=t.float64, device="cuda", generator=gen_))
+                ref = S0.clone()
+                self._solve_sectors(ref, nk)
+                self.sym, self.ginv = sym, ginv
+                got = S0.clone()
+                self._solve_sectors(got, nk)
+                err = float(t.linalg.vector_norm(got - ref) / t.linalg.vector_norm(ref))
+                self.syminv_err = err
+                if err <= SYMINV_TOL:
+                    self.factors = None          # the ragged factors are not needed any more
+                    self.bytes_local = int(ginv.numel()) * 16
+                else:
+                    self.sym = self.ginv = None
         return True
+
+    def _solve_sectors(self, recv, nk):
+        """Sector block solves on the received frequency columns (in place)."""
+        L, B = self.L, self.B
+        sd, sp = self.sec, self.sec.plan
+        U = B.empty(max(1, sp.nsec * sp.dmax * nk))
+        if self.ginv is not None:
+            nv.call("vx_prec1_solve_syminv", L.dims[1], L.dims[2], nk, self.ginv.data_ptr(), self.sym.w.data_ptr(),
+                    self.items.data_ptr(), self.n_single, self.direct_r, self.klist.data_ptr(), sp.nsec, sp.dmax,
+                    self.sec_dims.ctypes.data, sd.norb, sd.orows.data_ptr(), sd.osec.data_ptr(),
+                    sd.ocoef.data_ptr(), self.flipk.data_ptr(), recv.data_ptr(), U.data_ptr(), nv.stream_ptr())
+            return
+        nv.call("vx_prec1_solve_sec_rag", L.dims[1], L.dims[2], nk, self.factors.data_ptr(),
+                self.perm.data_ptr(), self.items.data_ptr(), self.n_single, self.n_items, self.direct_r,
+                self.klist.data_ptr(), sp.nsec, sp.dmax, self.sec_dims.ctypes.data, sd.norb,
+                sd.orows.data_ptr(), sd.osec.data_ptr(), sd.ocoef.data_ptr(), self.flipk.data_ptr(),
+                recv.data_ptr(), U.data_ptr(), nv.stream_ptr())
 
     def apply(self, x_loc):
         L, B, C = self.L, self.B, self.C
@@ -422,13 +462,7 @@ class DistOneLevelPrec:
                      [L.nl * kown[s].size for s in range(L.P)])
         if self.sec is not None:
             if self.n_items:
-                sd, sp = self.sec, self.sec.plan
-                U = B.empty(max(1, sp.nsec * sp.dmax * nk))
-                nv.call("vx_prec1_solve_sec_rag", L.dims[1], L.dims[2], nk, self.factors.data_ptr(),
-                        self.perm.data_ptr(), self.items.data_ptr(), self.n_single, self.n_items, self.direct_r,
-                        self.klist.data_ptr(), sp.nsec, sp.dmax, self.sec_dims.ctypes.data, sd.norb,
-                        sd.orows.data_ptr(), sd.osec.data_ptr(), sd.ocoef.data_ptr(), self.flipk.data_ptr(),
-                        recv.data_ptr(), U.data_ptr(), nv.stream_ptr())
+                self._solve_sectors(recv, nk)
         elif self.n_items:
             B.solve(recv, self.n, self.factors, self.perm, self.items, self.n_single, self.n_items, self.klist, nk)
         back = B.empty(max(1, L.nl * nx))

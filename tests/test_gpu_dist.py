@@ -352,7 +352,7 @@ def test_sharded_sector_factors_loopback(P):
             bl = torch.from_numpy(L.local_slice(W.b).copy()).cuda()
             xs, rep = gmres_sharded(lambda v: op.apply(m, v), bl, B, C, apply_pinv=prec.apply, tol=1e-8,
                                     maxit=300, restart=15)
-            results[rank] = (y_pc, xs.cpu().numpy(), rep.iterations, prec.bytes_local)
+            results[rank] = (y_pc, xs.cpu().numpy(), rep.iterations, prec.bytes_local, prec.ginv is not None)
         except Exception as e:  # surface worker failures in the main thread
             errors.append(e)
             comm.bar.abort()
@@ -376,5 +376,8 @@ def test_sharded_sector_factors_loopback(P):
     assert relerr(xs, x1) < 1e-6
     # every rank holds a share of the symmetry-reduced factors
     assert all(r[3] > 0 for r in results)
-    # (ragged LU sector factors per rank; the single-GPU object may store the symmetric half)
+    # (symmetric inverses per rank when the blocks are eligible, else ragged LU sector factors)
     assert sum(r[3] for r in results) <= 1.5 * 16 * sum(d * d * c for d, c in p.stored_blocks)
+    if p.factor_layout == "symmetric-inverse":
+        assert all(r[4] for r in results), "ranks did not keep the symmetric inverses"
+        assert sum(r[3] for r in results) <= 1.5 * p.factor_bytes_per_apply
