@@ -295,6 +295,9 @@ int vx_h2d_threads(void);
 int vx_host_alloc(size_t bytes, void** out);
 int vx_host_free(void* p);
 int vx_d2h_pinned(void* dst, const void* src, size_t bytes, void* stream);
+/* vx_d2h_pinned without the final stream synchronisation (the caller overlaps
+ * the copy with work on another stream, e.g. gmres's true-residual matvec). */
+int vx_d2h_pinned_async(void* dst, const void* src, size_t bytes, void* stream);
 
 /* ---- ragged ("packed") factor storage for the 1-level block solves.
  * The build writes every block in the padded tile geometry of dmax (tiles of

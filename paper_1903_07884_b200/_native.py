@@ -124,6 +124,7 @@ _SIGS = {
     "vx_host_alloc": (c_int, [c_size_t, C.POINTER(C.c_void_p)]),
     "vx_host_free": (c_int, [P]),
     "vx_d2h_pinned": (c_int, [P, P, c_size_t, P]),
+    "vx_d2h_pinned_async": (c_int, [P, P, c_size_t, P]),
     "vx_solve_variant": (c_int, [c_int]),
     "vx_lu_variant": (c_int, [c_int]),
     "vx_timing_enable": (c_int, [c_int]),
@@ -336,6 +337,46 @@ def _pinned_release(ptr: int, nbytes: int):
             lst.append(ptr)
             return
     query("vx_host_free", ptr)
+
+
+_copy_stream = None
+
+
+class HostCopy:
+    """A device -> host copy of a large result in flight on a side stream
+    (to_host_begin); result() waits for it and returns the numpy array."""
+
+    def __init__(self, t):
+        global _copy_stream
+        th = torch()
+        self._arr = None
+        self._t = None
+        np_dtype = {th.complex128: np.complex128, th.float64: np.float64}.get(t.dtype)
+        if t.numel() * t.element_size() < (1 << 20) or not t.is_cuda or np_dtype is None:
+            self._t = t
+            return
+        t = t.contiguous()
+        nbytes = t.numel() * t.element_size()
+        if _copy_stream is None:
+            _copy_stream = th.cuda.Stream()
+        self._stream = _copy_stream
+        self._stream.wait_stream(th.cuda.current_stream())   # t is final on the caller's stream
+        self._keep = t
+        blk = _pinned_acquire(nbytes)
+        call("vx_d2h_pinned_async", blk.ptr, t.data_ptr(), nbytes, self._stream.cuda_stream)
+        self._arr = np.asarray(blk).view(np_dtype).reshape(tuple(t.shape))
+
+    def result(self):
+        if self._arr is None:
+            return to_host(self._t)
+        self._stream.synchronize()
+        self._keep = None
+        return self._arr
+
+
+def to_host_begin(t) -> HostCopy:
+    """Start copying a device tensor to the host without waiting for it."""
+    return HostCopy(t)
 
 
 def to_host(t):

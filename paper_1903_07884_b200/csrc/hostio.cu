@@ -177,3 +177,11 @@ extern "C" int vx_d2h_pinned(void* dst, const void* src, size_t bytes, void* str
   VX_CUDA(cudaStreamSynchronize(s));
   return VX_OK;
 }
+
+// the same copy without the final synchronisation: the caller overlaps it with
+// work on another stream and synchronises `stream` before reading dst
+extern "C" int vx_d2h_pinned_async(void* dst, const void* src, size_t bytes, void* stream) {
+  VX_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, static_cast<cudaStream_t>(stream)));
+  return VX_OK;
+}
+

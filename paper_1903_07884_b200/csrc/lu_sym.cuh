@@ -379,7 +379,7 @@ template <int R, int MINB>
 __global__ void __launch_bounds__((SYM_WARPS + 1) * 32, MINB)
     lu_solve_sym_kernel(SymGeom sg, const double2* __restrict__ F, const int* __restrict__ items, int nwork,
                         const int* __restrict__ klist, double2* Y, long s_row, long s_k, int S, int q, int l2hint,
-                        int pfwin, int dbg) {
+                        int pfwin) {
   extern __shared__ __align__(128) unsigned char smraw[];
   constexpr int T2 = 1024;
   const int npad = (sg.dmax + 31) / 32 * 32;
@@ -445,19 +445,16 @@ __global__ void __launch_bounds__((SYM_WARPS + 1) * 32, MINB)
         for (int ch = 0; ch < (cnt + R - 1) / R; ++ch) {
           fwd = true;
           pf = 0;
-          if (!(dbg & 2))
           for (int i = 0; i < nt; ++i) {
             for (int j = 0; j < i; ++j) tile(i, j);
             tile(i, i);
           }
           fwd = false;
-          if (!(dbg & 1)) {
           for (int i = nt - 1; i >= 0; --i) {
             for (int j = nt - 1; j > i; --j) tile(j, i);
             if (i + 1 < nt) tile(i + 1, i + 1);
           }
           tile(0, 0);
-          }
         }
       }
     }
@@ -625,9 +622,8 @@ __global__ void __launch_bounds__((SYM_WARPS + 1) * 32, MINB)
         }
         done_partials();
       };
-      if (!(dbg & 2))
       for (int i = 0; i < nt; ++i) {
-        const int ti = min(32, nb - 32 * i), nrb = (dbg & 4) ? 0 : (ti + 7) >> 3;
+        const int ti = min(32, nb - 32 * i), nrb = (ti + 7) >> 3;
         zero(acc);
         for (int j = 0; j + 1 < i; ++j) {
           fwd_tile(wait_tile(), nrb, 32 * j);
@@ -642,8 +638,7 @@ __global__ void __launch_bounds__((SYM_WARPS + 1) * 32, MINB)
         release_tile();
         put_partials(false);
       }
-      if (!(dbg & 2)) finish_fwd(nt - 1);
-      if (dbg & 1) continue;
+      finish_fwd(nt - 1);
       // ---------------- backward: t_i = c_i - sum_{j>i} L'_ji^T t_j with c = y / (u W);
       // z_{i+1} = inv(L_{i+1})^T t_{i+1} rides one step behind
       auto finish_bwd = [&](int p, double2 hv) {  // t_p slice <- c_p + partials; z_{p+1} -> global
@@ -671,11 +666,11 @@ __global__ void __launch_bounds__((SYM_WARPS + 1) * 32, MINB)
         double2 hv = cmk(0.0, 0.0);
         if (dep) hv = hval(i + 1);
         for (int j = nt - 1; j > i + 1; --j) {
-          bwd_tile(wait_tile(), (dbg & 4) ? 0 : min(32, nb - 32 * j), 32 * j);
+          bwd_tile(wait_tile(), min(32, nb - 32 * j), 32 * j);
           release_tile();
         }
         if (dep) {
-          const int tp = (dbg & 4) ? 0 : min(32, nb - 32 * (i + 1));
+          const int tp = min(32, nb - 32 * (i + 1));
           finish_bwd(i + 1, hv);
           bwd_tile(wait_tile(), tp, 32 * (i + 1));
           release_tile();
@@ -711,9 +706,9 @@ static int launch_solve_sym_t(const SymGeom& sg, const double2* F, const int* it
   // 3 CTAs per SM: the in-flight triangles fit L2, so DRAM traffic ~= the stored bytes
   static const int minb = env_int("VX_SYM_MINB", 3);
   static const int l2hint = env_int("VX_SYM_L2HINT", 1);
-  // forward tiles are requested into L2 this many KB ahead of the ring
-  static const int pfwin = env_int("VX_SYM_PF", 64) * 64;  // entries (16 bytes)
-  static const int dbg = env_int("VX_SYM_DBG", 0);
+  // forward tiles can be requested into L2 this many KB ahead of the ring (measured: no
+  // effect on this kernel -- it is bound by its two dependent passes, not by HBM latency)
+  static const int pfwin = env_int("VX_SYM_PF", 0) * 64;  // entries (16 bytes)
   const int S = slots_env < 2 ? 2 : (slots_env > 12 ? 12 : slots_env);
   const int npad = (sg.dmax + 31) / 32 * 32;
   const size_t smem = (((size_t)2 * S + 2) * 8 + 127) / 128 * 128 + (size_t)S * 1024 * sizeof(double2) +
@@ -722,7 +717,7 @@ static int launch_solve_sym_t(const SymGeom& sg, const double2* F, const int* it
   VX_REQUIRE((int)smem + 1024 <= device_smem_optin(), "symmetric solve smem %zu too large", smem);
   VX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   kern<<<nblocks, (SYM_WARPS + 1) * 32, smem, s>>>(sg, F, items, nblocks, klist, Y, s_row, s_k, S, q, l2hint,
-                                                   pfwin, dbg);
+                                                   pfwin);
   VX_CHECK_LAUNCH("lu_solve_sym_kernel");
   return VX_OK;
 }

@@ -129,15 +129,20 @@ __global__ void __launch_bounds__(256) lu_sym_invert_kernel(SymGeom sg, const do
 
 // ------------------------------------------------------------------ apply
 // x = G (b / W): one CTA per work item (a stored sector block and its one or
-// two right-hand sides), 4 tensor-core warps + a producer warp.  The producer
-// streams the block's storage in order as UNITS of up to 16 tile rows (8 KB)
-// into an S-slot mbarrier ring; unit n belongs to warp n mod 4 alone, which
-// runs both products of the unit on the FP64 tensor cores (fragment scheme of
-// lu_sym.cuh: A = stored entries, B = (Re, Im) columns of the two right-hand
-// sides) -- rows of tile row i from the unit times c_j, and columns of tile
-// row j from the unit's transpose times c_i -- and adds the results into ITS
-// OWN partial vector in shared memory (no atomics; the four partial vectors
-// are summed in a fixed order at the end: bitwise reproducible).
+// two right-hand sides: the x-mirror pair), 4 tensor-core warps + a producer
+// warp.  The producer streams the block's storage in order, one 16 KB tile per
+// slot of an in-order mbarrier ring (plus an L2 prefetch window ahead of it);
+// every tile is consumed by all four warps on the FP64 tensor cores (fragment
+// scheme of lu_sym.cuh: A = stored entries, B = (Re, Im) columns of the two
+// right-hand sides).  Warp w OWNS entries 8w .. 8w+7 of every tile row of the
+// result: it computes rows 8w.. of (tile x c_j) and columns 8w.. of
+// (tile^T x c_i).  The result vector therefore exists once in shared memory
+// (no per-warp partial vectors, no reduction, no atomics: bitwise
+// reproducible), and the c_i fragments of the transposed products stay in
+// registers for a whole tile row.
+// (A first version gave each warp its own 8 KB units and partial vector: same
+// speed on c1, but its ring needed a slot-per-warp protocol and its shared
+// memory grew with 4 x the block size; profiles/r02_symv_v1_ncu.txt, v2.)
 constexpr int SYMV_WARPS = 4;
 
 // Per-lane fragment offsets (doubles), fixed for the whole kernel, so that every
@@ -172,318 +177,6 @@ __device__ __forceinline__ SymvLane symv_lane(int lane) {
   return L;
 }
 
-// a full 16 x 32 unit of tile (i, j), j < i: rows 16 h .. 16 h + 15 of tile row i
-// times c_j into (n0, n1), and the unit's transpose times c_i (rows) into aT.
-// Eight stages of 8 products; the 11 fragment loads of stage s + 1 are issued
-// before the products of stage s (explicit double buffer: the tensor pipe
-// never waits for a shared-memory round trip).
-struct SymvStage {
-  double an[4], bn[2], at[4], bt;
-};
-__device__ __forceinline__ void symv_stage_load(SymvStage& f, int st, const double* __restrict__ A,
-                                                const SymvLane& L, const double* __restrict__ cj,
-                                                const double* __restrict__ ci) {
-#pragma unroll
-  for (int u = 0; u < 2; ++u) {
-    const int kc = 2 * st + u;
-    const double* An = A + L.nb[kc & 3] + 16 * (kc >> 2);
-    f.bn[u] = cj[L.cb + 12 * kc];
-    f.an[2 * u] = An[0];
-    f.an[2 * u + 1] = An[512];
-  }
-  f.bt = ci[L.cb + 12 * st];
-  const double* At = A + L.tb[st & 1] + 128 * st;
-#pragma unroll
-  for (int cb = 0; cb < 4; ++cb) f.at[cb] = At[16 * cb];
-}
-__device__ __forceinline__ void symv_stage_mma(const SymvStage& f, double (&n0)[2], double (&n1)[2],
-                                               double (&aT)[4][2]) {
-  dmma_884(n0[0], n0[1], f.an[0], f.bn[0]);
-  dmma_884(n1[0], n1[1], f.an[1], f.bn[0]);
-  dmma_884(aT[0][0], aT[0][1], f.at[0], f.bt);
-  dmma_884(aT[1][0], aT[1][1], f.at[1], f.bt);
-  dmma_884(n0[0], n0[1], f.an[2], f.bn[1]);
-  dmma_884(n1[0], n1[1], f.an[3], f.bn[1]);
-  dmma_884(aT[2][0], aT[2][1], f.at[2], f.bt);
-  dmma_884(aT[3][0], aT[3][1], f.at[3], f.bt);
-}
-__device__ __forceinline__ void symv_unit_full(const double* __restrict__ A, const SymvLane& L,
-                                               const double* __restrict__ cj, const double* __restrict__ ci,
-                                               double (&n0)[2], double (&n1)[2], double (&aT)[4][2]) {
-  SymvStage f0, f1;
-  symv_stage_load(f0, 0, A, L, cj, ci);
-#pragma unroll
-  for (int st = 0; st < 8; st += 2) {
-    symv_stage_load(f1, st + 1, A, L, cj, ci);
-    symv_stage_mma(f0, n0, n1, aT);
-    if (st + 2 < 8) symv_stage_load(f0, st + 2, A, L, cj, ci);
-    symv_stage_mma(f1, n0, n1, aT);
-  }
-}
-
-// a partial unit (rows < 16: the last tile row of a block)
-__device__ __forceinline__ void symv_unit_part(const double* __restrict__ A, const SymvLane& L, int rows,
-                                               const double* __restrict__ cj, const double* __restrict__ ci,
-                                               double (&n0)[2], double (&n1)[2], double (&aT)[4][2]) {
-  const bool two = rows > 8;
-#pragma unroll 4
-  for (int kc = 0; kc < 16; ++kc) {
-    const double b = cj[L.cb + 12 * kc];
-    const double* An = A + L.nb[kc & 3] + 16 * (kc >> 2);
-    dmma_884(n0[0], n0[1], An[0], b);
-    if (two) dmma_884(n1[0], n1[1], An[512], b);
-  }
-  for (int kc = 0; 2 * kc < rows; ++kc) {
-    const bool ok = 2 * kc + (L.t >> 1) < rows;
-    const double bt = ci[L.cb + 12 * kc];
-    const double* At = A + L.tb[kc & 1] + 128 * kc;
-#pragma unroll
-    for (int cb = 0; cb < 4; ++cb) {
-      const double a = ok ? At[16 * cb] : 0.0;
-      dmma_884(aT[cb][0], aT[cb][1], a, bt);
-    }
-  }
-}
-
-// rows [16 H, 16 H + 16) of the diagonal trapezoid of tile row i (ti rows): the
-// product covers the columns < 8 rb + 8 of row block rb (both triangles of the
-// diagonal 8 x 8 blocks are stored), the transposed product the blocks cb < rb
-template <int H>
-__device__ __forceinline__ void symv_unit_diag(const double* __restrict__ A, const SymvLane& L, int ti,
-                                               const double* __restrict__ ci, double (&n0)[2], double (&n1)[2],
-                                               double (&aT)[4][2]) {
-  const double* Ad = A - 2 * trap_off(16 * H);
-#pragma unroll
-  for (int rl = 0; rl < 2; ++rl) {
-    constexpr int dummy = 0;
-    (void)dummy;
-    const int rb = 2 * H + rl;
-    if (8 * rb >= ti) continue;
-    const int len = 8 * rb + 8;  // entries per row of this row block
-    const double* Ab = Ad + 2 * (32 * rb * (rb + 1));
-    // product: row 8 rb + g
-    const double* Arow = Ab + 2 * L.g * len;
-#pragma unroll
-    for (int kc = 0; kc < 4 * rb + 4; ++kc) {
-      const double b = ci[L.cb + 12 * kc];
-      const double a = Arow[(L.nb[kc & 3] - L.g * 64) + 16 * (kc >> 2)];
-      if (rl == 0) dmma_884(n0[0], n0[1], a, b);
-      else dmma_884(n1[0], n1[1], a, b);
-    }
-    // transposed product: contracted rows 8 rb + 2 kc + (t >> 1), outputs 8 cb + g, cb < rb
-    if (rb > 0) {
-#pragma unroll
-      for (int kc = 0; kc < 4; ++kc) {
-        const int r = 2 * kc + (L.t >> 1);  // row inside the row block
-        const bool ok = 8 * rb + r < ti;
-        const double bt = ci[L.cb + 12 * (4 * rb + kc)];
-        const double* At = Ab + 2 * r * len + (L.tb[kc & 1] - (L.t >> 1) * 64);
-#pragma unroll
-        for (int cb = 0; cb < 4; ++cb)
-          if (cb < rb) {
-            const double a = ok ? At[16 * cb] : 0.0;
-            dmma_884(aT[cb][0], aT[cb][1], a, bt);
-          }
-      }
-    }
-  }
-}
-
-template <int R, int MINB>
-__global__ void __launch_bounds__((SYMV_WARPS + 1) * 32, MINB)
-    symv_inv_kernel(SymGeom sg, const double2* __restrict__ G, const int* __restrict__ items, int nwork,
-                    const int* __restrict__ klist, double2* Y, long s_row, long s_k, int S, int q, int pfwin) {
-  extern __shared__ __align__(128) unsigned char smraw[];
-  constexpr int NC = SYMV_WARPS * 32;
-  constexpr int U2 = 512;  // entries per ring slot (8 KB)
-  const int npad = (sg.dmax + 31) / 32 * 32, ntm = npad / 32;
-  const uint32_t D = (uint32_t)S / SYMV_WARPS;  // slots per warp
-  uint64_t* full = reinterpret_cast<uint64_t*>(smraw);
-  uint64_t* empty = full + S;
-  double2* slots = reinterpret_cast<double2*>(smraw + (2 * S * 8 + 127) / 128 * 128);
-  double2* pt = slots + (long)S * U2;                                    // [SYMV_WARPS][ntm][32][2]
-  double* c3 = reinterpret_cast<double*>(pt + (long)SYMV_WARPS * ntm * 64);  // [npad][2][3]: c = b / W, signed
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (tid == 0) {
-    for (int s = 0; s < S; ++s) {
-      mbar_init(full + s, 1);
-      mbar_init(empty + s, 1);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-
-  if (warp == SYMV_WARPS) {
-    if (lane == 0) {
-      uint32_t n = 0;  // units emitted (all work items)
-      for (int w = blockIdx.x; w < nwork; w += gridDim.x) {
-        const int slot = items[3 * w], cnt = items[3 * w + 2];
-        int nb, sec;
-        const double2* Gb = sym_block(sg, G, slot, nb, sec);
-        const int nt = (nb + 31) / 32;
-        // the block's storage is one contiguous stream in unit order: request it from
-        // HBM into L2 a window ahead of the ring (each warp owns few slots, so the
-        // ring's own loads should only see L2 latency)
-        const long total = sym_size(nb);
-        for (int ch = 0; ch < (cnt + R - 1) / R; ++ch) {
-          long pf = 0;
-          auto prefetch_to = [&](long upto) {
-            upto = upto < total ? upto : total;
-            while (pf < upto) {
-              const long m = upto - pf < 1024 ? upto - pf : 1024;
-              bulk_prefetch_l2(Gb + pf, (uint32_t)(m * sizeof(double2)));
-              pf += m;
-            }
-          };
-          for (int i = 0; i < nt; ++i) {
-            const int ti = min(32, nb - 32 * i), nh = ti > 16 ? 2 : 1;
-            const double2* band = Gb + sym_band(i);
-            for (int j = 0; j <= i; ++j)
-              for (int h = 0; h < nh; ++h) {
-                const int rows = min(16, ti - 16 * h);
-                const double2* src;
-                uint32_t elems;
-                if (j < i) {
-                  src = band + 32L * ti * j + 512 * h;
-                  elems = (uint32_t)rows * 32;
-                } else {
-                  src = band + 32L * ti * i + trap_off(16 * h);
-                  elems = (uint32_t)(trap_off(16 * h + rows) - trap_off(16 * h));
-                }
-                if (pfwin > 0) prefetch_to((src - Gb) + elems + pfwin);
-                const uint32_t k = n / SYMV_WARPS;
-                const int s = (int)(n % SYMV_WARPS) + SYMV_WARPS * (int)(k % D);
-                const uint32_t use = k / D;
-                if (use > 0) mbar_wait_hint(empty + s, (use - 1) & 1u);
-                mbar_expect_tx(full + s, elems * (uint32_t)sizeof(double2));
-                bulk_g2s(slots + s * U2, src, elems * (uint32_t)sizeof(double2), full + s);
-                ++n;
-              }
-          }
-        }
-      }
-    }
-    return;
-  }
-
-  const SymvLane L = symv_lane(lane);
-  double2* ptw = pt + (long)warp * ntm * 64;
-  // add C fragments (blocks of 8 entries x 2 right-hand sides) into the warp's partial vector
-  auto rmw1 = [&](int panel, int blk, const double (&a)[2]) {
-    if (L.t < 2) {
-      double2* p = ptw + (((panel * 32 + 8 * blk + L.g) << 1) + L.t);
-      const double2 o = *p;
-      *p = cmk(o.x + a[0], o.y + a[1]);
-    }
-  };
-  uint32_t n = 0;  // units seen (all work items): unit n is warp n % 4's
-  for (int w = blockIdx.x; w < nwork; w += gridDim.x) {
-    const int slot = items[3 * w], beg = items[3 * w + 1], cnt = items[3 * w + 2];
-    int nb, sec;
-    (void)sym_block(sg, G, slot, nb, sec);
-    const int nt = (nb + 31) / 32;
-    const double2* wrow = sg.w + (long)sec * sg.dmax;
-    for (int ch = 0; ch < (cnt + R - 1) / R; ++ch) {
-      const int rho0 = ch * R;
-      const int nr = min(R, cnt - rho0);
-      long rb0 = 0, rb1 = 0;
-      {
-        const int k0 = klist ? klist[beg + rho0] : beg + rho0;
-        rb0 = rhs_base(k0, rho0, 1, s_k);
-        if (nr > 1) {
-          const int k1 = klist ? klist[beg + rho0 + 1] : beg + rho0 + 1;
-          rb1 = rhs_base(k1, rho0 + 1, 1, s_k);
-        }
-      }
-      consumers_sync(NC);  // the previous item's final reduction is done with c3 / pt
-      for (int idx = tid; idx < npad * 2; idx += NC) {
-        const int row = idx >> 1, rr = idx & 1;
-        double2 v = cmk(0.0, 0.0);
-        if (row < nb && rr < nr) {
-          const long rb = rr ? rb1 : rb0;
-          v = cdiv(cflip(Y[(long)row * s_row + (rb & ROFF)], flip_row((int)(rb >> 56), row, q)), wrow[row]);
-        }
-        double* o = c3 + 3 * idx;
-        o[0] = v.y;
-        o[1] = v.x;
-        o[2] = -v.y;
-      }
-      for (int idx = lane; idx < ntm * 64; idx += 32) ptw[idx] = cmk(0.0, 0.0);
-      consumers_sync(NC);
-      double accN[4][2];
-#pragma unroll
-      for (int b = 0; b < 4; ++b) accN[b][0] = accN[b][1] = 0.0;
-      for (int i = 0; i < nt; ++i) {
-        const int ti = min(32, nb - 32 * i), nh = ti > 16 ? 2 : 1;
-        const double* ci = c3 + 192 * i;
-        bool mine = false;
-        for (int j = 0; j <= i; ++j)
-          for (int h = 0; h < nh; ++h, ++n) {
-            if ((int)(n % SYMV_WARPS) != warp) continue;
-            mine = true;
-            // the warp's k-th unit sits in ITS slot warp + 4 (k mod D): only the owner ever
-            // waits on a slot, so it sees the slot's phases one after the other
-            const uint32_t k = n / SYMV_WARPS;
-            const int s = warp + SYMV_WARPS * (int)(k % D);
-            mbar_wait_hint(full + s, (k / D) & 1u);
-            const double* A = reinterpret_cast<const double*>(slots + s * U2);
-            const int rows = min(16, ti - 16 * h);
-            double accT[4][2];
-#pragma unroll
-            for (int b = 0; b < 4; ++b) accT[b][0] = accT[b][1] = 0.0;
-            if (j < i) {
-              const double* cj = c3 + 192 * j;
-              if (rows == 16) {
-                if (h == 0) symv_unit_full(A, L, cj, ci, accN[0], accN[1], accT);
-                else symv_unit_full(A, L, cj, ci + 96, accN[2], accN[3], accT);
-              } else {
-                if (h == 0) symv_unit_part(A, L, rows, cj, ci, accN[0], accN[1], accT);
-                else symv_unit_part(A, L, rows, cj, ci + 96, accN[2], accN[3], accT);
-              }
-              __syncwarp();
-              if (lane == 0) mbar_arrive(empty + s);
-#pragma unroll
-              for (int cb = 0; cb < 4; ++cb) rmw1(j, cb, accT[cb]);
-            } else {
-              if (h == 0) symv_unit_diag<0>(A, L, ti, ci, accN[0], accN[1], accT);
-              else symv_unit_diag<1>(A, L, ti, ci, accN[2], accN[3], accT);
-              __syncwarp();
-              if (lane == 0) mbar_arrive(empty + s);
-#pragma unroll
-              for (int cb = 0; cb < 3; ++cb) rmw1(i, cb, accT[cb]);
-            }
-          }
-        if (mine) {  // rows of tile row i accumulated over this warp's units of the band
-#pragma unroll
-          for (int b = 0; b < 4; ++b) {
-            rmw1(i, b, accN[b]);
-            accN[b][0] = accN[b][1] = 0.0;
-          }
-        }
-      }
-      consumers_sync(NC);
-      for (int idx = tid; idx < nb * 2; idx += NC) {
-        const int row = idx >> 1, rr = idx & 1;
-        if (rr < nr) {
-          double2 s = pt[idx];  // == ((panel * 32 + row % 32) << 1) + rr
-#pragma unroll
-          for (int ww = 1; ww < SYMV_WARPS; ++ww) s = cadd(s, pt[(long)ww * ntm * 64 + idx]);
-          const long rb = rr ? rb1 : rb0;
-          Y[(long)row * s_row + (rb & ROFF)] = cflip(s, flip_row((int)(rb >> 56), row, q));
-        }
-      }
-    }
-  }
-}
-
-// ------------------------------------------------------------------ apply, output-owned variant
-// Same stream, different split of the work: every tile (16 KB) is consumed by
-// all four warps; warp w OWNS entries 8w .. 8w+7 of every tile row of the
-// result, i.e. it computes rows 8w.. of (tile x c_j) and columns 8w.. of
-// (tile^T x c_i).  The result vector therefore exists once (no per-warp partial
-// vectors, no final reduction), the ring is a plain in-order ring shared by the
-// warps (1 tile in use + S - 1 in flight per CTA), and the c_i fragments of the
-// transposed products stay in registers for a whole tile row.
 struct Symv2Stage {
   double an[2], bn[2], at[2];
 };
@@ -713,30 +406,14 @@ static int launch_symv2_inv_t(const SymGeom& sg, const double2* G, const int* it
                       (size_t)npad * 2 * sizeof(double2) + (size_t)npad * 6 * sizeof(double);
   auto kern = minb == 2 ? symv2_inv_kernel<R, 2> : minb == 4 ? symv2_inv_kernel<R, 4> : symv2_inv_kernel<R, 3>;
   VX_REQUIRE((int)smem + 1024 <= device_smem_optin(), "symmetric inverse apply smem %zu too large", smem);
-  VX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  static size_t smem_set[3] = {0, 0, 0};  // per kernel variant: raise the limit once per size, not per launch
+  size_t& have = smem_set[minb == 2 ? 0 : minb == 4 ? 2 : 1];
+  if (have < smem) {
+    VX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    have = smem;
+  }
   kern<<<nblocks, (SYMV_WARPS + 1) * 32, smem, s>>>(sg, G, items, nblocks, klist, Y, s_row, s_k, S, q, pfwin);
   VX_CHECK_LAUNCH("symv2_inv_kernel");
-  return VX_OK;
-}
-
-template <int R>
-static int launch_symv_inv_t(const SymGeom& sg, const double2* G, const int* items, int nblocks, const int* klist,
-                             double2* Y, long s_row, long s_k, int q, cudaStream_t s) {
-  static const int variant = env_int("VX_SYMV_VARIANT", 2);
-  if (variant == 2) return launch_symv2_inv_t<R>(sg, G, items, nblocks, klist, Y, s_row, s_k, q, s);
-  // ring slots: a multiple of the 4 consumer warps (each warp owns S / 4 of them)
-  static const int slots_env = env_int("VX_SYMV_SLOTS", 4);
-  static const int minb = env_int("VX_SYMV_MINB", 3);
-  static const int pfwin = env_int("VX_SYMV_PF", 24) * 64;  // L2 prefetch window, entries
-  const int S = slots_env < 4 ? 4 : (slots_env > 24 ? 24 : slots_env / SYMV_WARPS * SYMV_WARPS);
-  const int npad = (sg.dmax + 31) / 32 * 32;
-  const size_t smem = ((size_t)2 * S * 8 + 127) / 128 * 128 + (size_t)S * 512 * sizeof(double2) +
-                      (size_t)SYMV_WARPS * (npad / 32) * 64 * sizeof(double2) + (size_t)npad * 6 * sizeof(double);
-  auto kern = minb == 2 ? symv_inv_kernel<R, 2> : minb == 4 ? symv_inv_kernel<R, 4> : symv_inv_kernel<R, 3>;
-  VX_REQUIRE((int)smem + 1024 <= device_smem_optin(), "symmetric inverse apply smem %zu too large", smem);
-  VX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  kern<<<nblocks, (SYMV_WARPS + 1) * 32, smem, s>>>(sg, G, items, nblocks, klist, Y, s_row, s_k, S, q, pfwin);
-  VX_CHECK_LAUNCH("symv_inv_kernel");
   return VX_OK;
 }
 
@@ -744,6 +421,6 @@ static int launch_symv_inv(const SymGeom& sg, const double2* G, const int* items
                            const int* klist, double2* Y, long s_row, long s_k, int q, cudaStream_t s) {
   if (nblocks <= 0) return VX_OK;
   VX_REQUIRE(direct_r == 1 || direct_r == 2, "symmetric inverse apply: direct_r must be 1 or 2");
-  return direct_r == 2 ? launch_symv_inv_t<2>(sg, G, items, nblocks, klist, Y, s_row, s_k, q, s)
-                       : launch_symv_inv_t<1>(sg, G, items, nblocks, klist, Y, s_row, s_k, q, s);
+  return direct_r == 2 ? launch_symv2_inv_t<2>(sg, G, items, nblocks, klist, Y, s_row, s_k, q, s)
+                       : launch_symv2_inv_t<1>(sg, G, items, nblocks, klist, Y, s_row, s_k, q, s);
 }

@@ -169,6 +169,25 @@ _WS_LOCK = threading.Lock()
 _WS_CACHE: dict = {}
 
 
+_KEEP_Z_CACHE: dict = {}
+
+
+def _keep_z_fits(t, n, mmax) -> bool:
+    """Whether a second basis Z = P^-1 V fits comfortably (a quarter of the free
+    device memory).  Asked ONCE per (device, n, mmax): cudaMemGetInfo takes
+    2-60 ms on a busy driver (tools/stall_probe.py traced every slow solve of
+    the bench to this call), and the answer only changes with the shape."""
+    key = (t.cuda.current_device(), n, mmax)
+    fits = _KEEP_Z_CACHE.get(key)
+    if fits is None:
+        free, _ = t.cuda.mem_get_info()
+        with _WS_LOCK:
+            have = any(k[:3] == key and k[3] for k in _WS_CACHE)   # a cached workspace already holds Z
+        fits = have or (mmax + 1) * n * 16 <= free // 4
+        _KEEP_Z_CACHE[key] = fits
+    return fits
+
+
 def _workspace(n, m, keep_z):
     """A reusable Krylov workspace (bases of up to m+1 rows); one per shape,
     handed to one solve at a time, so repeated solves do not re-allocate
@@ -190,6 +209,7 @@ def clear_workspace() -> None:
     """Drop the cached Krylov workspace (its device memory returns to torch)."""
     with _WS_LOCK:
         _WS_CACHE.clear()
+    _KEEP_Z_CACHE.clear()
 
 
 def _aliases(a, b) -> bool:
@@ -230,6 +250,11 @@ class GivensQR:
         for col, vals in enumerate(self.r_cols[:j]):
             r_mat[: col + 1, col] = vals
         return np.linalg.solve(r_mat, np.asarray(self.g[:j], dtype=np.complex128))
+
+
+# debugging aid (tools/stall_probe.py): a list that receives, per Arnoldi step,
+# (j, host seconds spent launching, host seconds waiting for the step's event)
+TRACE = None
 
 
 def _speculate(residuals, tol) -> bool:
@@ -302,7 +327,10 @@ def _gmres_cycle(K: _Krylov, op, r0, beta, bnorm, tol, m, residuals, P=None, A=N
     converged = lucky = False
     j = 0
     launched = 0
+    trace = TRACE
     while j < m:
+        if trace is not None:
+            tr0 = time.perf_counter()
         if launched <= j:
             launch(j)
             launched = j + 1
@@ -310,7 +338,11 @@ def _gmres_cycle(K: _Krylov, op, r0, beta, bnorm, tol, m, residuals, P=None, A=N
             launch(j + 1)
             launched = j + 2
         b = j % 2
+        if trace is not None:
+            tr1 = time.perf_counter()
         K.ev[b].synchronize()
+        if trace is not None:
+            trace.append((j, tr1 - tr0, time.perf_counter() - tr1))
         h = K.h_host[b][: j + 2].numpy().copy()
         norm_before = float(K.s_host[b][0])
         lucky = h[j + 1].real <= 1e-14 * max(norm_before, 1e-300)
@@ -375,11 +407,15 @@ def _gmres(apply_a, b, *, apply_pinv=None, tol: float = 1e-4, maxit: int = 2000,
     # keep Z = P^-1 V when a preconditioner is given and a second basis fits
     # comfortably (a quarter of the free device memory)
     keep_z = False
+    marks = [("start", t0)] if TRACE is not None else None
     if apply_pinv is not None and os.environ.get("VX_KEEP_Z", "1") != "0":
-        free, _ = t.cuda.mem_get_info()
-        keep_z = (mmax + 1) * n * 16 <= free // 4
+        keep_z = _keep_z_fits(t, n, mmax)
+    if marks is not None:
+        marks.append(("mem_get_info", time.perf_counter()))
     K = _workspace(n, mmax, keep_z)
     bnorm = K.norm(bd)
+    if marks is not None:
+        marks.append(("workspace+norm", time.perf_counter()))
 
     def _out(xd):
         return xd if on_device else nv.to_host(xd)
@@ -404,14 +440,25 @@ def _gmres(apply_a, b, *, apply_pinv=None, tol: float = 1e-4, maxit: int = 2000,
             converged = True
             break
         m = maxit - total if restart is None else min(restart, maxit - total)
+        if marks is not None:
+            marks.append(("r0", time.perf_counter()))
         u, used, converged = _gmres_cycle(K, op, r0, beta, bnorm, tol, m, residuals, P=P, A=A)
         total += used
+        if marks is not None:
+            marks.append(("cycle", time.perf_counter()))
         x = K.axpby(1.0, x, 1.0, u if (P is None or K.keep_z) else P(u))
+    # host callers: the copy of x to the host runs on a side stream while the
+    # true-residual matvec (reference solver.py:166) runs on this one
+    pending = None if on_device else nv.to_host_begin(x)
     true_res = K.norm(K.axpby(1.0, bd, -1.0, A(x))) / bnorm
     _release(K)
+    x_out = x if on_device else pending.result()
+    if marks is not None:
+        marks.append(("true_residual+out", time.perf_counter()))
+        TRACE.append(("phases", [(nm, round((tt - marks[i][1]) * 1e3, 2)) for i, (nm, tt) in enumerate(marks[1:])]))
     report = SolveReport(iterations=int(total), residuals=residuals, converged=bool(converged),
                          solve_seconds=time.perf_counter() - t0, true_residual=float(true_res))
-    return _out(x), report
+    return x_out, report
 
 
 def spectrum(dense_a, dense_pinv=None) -> np.ndarray:
