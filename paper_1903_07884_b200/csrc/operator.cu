@@ -297,13 +297,16 @@ __global__ void __launch_bounds__(ZR_T)
 // the one-thread-per-column kernel -> full occupancy; loads of the 3 spectra a
 // lane needs hit L1 for the entries its column partners also use.
 constexpr int ZS_COLS = 10;
+#ifndef ZMUL_MINB_BIG
+#define ZMUL_MINB_BIG 2
+#endif
 
 __device__ __forceinline__ double2 shfl_c(double2 v, int src) {
   return cmk(__shfl_sync(0xffffffffu, v.x, src), __shfl_sync(0xffffffffu, v.y, src));
 }
 
 template <int PZ>
-__global__ void __launch_bounds__(256, (PZ <= 16 ? 3 : 2))
+__global__ void __launch_bounds__(256, (PZ <= 16 ? 3 : ZMUL_MINB_BIG))
     op_zmul_shfl_kernel(double2* __restrict__ B, SpecView sv, int nz, long cols, double scale) {
   const int lane = threadIdx.x & 31;
   const long warp = (blockIdx.x * (long)blockDim.x + threadIdx.x) >> 5;

@@ -345,6 +345,7 @@ def _gmres_cycle(K: _Krylov, op, r0, beta, bnorm, tol, m, residuals, P=None, A=N
             trace.append((j, tr1 - tr0, time.perf_counter() - tr1))
         h = K.h_host[b][: j + 2].numpy().copy()
         norm_before = float(K.s_host[b][0])
+        K.reorth_passes += int(K.s_host[b][2] != 0.0)   # the DGKS second pass ran in this step
         lucky = h[j + 1].real <= 1e-14 * max(norm_before, 1e-300)
         qr.add_column(h, j, residuals, tol)
         j += 1
@@ -413,6 +414,7 @@ def _gmres(apply_a, b, *, apply_pinv=None, tol: float = 1e-4, maxit: int = 2000,
     if marks is not None:
         marks.append(("mem_get_info", time.perf_counter()))
     K = _workspace(n, mmax, keep_z)
+    K.reorth_passes = 0
     bnorm = K.norm(bd)
     if marks is not None:
         marks.append(("workspace+norm", time.perf_counter()))
@@ -458,6 +460,7 @@ def _gmres(apply_a, b, *, apply_pinv=None, tol: float = 1e-4, maxit: int = 2000,
         TRACE.append(("phases", [(nm, round((tt - marks[i][1]) * 1e3, 2)) for i, (nm, tt) in enumerate(marks[1:])]))
     report = SolveReport(iterations=int(total), residuals=residuals, converged=bool(converged),
                          solve_seconds=time.perf_counter() - t0, true_residual=float(true_res))
+    report.reorth_passes = int(K.reorth_passes)   # steps whose DGKS re-orthogonalisation fired (not in to_dict)
     return x_out, report
 
 

@@ -85,3 +85,48 @@ def test_sector_dims_c1():
     assert sorted(p.dims) == [176, 176, 187, 187] and p.dmax == 187
     p = sector_plan(25, 11, False, True)
     assert sum(p.dims) == 3 * 25 * 11 and p.nsec == 2
+
+
+def test_mirror_store_plan_matches_the_sequential_rule():
+    """_mirror_store (vectorised) == the one-block-at-a-time rule: block k shares the factor
+    of nx - k when that frequency is present and smaller, else owns a new slot."""
+    from paper_1903_07884_b200.circulant import _mirror_store
+
+    def rule(ks, nx, share):
+        pos = {int(k): i for i, k in enumerate(ks)}
+        store, flip, kset = np.empty(ks.size, np.int64), np.zeros(ks.size, bool), []
+        for i, k in enumerate(ks):
+            km = (nx - int(k)) % nx
+            if share and km < k and km in pos:
+                store[i], flip[i] = store[pos[km]], True
+            else:
+                store[i] = len(kset)
+                kset.append(int(k))
+        return np.asarray(kset, np.int64), store, flip
+
+    rng = np.random.default_rng(3)
+    for nx in (1, 2, 5, 8, 200, 367, 5000):
+        for share in (True, False):
+            for trial in range(4):
+                ks = np.arange(nx) if trial == 0 else np.sort(rng.choice(nx, size=max(1, nx // 3), replace=False))
+                for got, want in zip(_mirror_store(ks, nx, share), rule(ks, nx, share)):
+                    assert np.array_equal(got, want), (nx, share, trial)
+
+
+def test_constant_along_x_check():
+    """reference circulant.py:81-96: exactly constant maps pass on the fast path, a deviation
+    above 1e-12 max|m| raises, NaN raises."""
+    from paper_1903_07884_b200.circulant import _constant_along
+
+    m = np.repeat((0.5 + 0.1j * np.arange(12.0)).reshape(3, 4, 1), 50, axis=2)
+    _constant_along(m, 2, "x")
+    m2 = m.copy()
+    m2[1, 2, 7] += 1e-14
+    _constant_along(m2, 2, "x")           # within tolerance: slow path
+    m2[1, 2, 7] += 1e-9
+    with pytest.raises(ValueError):
+        _constant_along(m2, 2, "x")
+    m3 = m.copy()
+    m3[0, 0, 3] = np.nan
+    with pytest.raises(ValueError):
+        _constant_along(m3, 2, "x")
