@@ -60,3 +60,30 @@ def test_no_cpu_fallback_without_gpu():
 
     with pytest.raises(NativeError):
         plan_operator(assemble_kernel(VoxelGrid(4, 3, 2, 0.05), 6.28))
+
+
+def test_symmetric_layout_stride_formula():
+    """vx_lu_sym_stride (host function, no GPU): per block of dimension d the symmetric layouts
+    (factors and inverses, csrc/lu_sym.cuh) hold, per tile row i of t_i rows, i off-diagonal
+    t_i x 32 tiles and the diagonal trapezoid of 8-row blocks (row r: 8 (r // 8) + 8 entries)."""
+    import numpy as np
+
+    from paper_1903_07884_b200 import _native as nv
+
+    def trap(t):
+        return sum(8 * (r // 8) + 8 for r in range(t))
+
+    def size(d):
+        nt = (d + 31) // 32
+        tot = 0
+        for i in range(nt):
+            ti = min(32, d - 32 * i)
+            tot += 32 * ti * i + trap(ti)
+        return tot
+
+    nv.load()
+    for dims in ([33], [36, 36, 36, 36], [187, 187, 176, 176], [413, 412], [462, 462], [1024]):
+        a = np.ascontiguousarray(dims, np.int32)
+        assert int(nv.query("vx_lu_sym_stride", len(dims), a.ctypes.data)) == sum(size(d) for d in dims)
+    # the lower triangle plus the trapezoid padding: ~0.52 of the LU bytes at c1's sector sizes
+    assert size(187) / 187 ** 2 < 0.53
