@@ -212,6 +212,14 @@ int vx_op_x_forward(int nx, int px, int nlines, const vx_c128* x, vx_c128* A, vo
 long vx_op_yz_work_elems(int ny, int nz, int nkx, int py);
 int vx_op_yz(int ny, int nz, int nkx, int px, int py, int pz, const vx_c128* spectra_local, vx_c128* A,
              vx_c128* work, void* stream);
+/* vx_op_yz on a rank's spectra compacted in y and z (vx_spec_compact_yz: the
+ * k <= P/2 halves of a parity-symmetric kernel's spectra, every local kx kept:
+ * (pz/2+1, py/2+1, nkx, 6), vx_spec_compact_yz_elems entries) -- a quarter of
+ * the bytes of the slice vx_op_yz reads (operator.py:87-97 on a rank's columns). */
+int vx_op_yz_compact(int ny, int nz, int nkx, int px, int py, int pz, const vx_c128* spectra_cyz, vx_c128* A,
+                     vx_c128* work, void* stream);
+long vx_spec_compact_yz_elems(int nkx, int py, int pz);
+int vx_spec_compact_yz(int nkx, int py, int pz, const vx_c128* full, vx_c128* compact, void* stream);
 int vx_op_x_inverse(int nx, int ny, int nz, int px, int nlines, long line0, const vx_c128* A,
                     const vx_c128* m, const vx_c128* x_local, vx_c128* y_local, void* stream);
 /* All-to-all pack/unpack: out = concat_s A[:, colmap[col_off[s]:col_off[s+1]]]. */

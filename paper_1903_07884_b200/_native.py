@@ -78,6 +78,9 @@ _SIGS = {
     "vx_op_x_forward": (c_int, [c_int, c_int, c_int, P, P, P]),
     "vx_op_yz_work_elems": (c_long, [c_int] * 4),
     "vx_op_yz": (c_int, [c_int] * 6 + [P, P, P, P]),
+    "vx_op_yz_compact": (c_int, [c_int] * 6 + [P, P, P, P]),
+    "vx_spec_compact_yz_elems": (c_long, [c_int, c_int, c_int]),
+    "vx_spec_compact_yz": (c_int, [c_int, c_int, c_int, P, P, P]),
     "vx_op_x_inverse": (c_int, [c_int] * 5 + [c_long, P, P, P, P, P]),
     "vx_gather_cols": (c_int, [c_long, P, c_long, c_int, P, P, c_long, P, P]),
     "vx_scatter_cols": (c_int, [c_long, P, c_int, P, P, c_long, P, c_long, P]),

@@ -60,6 +60,7 @@ struct SpecView {
   const double2* S;
   int compact;
   int Pz, Py, Px, Hz, Hy, Hx;
+  int Mx;  // x-mirror period (Px); huge for spectra compacted in y and z only (a rank's kx columns)
   FastDiv fdPx;
 };
 
@@ -100,7 +101,7 @@ __global__ void __launch_bounds__(512, (RMAX <= 8 ? 2 : 1))
       for (int p = 0; p < 6; ++p) sp[p] = ld_stream(sv.S + p * sstr + so);
     } else {
       const int ky = (int)sv.fdPx.div((unsigned)col), kx = (int)(col - (long)ky * sv.Px);
-      const bool mz = 2 * kz > sv.Pz, my = 2 * ky > sv.Py, mx = 2 * kx > sv.Px;
+      const bool mz = 2 * kz > sv.Pz, my = 2 * ky > sv.Py, mx = 2 * kx > sv.Mx;
       const int kzs = mz ? sv.Pz - kz : kz, kys = my ? sv.Py - ky : ky, kxs = mx ? sv.Px - kx : kx;
       const long so = (((long)kzs * sv.Hy + kys) * sv.Hx + kxs) * 6;
       const long sstr = 1;
@@ -246,7 +247,7 @@ __global__ void __launch_bounds__(ZR_T)
   if (sv.compact) {
     const int ky = (int)sv.fdPx.div((unsigned)col), kx = (int)(col - (long)ky * sv.Px);
     my = 2 * ky > sv.Py;
-    mx = 2 * kx > sv.Px;
+    mx = 2 * kx > sv.Mx;
     so0 = ((long)(my ? sv.Py - ky : ky) * sv.Hx + (mx ? sv.Px - kx : kx)) * 6;
     sstr = 1;
     kstr = (long)sv.Hy * sv.Hx * 6;
@@ -336,7 +337,7 @@ __global__ void __launch_bounds__(256, (PZ <= 16 ? 3 : ZMUL_MINB_BIG))
   if (sv.compact) {
     const int ky = (int)sv.fdPx.div((unsigned)col), kx = (int)(col - (long)ky * sv.Px);
     my = 2 * ky > sv.Py;
-    mx = 2 * kx > sv.Px;
+    mx = 2 * kx > sv.Mx;
     so0 = ((long)(my ? sv.Py - ky : ky) * sv.Hx + (mx ? sv.Px - kx : kx)) * 6;
     sstr = 1;
     kstr = (long)sv.Hy * sv.Hx * 6;
@@ -449,7 +450,7 @@ __global__ void __launch_bounds__(256)
   if (sv.compact) {
     const int ky = (int)sv.fdPx.div((unsigned)col), kx = (int)(col - (long)ky * sv.Px);
     my = 2 * ky > sv.Py;
-    mx = 2 * kx > sv.Px;
+    mx = 2 * kx > sv.Mx;
     so0 = ((long)(my ? sv.Py - ky : ky) * sv.Hx + (mx ? sv.Px - kx : kx)) * 6;
     sstr = 1;
     kstr = (long)sv.Hy * sv.Hx * 6;
@@ -712,7 +713,7 @@ __global__ void __launch_bounds__(256, 2)
       bool my = false, mx = false;
       if (sv.compact) {
         my = 2 * ky > sv.Py;
-        mx = 2 * kx > sv.Px;
+        mx = 2 * kx > sv.Mx;
         so0 = ((long)(my ? sv.Py - ky : ky) * sv.Hx + (mx ? sv.Px - kx : kx)) * 6;
         sstr = 1;
         kstr = (long)sv.Hy * sv.Hx * 6;
@@ -964,7 +965,7 @@ __global__ void __launch_bounds__(512, 2) op_yz_fused_kernel(FftPlan fy, FftPlan
 #pragma unroll
       for (int q = 0; q < 6; ++q) sp[q] = ld_stream(sv.S + q * sstr + so);
     } else {
-      const bool mz = 2 * kz > sv.Pz, my = 2 * ky > sv.Py, mx = 2 * kx > sv.Px;
+      const bool mz = 2 * kz > sv.Pz, my = 2 * ky > sv.Py, mx = 2 * kx > sv.Mx;
       const int kzs = mz ? sv.Pz - kz : kz, kys = my ? sv.Py - ky : ky, kxs = mx ? sv.Px - kx : kx;
       const long so = (((long)kzs * sv.Hy + kys) * sv.Hx + kxs) * 6;
       const long sstr = 1;
@@ -1043,6 +1044,12 @@ static SpecView spec_view(const vx_c128* spectra, int compact, int px, int py, i
   v.compact = compact;
   v.Pz = pz; v.Py = py; v.Px = px;
   v.Hz = pz / 2 + 1; v.Hy = py / 2 + 1; v.Hx = px / 2 + 1;
+  v.Mx = px;
+  if (compact == 2) {  // compacted in y and z only: every local kx column is stored
+    v.compact = 1;
+    v.Hx = px;
+    v.Mx = 1 << 30;
+  }
   v.fdPx = FastDiv((unsigned)px);
   return v;
 }
@@ -1104,6 +1111,25 @@ extern "C" int vx_op_yz(int ny, int nz, int nkx, int px, int py, int pz, const v
                1.0 / ((double)px * py * pz), as_stream(stream));
 }
 
+// vx_op_yz on spectra compacted in y and z (vx_spec_compact_yz): a rank's kx columns of the
+// parity-symmetric kernel's spectra at a quarter of the bytes (and one load per kz mirror pair)
+extern "C" int vx_op_yz_compact(int ny, int nz, int nkx, int px, int py, int pz, const vx_c128* spectra_cyz,
+                                vx_c128* A, vx_c128* work, void* stream) {
+  VX_REQUIRE(ny >= 1 && nz >= 1 && nkx >= 0, "bad yz arguments");
+  VX_REQUIRE(fft_is_smooth(py) && fft_is_smooth(pz), "padded dims must be 13-smooth");
+  if (nkx == 0) return VX_OK;
+  FftPlan fy, fz;
+  int st;
+  if ((st = fft_get_plan(py, &fy)) || (st = fft_get_plan(pz, &fz))) return st;
+  return op_yz(fy, fz, ny, nz, nkx, py, pz, spec_view(spectra_cyz, 2, nkx, py, pz),
+               reinterpret_cast<double2*>(A), reinterpret_cast<double2*>(work),
+               1.0 / ((double)px * py * pz), as_stream(stream));
+}
+
+extern "C" long vx_spec_compact_yz_elems(int nkx, int py, int pz) {
+  return 6L * (pz / 2 + 1) * (py / 2 + 1) * nkx;
+}
+
 extern "C" int vx_op_x_inverse(int nx, int ny, int nz, int px, int nlines, long line0,
                                const vx_c128* A, const vx_c128* m, const vx_c128* x_local,
                                vx_c128* y_local, void* stream) {
@@ -1119,8 +1145,8 @@ extern "C" int vx_op_x_inverse(int nx, int ny, int nz, int px, int nlines, long 
 namespace vx {
 // gather the k <= P/2 half-octant of full spectra (6, pz, py, px)
 __global__ void spec_compact_kernel(const double2* __restrict__ full, double2* __restrict__ out, int px, int py,
-                                    int pz) {
-  const int hx = px / 2 + 1, hy = py / 2 + 1, hz = pz / 2 + 1;
+                                    int pz, int hx) {
+  const int hy = py / 2 + 1, hz = pz / 2 + 1;
   const long total = 6L * hz * hy * hx;
   for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < total; i += (long)gridDim.x * blockDim.x) {
     long r = i;
@@ -1179,7 +1205,19 @@ extern "C" int vx_op_compact(int px, int py, int pz, const vx_c128* full, vx_c12
   const long total = vx_op_compact_elems(px, py, pz);
   const unsigned g = div_up(total, 256) < 8192 ? div_up(total, 256) : 8192;
   spec_compact_kernel<<<g, 256, 0, as_stream(stream)>>>(reinterpret_cast<const double2*>(full),
-                                                        reinterpret_cast<double2*>(compact), px, py, pz);
+                                                        reinterpret_cast<double2*>(compact), px, py, pz, px / 2 + 1);
+  VX_CHECK_LAUNCH("spec_compact_kernel");
+  return VX_OK;
+}
+
+// the k <= P/2 halves in y and z of a rank's kx columns (full: (6, pz, py, nkx)), all nkx kept
+extern "C" int vx_spec_compact_yz(int nkx, int py, int pz, const vx_c128* full, vx_c128* compact, void* stream) {
+  VX_REQUIRE(nkx >= 0 && py >= 1 && pz >= 1, "bad compaction arguments");
+  const long total = vx_spec_compact_yz_elems(nkx, py, pz);
+  if (total == 0) return VX_OK;
+  const unsigned g = div_up(total, 256) < 8192 ? div_up(total, 256) : 8192;
+  spec_compact_kernel<<<g, 256, 0, as_stream(stream)>>>(reinterpret_cast<const double2*>(full),
+                                                        reinterpret_cast<double2*>(compact), nkx, py, pz, nkx);
   VX_CHECK_LAUNCH("spec_compact_kernel");
   return VX_OK;
 }

@@ -30,6 +30,7 @@ from ``tests/`` to check the data movement against the oracle.
 
 from __future__ import annotations
 
+import os
 import time
 
 import numpy as np
@@ -123,16 +124,29 @@ class CudaBackend:
 
         return plan_operator(kernel, compact=False).spectra_device
 
+    def symmetric(self, kernel) -> bool:
+        """Parity-symmetric generators (what plan_operator's compact spectra need)."""
+        from .operator import SYMMETRY_RTOL, kernel_asymmetry
+
+        return os.environ.get("VX_SHARD_COMPACT", "1") != "0" and kernel_asymmetry(kernel) <= SYMMETRY_RTOL
+
+    def compact_yz(self, spec_loc):
+        """A rank's kx columns (6, pz, py, nkx) -> the y / z half-octant (pz/2+1, py/2+1, nkx, 6)."""
+        pz, py, nkx = (int(v) for v in spec_loc.shape[1:])
+        out = self.empty(max(1, int(nv.query("vx_spec_compact_yz_elems", nkx, py, pz))))
+        nv.call("vx_spec_compact_yz", nkx, py, pz, spec_loc.data_ptr(), out.data_ptr(), nv.stream_ptr())
+        return out
+
     def x_forward(self, x_loc, nl, nx, px):
         A = self.empty((nl, px))
         nv.call("vx_op_x_forward", nx, px, nl, x_loc.data_ptr(), A.data_ptr(), nv.stream_ptr())
         return A
 
-    def op_yz(self, A, spectra_loc, dims, nkx, px, py, pz):
+    def op_yz(self, A, spectra_loc, dims, nkx, px, py, pz, compact=False):
         nx, ny, nz = dims
         work = self.empty(int(nv.query("vx_op_yz_work_elems", ny, nz, nkx, py)))
-        nv.call("vx_op_yz", ny, nz, nkx, px, py, pz, spectra_loc.data_ptr(), A.data_ptr(), work.data_ptr(),
-                nv.stream_ptr())
+        nv.call("vx_op_yz_compact" if compact else "vx_op_yz", ny, nz, nkx, px, py, pz, spectra_loc.data_ptr(),
+                A.data_ptr(), work.data_ptr(), nv.stream_ptr())
 
     def x_inverse(self, A, dims, px, nl, line0, m_full, x_loc):
         nx, ny, nz = dims
@@ -268,6 +282,11 @@ class DistOperator:
         k0, k1 = layout.kxb[layout.rank], layout.kxb[layout.rank + 1]
         self.spec_loc = spec[..., k0:k1].contiguous()
         del spec
+        # parity-symmetric kernels: keep only the y / z half-octant of the rank's columns (a quarter
+        # of the bytes; the z-multiply then shares one spectra load between kz and its mirror)
+        self.compact = bool(getattr(backend, "symmetric", lambda k: False)(kernel)) and k1 > k0
+        if self.compact:
+            self.spec_loc = backend.compact_yz(self.spec_loc)
         off, cmap = layout.op_cols()
         self.col_off, self.colmap = backend.ints(off), backend.ints(cmap)
 
@@ -281,7 +300,10 @@ class DistOperator:
         C.all_to_all(recv, send[:L.nl * px],
                      [L.lines_of(r) * nkx for r in range(L.P)],
                      [L.nl * (L.kxb[s + 1] - L.kxb[s]) for s in range(L.P)])
-        B.op_yz(recv, self.spec_loc, L.dims, nkx, px, self.py, self.pz)
+        if self.compact:
+            B.op_yz(recv, self.spec_loc, L.dims, nkx, px, self.py, self.pz, compact=True)
+        else:
+            B.op_yz(recv, self.spec_loc, L.dims, nkx, px, self.py, self.pz)
         back = B.empty(L.nl * px)
         C.all_to_all(back, recv,
                      [L.nl * (L.kxb[s + 1] - L.kxb[s]) for s in range(L.P)],
