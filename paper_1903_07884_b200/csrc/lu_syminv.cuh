@@ -397,8 +397,11 @@ __global__ void __launch_bounds__((SYMV_WARPS + 1) * 32, MINB)
 template <int R>
 static int launch_symv2_inv_t(const SymGeom& sg, const double2* G, const int* items, int nblocks, const int* klist,
                               double2* Y, long s_row, long s_k, int q, cudaStream_t s) {
-  static const int slots_env = env_int("VX_SYMV2_SLOTS", 3);
-  static const int minb = env_int("VX_SYMV_MINB", 3);
+  // measured (c1 / c2 / c3 applies, ms): 96 registers + a 2-slot ring (4 CTAs per SM at c1)
+  // 0.667 / 0.760 / 1.239; 128 registers + 3 slots 0.681 / 0.801 / 1.260 -- the extra resident
+  // CTA covers the other CTAs' right-hand-side gathers, a third slot does not pay
+  static const int slots_env = env_int("VX_SYMV2_SLOTS", 2);
+  static const int minb = env_int("VX_SYMV_MINB", 4);
   static const int pfwin = env_int("VX_SYMV_PF", 24) * 64;  // L2 prefetch window, entries
   const int S = slots_env < 2 ? 2 : (slots_env > 12 ? 12 : slots_env);
   const int npad = (sg.dmax + 31) / 32 * 32;
