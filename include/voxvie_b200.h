@@ -238,6 +238,21 @@ int vx_cgs_dots(long n, int nvec, const vx_c128* V, long ldv, const vx_c128* w, 
                 vx_c128* part, void* stream);
 int vx_cgs_update(long n, int nvec, const vx_c128* V, long ldv, const vx_c128* coef, vx_c128* w,
                   vx_c128* out_norm2, vx_c128* part, void* stream);
+/* The same stages with the DGKS decision on the device (the sharded solver's
+ * device-driven step, dist.py): vx_dgks_ctl turns the all-reduced ||w0||^2,
+ * ||w1||^2 into ctl = (||w0||, ||w1||, fired, .) (reference solver.py:69-73);
+ * vx_cgs_dots_cond / vx_cgs_update_cond run (and return zeros otherwise) only
+ * when ctl[2] is set; vx_dgks_finish forms the Hessenberg column h = d (+ c),
+ * h[nvec] = ctl[3] = the final norm; vx_scale_dev is v = w / hn.re with the
+ * scalar on the device (reference solver.py:77). */
+int vx_cgs_dots_cond(long n, int nvec, const vx_c128* V, long ldv, const vx_c128* w, vx_c128* out, vx_c128* part,
+                     const double* ctl, void* stream);
+int vx_cgs_update_cond(long n, int nvec, const vx_c128* V, long ldv, const vx_c128* coef, vx_c128* w,
+                       vx_c128* out_norm2, vx_c128* part, const double* ctl, void* stream);
+int vx_dgks_ctl(const vx_c128* n0sq, const vx_c128* n1sq, double* ctl, void* stream);
+int vx_dgks_finish(int nvec, const vx_c128* d, const vx_c128* c, const vx_c128* n2sq, double* ctl, vx_c128* hcol,
+                   void* stream);
+int vx_scale_dev(long n, const vx_c128* w, vx_c128* out, const vx_c128* hn, void* stream);
 
 /* --------------------------------------------------------------- blocked */
 /* BlockedPrec.apply gather/scatter (circulant.py:558-563, 603-607): box

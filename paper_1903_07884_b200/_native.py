@@ -120,6 +120,11 @@ _SIGS = {
     "vx_prec1_solve": (c_int, [c_int, c_int, P, P, P, c_int, c_int, c_int, P, P, c_long, c_long, P]),
     "vx_cgs_dots": (c_int, [c_long, c_int, P, c_long, P, P, P, P]),
     "vx_cgs_update": (c_int, [c_long, c_int, P, c_long, P, P, P, P, P]),
+    "vx_cgs_dots_cond": (c_int, [c_long, c_int, P, c_long, P, P, P, P, P]),
+    "vx_cgs_update_cond": (c_int, [c_long, c_int, P, c_long, P, P, P, P, P, P]),
+    "vx_dgks_ctl": (c_int, [P, P, P, P]),
+    "vx_dgks_finish": (c_int, [c_int, P, P, P, P, P, P]),
+    "vx_scale_dev": (c_int, [c_long, P, P, P, P]),
     "vx_launch_count": (c_long, []),
     "vx_h2d_staged": (c_int, [P, P, c_size_t, P]),
     "vx_assemble_green": (c_int, [c_int] * 3 + [c_double] * 3 + [c128, P, P]),

@@ -299,6 +299,47 @@ __global__ void __launch_bounds__(AR_THREADS) sum_rows_kernel(int rows, int G, c
   }
 }
 
+// out[i] = sum_b part[i*G + b] if the device flag cond[2] is set, else 0 (the
+// conditional DGKS pass of the sharded step: the value is all-reduced either way)
+__global__ void __launch_bounds__(AR_THREADS) sum_rows_cond_kernel(int rows, int G,
+                                                                   const double2* __restrict__ part,
+                                                                   double2* __restrict__ out,
+                                                                   const double* __restrict__ cond) {
+  __shared__ double2 sh[AR_THREADS / 32];
+  const bool on = cond[2] != 0.0;
+  for (int i = blockIdx.x; i < rows; i += gridDim.x) {
+    double2 v = cmk(0.0, 0.0);
+    if (on)
+      for (int b = threadIdx.x; b < G; b += AR_THREADS) v = cadd(v, part[(long)i * G + b]);
+    v = block_sum(v, sh);
+    if (threadIdx.x == 0) out[i] = v;
+  }
+}
+
+// DGKS decision of the sharded step from the all-reduced squared norms
+// (reference solver.py:69-73): ctl = (||w0||, ||w1||, fired, .)
+__global__ void dgks_ctl_kernel(const double2* __restrict__ n0sq, const double2* __restrict__ n1sq,
+                                double* __restrict__ ctl) {
+  const double n0 = sqrt(n0sq->x), n1 = sqrt(n1sq->x);
+  ctl[0] = n0;
+  ctl[1] = n1;
+  ctl[2] = (n1 < 0.7071 * n0) ? 1.0 : 0.0;
+}
+
+// Hessenberg column of the sharded step: h = d (+ c when the second pass ran),
+// h[nvec] = ctl[3] = the final norm (||w2|| from the all-reduced n2sq if it ran, else ||w1||)
+__global__ void dgks_finish_kernel(int nvec, const double2* __restrict__ d, const double2* __restrict__ c,
+                                   const double2* __restrict__ n2sq, double* __restrict__ ctl,
+                                   double2* __restrict__ hcol) {
+  const bool on = ctl[2] != 0.0;
+  for (int i = threadIdx.x; i < nvec; i += blockDim.x) hcol[i] = on ? cadd(d[i], c[i]) : d[i];
+  if (threadIdx.x == 0) {
+    const double nf = on ? sqrt(n2sq->x) : ctl[1];
+    ctl[3] = nf;
+    hcol[nvec] = cmk(nf, 0.0);
+  }
+}
+
 __global__ void scale_kernel(long n, const double2* __restrict__ w, double2* __restrict__ out,
                              const double2* __restrict__ hn) {
   const double s = hn->x;
@@ -512,3 +553,65 @@ extern "C" int vx_basis_combine_ptrs(long n, int nvec, const void* zptrs, const 
   VX_CHECK_LAUNCH("combine_ptrs_kernel");
   return VX_OK;
 }
+
+// ---- device-driven Arnoldi step of the SHARDED solver (dist.py): the stages of
+// vx_arnoldi_step as separate calls so that the caller can all-reduce every
+// partial result between them on the same stream, with the DGKS decision taken
+// on the device (ctl[2]) -- no host read inside a step.
+extern "C" int vx_cgs_dots_cond(long n, int nvec, const vx_c128* V, long ldv, const vx_c128* w, vx_c128* out,
+                                vx_c128* part, const double* ctl, void* stream) {
+  VX_REQUIRE(n >= 1 && nvec >= 0 && ldv >= n && ctl, "bad cgs_dots_cond arguments");
+  cudaStream_t s = as_stream(stream);
+  const int G = ar_grid(n);
+  double2* pd = reinterpret_cast<double2*>(part);
+  dots_kernel<<<G, AR_THREADS, 0, s>>>(n, nvec, reinterpret_cast<const double2*>(V), ldv,
+                                       reinterpret_cast<const double2*>(w), pd, ctl);
+  sum_rows_cond_kernel<<<nvec + 1, AR_THREADS, 0, s>>>(nvec + 1, G, pd, reinterpret_cast<double2*>(out), ctl);
+  count_launch();
+  VX_CHECK_LAUNCH("cgs_dots_cond");
+  return VX_OK;
+}
+
+extern "C" int vx_cgs_update_cond(long n, int nvec, const vx_c128* V, long ldv, const vx_c128* coef, vx_c128* w,
+                                  vx_c128* out_norm2, vx_c128* part, const double* ctl, void* stream) {
+  VX_REQUIRE(n >= 1 && nvec >= 0 && ldv >= n && ctl, "bad cgs_update_cond arguments");
+  cudaStream_t s = as_stream(stream);
+  const int G = ar_grid(n);
+  double2* pd = reinterpret_cast<double2*>(part);
+  update_kernel<<<G, AR_THREADS, 0, s>>>(n, nvec, reinterpret_cast<const double2*>(V), ldv,
+                                         reinterpret_cast<const double2*>(coef), reinterpret_cast<double2*>(w),
+                                         pd, ctl);
+  sum_rows_cond_kernel<<<1, AR_THREADS, 0, s>>>(1, G, pd, reinterpret_cast<double2*>(out_norm2), ctl);
+  count_launch();
+  VX_CHECK_LAUNCH("cgs_update_cond");
+  return VX_OK;
+}
+
+extern "C" int vx_dgks_ctl(const vx_c128* n0sq, const vx_c128* n1sq, double* ctl, void* stream) {
+  VX_REQUIRE(n0sq && n1sq && ctl, "bad dgks_ctl arguments");
+  dgks_ctl_kernel<<<1, 1, 0, as_stream(stream)>>>(reinterpret_cast<const double2*>(n0sq),
+                                                  reinterpret_cast<const double2*>(n1sq), ctl);
+  VX_CHECK_LAUNCH("dgks_ctl_kernel");
+  return VX_OK;
+}
+
+extern "C" int vx_dgks_finish(int nvec, const vx_c128* d, const vx_c128* c, const vx_c128* n2sq, double* ctl,
+                              vx_c128* hcol, void* stream) {
+  VX_REQUIRE(nvec >= 0 && d && c && n2sq && ctl && hcol, "bad dgks_finish arguments");
+  dgks_finish_kernel<<<1, 128, 0, as_stream(stream)>>>(nvec, reinterpret_cast<const double2*>(d),
+                                                       reinterpret_cast<const double2*>(c),
+                                                       reinterpret_cast<const double2*>(n2sq), ctl,
+                                                       reinterpret_cast<double2*>(hcol));
+  VX_CHECK_LAUNCH("dgks_finish_kernel");
+  return VX_OK;
+}
+
+extern "C" int vx_scale_dev(long n, const vx_c128* w, vx_c128* out, const vx_c128* hn, void* stream) {
+  VX_REQUIRE(n >= 1 && w && out && hn, "bad scale arguments");
+  scale_kernel<<<stream_grid(n), 256, 0, as_stream(stream)>>>(n, reinterpret_cast<const double2*>(w),
+                                                             reinterpret_cast<double2*>(out),
+                                                             reinterpret_cast<const double2*>(hn));
+  VX_CHECK_LAUNCH("scale_kernel");
+  return VX_OK;
+}
+

@@ -38,7 +38,7 @@ import numpy as np
 from . import _native as nv
 from .circulant import _check_cap, _coerce_mtilde, _coerce_mz, _select_kept
 from .errors import BreakdownError, PreconditionerBuildError
-from .solver import GivensQR, SolveReport
+from .solver import GivensQR, SolveReport, _speculate
 
 
 def split_even(n: int, P: int) -> list:
@@ -252,6 +252,51 @@ class CudaBackend:
 
     def part(self, n, nvec):
         return self.empty(int(nv.query("vx_arnoldi_part_elems", n, nvec + 2)))
+
+    # ---- device-driven Arnoldi step: no host read between the operator and the next operator
+    device_driven = True
+
+    def step_workspace(self, mmax):
+        """Pinned result buffers (two, alternating by step parity) and events of a solve."""
+        t = self.t
+        return {"h": [t.empty(mmax + 2, dtype=t.complex128).pin_memory() for _ in range(2)],
+                "ctl": [t.empty(4, dtype=t.float64).pin_memory() for _ in range(2)],
+                "ev": [t.cuda.Event() for _ in range(2)]}
+
+    def arnoldi_step(self, C, V, j, w, part, ws):
+        """Classical Gram-Schmidt of w against V[0..j] with the reference's DGKS second pass
+        (solver.py:62-77) on line-sharded vectors: local partial sums, all-reduced on the stream,
+        the decision taken on the device; V[j+1] = w / ||w|| is formed on the device.  Returns a
+        handle whose result() waits for this step only and gives (h[0..j+1], ||w0||, fired)."""
+        t = self.t
+        n, nvec, ldv = w.numel(), j + 1, V.shape[1]
+        st = nv.stream_ptr()
+        d = self.empty(nvec + 1)
+        nv.call("vx_cgs_dots", n, nvec, V.data_ptr(), ldv, w.data_ptr(), d.data_ptr(), part.data_ptr(), st)
+        C.all_reduce(d)
+        n1 = self.empty(1)
+        nv.call("vx_cgs_update", n, nvec, V.data_ptr(), ldv, d.data_ptr(), w.data_ptr(), n1.data_ptr(),
+                part.data_ptr(), st)
+        C.all_reduce(n1)
+        ctl = t.empty(4, dtype=t.float64, device="cuda")
+        nv.call("vx_dgks_ctl", d[nvec:].data_ptr(), n1.data_ptr(), ctl.data_ptr(), st)
+        c = self.empty(nvec + 1)
+        nv.call("vx_cgs_dots_cond", n, nvec, V.data_ptr(), ldv, w.data_ptr(), c.data_ptr(), part.data_ptr(),
+                ctl.data_ptr(), st)
+        C.all_reduce(c)
+        n2 = self.empty(1)
+        nv.call("vx_cgs_update_cond", n, nvec, V.data_ptr(), ldv, c.data_ptr(), w.data_ptr(), n2.data_ptr(),
+                part.data_ptr(), ctl.data_ptr(), st)
+        C.all_reduce(n2)
+        hcol = self.empty(nvec + 1)
+        nv.call("vx_dgks_finish", nvec, d.data_ptr(), c.data_ptr(), n2.data_ptr(), ctl.data_ptr(),
+                hcol.data_ptr(), st)
+        nv.call("vx_scale_dev", n, w.data_ptr(), V[j + 1].data_ptr(), hcol[nvec:].data_ptr(), st)
+        b = j % 2
+        ws["h"][b][: nvec + 1].copy_(hcol, non_blocking=True)
+        ws["ctl"][b].copy_(ctl, non_blocking=True)
+        ws["ev"][b].record()
+        return _DevStep(ws, b, nvec, (d, n1, c, n2, ctl, hcol, w))
 
     def axpby(self, a, x, b, y, out=None):
         out = self.empty(x.numel()) if out is None else out
@@ -649,6 +694,47 @@ def _norm(B, C, x, part):
     return float(np.sqrt(B.to_host(d)[0].real))
 
 
+class _DevStep:
+    """A device-driven Arnoldi step in flight (CudaBackend.arnoldi_step)."""
+
+    def __init__(self, ws, b, nvec, keep):
+        self.ws, self.b, self.nvec = ws, b, nvec
+        self.keep = keep   # the step's device buffers stay alive until it has been read
+
+    def result(self):
+        ws, b = self.ws, self.b
+        ws["ev"][b].synchronize()
+        h = ws["h"][b][: self.nvec + 1].numpy().copy()
+        cv = ws["ctl"][b].numpy()
+        self.keep = None
+        return h, float(cv[0]), bool(cv[2] != 0.0)
+
+
+class _HostStep:
+    """Host-driven Arnoldi step (backends without a device-side DGKS decision: the CPU test
+    backend): CGS against V[0..j], the reference's DGKS second pass, v_{j+1} = w / ||w||; every
+    partial result is all-reduced and read on the host before the next stage."""
+
+    def __init__(self, B, C, V, j, w, part):
+        d = C.all_reduce(B.cgs_dots(V, j + 1, w, part))
+        dh = B.to_host(d)
+        h = np.empty(j + 2, np.complex128)
+        h[: j + 1] = dh[: j + 1]
+        n0 = float(np.sqrt(dh[j + 1].real))
+        n1 = float(np.sqrt(B.to_host(C.all_reduce(B.cgs_update(V, j + 1, d, w, part)))[0].real))
+        fired = n1 < 0.7071 * n0   # DGKS second pass (reference solver.py:69-73)
+        if fired:
+            c = C.all_reduce(B.cgs_dots(V, j + 1, w, part))
+            h[: j + 1] += B.to_host(c)[: j + 1]
+            n1 = float(np.sqrt(B.to_host(C.all_reduce(B.cgs_update(V, j + 1, c, w, part)))[0].real))
+        h[j + 1] = n1
+        B.axpby(1.0 / n1 if n1 > 0 else 0.0, w, 0.0, None, out=V[j + 1])
+        self._res = (h, n0, bool(fired))
+
+    def result(self):
+        return self._res
+
+
 class _Basis:
     """Krylov basis rows on the backend, grown geometrically (as the
     single-GPU solver._Krylov): a solve that converges in a few iterations
@@ -704,6 +790,9 @@ def _gmres_sharded(apply_a, b_loc, backend, comm: _Comm, *, apply_pinv=None, tol
     residuals = [1.0]
     total = 0
     converged = False
+    reorth = 0
+    ws = B.step_workspace(mmax) if getattr(B, "device_driven", False) and \
+        os.environ.get("VX_SHARD_DEVICE_STEP", "1") != "0" else None
     while total < maxit and not converged:
         r0 = B.axpby(1.0, b_loc, -1.0, apply_a(x)) if total else B.axpby(1.0, b_loc, 0.0, None)
         beta = _norm(B, C, r0, part)
@@ -716,22 +805,32 @@ def _gmres_sharded(apply_a, b_loc, backend, comm: _Comm, *, apply_pinv=None, tol
         qr = GivensQR(beta)
         j = 0
         lucky = False
+        pending = {}
+
+        def launch(jj):
+            # step jj: operator, orthogonalisation and v_{jj+1}, all enqueued (device-driven
+            # backends) or computed (host-driven ones) without looking at earlier results
+            Vc = basis.ensure(jj + 2)
+            w = op(Vc[jj])
+            if ws is not None:
+                pending[jj] = B.arnoldi_step(C, Vc, jj, w, part, ws)
+            else:
+                pending[jj] = _HostStep(B, C, Vc, jj, B.axpby(1.0, w, 0.0, None), part)
+
+        launched = 0
         while j < m:
-            w = B.axpby(1.0, op(V[j]), 0.0, None)
-            d = C.all_reduce(B.cgs_dots(V, j + 1, w, part))
-            dh = B.to_host(d)
-            h = np.empty(j + 2, np.complex128)
-            h[: j + 1] = dh[: j + 1]
-            n0 = float(np.sqrt(dh[j + 1].real))
-            n1 = float(np.sqrt(B.to_host(C.all_reduce(B.cgs_update(V, j + 1, d, w, part)))[0].real))
-            if n1 < 0.7071 * n0:  # DGKS second pass (reference solver.py:69-73)
-                c = C.all_reduce(B.cgs_dots(V, j + 1, w, part))
-                h[: j + 1] += B.to_host(c)[: j + 1]
-                n1 = float(np.sqrt(B.to_host(C.all_reduce(B.cgs_update(V, j + 1, c, w, part)))[0].real))
-            h[j + 1] = n1
-            lucky = n1 <= 1e-14 * max(n0, 1e-300)
-            V = basis.ensure(j + 2)
-            B.axpby(1.0 / n1 if n1 > 0 else 0.0, w, 0.0, None, out=V[j + 1])
+            if launched <= j:
+                launch(j)
+                launched = j + 1
+            # one step of lookahead (as solver._gmres_cycle): the next step is enqueued before this
+            # one's Hessenberg column is read, unless the residual trend says this one converges
+            if ws is not None and launched == j + 1 and j + 1 < m and _speculate(residuals, tol):
+                launch(j + 1)
+                launched = j + 2
+            h, n0, fired = pending.pop(j).result()
+            reorth += int(fired)
+            lucky = h[j + 1].real <= 1e-14 * max(n0, 1e-300)
+            V = basis.V
             qr.add_column(h, j, residuals, tol)
             j += 1
             est = abs(qr.g[j]) / bnorm
@@ -745,5 +844,7 @@ def _gmres_sharded(apply_a, b_loc, backend, comm: _Comm, *, apply_pinv=None, tol
         u = B.combine(V, j, qr.solve(j))
         x = B.axpby(1.0, x, 1.0, u if apply_pinv is None else apply_pinv(u))
     true_res = _norm(B, C, B.axpby(1.0, b_loc, -1.0, apply_a(x)), part) / bnorm
-    return x, SolveReport(iterations=int(total), residuals=residuals, converged=bool(converged),
-                          solve_seconds=time.perf_counter() - t0, true_residual=float(true_res))
+    report = SolveReport(iterations=int(total), residuals=residuals, converged=bool(converged),
+                         solve_seconds=time.perf_counter() - t0, true_residual=float(true_res))
+    report.reorth_passes = int(reorth)
+    return x, report
