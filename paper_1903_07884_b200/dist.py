@@ -311,6 +311,16 @@ class CudaBackend:
                 nv.stream_ptr())
         return u
 
+    def combine_list(self, zs, y):
+        """u = sum_i y_i z_i over separately stored vectors (the kept z_j = P^-1 v_j)."""
+        t = self.t
+        n = zs[0].numel()
+        u = self.empty(n)
+        yd = nv.device_c128(np.asarray(y, np.complex128))
+        ptrs = t.tensor([z.data_ptr() for z in zs], dtype=t.int64).cuda()
+        nv.call("vx_basis_combine_ptrs", n, len(zs), ptrs.data_ptr(), yd.data_ptr(), u.data_ptr(), nv.stream_ptr())
+        return u
+
     def to_host(self, t):
         return t.cpu().numpy()
 
@@ -791,6 +801,7 @@ def _gmres_sharded(apply_a, b_loc, backend, comm: _Comm, *, apply_pinv=None, tol
     total = 0
     converged = False
     reorth = 0
+    keep_z = apply_pinv is not None and hasattr(B, "combine_list") and os.environ.get("VX_KEEP_Z", "1") != "0"
     ws = B.step_workspace(mmax) if getattr(B, "device_driven", False) and \
         os.environ.get("VX_SHARD_DEVICE_STEP", "1") != "0" else None
     while total < maxit and not converged:
@@ -806,12 +817,23 @@ def _gmres_sharded(apply_a, b_loc, backend, comm: _Comm, *, apply_pinv=None, tol
         j = 0
         lucky = False
         pending = {}
+        zl = []
 
         def launch(jj):
             # step jj: operator, orthogonalisation and v_{jj+1}, all enqueued (device-driven
             # backends) or computed (host-driven ones) without looking at earlier results
             Vc = basis.ensure(jj + 2)
-            w = op(Vc[jj])
+            if keep_z:
+                # z_j = P^-1 v_j is needed for the operator anyway: kept, so the cycle's
+                # correction is u = Z y with no extra preconditioner apply (as solver._gmres_cycle)
+                z = apply_pinv(Vc[jj])
+                if any(z.data_ptr() == q.data_ptr() for q in zl[:jj]):
+                    z = z.clone()   # the callable reuses its output buffer
+                del zl[jj:]
+                zl.append(z)
+                w = apply_a(z)
+            else:
+                w = op(Vc[jj])
             if ws is not None:
                 pending[jj] = B.arnoldi_step(C, Vc, jj, w, part, ws)
             else:
@@ -841,8 +863,11 @@ def _gmres_sharded(apply_a, b_loc, backend, comm: _Comm, *, apply_pinv=None, tol
                     raise BreakdownError(f"Arnoldi breakdown at iteration {len(residuals) - 1}")
                 break
         total += j
-        u = B.combine(V, j, qr.solve(j))
-        x = B.axpby(1.0, x, 1.0, u if apply_pinv is None else apply_pinv(u))
+        if keep_z:
+            x = B.axpby(1.0, x, 1.0, B.combine_list(zl[:j], qr.solve(j)))
+        else:
+            u = B.combine(V, j, qr.solve(j))
+            x = B.axpby(1.0, x, 1.0, u if apply_pinv is None else apply_pinv(u))
     true_res = _norm(B, C, B.axpby(1.0, b_loc, -1.0, apply_a(x)), part) / bnorm
     report = SolveReport(iterations=int(total), residuals=residuals, converged=bool(converged),
                          solve_seconds=time.perf_counter() - t0, true_residual=float(true_res))

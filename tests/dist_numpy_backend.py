@@ -135,5 +135,8 @@ class NumpyBackend:
     def combine(self, V, nvec, y):
         return torch.from_numpy(np.asarray(y) @ V.numpy()[:nvec])
 
+    def combine_list(self, zs, y):
+        return torch.from_numpy(sum(complex(c) * z.numpy() for c, z in zip(np.asarray(y), zs)))
+
     def to_host(self, t):
         return t.numpy()
