@@ -1,6 +1,6 @@
 """One-off full-size check of BASELINE c4 (2-level, restart 100): the GPU
 residual history of the first restart cycle against the CPU oracle's on the
-same arrays (~8 min of CPU).  usage: python tools/check_c4.py [maxit]"""
+same arrays (~8 min of CPU).  usage: python tests/manual_check_c4.py [maxit]"""
 import sys
 import time
 from pathlib import Path
