@@ -436,8 +436,11 @@ def _gmres(apply_a, b, *, apply_pinv=None, tol: float = 1e-4, maxit: int = 2000,
     total = 0
     converged = False
     while total < maxit and not converged:
-        r0 = K.axpby(1.0, bd, -1.0, A(x)) if total else K.axpby(1.0, bd, 0.0, None)
-        beta = K.norm(r0)
+        if total:
+            r0 = K.axpby(1.0, bd, -1.0, A(x))
+            beta = K.norm(r0)
+        else:
+            r0, beta = bd, bnorm   # x0 = 0: the first residual is b itself (read only by the cycle)
         if beta / bnorm <= tol:
             converged = True
             break
