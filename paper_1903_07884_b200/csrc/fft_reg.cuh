@@ -101,4 +101,80 @@ __global__ void __launch_bounds__(128)
     if (e < n_out) dst[e * out_es] = cscale(v[e], scale);
 }
 
+// Two-pass column transform for lengths L = R1 * R2 beyond the one-thread
+// register kernel (c3's py = 112, c4's 800): CW adjacent columns per CTA
+// (consecutive x: every global access is a coalesced run of CW entries), R2
+// threads per column run the R1-point sub-transforms of the stride-R2
+// subsequences in registers (zero padding in the load), multiply by the
+// twiddles w_L^{b k1} and exchange through shared memory; R1 threads per
+// column then run the R2-point transforms and store the (cropped) outputs in
+// natural order: X[k1 + R1 k2] = sum_b w_R2^{b k2} w_L^{b k1} DFT_R1(x[R2 a + b])[k1].
+template <int R1, int R2>
+struct Cols2Cfg {
+  static constexpr int L = R1 * R2;
+  static constexpr int TP = R1 > R2 ? R1 : R2;
+  // columns per CTA: 256 threads, at least 8 columns (128-byte runs), shared memory <= ~100 KB
+  static constexpr int CW = (256 / TP) < 8 ? 8 : ((256 / TP) > 16 ? 16 : (256 / TP));
+  static constexpr int THREADS = CW * TP;
+  static constexpr size_t SMEM = (size_t)CW * L * sizeof(double2);
+};
+
+template <int R1, int R2, bool INV>
+__global__ void __launch_bounds__(Cols2Cfg<R1, R2>::THREADS)
+    cols2_kernel(const double2* __restrict__ in, long in_os, long in_es, int n_in, double2* __restrict__ out,
+                 long out_os, long out_es, int n_out, long ncols, FastDiv fd_inner, int n_inner, double scale,
+                 const double2* __restrict__ tw) {
+  using C = Cols2Cfg<R1, R2>;
+  constexpr int L = C::L, CW = C::CW;
+  extern __shared__ double2 c2sm[];  // entry (k1, b) of column ci at ((k1 * R2 + b) * CW + ci)
+  const int ci = threadIdx.x % CW, t = threadIdx.x / CW;
+  const long c = (long)blockIdx.x * CW + ci;
+  const bool colok = c < ncols;
+  const long cc = colok ? c : 0;
+  const int o = (int)fd_inner.div((unsigned)cc), i = (int)(cc - (long)o * n_inner);
+  if (t < R2) {
+    const double2* src = in + (long)o * in_os + i;
+    double2 v[R1];
+#pragma unroll
+    for (int a = 0; a < R1; ++a) {
+      const int e = R2 * a + t;
+      v[a] = (colok && e < n_in) ? __ldg(src + (long)e * in_es) : cmk(0.0, 0.0);
+    }
+    reg_fft<R1, INV>(v);
+#pragma unroll
+    for (int k1 = 0; k1 < R1; ++k1) {
+      double2 x = v[k1];
+      if (t != 0 && k1 != 0) {
+        double2 w = __ldg(tw + (t * k1) % L);
+        if (INV) w.y = -w.y;
+        x = cmul(x, w);
+      }
+      c2sm[(k1 * R2 + t) * CW + ci] = x;
+    }
+  }
+  __syncthreads();
+  if (t < R1) {
+    double2 u[R2];
+#pragma unroll
+    for (int b = 0; b < R2; ++b) u[b] = c2sm[(t * R2 + b) * CW + ci];
+    reg_fft<R2, INV>(u);
+    double2* dst = out + (long)o * out_os + i;
+#pragma unroll
+    for (int k2 = 0; k2 < R2; ++k2) {
+      const int e = t + R1 * k2;
+      if (colok && e < n_out) dst[(long)e * out_es] = cscale(u[k2], scale);
+    }
+  }
+}
+
+// (R1, R2) of the supported two-pass lengths
+#define VX_COLS2_PAIRS(X) X(8, 8) X(12, 6) X(16, 5) X(16, 6) X(20, 5) X(16, 7) X(24, 5) X(16, 8) X(32, 25)
+
+__host__ inline bool cols2_supported(int n) {
+#define VX_C2_CASE(A, B) if (n == (A) * (B)) return true;
+  VX_COLS2_PAIRS(VX_C2_CASE)
+#undef VX_C2_CASE
+  return false;
+}
+
 }  // namespace vx

@@ -554,6 +554,29 @@ static int launch_reg_cols(int L, const double2* in, long in_os, long in_es, int
   return VX_OK;
 }
 
+template <bool INV>
+static int launch_cols2(const FftPlan& f, const double2* in, long in_os, long in_es, int n_in, double2* out,
+                        long out_os, long out_es, int n_out, long ncols, int n_inner, double scale,
+                        cudaStream_t s) {
+  if (ncols <= 0) return VX_OK;
+  const FastDiv fd((unsigned)n_inner);
+#define VX_C2_LAUNCH(A, B)                                                                                   \
+  if (f.L == (A) * (B)) {                                                                                    \
+    using C = Cols2Cfg<A, B>;                                                                                \
+    auto k = cols2_kernel<A, B, INV>;                                                                        \
+    if (C::SMEM > 48 * 1024)                                                                                 \
+      VX_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));          \
+    k<<<(unsigned)div_up(ncols, C::CW), C::THREADS, C::SMEM, s>>>(in, in_os, in_es, n_in, out, out_os, out_es, \
+                                                                  n_out, ncols, fd, n_inner, scale, f.tw);   \
+    VX_CHECK_LAUNCH("cols2_kernel");                                                                         \
+    return VX_OK;                                                                                            \
+  }
+  VX_COLS2_PAIRS(VX_C2_LAUNCH)
+#undef VX_C2_LAUNCH
+  set_error("no two-pass column FFT for length %d", f.L);
+  return VX_EINVAL;
+}
+
 static int launch_zmul_reg(int PZ, double2* B, const SpecView& sv, int nz, long cols, double scale,
                            cudaStream_t s) {
   static const int shfl = env_int("VX_ZMUL_SHFL", 1);
@@ -841,8 +864,13 @@ static int op_yz(const FftPlan& fy, const FftPlan& fz, int ny, int nz, int nkx, 
   const long cols = (long)py * nkx;
   const bool reg_y = reg_fft_enabled() && reg_fft_supported(py);
   const bool reg_z = reg_fft_enabled() && reg_fft_supported(pz) && pz <= REG_ZMUL_MAX;
+  static const int use_cols2 = env_int("VX_COLS2", 1);
+  const bool two_y = !reg_y && use_cols2 && reg_fft_enabled() && !fy.bluestein && fy.L == py && cols2_supported(py);
   if (reg_y) {
     if ((st = launch_reg_cols<false>(py, A, (long)ny * nkx, nkx, ny, B, cols, nkx, py, 3L * nz * nkx, nkx, 1.0, s)))
+      return st;
+  } else if (two_y) {
+    if ((st = launch_cols2<false>(fy, A, (long)ny * nkx, nkx, ny, B, cols, nkx, py, 3L * nz * nkx, nkx, 1.0, s)))
       return st;
   } else {
     LoadStrided ld{A, {(long)ny * nkx, 1, nkx, nkx}};
@@ -867,6 +895,9 @@ static int op_yz(const FftPlan& fy, const FftPlan& fz, int ny, int nz, int nkx, 
   }
   if (reg_y) {
     if ((st = launch_reg_cols<true>(py, B, cols, nkx, py, A, (long)ny * nkx, nkx, ny, 3L * nz * nkx, nkx, 1.0, s)))
+      return st;
+  } else if (two_y) {
+    if ((st = launch_cols2<true>(fy, B, cols, nkx, py, A, (long)ny * nkx, nkx, ny, 3L * nz * nkx, nkx, 1.0, s)))
       return st;
   } else {
     LoadStrided ld{B, {cols, 1, nkx, nkx}};

@@ -236,3 +236,29 @@ def test_operator_register_fft_lengths(rng, ny):
         nv.call("vx_op_reg_fft", 1)
     assert relerr(y_reg, ref) < 1e-12
     assert relerr(y_reg, y_smem) < 1e-13
+
+
+@pytest.mark.parametrize("ny,py", [(32, 64), (36, 72), (40, 80), (48, 96), (50, 100), (56, 112), (60, 120), (64, 128),
+                                   (400, 800)])
+def test_operator_two_pass_column_lengths(rng, monkeypatch, ny, py):
+    """The two-pass register column transforms (cols2_kernel: padded y of 64 .. 128 and c4's 800)
+    against the oracle and against the generic shared-memory engine (VX_COLS2=0 is read once per
+    process, so the comparison run uses vx_op_reg_fft(0), which disables both register paths)."""
+    from paper_1903_07884_b200 import _native as nv
+    from paper_1903_07884_b200 import workloads
+    from paper_1903_07884_b200.operator import apply_system, plan_operator
+
+    W = workloads.small(5, ny, 2, delta=0.03e-6)
+    plan = plan_operator(W.kernel())
+    assert plan.padded_shape[1] == py
+    x = random_field(rng, W.grid.n_unknowns)
+    spec = O.plan_spectra(W.kernel().tensors, W.grid.dims)
+    ref = O.apply_system(spec, W.grid.dims, W.m, x)
+    y2 = apply_system(plan, W.m, x)
+    nv.call("vx_op_reg_fft", 0)
+    try:
+        y_smem = apply_system(plan, W.m, x)
+    finally:
+        nv.call("vx_op_reg_fft", 1)
+    assert relerr(y2, ref) < 1e-12
+    assert relerr(y2, y_smem) < 1e-13
