@@ -2352,7 +2352,13 @@ extern "C" int vx_prec2_apply(int nx, int ny, int nz, int nrhs, const vx_c128* f
     StoreStrided sv{S, {pitch, 1, nrhs, nrhs}, 1.0};
     if ((st = launch_fft_auto(px, ld, sv, q3 * nrhs, nx, nx, false, nrhs == 1, s))) return st;
   }
-  {
+  // y-DFT of the (c, z) planes' columns, in place: two-pass register transforms when ny has one
+  static const int use_cols2 = env_int("VX_COLS2", 1);
+  const bool two_y = use_cols2 && !py.bluestein && py.L == ny && cols2_supported(ny);
+  if (two_y) {
+    if ((st = launch_cols2<false>(py, S, plane, pitch, ny, S, plane, pitch, ny, 3L * nz * pitch, (int)pitch, 1.0, s)))
+      return st;
+  } else {
     LoadStrided ld{S, {plane, 1, pitch, (int)pitch}};
     StoreStrided sv{S, {plane, 1, pitch, (int)pitch}, 1.0};
     if ((st = launch_fft_auto(py, ld, sv, 3 * nz * (int)pitch, ny, ny, false, false, s))) return st;
@@ -2362,7 +2368,10 @@ extern "C" int vx_prec2_apply(int nx, int ny, int nz, int nrhs, const vx_c128* f
   if (!items) n_items = nx * ny;
   if ((st = solve_items(g, F, perm, items, n_items, n_items, klist, nrhs, S, plane, nrhs, s, -1, direct_r)))
     return st;
-  {
+  if (two_y) {
+    if ((st = launch_cols2<true>(py, S, plane, pitch, ny, S, plane, pitch, ny, 3L * nz * pitch, (int)pitch, 1.0, s)))
+      return st;
+  } else {
     LoadStrided ld{S, {plane, 1, pitch, (int)pitch}};
     StoreStrided sv{S, {plane, 1, pitch, (int)pitch}, 1.0};
     if ((st = launch_fft_auto(py, ld, sv, 3 * nz * (int)pitch, ny, ny, true, false, s))) return st;

@@ -168,7 +168,8 @@ __global__ void __launch_bounds__(Cols2Cfg<R1, R2>::THREADS)
 }
 
 // (R1, R2) of the supported two-pass lengths
-#define VX_COLS2_PAIRS(X) X(8, 8) X(12, 6) X(16, 5) X(16, 6) X(20, 5) X(16, 7) X(24, 5) X(16, 8) X(32, 25)
+#define VX_COLS2_PAIRS(X) \
+  X(8, 8) X(12, 6) X(16, 5) X(16, 6) X(20, 5) X(16, 7) X(24, 5) X(16, 8) X(20, 20) X(32, 25)
 
 __host__ inline bool cols2_supported(int n) {
 #define VX_C2_CASE(A, B) if (n == (A) * (B)) return true;
@@ -176,5 +177,30 @@ __host__ inline bool cols2_supported(int n) {
 #undef VX_C2_CASE
   return false;
 }
+
+// launch the two-pass column transform of length f.L (f.tw: the plan's twiddle table)
+template <bool INV>
+inline int launch_cols2(const FftPlan& f, const double2* in, long in_os, long in_es, int n_in, double2* out,
+                        long out_os, long out_es, int n_out, long ncols, int n_inner, double scale,
+                        cudaStream_t s) {
+  if (ncols <= 0) return VX_OK;
+  const FastDiv fd((unsigned)n_inner);
+#define VX_C2_LAUNCH(A, B)                                                                                   \
+  if (f.L == (A) * (B)) {                                                                                    \
+    using C = Cols2Cfg<A, B>;                                                                                \
+    auto k = cols2_kernel<A, B, INV>;                                                                        \
+    if (C::SMEM > 48 * 1024)                                                                                 \
+      VX_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));          \
+    k<<<(unsigned)div_up(ncols, C::CW), C::THREADS, C::SMEM, s>>>(in, in_os, in_es, n_in, out, out_os, out_es, \
+                                                                  n_out, ncols, fd, n_inner, scale, f.tw);   \
+    VX_CHECK_LAUNCH("cols2_kernel");                                                                         \
+    return VX_OK;                                                                                            \
+  }
+  VX_COLS2_PAIRS(VX_C2_LAUNCH)
+#undef VX_C2_LAUNCH
+  set_error("no two-pass column FFT for length %d", f.L);
+  return VX_EINVAL;
+}
+
 
 }  // namespace vx

@@ -155,6 +155,16 @@ extern "C" int vx_fft_lines(int n, int n_lines, int n_inner, const vx_c128* in, 
   LoadStrided ld{reinterpret_cast<const double2*>(in), {in_os, in_is, in_es, n_inner}};
   StoreStrided sv{reinterpret_cast<double2*>(out), {out_os, out_is, out_es, n_inner}, scale};
   const bool contig = (in_es == 1 && out_es == 1);
+  // columns (consecutive lines are adjacent in memory) of a two-pass length: register transforms
+  static const int use_cols2 = env_int("VX_COLS2", 1);
+  if (use_cols2 && !contig && in_is == 1 && out_is == 1 && !p.bluestein && p.L == n && cols2_supported(n)) {
+    const double2* ip = reinterpret_cast<const double2*>(in);
+    double2* op = reinterpret_cast<double2*>(out);
+    return inverse ? launch_cols2<true>(p, ip, in_os, in_es, n_in, op, out_os, out_es, n_out, n_lines, n_inner,
+                                        scale, as_stream(stream))
+                   : launch_cols2<false>(p, ip, in_os, in_es, n_in, op, out_os, out_es, n_out, n_lines, n_inner,
+                                         scale, as_stream(stream));
+  }
   return launch_fft_auto(p, ld, sv, n_lines, n_in, n_out, inverse != 0, contig, as_stream(stream));
 }
 
@@ -552,29 +562,6 @@ static int launch_reg_cols(int L, const double2* in, long in_os, long in_es, int
   }
   VX_CHECK_LAUNCH("reg_cols_kernel");
   return VX_OK;
-}
-
-template <bool INV>
-static int launch_cols2(const FftPlan& f, const double2* in, long in_os, long in_es, int n_in, double2* out,
-                        long out_os, long out_es, int n_out, long ncols, int n_inner, double scale,
-                        cudaStream_t s) {
-  if (ncols <= 0) return VX_OK;
-  const FastDiv fd((unsigned)n_inner);
-#define VX_C2_LAUNCH(A, B)                                                                                   \
-  if (f.L == (A) * (B)) {                                                                                    \
-    using C = Cols2Cfg<A, B>;                                                                                \
-    auto k = cols2_kernel<A, B, INV>;                                                                        \
-    if (C::SMEM > 48 * 1024)                                                                                 \
-      VX_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));          \
-    k<<<(unsigned)div_up(ncols, C::CW), C::THREADS, C::SMEM, s>>>(in, in_os, in_es, n_in, out, out_os, out_es, \
-                                                                  n_out, ncols, fd, n_inner, scale, f.tw);   \
-    VX_CHECK_LAUNCH("cols2_kernel");                                                                         \
-    return VX_OK;                                                                                            \
-  }
-  VX_COLS2_PAIRS(VX_C2_LAUNCH)
-#undef VX_C2_LAUNCH
-  set_error("no two-pass column FFT for length %d", f.L);
-  return VX_EINVAL;
 }
 
 static int launch_zmul_reg(int PZ, double2* B, const SpecView& sv, int nz, long cols, double scale,
