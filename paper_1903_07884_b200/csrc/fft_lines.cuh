@@ -67,9 +67,12 @@ struct StoreSystem {
     const long i = b + e;
     v = cscale(v, scale);
     if (m) {
-      // a line never straddles a component (nvox is a multiple of pitch), so
-      // the modulo depends on the line only (hoisted out of the element loop)
-      const double2 mv = __ldg(m + ((moff + b) % nvox) + e);
+      // a line never straddles a component (nvox is a multiple of pitch) and the global index is
+      // below 3 nvox (three field components): the voxel index without a 64-bit modulo per element
+      long gi = moff + b;
+      if (gi >= 2 * nvox) gi -= 2 * nvox;
+      else if (gi >= nvox) gi -= nvox;
+      const double2 mv = __ldg(m + gi + e);
       const double2 xv = __ldg(x + i);
       v = csub(xv, cmul(mv, v));
     }
