@@ -312,6 +312,12 @@ constexpr int ZS_COLS = 10;
 #define ZMUL_MINB_BIG 2
 #endif
 
+// v or -v: XOR of the sign bits (m = 0 or 0x80000000)
+__device__ __forceinline__ double2 sign_flip(double2 v, unsigned m) {
+  return cmk(__hiloint2double(__double2hiint(v.x) ^ (int)m, __double2loint(v.x)),
+             __hiloint2double(__double2hiint(v.y) ^ (int)m, __double2loint(v.y)));
+}
+
 __device__ __forceinline__ double2 shfl_c(double2 v, int src) {
   return cmk(__shfl_sync(0xffffffffu, v.x, src), __shfl_sync(0xffffffffu, v.y, src));
 }
@@ -363,14 +369,15 @@ __global__ void __launch_bounds__(256, (PZ <= 16 ? 3 : ZMUL_MINB_BIG))
     // compact spectra: S(PZ - kz) = +-S(kz) (sign by the z parity of the
     // component), so kz and its mirror share ONE load of the three spectra --
     // the loads, not the arithmetic, fill the L1 data pipe of this kernel
-    const bool z0 = odd_z(p0), z1 = odd_z(p1), z2 = odd_z(p2);
+    // signs as XOR masks on the high words (integer pipe) instead of FP64 negations / selects
+    const unsigned m0 = n0 ? 0x80000000u : 0u, m1 = n1 ? 0x80000000u : 0u, m2 = n2 ? 0x80000000u : 0u;
+    const unsigned zm0 = odd_z(p0) ? 0x80000000u : 0u, zm1 = odd_z(p1) ? 0x80000000u : 0u,
+                   zm2 = odd_z(p2) ? 0x80000000u : 0u;
 #pragma unroll
     for (int kz = 0; kz <= PZ / 2; ++kz) {
       const long ko = (long)kz * kstr;
       double2 s0 = __ldg(S0 + ko), s1 = __ldg(S1 + ko), s2 = __ldg(S2 + ko);
-      if (n0) s0 = cmk(-s0.x, -s0.y);
-      if (n1) s1 = cmk(-s1.x, -s1.y);
-      if (n2) s2 = cmk(-s2.x, -s2.y);
+      s0 = sign_flip(s0, m0), s1 = sign_flip(s1, m1), s2 = sign_flip(s2, m2);
       {
         const double2 x0 = shfl_c(v[kz], j), x1 = shfl_c(v[kz], ZS_COLS + j), x2 = shfl_c(v[kz], 2 * ZS_COLS + j);
         double2 acc = cmul(s0, x0);
@@ -380,9 +387,7 @@ __global__ void __launch_bounds__(256, (PZ <= 16 ? 3 : ZMUL_MINB_BIG))
       }
       const int km = PZ - kz;
       if (kz > 0 && km > kz && km < PZ) {
-        if (z0) s0 = cmk(-s0.x, -s0.y);
-        if (z1) s1 = cmk(-s1.x, -s1.y);
-        if (z2) s2 = cmk(-s2.x, -s2.y);
+        s0 = sign_flip(s0, zm0), s1 = sign_flip(s1, zm1), s2 = sign_flip(s2, zm2);
         const double2 x0 = shfl_c(v[km], j), x1 = shfl_c(v[km], ZS_COLS + j), x2 = shfl_c(v[km], 2 * ZS_COLS + j);
         double2 acc = cmul(s0, x0);
         cfma(acc, s1, x1);
