@@ -3,11 +3,13 @@
 // apply_n / apply_system / gmres passes, reference operator.py:82-105,
 // solver.py:114).  A pageable cudaMemcpy stages through one driver buffer with
 // a single host thread (~10 GB/s); here a small persistent pool of host threads
-// copies 2 MB chunks into a ring of pinned slots and each issues the DMA of its
-// own chunk on the caller's stream, so the host copy runs at memory bandwidth
-// and overlaps the PCIe/C2C transfer.  Semantics match cudaMemcpy from
+// copies 2 MB chunks into a ring of pinned slots (non-temporal stores) and each
+// issues the DMA of its own chunk on the caller's stream, so the host copy runs
+// at memory bandwidth and overlaps the PCIe/C2C transfer.  Semantics match cudaMemcpy from
 // pageable memory: the call returns once `src` has been consumed; the DMA may
 // still be in flight on `stream`.
+#include <emmintrin.h>
+
 #include <atomic>
 #include <condition_variable>
 #include <cstring>
@@ -50,6 +52,27 @@ struct Pool {
 Pool* g_pool = nullptr;
 std::once_flag g_once;
 
+// pageable -> pinned slot with non-temporal stores: the slot is read next by
+// the DMA engine, not by this core, so the lines need not be fetched for
+// ownership nor kept in this core's caches (VX_H2D_NT=0: plain memcpy)
+void copy_stream(char* dst, const char* src, size_t n) {
+  static const int nt = [] { const char* e = getenv("VX_H2D_NT"); return e ? atoi(e) : 1; }();
+  if (!nt || (reinterpret_cast<uintptr_t>(dst) & 15)) { std::memcpy(dst, src, n); return; }
+  size_t i = 0;
+  for (; i + 64 <= n; i += 64) {
+    const __m128i a = _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + i));
+    const __m128i b = _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + i + 16));
+    const __m128i c = _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + i + 32));
+    const __m128i d = _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + i + 48));
+    _mm_stream_si128(reinterpret_cast<__m128i*>(dst + i), a);
+    _mm_stream_si128(reinterpret_cast<__m128i*>(dst + i + 16), b);
+    _mm_stream_si128(reinterpret_cast<__m128i*>(dst + i + 32), c);
+    _mm_stream_si128(reinterpret_cast<__m128i*>(dst + i + 48), d);
+  }
+  if (i < n) std::memcpy(dst + i, src + i, n - i);
+  _mm_sfence();
+}
+
 void run_chunks(Pool* p, Job* j) {
   cudaSetDevice(j->device);
   for (;;) {
@@ -59,7 +82,7 @@ void run_chunks(Pool* p, Job* j) {
     size_t n = j->bytes - off < kChunk ? j->bytes - off : kChunk;
     // the slot's previous DMA (an earlier round or call) must have drained
     if (cudaEventSynchronize(p->ev[c]) != cudaSuccess) { j->err = 1; continue; }
-    std::memcpy(p->slot[c], j->src + off, n);
+    copy_stream(p->slot[c], j->src + off, n);
     if (cudaMemcpyAsync(j->dst + off, p->slot[c], n, cudaMemcpyHostToDevice, j->stream) != cudaSuccess ||
         cudaEventRecord(p->ev[c], j->stream) != cudaSuccess)
       j->err = 1;
