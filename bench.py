@@ -347,7 +347,7 @@ def solve_kernel_traffic(name, W, world, layout=None):
     ragged = os.environ.get("VX_RAGGED", "1") != "0" and W.prec["kind"] in ("one-level", "blocked")
     kname = "lu_solve_rag_kernel<2>" if ragged else "lu_solve_pipe_kernel<2>"
     if W.prec["kind"] == "two-level":
-        kname = "lu_solve_small_kernel"
+        kname = ("lu_apply_small_inv_kernel<%d>" % (3 * W.grid.nz)) if layout == "inverse" else "lu_solve_small_kernel"
     elif W.prec["kind"] == "reduced-one-level":
         kname = "lu_solve_rag_kernel<2> + rep_gemm_kernel"
     if layout == "symmetric-inverse":

@@ -202,6 +202,16 @@ long vx_prec2_work_elems(int nx, int ny, int nz, int nrhs);
 int vx_prec2_apply(int nx, int ny, int nz, int nrhs, const vx_c128* factors, const int* perm,
                    const int* items, int n_items, int direct_r, const int* klist,
                    const vx_c128* x, vx_c128* y, vx_c128* work, void* stream);
+/* The same apply on explicit block inverses (3 nz <= 32): vx_lu_small_invert
+ * turns the packed factors of vx_lu2_build into G = A^-1, column-major
+ * (n, n) per slot, and vx_prec2_apply_inv replaces the two triangular
+ * products of TwoLevelPrec.apply's lu_solve (circulant.py:388-390) by one
+ * streaming product per block. */
+int vx_lu_small_invert(int n, int nslots, const vx_c128* factors, const int* perm, vx_c128* inverses,
+                       void* stream);
+int vx_prec2_apply_inv(int nx, int ny, int nz, int nrhs, const vx_c128* inverses, const int* items,
+                       int n_items, const int* klist, const vx_c128* x, vx_c128* y, vx_c128* work,
+                       void* stream);
 
 /* ------------------------------------------------------ sharded (multi-GPU) */
 /* Pieces of vx_op_apply for the x-slab/line-sharded matvec:

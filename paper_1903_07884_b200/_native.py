@@ -67,6 +67,8 @@ _SIGS = {
     "vx_lu2_build": (c_int, [c_int] * 3 + [P, P, P, c_int, P, P, P, P, P]),
     "vx_prec2_work_elems": (c_long, [c_int] * 4),
     "vx_prec2_apply": (c_int, [c_int] * 4 + [P, P, P, c_int, c_int, P, P, P, P, P]),
+    "vx_lu_small_invert": (c_int, [c_int, c_int, P, P, P, P]),
+    "vx_prec2_apply_inv": (c_int, [c_int] * 4 + [P, P, c_int, P, P, P, P, P]),
     "vx_box_gather": (c_int, [c_int] * 10 + [P, P, P]),
     "vx_box_scatter": (c_int, [c_int] * 10 + [P, P, P]),
     "vx_arnoldi_part_elems": (c_long, [c_long, c_int]),

@@ -216,6 +216,7 @@ def _sym_weights(plan, m_yz: np.ndarray) -> np.ndarray:
 # vector: one block among 10^4 with a relative error e contributes e / 100, so 1e-13 bounds every
 # block's error by 1e-11; observed 5e-16 .. 1.4e-15 on c0-c3)
 SYMINV_TOL = 1e-13
+SMALLINV_TOL = 1e-13   # explicit inverses of the 2-level blocks vs their factor solves
 
 
 class _SymFactors:
@@ -1023,10 +1024,44 @@ class TwoLevelPrec:
     def piv(self) -> np.ndarray:
         return self._piv.cpu().numpy()[self._store].reshape(self.grid.ny, self.grid.nx, -1)
 
+    _ginv = None
+    _inv_err = None
+
+    @property
+    def factor_layout(self) -> str:
+        return "inverse" if self._ginv is not None else "factors"
+
+    def _make_inverse(self):
+        """Explicit inverses of the single-tile blocks (3 nz <= 32), kept only if
+        they reproduce the factor solve on a seeded random vector to
+        SMALLINV_TOL (relative, max norm); VX_SMALLINV=0 keeps the factors."""
+        n = self.block_size
+        if n > 32 or os.environ.get("VX_SMALLINV", "1") == "0":
+            return
+        t = _torch()
+        nslots = int(self._fac.shape[0])
+        g = t.empty((nslots, n * n), dtype=t.complex128, device="cuda")
+        nv.call("vx_lu_small_invert", n, nslots, self._fac.data_ptr(), self._perm.data_ptr(), g.data_ptr(),
+                nv.stream_ptr())
+        gen = t.Generator(device="cuda").manual_seed(20190307)
+        probe = t.randn((self.grid.n_unknowns, 1, 2), dtype=t.float64, device="cuda", generator=gen)
+        probe = t.view_as_complex(probe).contiguous()
+        want = self._apply_dev(probe, 1)
+        self._ginv = g
+        got = self._apply_dev(probe, 1)
+        err = float((got - want).abs().max() / want.abs().max())
+        self._inv_err = err
+        if not err <= SMALLINV_TOL:
+            self._ginv = None
+
     def _apply_dev(self, xd, r):
         nx, ny, nz = self.grid.dims
         y = nv.empty_c128((self.grid.n_unknowns, r))
         work = nv.empty_c128(int(nv.query("vx_prec2_work_elems", nx, ny, nz, r)))
+        if self._ginv is not None:
+            nv.call("vx_prec2_apply_inv", nx, ny, nz, r, self._ginv.data_ptr(), nv.ptr(self._items), self._n_items,
+                    nv.ptr(self._klist), xd.data_ptr(), y.data_ptr(), work.data_ptr(), nv.stream_ptr())
+            return y
         nv.call("vx_prec2_apply", nx, ny, nz, r, self._fac.data_ptr(), self._perm.data_ptr(),
                 nv.ptr(self._items), self._n_items, self._direct_r, nv.ptr(self._klist),
                 xd.data_ptr(), y.data_ptr(), work.data_ptr(), nv.stream_ptr())
@@ -1094,9 +1129,9 @@ def _build_two_level_dev(grid, gen, mtilde, cap_bytes):
     if bad >= 0:
         l, k = divmod(int(kset[bad]), nx)
         raise PreconditionerBuildError(f"2-level build failed: singular block (k={k}, l={l})")
-    if nb == nx * ny:
-        return TwoLevelPrec(grid, fac, perm, piv)
-    return TwoLevelPrec(grid, fac, perm, piv, store, flips)
+    prec = TwoLevelPrec(grid, fac, perm, piv) if nb == nx * ny else TwoLevelPrec(grid, fac, perm, piv, store, flips)
+    prec._make_inverse()
+    return prec
 
 
 def build_two_level(kernel: ToeplitzKernel, mtilde, *, cap_bytes: int = 2 ** 31) -> TwoLevelPrec:

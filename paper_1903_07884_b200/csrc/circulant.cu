@@ -1857,6 +1857,136 @@ static int launch_solve_small(const LuGeom& g, const double2* F, const int* perm
   return VX_OK;
 }
 
+// Single-tile blocks held as explicit inverses G = A^-1, column-major per slot
+// (entry (r, c) at c n + r): one warp per work item, lane = row, y_r = sum_c
+// G[r, c] x_c for up to SINV_R right-hand sides (the x / y mirror partners of a
+// shared block) at once.  No triangular dependency chain and no staging: the n
+// column loads of a lane are independent and coalesced (n x 16 bytes per
+// instruction), the x_c are warp-private shared-memory broadcasts.
+#ifndef VX_SINV_WARPS
+#define VX_SINV_WARPS 4
+#endif
+constexpr int SINV_WARPS = VX_SINV_WARPS, SINV_R = 4;
+
+// N = n at compile time (n = 3 nz in the 2-level scheme): the lane's whole row
+// of G sits in registers, loaded BEFORE the gather of x so both round trips to
+// memory overlap; N = 0: runtime n, columns streamed eight at a time.
+template <int N>
+__global__ void __launch_bounds__(SINV_WARPS * 32)
+    lu_apply_small_inv_kernel(int n_rt, long gblk, const double2* __restrict__ G, const int* __restrict__ items,
+                              int item0, int nitems, const int* __restrict__ klist, int nrhs, double2* Y,
+                              long s_row, long s_k) {
+  __shared__ double2 xs[SINV_WARPS][SINV_R][32];
+  const int n = N ? N : n_rt;
+  const int lane = threadIdx.x & 31, wrp = threadIdx.x >> 5;
+  const int it = blockIdx.x * SINV_WARPS + wrp;
+  if (it >= nitems) return;
+  int slot, beg, cnt;
+  if (items) {
+    slot = items[3 * (item0 + it)];
+    beg = items[3 * (item0 + it) + 1];
+    cnt = items[3 * (item0 + it) + 2];
+  } else {
+    slot = item0 + it;
+    beg = slot;
+    cnt = 1;
+  }
+  const double2* Gs = G + (long)slot * gblk + lane;
+  const bool row = lane < n;
+  double2 g[N ? N : 1];
+  if constexpr (N > 0) {
+#pragma unroll
+    for (int c = 0; c < N; ++c) g[c] = row ? ld_stream(Gs + c * N) : cmk(0.0, 0.0);
+  }
+  const int q = n / 3, total = cnt * nrhs;
+  for (int r0 = 0; r0 < total; r0 += SINV_R) {
+    long base[SINV_R];
+    int f2[SINV_R];
+#pragma unroll
+    for (int rr = 0; rr < SINV_R; ++rr) {
+      const int rho = r0 + rr < total ? r0 + rr : total - 1;
+      const int kraw = klist ? klist[beg + rho / nrhs] : beg + rho / nrhs;
+      base[rr] = (long)(kraw & KIDX) * s_k + (rho % nrhs);
+      f2[rr] = kraw >> 29;
+      xs[wrp][rr][lane] = row ? cflip(Y[(long)lane * s_row + base[rr]], flip_row(f2[rr], lane, q)) : cmk(0.0, 0.0);
+    }
+    __syncwarp();
+    double2 acc[SINV_R];
+#pragma unroll
+    for (int rr = 0; rr < SINV_R; ++rr) acc[rr] = cmk(0.0, 0.0);
+    if constexpr (N > 0) {
+#pragma unroll
+      for (int c = 0; c < N; ++c) {
+#pragma unroll
+        for (int rr = 0; rr < SINV_R; ++rr) cfma(acc[rr], g[c], xs[wrp][rr][c]);
+      }
+    } else {
+#pragma unroll 8
+      for (int c = 0; c < n; ++c) {
+        const double2 gc = row ? ld_stream(Gs + c * n) : cmk(0.0, 0.0);
+#pragma unroll
+        for (int rr = 0; rr < SINV_R; ++rr) cfma(acc[rr], gc, xs[wrp][rr][c]);
+      }
+    }
+#pragma unroll
+    for (int rr = 0; rr < SINV_R; ++rr)
+      if (row && r0 + rr < total) Y[(long)lane * s_row + base[rr]] = cflip(acc[rr], flip_row(f2[rr], lane, q));
+    __syncwarp();
+  }
+}
+
+// G = A^-1 from the packed inverse-triangle tile: the solve of
+// lu_solve_small_kernel applied to the n columns of the identity
+__global__ void __launch_bounds__(SMALL_WARPS * 32)
+    lu_small_invert_kernel(int n, long blk, const double2* __restrict__ F, const int* __restrict__ perm, int nslots,
+                           double2* __restrict__ G) {
+  extern __shared__ double2 smd[];
+  const int lane = threadIdx.x & 31, wrp = threadIdx.x >> 5;
+  const int slot = blockIdx.x * SMALL_WARPS + wrp;
+  if (slot >= nslots) return;
+  double2* Ds = smd + (long)wrp * n * n;
+  const double2* D = F + (long)slot * blk;
+  for (int i = lane; i < n * n; i += 32) Ds[i] = D[i];
+  const int pr = lane < n ? perm[(long)slot * n + lane] : -1;
+  __syncwarp();
+  for (int j = 0; j < n; ++j) {
+    const double2 yv = cmk(pr == j ? 1.0 : 0.0, 0.0);
+    double2 o = yv;
+    for (int c = 0; c < n; ++c) {
+      const double2 yc = cmk(__shfl_sync(0xffffffffu, yv.x, c), __shfl_sync(0xffffffffu, yv.y, c));
+      if (lane > c && lane < n) cfma(o, Ds[c * n + lane], yc);
+    }
+    double2 x = cmk(0.0, 0.0);
+    for (int c = 0; c < n; ++c) {
+      const double2 oc = cmk(__shfl_sync(0xffffffffu, o.x, c), __shfl_sync(0xffffffffu, o.y, c));
+      if (c >= lane && lane < n) cfma(x, Ds[c * n + lane], oc);
+    }
+    if (lane < n) G[((long)slot * n + j) * n + lane] = x;
+  }
+}
+
+static int launch_apply_small_inv(int n, const double2* G, const int* items, int nitems, const int* klist, int nrhs,
+                                  double2* Y, long s_row, long s_k, cudaStream_t s) {
+  if (nitems <= 0) return VX_OK;
+  Span span("prec_solve", s);
+  const unsigned grid = div_up(nitems, SINV_WARPS);
+  switch (n) {
+#define VX_SINV_CASE(N_)                                                                            \
+  case N_:                                                                                          \
+    lu_apply_small_inv_kernel<N_><<<grid, SINV_WARPS * 32, 0, s>>>(n, (long)n * n, G, items, 0, nitems, klist, nrhs, \
+                                                                   Y, s_row, s_k);                  \
+    break;
+    VX_SINV_CASE(6) VX_SINV_CASE(9) VX_SINV_CASE(12) VX_SINV_CASE(15) VX_SINV_CASE(18) VX_SINV_CASE(21)
+    VX_SINV_CASE(24) VX_SINV_CASE(27) VX_SINV_CASE(30)
+#undef VX_SINV_CASE
+    default:
+      lu_apply_small_inv_kernel<0><<<grid, SINV_WARPS * 32, 0, s>>>(n, (long)n * n, G, items, 0, nitems, klist, nrhs,
+                                                                    Y, s_row, s_k);
+  }
+  VX_CHECK_LAUNCH("lu_apply_small_inv_kernel");
+  return VX_OK;
+}
+
 template <int R>
 static int launch_solve_pipe(const LuGeom& g, const double2* F, const int* perm, const int* items,
                              int item0, int nblocks, const int* klist, int nrhs, double2* Y, long s_row,
@@ -2333,9 +2463,9 @@ extern "C" long vx_prec2_work_elems(int nx, int ny, int nz, int nrhs) {
   return 3L * nx * ny * nz * nrhs;
 }
 
-extern "C" int vx_prec2_apply(int nx, int ny, int nz, int nrhs, const vx_c128* factors,
-                              const int* perm, const int* items, int n_items, int direct_r, const int* klist,
-                              const vx_c128* x, vx_c128* y, vx_c128* work, void* stream) {
+static int prec2_apply_impl(int nx, int ny, int nz, int nrhs, const vx_c128* factors, bool inverse,
+                            const int* perm, const int* items, int n_items, int direct_r, const int* klist,
+                            const vx_c128* x, vx_c128* y, vx_c128* work, void* stream) {
   VX_REQUIRE(nx >= 1 && ny >= 1 && nz >= 1 && nrhs >= 1, "bad 2-level apply arguments");
   VX_REQUIRE(direct_r == 1 || direct_r == 2 || direct_r == 4, "direct_r must be 1, 2 or 4");
   cudaStream_t s = as_stream(stream);
@@ -2366,8 +2496,12 @@ extern "C" int vx_prec2_apply(int nx, int ny, int nz, int nrhs, const vx_c128* f
   LuGeom g = lu_geom(3 * nz);
   const double2* F = reinterpret_cast<const double2*>(factors);
   if (!items) n_items = nx * ny;
-  if ((st = solve_items(g, F, perm, items, n_items, n_items, klist, nrhs, S, plane, nrhs, s, -1, direct_r)))
+  if (inverse) {
+    VX_REQUIRE(3 * nz <= 32, "explicit block inverses cover 3 nz <= 32 only");
+    if ((st = launch_apply_small_inv(3 * nz, F, items, n_items, klist, nrhs, S, plane, nrhs, s))) return st;
+  } else if ((st = solve_items(g, F, perm, items, n_items, n_items, klist, nrhs, S, plane, nrhs, s, -1, direct_r))) {
     return st;
+  }
   if (two_y) {
     if ((st = launch_cols2<true>(py, S, plane, pitch, ny, S, plane, pitch, ny, 3L * nz * pitch, (int)pitch, 1.0, s)))
       return st;
@@ -2381,6 +2515,34 @@ extern "C" int vx_prec2_apply(int nx, int ny, int nz, int nrhs, const vx_c128* f
     StoreStrided sv{reinterpret_cast<double2*>(y), {pitch, 1, nrhs, nrhs}, 1.0 / ((double)nx * ny)};
     if ((st = launch_fft_auto(px, ld, sv, q3 * nrhs, nx, nx, true, nrhs == 1, s))) return st;
   }
+  return VX_OK;
+}
+
+extern "C" int vx_prec2_apply(int nx, int ny, int nz, int nrhs, const vx_c128* factors,
+                              const int* perm, const int* items, int n_items, int direct_r, const int* klist,
+                              const vx_c128* x, vx_c128* y, vx_c128* work, void* stream) {
+  return prec2_apply_impl(nx, ny, nz, nrhs, factors, false, perm, items, n_items, direct_r, klist, x, y, work,
+                          stream);
+}
+
+extern "C" int vx_prec2_apply_inv(int nx, int ny, int nz, int nrhs, const vx_c128* inverses, const int* items,
+                                  int n_items, const int* klist, const vx_c128* x, vx_c128* y, vx_c128* work,
+                                  void* stream) {
+  return prec2_apply_impl(nx, ny, nz, nrhs, inverses, true, nullptr, items, n_items, 1, klist, x, y, work, stream);
+}
+
+extern "C" int vx_lu_small_invert(int n, int nslots, const vx_c128* factors, const int* perm, vx_c128* inverses,
+                                  void* stream) {
+  VX_REQUIRE(n >= 1 && n <= 32 && nslots >= 0, "vx_lu_small_invert: single-tile blocks (n <= 32) only");
+  if (nslots == 0) return VX_OK;
+  const LuGeom g = lu_geom(n);
+  VX_REQUIRE(g.nt == 1, "vx_lu_small_invert: block of %d rows is not a single tile", n);
+  const size_t smem = (size_t)SMALL_WARPS * n * n * sizeof(double2);
+  if (smem > 48 * 1024)
+    VX_CUDA(cudaFuncSetAttribute(lu_small_invert_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  lu_small_invert_kernel<<<div_up(nslots, SMALL_WARPS), SMALL_WARPS * 32, smem, as_stream(stream)>>>(
+      n, g.blk, reinterpret_cast<const double2*>(factors), perm, nslots, reinterpret_cast<double2*>(inverses));
+  VX_CHECK_LAUNCH("lu_small_invert_kernel");
   return VX_OK;
 }
 
