@@ -329,6 +329,35 @@ def test_two_level_vs_oracle_disk_like(rng, C):
     assert relerr(p.apply(x), O.apply_prec(ref, x)) < 1e-10
 
 
+@pytest.mark.parametrize("dims", [(37, 40, 8), (12, 9, 10), (16, 10, 3), (9, 8, 11)])
+def test_two_level_block_inverses_equal_factor_solves(rng, C, monkeypatch, dims):
+    """3 nz <= 32: the blocks are applied as explicit inverses (one product per
+    block); the result equals the two triangular solves on the factors
+    (VX_SMALLINV=0) and the oracle, single and multiple right-hand sides.
+    3 nz = 33 stays on the factors."""
+    from paper_1903_07884_b200 import workloads
+
+    W = workloads.small(*dims, delta=0.03e-6)
+    kern = W.kernel()
+    m = np.full(W.grid.shape, 0.75 - 0.01j)
+    p = C.build_two_level(kern, m)
+    small = 3 * dims[2] <= 32
+    assert p.factor_layout == ("inverse" if small else "factors")
+    if small:
+        assert p._inv_err <= C.SMALLINV_TOL
+    monkeypatch.setenv("VX_SMALLINV", "0")
+    pf = C.build_two_level(kern, m)
+    assert pf.factor_layout == "factors"
+    ref = O.build_two_level(kern.tensors, W.grid.dims, m)
+    x = random_field(rng, W.grid.n_unknowns)
+    y = p.apply(x)
+    assert relerr(y, pf.apply(x)) < 1e-12
+    assert relerr(y, O.apply_prec(ref, x)) < 1e-10
+    xs = np.stack([random_field(rng, W.grid.n_unknowns) for _ in range(3)], axis=1)
+    assert relerr(p.apply(xs), pf.apply(xs)) < 1e-12
+    np.testing.assert_allclose(p.lu, pf.lu, rtol=0, atol=0)
+
+
 @pytest.mark.parametrize("dims,tol", [((60, 7, 3), 0.05), ((40, 12, 4), 1e-3), ((24, 22, 11), 1e-3)])
 def test_reduced_representative_gemm_path(rng, C, monkeypatch, dims, tol):
     """The representative block's frequencies through the explicit-inverse GEMM
