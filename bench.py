@@ -585,7 +585,7 @@ def run_ours(args):
             fb = fb_launch = getattr(prec, "factor_bytes_per_apply", None)
     elif getattr(pl[0], "ginv", None) is not None:
         # sharded symmetric inverses: this rank's stored triangles per launch; every rank's per iteration
-        layout = "symmetric-inverse"
+        layout = "inverse" if W.prec["kind"] == "two-level" else "symmetric-inverse"
         fb_launch = int(pl[0].bytes_local)
         loc = sum(int(q.bytes_local) for q in pl)
         fb = int(reduce_sum(torch, world, loc)) if world > 1 else loc
@@ -673,8 +673,9 @@ def run_ours(args):
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         mean_j = int(max(1, min(W.restart, its_per_solve) // 2))
         sec, cores, desc, parts = cpu_iteration_sample(W, kern, m_host, args.cpu_sample_blocks, mean_j,
-                                                       spectra=plan.spectra if plan.padded_shape == tuple(
-                                                           2 * d for d in W.grid.shape) else None)
+                                                       spectra=plan.spectra if (not sharded and plan.padded_shape
+                                                                                == tuple(2 * d for d in W.grid.shape))
+                                                       else None)
         cpu = {"value": 1.0 / sec, "unit": "it/s", "cores": cores, "kind": "port", "sample": desc,
                "seconds_per_iteration": sec, **parts,
                "tts_s_estimate": None}

@@ -241,6 +241,10 @@ int vx_scatter_cols(long nrows, const vx_c128* in, int P, const int* col_off, co
 int vx_prec1_solve(int n, int nrhs, const vx_c128* factors, const int* perm, const int* items,
                    int n_single, int n_items, int direct_r, const int* klist, vx_c128* Y, long s_row,
                    long s_k, void* stream);
+/* The same call on explicit single-tile inverses (vx_lu_small_invert), n <= 32:
+ * a rank's share of TwoLevelPrec.apply's block solves (circulant.py:388-390). */
+int vx_small_inv_apply(int n, int nrhs, const vx_c128* inverses, const int* items, int n_items,
+                       const int* klist, vx_c128* Y, long s_row, long s_k, void* stream);
 /* Local halves of one classical Gram-Schmidt pass (the all-reduce goes in
  * between): out[0..nvec) = V^H w, out[nvec] = ||w||^2; then w -= V coef and
  * out_norm2 = ||w||^2. */

@@ -120,6 +120,7 @@ _SIGS = {
     "vx_rep_variant": (c_int, [c_int]),
     "vx_op_reg_fft": (c_int, [c_int]),
     "vx_prec1_solve": (c_int, [c_int, c_int, P, P, P, c_int, c_int, c_int, P, P, c_long, c_long, P]),
+    "vx_small_inv_apply": (c_int, [c_int, c_int, P, P, c_int, P, P, c_long, c_long, P]),
     "vx_cgs_dots": (c_int, [c_long, c_int, P, c_long, P, P, P, P]),
     "vx_cgs_update": (c_int, [c_long, c_int, P, c_long, P, P, P, P, P]),
     "vx_cgs_dots_cond": (c_int, [c_long, c_int, P, c_long, P, P, P, P, P]),

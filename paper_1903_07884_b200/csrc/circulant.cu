@@ -2606,6 +2606,14 @@ extern "C" int vx_prec1_solve(int n, int nrhs, const vx_c128* factors, const int
                      nrhs, reinterpret_cast<double2*>(Y), s_row, s_k, as_stream(stream), -1, direct_r);
 }
 
+// the block products of vx_prec2_apply_inv on a caller-laid-out array (a rank's (3nz, ny*nk) columns)
+extern "C" int vx_small_inv_apply(int n, int nrhs, const vx_c128* inverses, const int* items, int n_items,
+                                  const int* klist, vx_c128* Y, long s_row, long s_k, void* stream) {
+  VX_REQUIRE(n >= 1 && n <= 32 && nrhs >= 1 && n_items >= 0, "bad block-inverse apply arguments");
+  return launch_apply_small_inv(n, reinterpret_cast<const double2*>(inverses), items, n_items, klist, nrhs,
+                                reinterpret_cast<double2*>(Y), s_row, s_k, as_stream(stream));
+}
+
 extern "C" int vx_lu_variant(int monolithic) {
   vx::g_lu_monolithic = monolithic ? 1 : 0;
   return VX_OK;

@@ -36,7 +36,7 @@ import time
 import numpy as np
 
 from . import _native as nv
-from .circulant import _check_cap, _coerce_mtilde, _coerce_mz, _select_kept
+from .circulant import SMALLINV_TOL, _check_cap, _coerce_mtilde, _coerce_mz, _select_kept
 from .errors import BreakdownError, PreconditionerBuildError
 from .solver import GivensQR, SolveReport, _speculate
 
@@ -237,6 +237,17 @@ class CudaBackend:
     def solve(self, Y, n, factors, perm, items, n_single, n_items, klist, s_row):
         nv.call("vx_prec1_solve", n, 1, factors.data_ptr(), perm.data_ptr(), items.data_ptr(), n_single, n_items,
                 1, klist.data_ptr(), Y.data_ptr(), s_row, 1, nv.stream_ptr())
+
+    def invert_small(self, n, factors, perm):
+        """Explicit inverses of single-tile blocks (n <= 32), column-major per slot."""
+        g = self.empty(max(1, int(factors.shape[0]) * n * n))
+        nv.call("vx_lu_small_invert", n, int(factors.shape[0]), factors.data_ptr(), perm.data_ptr(), g.data_ptr(),
+                nv.stream_ptr())
+        return g
+
+    def solve_inv(self, Y, n, ginv, items, n_items, klist, s_row):
+        nv.call("vx_small_inv_apply", n, 1, ginv.data_ptr(), items.data_ptr(), n_items, klist.data_ptr(),
+                Y.data_ptr(), s_row, 1, nv.stream_ptr())
 
     def cgs_dots(self, V, nvec, w, part):
         out = self.empty(nvec + 1)
@@ -581,6 +592,28 @@ class DistTwoLevelPrec:
         self.klist = backend.ints(np.arange(max(1, self.n_slots)))
         off, cmap = layout.prec_cols()
         self.col_off, self.colmap = backend.ints(off), backend.ints(cmap)
+        self.ginv = None
+        self.ginv_err = None
+        self._init_inverse(ny * nk)
+
+    def _init_inverse(self, s_row):
+        """Single-tile blocks as explicit inverses where the backend has them (the
+        GPU one), kept only if they reproduce the factor solve on a seeded
+        random array (the single-GPU TwoLevelPrec's rule); VX_SMALLINV=0: factors."""
+        B = self.B
+        if (self.n > 32 or not self.n_slots or not hasattr(B, "invert_small")
+                or os.environ.get("VX_SMALLINV", "1") == "0"):
+            return
+        g = B.invert_small(self.n, self.factors, self.perm)
+        rng = np.random.default_rng(20190307)
+        probe = rng.normal(size=self.n * s_row) + 1j * rng.normal(size=self.n * s_row)
+        y0, y1 = B.to_dev(probe), B.to_dev(probe)
+        B.solve(y0, self.n, self.factors, self.perm, self.items, self.n_slots, self.n_slots, self.klist, s_row)
+        B.solve_inv(y1, self.n, g, self.items, self.n_slots, self.klist, s_row)
+        a, b = np.asarray(B.to_host(y0)), np.asarray(B.to_host(y1))
+        self.ginv_err = float(np.abs(a - b).max() / np.abs(a).max())
+        if self.ginv_err <= SMALLINV_TOL:
+            self.ginv = g
 
     def apply(self, x_loc):
         L, B, C = self.L, self.B, self.C
@@ -594,8 +627,11 @@ class DistTwoLevelPrec:
                      [L.nl * L.kown[s].size for s in range(L.P)])
         if self.n_slots:
             B.dft_y(recv, 3 * nz, ny, nk, False)
-            B.solve(recv, self.n, self.factors, self.perm, self.items, self.n_slots, self.n_slots, self.klist,
-                    ny * nk)
+            if self.ginv is not None:
+                B.solve_inv(recv, self.n, self.ginv, self.items, self.n_slots, self.klist, ny * nk)
+            else:
+                B.solve(recv, self.n, self.factors, self.perm, self.items, self.n_slots, self.n_slots, self.klist,
+                        ny * nk)
             B.dft_y(recv, 3 * nz, ny, nk, True)
         back = B.empty(max(1, L.nl * nx))
         C.all_to_all(back[:L.nl * nx], recv[:L.nlines * nk],

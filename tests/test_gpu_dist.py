@@ -237,6 +237,12 @@ def test_sharded_two_level_loopback(P):
             m = torch.from_numpy(W.m.reshape(-1).copy()).cuda()
             xl = torch.from_numpy(L.local_slice(x).copy()).cuda()
             y_pc = prec.apply(xl).cpu().numpy()
+            # 12 x 12 blocks: applied as explicit inverses, equal to the rank's factor solves
+            assert prec.ginv is not None and prec.ginv_err <= 1e-13
+            ginv, prec.ginv = prec.ginv, None
+            y_fac = prec.apply(xl).cpu().numpy()
+            prec.ginv = ginv
+            assert relerr(y_pc, y_fac) < 1e-12
             bl = torch.from_numpy(L.local_slice(W.b).copy()).cuda()
             xs, rep = gmres_sharded(lambda v: op.apply(m, v), bl, B, C, apply_pinv=prec.apply, tol=1e-8,
                                     maxit=300, restart=15)
