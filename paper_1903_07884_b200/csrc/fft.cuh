@@ -51,6 +51,10 @@ struct FftPlan {
   const double2* tw_hi;     // [nhi] exp(-2 pi i 64 a / L)   (two-level twiddles:
   const double2* tw_lo;     // [64]  exp(-2 pi i b / L)       w^t = hi[t>>6] * lo[t&63])
   int nhi;
+  // register Bluestein (fft_blue.cuh): convolution length R*R >= 2n-1 with R a register DFT length
+  int blue_R;                // 0: none
+  const double2* blue_bhat;  // [R*R] FFT_{R^2}(conj chirp, wrapped) / R^2, natural order
+  const double2* blue_tw;    // [R*R] exp(-2 pi i j / R^2)
   FastDiv fd_m[FFT_MAX_STAGES];   // butterfly span m of stage st (DIF order)
   FastDiv fd_nb[FFT_MAX_STAGES];  // butterflies per line L / R_st
 };

@@ -21,6 +21,7 @@
 
 #include "fft_lines.cuh"
 #include "fft_reg.cuh"
+#include "fft_blue.cuh"
 
 #include <cooperative_groups.h>
 
@@ -272,6 +273,7 @@ int launch_fft_contig(const FftPlan& p, const Loader& ld, const Storer& st, int 
                       bool inv, cudaStream_t s) {
   if (fft_long_enabled() && !p.bluestein && fft_long_supported(p.n))
     return launch_fft_long(p, ld, st, n_lines, n_in, n_out, inv, s);
+  if (blue_reg_supported(p)) return launch_blue_reg(p, ld, st, n_lines, n_in, n_out, inv, s);
   return launch_fft_lines(p, ld, st, n_lines, n_in, n_out, inv, true, s);
 }
 

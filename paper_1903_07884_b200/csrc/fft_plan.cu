@@ -207,6 +207,22 @@ int fft_get_plan(int n, FftPlan* out) {
     }
     if ((st = upload(chirp, &p.chirp))) return st;
     if ((st = upload(brev, &p.bhat_rev))) return st;
+    // register Bluestein: the smallest square R^2 >= 2n-1 of a register DFT length
+    for (int R : {16, 20, 24, 28, 32}) {
+      if (R * R < 2 * n - 1) continue;
+      const int M = R * R;
+      std::vector<double2> bm(M, make_double2(0, 0));
+      for (int l = 0; l < n; ++l) {
+        const double2 c = make_double2(chirp[l].x, -chirp[l].y);
+        bm[l] = c;
+        if (l) bm[M - l] = c;
+      }
+      host_fft(bm);
+      for (auto& v : bm) { v.x /= M; v.y /= M; }
+      if ((st = upload(bm, &p.blue_bhat)) || (st = upload(roots(M), &p.blue_tw))) return st;
+      p.blue_R = R;
+      break;
+    }
   }
   g_plans[{dev, n}] = p;
   *out = p;

@@ -47,6 +47,21 @@ def test_fft_contiguous_lengths(torch, rng, n):
     assert relerr(_fft_lines(torch, a, 1, True), scipy.fft.ifft(a, axis=1)) < 1e-13
 
 
+@pytest.mark.parametrize("n", [127, 131, 199, 211, 283, 293, 367, 389, 397, 509, 521, 2 * 211])
+def test_fft_register_bluestein_lengths(torch, rng, n):
+    """Non-smooth lengths on contiguous lines: the three-pass register Bluestein
+    (convolution length R^2 >= 2n-1, R = 16 / 20 / 24 / 28 / 32 -- both edges of
+    every bucket) and, above 2n-1 = 1024, the shared-memory stage engine; with
+    zero padding in and a cropped output."""
+    lines = 37
+    a = random_field(rng, lines * n).reshape(lines, n)
+    assert relerr(_fft_lines(torch, a, 1, False), scipy.fft.fft(a, axis=1)) < 1e-13
+    assert relerr(_fft_lines(torch, a, 1, True), scipy.fft.ifft(a, axis=1)) < 1e-13
+    short = a[:, : n // 2 + 1]
+    assert relerr(_fft_lines(torch, short, 1, False, n=n), scipy.fft.fft(short, n, axis=1)) < 1e-13
+    assert relerr(_fft_lines(torch, a, 1, True, n=n, n_out=n // 3), scipy.fft.ifft(a, axis=1)[:, : n // 3]) < 1e-13
+
+
 @pytest.mark.parametrize("shape,axis", [((3, 10, 7), 1), ((2, 44, 33), 1), ((5, 19, 16), 1),
                                         ((6, 16, 9), 0), ((4, 800, 3), 1), ((3, 11, 2, 5), 1)])
 def test_fft_strided(torch, rng, shape, axis):
