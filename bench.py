@@ -351,7 +351,7 @@ def solve_kernel_traffic(name, W, world, layout=None):
     elif W.prec["kind"] == "reduced-one-level":
         kname = "lu_solve_rag_kernel<2> + rep_gemm_kernel"
     if layout == "symmetric-inverse":
-        kname = "symv_inv_kernel<2>" + (" + rep_gemm_kernel" if W.prec["kind"] == "reduced-one-level" else "")
+        kname = "symv2_inv_kernel<2>" + (" + rep_gemm_kernel" if W.prec["kind"] == "reduced-one-level" else "")
         return kname, _committed_traffic(name, kname, world)
     if layout == "symmetric":
         kname = "lu_solve_sym_kernel<2>" + (" + rep_gemm_kernel" if W.prec["kind"] == "reduced-one-level" else "")
