@@ -226,8 +226,26 @@ def ptr(t) -> int | None:
 H2D_STAGED_MIN = int(os.environ.get("VX_H2D_STAGED_MIN", 4 << 20))
 
 
-def device_c128(a, device=None):
-    """Host array-like / tensor -> contiguous complex128 CUDA tensor."""
+_side_streams = {}
+
+
+def _upload_stream(t):
+    dev = t.cuda.current_device()
+    s = _side_streams.get(dev)
+    if s is None:
+        s = _side_streams[dev] = t.cuda.Stream(device=dev)
+    return s
+
+
+def device_c128(a, device=None, side=False):
+    """Host array-like / tensor -> contiguous complex128 CUDA tensor.
+
+    ``side``: a large host array is copied on the library's upload stream, so
+    the DMA overlaps work already queued on the current stream (an input that
+    is first read LATER on the current stream, e.g. the medium map uploaded
+    while the first preconditioner apply runs).  The tensor is allocated from
+    the upload stream's pool and handed to the current stream with an event
+    wait + ``record_stream`` (the caching allocator's cross-stream protocol)."""
     t = require_cuda()
     if isinstance(a, t.Tensor):
         if not a.is_cuda:
@@ -236,6 +254,14 @@ def device_c128(a, device=None):
     arr = np.ascontiguousarray(np.asarray(a, dtype=np.complex128))
     if arr.nbytes >= H2D_STAGED_MIN and device is None:
         # large pageable upload: threaded copy through the library's pinned ring
+        if side and os.environ.get("VX_H2D_SIDE", "1") != "0":
+            up, cur = _upload_stream(t), t.cuda.current_stream()
+            with t.cuda.stream(up):
+                out = t.empty(arr.shape, dtype=t.complex128, device="cuda")
+                call("vx_h2d_staged", out.data_ptr(), arr.ctypes.data, arr.nbytes, up.cuda_stream)
+            cur.wait_stream(up)
+            out.record_stream(cur)
+            return out
         out = t.empty(arr.shape, dtype=t.complex128, device="cuda")
         call("vx_h2d_staged", out.data_ptr(), arr.ctypes.data, arr.nbytes, stream_ptr())
         return out

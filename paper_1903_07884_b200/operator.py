@@ -188,7 +188,7 @@ def _medium_in(plan: OperatorPlan, m):
     a = np.asarray(m, dtype=np.complex128)
     if a.size != plan.grid.n_voxels:
         raise ValueError("coefficient map size does not match grid")
-    d = nv.device_c128(a.reshape(-1))
+    d = nv.device_c128(a.reshape(-1), side=True)   # first read by the epilogue of this apply's last kernel
     object.__setattr__(plan, "_m_cache", (m, d, tok))
     return d
 
