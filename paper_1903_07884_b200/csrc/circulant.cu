@@ -2180,6 +2180,10 @@ __global__ void box_copy_kernel(int nx, int ny, int nz, int x0, int y0, int z0, 
 // side stream, concurrently with the HBM-bound single-block solves (disjoint
 // spectral columns).
 constexpr int RG_M = 64, RG_N = 64, RG_K = 16;
+// smem row pitch of a k-row: +2 entries, so the four k-rows a quarter warp reads
+// (lanes = 4 k x 2 rows of one 16-byte phase) land on distinct bank groups; an
+// unpadded 1 KB pitch put them on the same one (4-way conflicts on every fragment load)
+constexpr int RG_LDA = RG_M + 2, RG_LDB = RG_N + 2;
 constexpr int RG_THREADS = 256;
 
 static inline int rep_kp(int n) { return (n + RG_K - 1) / RG_K * RG_K; }
@@ -2190,10 +2194,24 @@ __global__ void eye_cols_kernel(int n, long ld, double2* A) {
   if (i < n) A[(long)i * ld + i] = make_double2(1.0, 0.0);
 }
 
+// Up to four products in one launch (the sector blocks of the reduced scheme):
+// product z has n[z] rows, its inverse at A + a_off[z], its spectral rows at
+// S + s_off[z] and its gathered operand at Bt + z * bt_stride.
+struct RepBatch {
+  int nb;
+  int n[4];
+  long a_off[4];
+  long s_off[4];
+  long bt_stride;
+};
+
 // Bt[k][j] (ldb = padded column count) <- S[k*s_row + ks[j/nrhs]*s_k + j%nrhs],
-// zero outside k < n, j < ncols.
-__global__ void rep_gather_kernel(int n, int Kp, int ncols, int Np, int nrhs, const int* __restrict__ ks,
+// zero outside k < n, j < ncols; blockIdx.y = product of the batch.
+__global__ void rep_gather_kernel(RepBatch rb, int ncols, int Np, int nrhs, const int* __restrict__ ks,
                                   const double2* __restrict__ S, long s_row, long s_k, double2* __restrict__ Bt) {
+  const int z = blockIdx.y, n = rb.n[z], Kp = (n + RG_K - 1) / RG_K * RG_K;
+  S += rb.s_off[z];
+  Bt += z * rb.bt_stride;
   const long total = (long)Kp * Np;
   for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < total; i += (long)gridDim.x * blockDim.x) {
     const int k = (int)(i / Np), j = (int)(i - (long)k * Np);
@@ -2215,11 +2233,16 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 // K step 16, 3-stage cp.async ring; 8 warps as 2 (m) x 4 (n), warp tile 32 x 16
 // = 4 x 2 DMMA 8x8 blocks, each complex product = 4 real DMMAs.
 __global__ void __launch_bounds__(RG_THREADS, 2)
-    rep_gemm_kernel(int n, int Kp, const double2* __restrict__ A, long lda, const double2* __restrict__ Bt,
+    rep_gemm_kernel(RepBatch rb, const double2* __restrict__ A, long lda, const double2* __restrict__ Bt,
                     long ldb, int ncols, int nrhs, const int* __restrict__ ks, double2* S, long s_row, long s_k,
                     int RG_STAGES) {
   extern __shared__ __align__(128) double2 rg_sm[];
-  constexpr int TA = RG_K * RG_M, TB = RG_K * RG_N;
+  const int z = blockIdx.z, n = rb.n[z], Kp = (n + RG_K - 1) / RG_K * RG_K;
+  if ((int)blockIdx.y * RG_M >= n) return;  // row tiles beyond this product's block
+  A += rb.a_off[z];
+  Bt += z * rb.bt_stride;
+  S += rb.s_off[z];
+  constexpr int TA = RG_K * RG_LDA, TB = RG_K * RG_LDB;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = warp & 1, wn = warp >> 1;
   const int r4 = lane >> 2, c4 = lane & 3;
@@ -2231,16 +2254,16 @@ __global__ void __launch_bounds__(RG_THREADS, 2)
     double2* Bs = As + TA;
     const int k0 = kt * RG_K;
 #pragma unroll
-    for (int it = 0; it < TA / RG_THREADS; ++it) {
+    for (int it = 0; it < RG_K * RG_M / RG_THREADS; ++it) {
       const int e = tid + it * RG_THREADS;
       const int kk = e / RG_M, mm = e - kk * RG_M;
-      cp_async16(As + e, A + (long)(k0 + kk) * lda + m0 + mm);
+      cp_async16(As + kk * RG_LDA + mm, A + (long)(k0 + kk) * lda + m0 + mm);
     }
 #pragma unroll
-    for (int it = 0; it < TB / RG_THREADS; ++it) {
+    for (int it = 0; it < RG_K * RG_N / RG_THREADS; ++it) {
       const int e = tid + it * RG_THREADS;
       const int kk = e / RG_N, nn = e - kk * RG_N;
-      cp_async16(Bs + e, Bt + (long)(k0 + kk) * ldb + n0 + nn);
+      cp_async16(Bs + kk * RG_LDB + nn, Bt + (long)(k0 + kk) * ldb + n0 + nn);
     }
   };
 
@@ -2267,16 +2290,23 @@ __global__ void __launch_bounds__(RG_THREADS, 2)
       const int kk = k4 + c4;
       double2 a[4], b[2];
 #pragma unroll
-      for (int rb = 0; rb < 4; ++rb) a[rb] = As[kk * RG_M + wm * 32 + rb * 8 + r4];
+      for (int rb = 0; rb < 4; ++rb) a[rb] = As[kk * RG_LDA + wm * 32 + rb * 8 + r4];
 #pragma unroll
-      for (int cb = 0; cb < 2; ++cb) b[cb] = Bs[kk * RG_N + wn * 16 + cb * 8 + r4];
+      for (int cb = 0; cb < 2; ++cb) b[cb] = Bs[kk * RG_LDB + wn * 16 + cb * 8 + r4];
+      // the MMAs are volatile (program order): two sweeps over the 16 accumulators, so the
+      // second MMA on an accumulator issues 16 instructions after the first, not right behind it
 #pragma unroll
       for (int rb = 0; rb < 4; ++rb)
 #pragma unroll
         for (int cb = 0; cb < 2; ++cb) {
           dmma884(cr[rb][cb][0], cr[rb][cb][1], a[rb].x, b[cb].x);
-          dmma884(cr[rb][cb][0], cr[rb][cb][1], -a[rb].y, b[cb].y);
           dmma884(ci[rb][cb][0], ci[rb][cb][1], a[rb].x, b[cb].y);
+        }
+#pragma unroll
+      for (int rb = 0; rb < 4; ++rb)
+#pragma unroll
+        for (int cb = 0; cb < 2; ++cb) {
+          dmma884(cr[rb][cb][0], cr[rb][cb][1], -a[rb].y, b[cb].y);
           dmma884(ci[rb][cb][0], ci[rb][cb][1], a[rb].y, b[cb].x);
         }
     }
@@ -2320,28 +2350,42 @@ static SideStream* side_stream() {
 // exactly n rows; a sector inverse formed in the dmax geometry keeps
 // rep_mp(dmax) -- its rows / columns beyond n are the identity padding, so the
 // leading n x n part is the sector block's inverse).
-static int rep_gemm(int n, const double2* inv, int ncols, int nrhs, const int* ks, double2* S, long s_row,
-                    long s_k, double2* Bt, cudaStream_t s, long lda = -1) {
-  const int Kp = rep_kp(n), Mp = rep_mp(n);
-  if (lda < 0) lda = Mp;
+static int rep_gemm_batch(const RepBatch& rb, const double2* inv, int ncols, int nrhs, const int* ks, double2* S,
+                          long s_row, long s_k, double2* Bt, cudaStream_t s, long lda) {
+  int nmax = 0;
+  for (int z = 0; z < rb.nb; ++z) nmax = rb.n[z] > nmax ? rb.n[z] : nmax;
+  const int Mp = rep_mp(nmax);
   const int Np = (ncols + RG_N - 1) / RG_N * RG_N;
-  const long total = (long)Kp * Np;
+  const long total = (long)rep_kp(nmax) * Np;
   {
     const unsigned gb = div_up(total, 256) < 8192 ? div_up(total, 256) : 8192;
-    rep_gather_kernel<<<gb, 256, 0, s>>>(n, Kp, ncols, Np, nrhs, ks, S, s_row, s_k, Bt);
+    rep_gather_kernel<<<dim3(gb, rb.nb), 256, 0, s>>>(rb, ncols, Np, nrhs, ks, S, s_row, s_k, Bt);
     VX_CHECK_LAUNCH("rep_gather_kernel");
   }
   static const int stages = env_int("VX_RG_STAGES", 3) == 2 ? 2 : 3;
-  const size_t smem = (size_t)stages * (RG_K * RG_M + RG_K * RG_N) * sizeof(double2);
+  const size_t smem = (size_t)stages * (RG_K * RG_LDA + RG_K * RG_LDB) * sizeof(double2);
   static bool attr = false;
   if (!attr) {
-    VX_CUDA(cudaFuncSetAttribute(rep_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 3 * 32768));
+    VX_CUDA(cudaFuncSetAttribute(rep_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)(3 * (RG_K * RG_LDA + RG_K * RG_LDB) * sizeof(double2))));
     attr = true;
   }
-  dim3 grid(Np / RG_N, Mp / RG_M);
-  rep_gemm_kernel<<<grid, RG_THREADS, smem, s>>>(n, Kp, inv, lda, Bt, Np, ncols, nrhs, ks, S, s_row, s_k, stages);
+  dim3 grid(Np / RG_N, Mp / RG_M, rb.nb);
+  rep_gemm_kernel<<<grid, RG_THREADS, smem, s>>>(rb, inv, lda, Bt, Np, ncols, nrhs, ks, S, s_row, s_k, stages);
   VX_CHECK_LAUNCH("rep_gemm_kernel");
   return VX_OK;
+}
+
+// lda: leading dimension of the k-major inverse (rep_mp(n) for an inverse of
+// exactly n rows; a sector inverse formed in the dmax geometry keeps
+// rep_mp(dmax) -- its rows / columns beyond n are the identity padding, so the
+// leading n x n part is the sector block's inverse).
+static int rep_gemm(int n, const double2* inv, int ncols, int nrhs, const int* ks, double2* S, long s_row,
+                    long s_k, double2* Bt, cudaStream_t s, long lda = -1) {
+  RepBatch rb{};
+  rb.nb = 1;
+  rb.n[0] = n;
+  return rep_gemm_batch(rb, inv, ncols, nrhs, ks, S, s_row, s_k, Bt, s, lda < 0 ? rep_mp(n) : lda);
 }
 
 }  // namespace vx
@@ -2808,12 +2852,18 @@ static int prec1_apply_sec(int nx, int ny, int nz, int nrhs, const vx_c128* fact
     }
     double2* Bt = S + (long)q3 * nx * nrhs + (long)nsec * dmax * pitch;
     const long lda = rep_mp(dmax);
+    // the sector blocks' products as ONE launch (four separate 207-CTA grids left a third of
+    // the 2-CTA/SM slots empty each time)
+    VX_REQUIRE(nsec <= 4, "representative GEMM batch holds at most 4 sectors");
+    RepBatch rb{};
+    rb.nb = nsec;
+    rb.bt_stride = (long)rep_kp(dmax) * (((long)rep->n * nrhs + RG_N - 1) / RG_N * RG_N);
     for (int sc = 0; sc < nsec; ++sc) {
-      const int d = sym ? sym->dims[sc] : (rg && rg->on ? rg->dims[sc] : dmax);
-      if ((st = rep_gemm(d, rep->inv + sc * rep->inv_stride, rep->n * nrhs, nrhs, rep->ks, U + (long)sc * dmax * pitch,
-                         pitch, nrhs, Bt, sr, lda)))
-        return st;
+      rb.n[sc] = sym ? sym->dims[sc] : (rg && rg->on ? rg->dims[sc] : dmax);
+      rb.a_off[sc] = sc * rep->inv_stride;
+      rb.s_off[sc] = (long)sc * dmax * pitch;
     }
+    if ((st = rep_gemm_batch(rb, rep->inv, rep->n * nrhs, nrhs, rep->ks, U, pitch, nrhs, Bt, sr, lda))) return st;
     if (n_single > 0 && (st = singles(n_single))) return st;
     if (ss) {
       VX_CUDA(cudaEventRecord(ss->join, sr));
@@ -2860,7 +2910,7 @@ extern "C" int vx_prec1_apply_sec_rag(int nx, int ny, int nz, int nrhs, const vx
 
 extern "C" long vx_prec1_sec_reduced_work_elems(int nx, int ny, int nz, int nrhs, int nsec, int dmax, int n_rep) {
   const long np = ((long)n_rep * nrhs + RG_N - 1) / RG_N * RG_N;
-  return vx_prec1_sec_work_elems(nx, ny, nz, nrhs, nsec, dmax) + (long)rep_kp(dmax) * np;
+  return vx_prec1_sec_work_elems(nx, ny, nz, nrhs, nsec, dmax) + (long)nsec * rep_kp(dmax) * np;
 }
 
 extern "C" int vx_prec1_apply_sec_reduced(int nx, int ny, int nz, int nrhs, const vx_c128* factors, const int* perm,
