@@ -344,10 +344,13 @@ __global__ void __launch_bounds__(256, (PZ <= 16 ? 3 : ZMUL_MINB_BIG))
 #pragma unroll
   for (int e = 0; e < PZ; ++e) v[e] = (active && e < nz) ? __ldg(src + (long)e * cols) : cmk(0.0, 0.0);
   reg_fft<PZ, false>(v);
-  // spectra this lane needs: PAIR_OF[c][0..2]
-  const int p0 = c == 0 ? 0 : (c == 1 ? 1 : 2);
-  const int p1 = c == 0 ? 1 : (c == 1 ? 3 : 4);
-  const int p2 = c == 0 ? 2 : (c == 1 ? 4 : 5);
+  // spectra this lane needs, in the order own component c, then c+1, c+2 (mod 3):
+  // PAIR_OF[c][c], PAIR_OF[c][c+1], PAIR_OF[c][c+2] -- the lane's own z-line needs no
+  // shuffle, the partners' values come with two rotating shuffles instead of three broadcasts
+  const int p0 = pair_of(c, c);
+  const int p1 = pair_of(c, (c + 1) % 3);
+  const int p2 = pair_of(c, (c + 2) % 3);
+  const int la = ((c + 1) % 3) * ZS_COLS + j, lb = ((c + 2) % 3) * ZS_COLS + j;
   long so0 = col, sstr = (long)PZ * cols, kstr = cols;
   bool my = false, mx = false;
   if (sv.compact) {
@@ -379,7 +382,7 @@ __global__ void __launch_bounds__(256, (PZ <= 16 ? 3 : ZMUL_MINB_BIG))
       double2 s0 = __ldg(S0 + ko), s1 = __ldg(S1 + ko), s2 = __ldg(S2 + ko);
       s0 = sign_flip(s0, m0), s1 = sign_flip(s1, m1), s2 = sign_flip(s2, m2);
       {
-        const double2 x0 = shfl_c(v[kz], j), x1 = shfl_c(v[kz], ZS_COLS + j), x2 = shfl_c(v[kz], 2 * ZS_COLS + j);
+        const double2 x0 = v[kz], x1 = shfl_c(v[kz], la), x2 = shfl_c(v[kz], lb);
         double2 acc = cmul(s0, x0);
         cfma(acc, s1, x1);
         cfma(acc, s2, x2);
@@ -388,7 +391,7 @@ __global__ void __launch_bounds__(256, (PZ <= 16 ? 3 : ZMUL_MINB_BIG))
       const int km = PZ - kz;
       if (kz > 0 && km > kz && km < PZ) {
         s0 = sign_flip(s0, zm0), s1 = sign_flip(s1, zm1), s2 = sign_flip(s2, zm2);
-        const double2 x0 = shfl_c(v[km], j), x1 = shfl_c(v[km], ZS_COLS + j), x2 = shfl_c(v[km], 2 * ZS_COLS + j);
+        const double2 x0 = v[km], x1 = shfl_c(v[km], la), x2 = shfl_c(v[km], lb);
         double2 acc = cmul(s0, x0);
         cfma(acc, s1, x1);
         cfma(acc, s2, x2);
@@ -400,7 +403,7 @@ __global__ void __launch_bounds__(256, (PZ <= 16 ? 3 : ZMUL_MINB_BIG))
     for (int kz = 0; kz < PZ; ++kz) {
       const long ko = (long)kz * kstr;
       const double2 s0 = __ldg(S0 + ko), s1 = __ldg(S1 + ko), s2 = __ldg(S2 + ko);
-      const double2 x0 = shfl_c(v[kz], j), x1 = shfl_c(v[kz], ZS_COLS + j), x2 = shfl_c(v[kz], 2 * ZS_COLS + j);
+      const double2 x0 = v[kz], x1 = shfl_c(v[kz], la), x2 = shfl_c(v[kz], lb);
       double2 acc = cmul(s0, x0);
       cfma(acc, s1, x1);
       cfma(acc, s2, x2);
