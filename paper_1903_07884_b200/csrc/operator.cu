@@ -311,6 +311,9 @@ constexpr int ZS_COLS = 10;
 #ifndef ZMUL_MINB_BIG
 #define ZMUL_MINB_BIG 2
 #endif
+#ifndef ZMUL_MINB_SMALL
+#define ZMUL_MINB_SMALL 2
+#endif
 
 // v or -v: XOR of the sign bits (m = 0 or 0x80000000)
 __device__ __forceinline__ double2 sign_flip(double2 v, unsigned m) {
@@ -323,7 +326,7 @@ __device__ __forceinline__ double2 shfl_c(double2 v, int src) {
 }
 
 template <int PZ>
-__global__ void __launch_bounds__(256, (PZ <= 16 ? 3 : ZMUL_MINB_BIG))
+__global__ void __launch_bounds__(256, (PZ <= 8 ? 3 : (PZ <= 16 ? ZMUL_MINB_SMALL : ZMUL_MINB_BIG)))
     op_zmul_shfl_kernel(double2* __restrict__ B, SpecView sv, int nz, long cols, double scale) {
   const int lane = threadIdx.x & 31;
   const long warp = (blockIdx.x * (long)blockDim.x + threadIdx.x) >> 5;
