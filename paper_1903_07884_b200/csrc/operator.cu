@@ -325,7 +325,7 @@ __device__ __forceinline__ double2 shfl_c(double2 v, int src) {
   return cmk(__shfl_sync(0xffffffffu, v.x, src), __shfl_sync(0xffffffffu, v.y, src));
 }
 
-template <int PZ>
+template <int PZ, bool COMPACT>
 __global__ void __launch_bounds__(256, (PZ <= 8 ? 3 : (PZ <= 16 ? ZMUL_MINB_SMALL : ZMUL_MINB_BIG)))
     op_zmul_shfl_kernel(double2* __restrict__ B, SpecView sv, int nz, long cols, double scale) {
   const int lane = threadIdx.x & 31;
@@ -335,7 +335,7 @@ __global__ void __launch_bounds__(256, (PZ <= 8 ? 3 : (PZ <= 16 ? ZMUL_MINB_SMAL
   long col = warp * ZS_COLS + j;
   const bool active = lane < 3 * ZS_COLS && col < cols;
   if (!active) col = 0;
-  if (sv.compact) {
+  if constexpr (COMPACT) {
     // rows ky = 0, 1, Py-1, 2, Py-2, ...: a row and its mirror (same compact
     // spectra) run back to back, so the second read hits L2
     const int lr = (int)sv.fdPx.div((unsigned)col);
@@ -356,7 +356,7 @@ __global__ void __launch_bounds__(256, (PZ <= 8 ? 3 : (PZ <= 16 ? ZMUL_MINB_SMAL
   const int la = ((c + 1) % 3) * ZS_COLS + j, lb = ((c + 2) % 3) * ZS_COLS + j;
   long so0 = col, sstr = (long)PZ * cols, kstr = cols;
   bool my = false, mx = false;
-  if (sv.compact) {
+  if constexpr (COMPACT) {
     const int ky = (int)sv.fdPx.div((unsigned)col), kx = (int)(col - (long)ky * sv.Px);
     my = 2 * ky > sv.Py;
     mx = 2 * kx > sv.Mx;
@@ -371,7 +371,7 @@ __global__ void __launch_bounds__(256, (PZ <= 8 ? 3 : (PZ <= 16 ? ZMUL_MINB_SMAL
   const double2* S0 = sv.S + p0 * sstr + so0;
   const double2* S1 = sv.S + p1 * sstr + so0;
   const double2* S2 = sv.S + p2 * sstr + so0;
-  if (sv.compact) {
+  if constexpr (COMPACT) {
     // compact spectra: S(PZ - kz) = +-S(kz) (sign by the z parity of the
     // component), so kz and its mirror share ONE load of the three spectra --
     // the loads, not the arithmetic, fill the L1 data pipe of this kernel
@@ -584,7 +584,10 @@ static int launch_zmul_reg(int PZ, double2* B, const SpecView& sv, int nz, long 
     switch (PZ) {
 #define VX_ZSH_LAUNCH(N)                                                           \
   case N:                                                                          \
-    if constexpr (N <= REG_ZMUL_MAX) op_zmul_shfl_kernel<N><<<g, 256, 0, s>>>(B, sv, nz, cols, scale); \
+    if constexpr (N <= REG_ZMUL_MAX) {                                                                  \
+      if (sv.compact) op_zmul_shfl_kernel<N, true><<<g, 256, 0, s>>>(B, sv, nz, cols, scale);           \
+      else op_zmul_shfl_kernel<N, false><<<g, 256, 0, s>>>(B, sv, nz, cols, scale);                     \
+    }                                                                                                   \
     break;
       VX_REG_LENGTHS(VX_ZSH_LAUNCH)
 #undef VX_ZSH_LAUNCH
