@@ -2209,8 +2209,11 @@ struct RepBatch {
 // zero outside k < n, j < ncols; blockIdx.y = product of the batch.
 __global__ void rep_gather_kernel(RepBatch rb, int ncols, int Np, int nrhs, const int* __restrict__ ks,
                                   const double2* __restrict__ S, long s_row, long s_k, double2* __restrict__ Bt) {
-  const int z = blockIdx.y, n = rb.n[z], Kp = (n + RG_K - 1) / RG_K * RG_K;
-  S += rb.s_off[z];
+  // selects, not rb.n[z]: a runtime index would copy the parameter struct to local memory
+  const int z = blockIdx.y;
+  const int n = z == 0 ? rb.n[0] : z == 1 ? rb.n[1] : z == 2 ? rb.n[2] : rb.n[3];
+  const int Kp = (n + RG_K - 1) / RG_K * RG_K;
+  S += z == 0 ? rb.s_off[0] : z == 1 ? rb.s_off[1] : z == 2 ? rb.s_off[2] : rb.s_off[3];
   Bt += z * rb.bt_stride;
   const long total = (long)Kp * Np;
   for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < total; i += (long)gridDim.x * blockDim.x) {
@@ -2237,11 +2240,14 @@ __global__ void __launch_bounds__(RG_THREADS, 2)
                     long ldb, int ncols, int nrhs, const int* __restrict__ ks, double2* S, long s_row, long s_k,
                     int RG_STAGES) {
   extern __shared__ __align__(128) double2 rg_sm[];
-  const int z = blockIdx.z, n = rb.n[z], Kp = (n + RG_K - 1) / RG_K * RG_K;
+  // selects, not rb.n[z]: a runtime index would copy the parameter struct to local memory
+  const int z = blockIdx.z;
+  const int n = z == 0 ? rb.n[0] : z == 1 ? rb.n[1] : z == 2 ? rb.n[2] : rb.n[3];
+  const int Kp = (n + RG_K - 1) / RG_K * RG_K;
   if ((int)blockIdx.y * RG_M >= n) return;  // row tiles beyond this product's block
-  A += rb.a_off[z];
+  A += z == 0 ? rb.a_off[0] : z == 1 ? rb.a_off[1] : z == 2 ? rb.a_off[2] : rb.a_off[3];
   Bt += z * rb.bt_stride;
-  S += rb.s_off[z];
+  S += z == 0 ? rb.s_off[0] : z == 1 ? rb.s_off[1] : z == 2 ? rb.s_off[2] : rb.s_off[3];
   constexpr int TA = RG_K * RG_LDA, TB = RG_K * RG_LDB;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = warp & 1, wn = warp >> 1;

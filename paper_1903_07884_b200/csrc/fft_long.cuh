@@ -27,8 +27,18 @@
 
 namespace vx {
 
+// CTA size cap: register codelets above 32 points (735 = 21 x 35) need more than the 128
+// registers a 512-thread CTA leaves per thread (they spill 300 bytes).  The forward
+// transform runs them at most 256 threads per CTA with up to 255 registers (c4: 0.083 ->
+// 0.068 ms); the inverse with the operator epilogue prefers two spilling CTAs per SM
+// (0.136 ms against 0.191 ms with one).
+template <int R1, int R2, int R3, bool INV>
+constexpr int fft_long_max_threads() {
+  return (!INV && (R1 > 32 || R2 > 32 || R3 > 32)) ? 256 : 512;
+}
+
 template <int R1, int R2, int R3, bool INV, class Loader, class Storer>
-__global__ void __launch_bounds__(512, 1)
+__global__ void __launch_bounds__((fft_long_max_threads<R1, R2, R3, INV>()), 1)
     fft_long_kernel(Loader ld, Storer st, const double2* __restrict__ tw_lo, const double2* __restrict__ tw_hi,
                     int nhi, int n_lines, int W, int n_in, int n_out) {
   constexpr int L = R1 * R2 * R3;
@@ -228,7 +238,7 @@ int launch_fft_long_t(const FftPlan& p, const Loader& ld, const Storer& st, int 
   // lines that fill the SM alone get up to 640 threads; shorter lines run
   // 2+ CTAs per SM with fewer threads each
   const size_t smem = ((size_t)W * L + 64 + p.nhi) * sizeof(double2);
-  const int cap = smem > 100 * 1024 ? 512 : 256;
+  const int cap = smem > 100 * 1024 ? fft_long_max_threads<R1, R2, R3, INV>() : 256;
   int thr = ((tasks < cap ? tasks : cap) + 31) / 32 * 32;
   auto kern = fft_long_kernel<R1, R2, R3, INV, Loader, Storer>;
   if (smem > 48 * 1024)
