@@ -401,7 +401,11 @@ static int launch_symv2_inv_t(const SymGeom& sg, const double2* G, const int* it
   // 0.667 / 0.760 / 1.239; 128 registers + 3 slots 0.681 / 0.801 / 1.260 -- the extra resident
   // CTA covers the other CTAs' right-hand-side gathers, a third slot does not pay
   static const int slots_env = env_int("VX_SYMV2_SLOTS", 2);
-  static const int minb = env_int("VX_SYMV_MINB", 4);
+  // resident CTAs per SM the kernel is compiled for (4: 96 registers, 3: 128).  Measured
+  // (apply kernel, ms): c1 (187-row sectors) 0.539 with 4 / 0.554 with 3; c3 (231 rows)
+  // 0.513 / 0.486; c2 (413 rows, three CTAs fit in shared memory either way) 0.670 / 0.616
+  static const int minb_env = env_int("VX_SYMV_MINB", 0);
+  const int minb = minb_env ? minb_env : (sg.dmax <= 208 ? 4 : 3);
   static const int pfwin = env_int("VX_SYMV_PF", 24) * 64;  // L2 prefetch window, entries
   const int S = slots_env < 2 ? 2 : (slots_env > 12 ? 12 : slots_env);
   const int npad = (sg.dmax + 31) / 32 * 32;
